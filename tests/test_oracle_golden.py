@@ -1,0 +1,192 @@
+"""Pin the CPU oracle against golden vectors produced by the reference itself.
+
+The golden files come from tests/golden/make_golden.py, which ran the
+reference ``irksolve`` (numba backend) in the build container.  Tolerances
+follow the reference's own backend-parity test (tests/test_backends.py:38-84,
+atol 1e-12) expressed relatively; GMRES must reproduce iteration counts
+exactly (the oracle is the same MGS algorithm).
+"""
+
+import numpy as np
+import pytest
+
+import oracle as O
+from paper_1701_07181_b200 import workloads as W
+from paper_1701_07181_b200.tableau import builtin_tableau, derive
+from tests.helpers import load_golden, pattern_of, random_blocks, rel, sha
+
+TOL = 1e-12
+
+
+@pytest.fixture(scope="module")
+def ks():
+    return load_golden("kernels_small")
+
+
+def line_pattern(T, periodic=True):
+    from paper_1701_07181_b200.meshes import line_mesh
+    g = line_mesh(T, periodic=periodic)
+    return g.adjacency, pattern_of(g.adjacency)
+
+
+def test_random_blocks_restatement(ks):
+    adj, _ = line_pattern(10)
+    np.testing.assert_array_equal(random_blocks(adj, 3, seed=3), ks["line_data"])
+
+
+def test_bsr_matvec(ks):
+    adj, (ip, ix, dp) = line_pattern(10)
+    y = O.bsr_matvec(ip, ix, ks["line_data"], ks["line_x"])
+    assert rel(y, ks["line_matvec"]) < TOL
+
+
+@pytest.mark.parametrize("tag,keep_key", [("", None), ("4", "line_keep4")])
+def test_ilu0_factor_solve(ks, tag, keep_key):
+    adj, (ip, ix, dp) = line_pattern(10)
+    keep = np.ones(len(ix), bool) if keep_key is None else ks[keep_key]
+    f, d, fail = O.ilu0_factor(ip, ix, dp, ks["line_data"], keep, True)
+    assert fail == -1
+    assert rel(f, ks[f"line_f{tag}"]) < TOL
+    assert rel(d, ks[f"line_dinv{tag}"]) < TOL
+    x = O.ilu0_solve(ip, ix, dp, f, d, keep, ks["line_x"])
+    assert rel(x, ks[f"line_solve{tag}"]) < TOL
+
+
+def test_keep_mask_restatement(ks):
+    from paper_1701_07181_b200.meshes import line_mesh, partition
+    g = partition(line_mesh(10, periodic=True), 4)
+    ip, ix, _ = pattern_of(g.adjacency)
+    np.testing.assert_array_equal(O.partition_keep_mask(ip, ix, g.partition_of),
+                                  ks["line_keep4"])
+
+
+def test_general_path_triangle(ks):
+    adj = [[1, 2], [0, 2], [0, 1]]
+    ip, ix, dp = pattern_of(adj)
+    keep = np.ones(len(ix), bool)
+    f, d, fail = O.ilu0_factor(ip, ix, dp, ks["tri_data"], keep, False)
+    assert fail == int(ks["tri_fail"]) == -1
+    assert rel(f, ks["tri_f"]) < TOL
+    assert rel(d, ks["tri_dinv"]) < TOL
+    assert rel(O.ilu0_solve(ip, ix, dp, f, d, keep, ks["tri_y"]), ks["tri_solve"]) < TOL
+    # the simplified sweep differs on this graph (tests/test_precond.py:136-151)
+    f2, _, _ = O.ilu0_factor(ip, ix, dp, ks["tri_data"], keep, True)
+    assert np.abs(f2 - ks["tri_f"]).max() > 1e-3
+
+
+@pytest.mark.parametrize("which", ["0", "2"])
+def test_singular_pivot_index(ks, which):
+    adj = line_pattern(4, periodic=False)[0]
+    ip, ix, dp = pattern_of(adj)
+    _, _, fail = O.ilu0_factor(ip, ix, dp, ks[f"sing_data{which}"], np.ones(len(ix), bool), True)
+    assert fail == int(ks[f"sing_fail{which}"]) == int(which)
+
+
+def _coupled_problem(ks):
+    adj, (ip, ix, dp) = line_pattern(8)
+    der = derive(builtin_tableau("RADAU35"))
+    jac = [np.ascontiguousarray(j) for j in ks["cpl_J"]]
+    return O.Problem(ip, ix, dp, jac, ks["cpl_M"], der.a_inv, 0.08), der
+
+
+def test_stage_matvec_distinct_j(ks):
+    prob, _ = _coupled_problem(ks)
+    assert rel(prob.matvec(ks["cpl_w"]), ks["cpl_matvec"]) < TOL
+
+
+@pytest.mark.parametrize("lit", [False, True])
+def test_coupled_factor_apply(ks, lit):
+    prob, _ = _coupled_problem(ks)
+    fac = O.stage_coupled_factorize(prob, literal_update=lit)
+    tag = "lit" if lit else "std"
+    assert rel(fac.fstage, ks[f"cpl_{tag}_fstage"]) < TOL
+    assert rel(fac.fcoupling, ks[f"cpl_{tag}_fcoupling"]) < TOL
+    assert rel(fac.dinv, ks[f"cpl_{tag}_dinv"]) < TOL
+    assert rel(fac.apply(ks["cpl_w"]), ks[f"cpl_{tag}_apply"]) < TOL
+
+
+def test_uncoupled_variants(ks):
+    prob, der = _coupled_problem(ks)
+    fac = O.stage_uncoupled_factorize(prob, der.shifts)
+    assert rel(fac.apply(ks["cpl_w"]), ks["unc_apply"]) < TOL
+    assert rel(np.stack([f[1] for f in fac.factors]), ks["unc_dinv"]) < TOL
+    assert rel(O.stage_uncoupled_factorize(prob, None).apply(ks["cpl_w"]), ks["unc0_apply"]) < TOL
+    bj = O.stage_uncoupled_factorize(prob, der.shifts, partition_of=np.arange(8))
+    assert rel(bj.apply(ks["cpl_w"]), ks["bj_apply"]) < TOL
+    part = np.repeat(np.arange(4), 2)
+    cp4 = O.stage_coupled_factorize(prob, partition_of=part)
+    assert rel(cp4.apply(ks["cpl_w"]), ks["cpl4_apply"]) < TOL
+    # stage-parallel apply is bitwise identical (criterion 11)
+    par = O.stage_uncoupled_factorize(prob, der.shifts, workers=3)
+    np.testing.assert_array_equal(par.apply(ks["cpl_w"]), fac.apply(ks["cpl_w"]))
+
+
+def test_gmres_restatement(ks):
+    prob, der = _coupled_problem(ks)
+    for tag, fac in (("cpl", O.stage_coupled_factorize(prob)),
+                     ("unc", O.stage_uncoupled_factorize(prob, der.shifts))):
+        x, st = O.gmres(prob.matvec, fac.apply, ks["gm_rhs"], O.GmresConfig(rel_tol=1e-8))
+        assert st.iterations == int(ks[f"gm_{tag}_iters"])
+        assert rel(x, ks[f"gm_{tag}_x"]) < 1e-10
+        np.testing.assert_allclose(st.residual_history, ks[f"gm_{tag}_hist"], rtol=1e-9)
+        x, st = O.gmres(prob.matvec, fac.apply, ks["gm_rhs"],
+                        O.GmresConfig(rel_tol=1e-10, restart=3))
+        assert st.iterations == int(ks[f"gm_{tag}_rst_iters"])
+        assert rel(x, ks[f"gm_{tag}_rst_x"]) < 1e-10
+
+
+@pytest.mark.parametrize("name", ["RADAU23", "RADAU35", "DIRK33"])
+def test_tableau_kats(ks, name):
+    d = derive(builtin_tableau(name))
+    np.testing.assert_allclose(d.a_inv, ks[f"tab_{name}_a_inv"], rtol=0, atol=1e-13)
+    np.testing.assert_allclose(d.shifts, ks[f"tab_{name}_shifts"], rtol=0, atol=1e-13)
+    if name == "RADAU23":  # tests/test_tableaux.py:94-97
+        np.testing.assert_allclose(d.a_inv, [[1.5, 0.5], [-4.5, 2.5]], atol=1e-13)
+        np.testing.assert_allclose(d.shifts, [4.5, 0.5], atol=1e-13)
+
+
+CASES = {
+    "cfg0": (W.CONFIGS[0], None, {}),
+    "cfg1_n8": (W.CONFIGS[1].scaled(N=8), None, {}),
+    "cfg1_n8_color": (W.CONFIGS[1].scaled(N=8, ordering="color"), None, {}),
+    "cfg1_n6_coupled": (W.CONFIGS[1].scaled(N=6, scheme="RADAU23"), "coupled", {}),
+    "cfg2_n4": (W.CONFIGS[2].scaled(N=4, nb=10), None, {}),
+    "cfg2_n3_full": (W.CONFIGS[2].scaled(N=3, nb=6), None, {}),
+    "cfg2_n4_p4": (W.CONFIGS[2].scaled(N=4, nb=10), None, {"partitions": 4}),
+    "cfg2_n4_color": (W.CONFIGS[2].scaled(N=4, nb=10, ordering="color"), None, {}),
+    "cfg1_n8_var": (W.CONFIGS[1].scaled(N=8, jstd="sqrtnb"), None, {"max_iters": 60}),
+}
+
+
+def oracle_case(name):
+    cfg, kind, opts = CASES[name]
+    g = load_golden(name)
+    wl = W.make_workload(cfg)
+    assert sha(wl.J, wl.M, wl.rhs) == str(g["input_sha"]), "generator drifted"
+    assert abs(wl.dt - float(g["dt"])) <= 1e-14 * wl.dt
+    prob = O.problem_from_workload(wl)
+    prob.dt = float(g["dt"])
+    part = None
+    if opts.get("partitions"):
+        from paper_1701_07181_b200.meshes import partition_bounds
+        b = partition_bounds(wl.pattern.T, opts["partitions"])
+        part = np.repeat(np.arange(opts["partitions"]), np.diff(b))
+    fac = O.make_preconditioner(prob, kind or cfg.precond, wl.shifts, part)
+    return cfg, g, wl, prob, fac, opts
+
+
+@pytest.mark.parametrize("name", list(CASES))
+def test_workload_case(name):
+    cfg, g, wl, prob, fac, opts = oracle_case(name)
+    assert rel(prob.matvec(g["w"]), g["matvec"]) < TOL
+    assert rel(fac.apply(g["w"]), g["apply"]) < TOL
+    x, st = O.gmres(prob.matvec, fac.apply, wl.rhs,
+                    O.GmresConfig(rel_tol=cfg.rtol, restart=cfg.restart,
+                                  max_iters=opts.get("max_iters", 500)))
+    assert st.iterations == int(g["iterations"])
+    assert st.converged == bool(g["converged"])
+    assert rel(x, g["x"]) < 1e-10
+    assert st.operator_applies == int(g["operator_applies"])
+    if "fdata" in g:
+        assert rel(np.stack([f[0] for f in fac.factors]), g["fdata"]) < TOL
+        assert rel(np.stack([f[1] for f in fac.factors]), g["dinv"]) < TOL
