@@ -1,0 +1,797 @@
+// Block ILU(0) factorisation on the GPU (pull / left-looking form).
+//
+// Reference (push form): numba_backend.py:43-72 (Alg. 1/2) and :94-125
+// (Alg. 3, stage-coupled).  For pivot i ascending the reference inverts D_i,
+// then for every upper neighbour j forms L_ji = B_ji D_i^-1 and updates
+// D_j -= L_ji U_ij.  Pulled to the row being finalised, row j receives those
+// updates in ascending i, exactly the order of the push form; the cross-stage
+// Schur updates of Alg. 3 (from stages l < k) precede the within-stage ones,
+// again as in the reference.  Row j only needs rows i < j that are complete,
+// so rows are processed level by level (level(j) = 1 + max level of its
+// lower neighbours); every (stage, row) task of a level runs as one CTA.
+//
+// A task: D = coef*M_j + alpha*J_jj; [coupled: G = C_lo * Dinv_{l,j},
+// D -= G * C_up]; for each kept lower neighbour i: L = (alpha*J_ji) Dinv_i,
+// D -= L U_ij [general: U_jk -= L U_ik fill updates]; Dinv_j = inv(D) by
+// Gauss-Jordan with partial pivoting (same pivot rows as LAPACK getrf, so
+// det = exp(sum log|pivot|) and the singular decision of
+// numba_backend.py:33-40 carry over), cond_1 = |D|_1 |D^-1|_1 > 1e14 fails.
+// Block products are FP64 4x4 register-tiled GEMMs from shared memory.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <climits>
+#include <cstring>
+#include <vector>
+
+#include "irk_internal.cuh"
+
+namespace irk {
+
+
+struct FactorArgs {
+    const int32_t *indptr, *indices, *diag, *lptr, *uptr, *tpos;
+    const uint8_t* keep;
+    const double* J[IRK_MAX_STAGES];
+    const double* M;
+    const double* Cexp;       // explicit couplings (s*s*T blocks) or NULL
+    double alpha;
+    double coef[IRK_MAX_STAGES];
+    double cmix[IRK_MAX_STAGES * IRK_MAX_STAGES];
+    double* L;
+    double* Dinv;
+    double* Dst;
+    double* U;                // stored upper blocks (general mode) or NULL
+    double* G;
+    unsigned long long* fail_key;
+    const int32_t* tasks;
+    int64_t ntasks;
+    int64_t T;
+    int s, nb, nbp4, ld, KC;
+    int coupled, literal, simplified;
+};
+
+__device__ __forceinline__ int pair_index(int hi, int lo) { return hi * (hi - 1) / 2 + lo; }
+
+// element (a,b) of a device-layout block
+__device__ __forceinline__ int64_t lay(int a, int b, int nb) {
+    return ((int64_t)(b >> 1) * nb + a) * 2 + (b & 1);
+}
+
+// smem tile At[c - c0][a] (k-major, ld) <- scale * A(a, c), c in [c0, c0+kc).
+// One 16-byte load per (column pair, row): consecutive threads read
+// consecutive rows of a pair (coalesced).  c0 and kc are even.
+__device__ void load_At(double* At, const double* __restrict__ A, double scale, int c0, int kc,
+                        const FactorArgs& F) {
+    const int nb = F.nb, ld = F.ld, n4 = F.nbp4;
+    const int tot = (kc >> 1) * n4;
+    for (int e = threadIdx.x; e < tot; e += blockDim.x) {
+        const int pp = e / n4, a = e - pp * n4;
+        const int p = (c0 >> 1) + pp;
+        double2 v = make_double2(0.0, 0.0);
+        if (A && a < nb && 2 * p < nb) {
+            v = reinterpret_cast<const double2*>(A)[(int64_t)p * nb + a];
+            v.x *= scale;
+            v.y *= scale;
+        }
+        At[(2 * pp) * ld + a] = v.x;
+        At[(2 * pp + 1) * ld + a] = v.y;
+    }
+}
+
+// smem tile Bs[c - c0][b] (k-major) <- scale * B(c, b), c in [c0, c0+kc)
+__device__ void load_Bs(double* Bs, const double* __restrict__ B, double scale, int c0, int kc,
+                        const FactorArgs& F) {
+    const int nb = F.nb, ld = F.ld;
+    const int tot = (F.nbp4 >> 1) * kc;
+    for (int e = threadIdx.x; e < tot; e += blockDim.x) {
+        const int p = e / kc, cc = e - p * kc;   // consecutive threads: consecutive rows c
+        const int c = c0 + cc;
+        double2 v = make_double2(0.0, 0.0);
+        if (B && c < nb && 2 * p < nb) {
+            v = reinterpret_cast<const double2*>(B)[(int64_t)p * nb + c];
+            v.x *= scale;
+            v.y *= scale;
+        }
+        *reinterpret_cast<double2*>(Bs + cc * ld + 2 * p) = v;
+    }
+}
+
+template <int MAXT>
+struct Tiles {
+    double acc[MAXT][4][4];
+    __device__ void zero() {
+#pragma unroll
+        for (int t = 0; t < MAXT; ++t)
+#pragma unroll
+            for (int x = 0; x < 4; ++x)
+#pragma unroll
+                for (int y = 0; y < 4; ++y) acc[t][x][y] = 0.0;
+    }
+};
+
+// acc(tile) += At[c][a0..a0+3] (x) Bs[c][b0..b0+3] for c < kc.
+// AT points at row 0 of the A operand's k-range (k-major, ld).
+template <int MAXT>
+__device__ __forceinline__ void mma_chunk(Tiles<MAXT>& T, const double* AT, const double* BS,
+                                          int kc, const FactorArgs& F) {
+    const int tpr = F.nbp4 >> 2;  // tiles per row
+    const int ntile = tpr * tpr;
+#pragma unroll
+    for (int t = 0; t < MAXT; ++t) {
+        const int tile = threadIdx.x + t * blockDim.x;
+        if (tile >= ntile) break;
+        const int a0 = (tile / tpr) * 4, b0 = (tile % tpr) * 4;
+#pragma unroll 4
+        for (int c = 0; c < kc; ++c) {
+            const double2 a01 = *reinterpret_cast<const double2*>(AT + c * F.ld + a0);
+            const double2 a23 = *reinterpret_cast<const double2*>(AT + c * F.ld + a0 + 2);
+            const double2 b01 = *reinterpret_cast<const double2*>(BS + c * F.ld + b0);
+            const double2 b23 = *reinterpret_cast<const double2*>(BS + c * F.ld + b0 + 2);
+            const double av[4] = {a01.x, a01.y, a23.x, a23.y};
+            const double bv[4] = {b01.x, b01.y, b23.x, b23.y};
+#pragma unroll
+            for (int x = 0; x < 4; ++x)
+#pragma unroll
+                for (int y = 0; y < 4; ++y) T.acc[t][x][y] = fma(av[x], bv[y], T.acc[t][x][y]);
+        }
+    }
+}
+
+struct Smem {
+    double* D;    // nbp4 x ld  (row-major D[a][b])
+    double* Lt;   // nbp4 x ld  (k-major L^T: Lt[c][a] = L(a,c))
+    double* At;   // KC x ld
+    double* Bs;   // KC x ld
+    double* colk; // nbp4
+    double* red;  // 64
+    int* piv;     // nbp4
+    int* misc;    // 8
+};
+
+__device__ Smem carve(const FactorArgs& F) {
+    extern __shared__ __align__(16) double smem[];
+    Smem S;
+    const int big = F.nbp4 * F.ld, chunk = F.KC * F.ld;
+    S.D = smem;
+    S.Lt = S.D + big;
+    S.At = S.Lt + big;
+    S.Bs = S.At + chunk;
+    S.colk = S.Bs + chunk;
+    S.red = S.colk + F.nbp4;
+    S.piv = reinterpret_cast<int*>(S.red + 64);
+    S.misc = S.piv + F.nbp4;
+    return S;
+}
+
+// out = A * B (A scaled by sa, B scaled by sb): result stays in tiles
+template <int MAXT>
+__device__ void gemm_global(Tiles<MAXT>& T, const double* A, double sa, const double* B, double sb,
+                            Smem& S, const FactorArgs& F) {
+    T.zero();
+    for (int c0 = 0; c0 < F.nbp4; c0 += F.KC) {
+        const int kc = min(F.KC, F.nbp4 - c0);
+        load_At(S.At, A, sa, c0, kc, F);
+        load_Bs(S.Bs, B, sb, c0, kc, F);
+        __syncthreads();
+        mma_chunk<MAXT>(T, S.At, S.Bs, kc, F);
+        __syncthreads();
+    }
+}
+
+// tiles = Lt(smem, full) * B
+template <int MAXT>
+__device__ void gemm_lt(Tiles<MAXT>& T, const double* B, double sb, Smem& S, const FactorArgs& F) {
+    T.zero();
+    for (int c0 = 0; c0 < F.nbp4; c0 += F.KC) {
+        const int kc = min(F.KC, F.nbp4 - c0);
+        load_Bs(S.Bs, B, sb, c0, kc, F);
+        __syncthreads();
+        mma_chunk<MAXT>(T, S.Lt + c0 * F.ld, S.Bs, kc, F);
+        __syncthreads();
+    }
+}
+
+template <int MAXT, typename Fn>
+__device__ __forceinline__ void for_tiles(Tiles<MAXT>& T, const FactorArgs& F, Fn fn) {
+    const int tpr = F.nbp4 >> 2;
+    const int ntile = tpr * tpr;
+#pragma unroll
+    for (int t = 0; t < MAXT; ++t) {
+        const int tile = threadIdx.x + t * blockDim.x;
+        if (tile >= ntile) break;
+        const int a0 = (tile / tpr) * 4, b0 = (tile % tpr) * 4;
+#pragma unroll
+        for (int x = 0; x < 4; ++x)
+#pragma unroll
+            for (int y = 0; y < 4; ++y) fn(a0 + x, b0 + y, T.acc[t][x][y]);
+    }
+}
+
+// store tiles as a device-layout block (rows/cols < nb) and as Lt in smem
+template <int MAXT>
+__device__ void store_L(Tiles<MAXT>& T, double* dst, Smem& S, const FactorArgs& F) {
+    for_tiles<MAXT>(T, F, [&](int a, int b, double v) {
+        S.Lt[b * F.ld + a] = v;
+        if (dst && a < F.nb && b < F.nb) dst[lay(a, b, F.nb)] = v;
+    });
+    __syncthreads();
+}
+
+template <int MAXT>
+__device__ void sub_into_D(Tiles<MAXT>& T, Smem& S, const FactorArgs& F) {
+    for_tiles<MAXT>(T, F, [&](int a, int b, double v) { S.D[a * F.ld + b] -= v; });
+    __syncthreads();
+}
+
+// copy smem rows of D (a<nb, b<nb) into a device-layout block
+__device__ void store_D(const double* D, double* dst, const FactorArgs& F) {
+    const int nb = F.nb, P = (nb + 1) >> 1;
+    for (int e = threadIdx.x; e < nb * P; e += blockDim.x) {
+        const int p = e / nb, a = e - p * nb;
+        double2 v;
+        v.x = D[a * F.ld + 2 * p];
+        v.y = (2 * p + 1 < nb) ? D[a * F.ld + 2 * p + 1] : 0.0;
+        reinterpret_cast<double2*>(dst)[e] = v;
+    }
+}
+
+__device__ double block_norm1(const double* D, Smem& S, const FactorArgs& F) {
+    // max column abs-sum, NaN propagating (np.abs(b).sum(axis=0).max())
+    const int nb = F.nb;
+    double v = -1.0;
+    int isnan_flag = 0;
+    for (int b = threadIdx.x; b < nb; b += blockDim.x) {
+        double s = 0.0;
+        for (int a = 0; a < nb; ++a) s += fabs(D[a * F.ld + b]);
+        if (s != s) isnan_flag = 1;
+        v = fmax(v, s);
+    }
+    // block reduce max over warps
+    for (int o = 16; o; o >>= 1) {
+        v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+        isnan_flag |= __shfl_xor_sync(0xffffffffu, isnan_flag, o);
+    }
+    const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+    if (l == 0) { S.red[w] = isnan_flag ? __longlong_as_double(0x7ff8000000000000LL) : v; }
+    __syncthreads();
+    double r = -1.0;
+    const int nw = (blockDim.x + 31) >> 5;
+    for (int i = 0; i < nw; ++i) {
+        const double x = S.red[i];
+        if (x != x) { r = x; break; }
+        r = fmax(r, x);
+    }
+    __syncthreads();
+    return r;
+}
+
+// In-place Gauss-Jordan inverse of S.D (nb x nb) with partial pivoting.
+// Returns (in all threads) whether the pivot is acceptable.
+__device__ bool gj_invert(Smem& S, const FactorArgs& F) {
+    const int nb = F.nb, ld = F.ld;
+    double* D = S.D;
+    const double n1 = block_norm1(D, S, F);
+    double logdet = 0.0;
+    int zero = 0;
+    for (int k = 0; k < nb; ++k) {
+        if (threadIdx.x < 32) {
+            double best = -1.0;
+            int bi = k;
+            for (int r = k + threadIdx.x; r < nb; r += 32) {
+                const double v = fabs(D[r * ld + k]);
+                if (v > best) { best = v; bi = r; }
+            }
+            for (int o = 16; o; o >>= 1) {
+                const double ob = __shfl_xor_sync(0xffffffffu, best, o);
+                const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+                if (ob > best || (ob == best && oi < bi)) { best = ob; bi = oi; }
+            }
+            if (threadIdx.x == 0) { S.misc[0] = bi; S.piv[k] = bi; }
+        }
+        __syncthreads();
+        const int p = S.misc[0];
+        if (p != k)
+            for (int b = threadIdx.x; b < nb; b += blockDim.x) {
+                const double t = D[k * ld + b];
+                D[k * ld + b] = D[p * ld + b];
+                D[p * ld + b] = t;
+            }
+        __syncthreads();
+        const double piv = D[k * ld + k];
+        if (threadIdx.x == 0) {
+            logdet += log(fabs(piv));
+            if (piv == 0.0) zero = 1;
+        }
+        for (int r = threadIdx.x; r < nb; r += blockDim.x) S.colk[r] = D[r * ld + k];
+        __syncthreads();
+        for (int b = threadIdx.x; b < nb; b += blockDim.x)
+            D[k * ld + b] = (b == k) ? 1.0 / piv : D[k * ld + b] / piv;
+        __syncthreads();
+        const int tot = nb * nb;
+        for (int e = threadIdx.x; e < tot; e += blockDim.x) {
+            const int r = e / nb, b = e - r * nb;
+            if (r == k) continue;
+            const double f = S.colk[r];
+            if (b == k) D[r * ld + k] = -f * D[k * ld + k];
+            else D[r * ld + b] -= f * D[k * ld + b];
+        }
+        __syncthreads();
+    }
+    for (int k = nb - 1; k >= 0; --k) {
+        const int p = S.piv[k];
+        if (p != k) {
+            for (int r = threadIdx.x; r < nb; r += blockDim.x) {
+                const double t = D[r * ld + k];
+                D[r * ld + k] = D[r * ld + p];
+                D[r * ld + p] = t;
+            }
+            __syncthreads();
+        }
+    }
+    const double n2 = block_norm1(D, S, F);
+    if (threadIdx.x == 0) {
+        const double det = exp(logdet);
+        const double cond = n1 * n2;
+        const bool bad = zero || det == 0.0 || !isfinite(det) || !(cond <= 1e14);
+        S.misc[1] = bad ? 1 : 0;
+    }
+    __syncthreads();
+    const bool ok = S.misc[1] == 0;
+    __syncthreads();
+    return ok;
+}
+
+template <int MAXT>
+__global__ void __launch_bounds__(256) k_factor(FactorArgs F) {
+    Smem S = carve(F);
+    const int nb = F.nb, ld = F.ld;
+    const int64_t bsz = (int64_t)nb * 2 * ((nb + 1) >> 1);
+    const int npairs = F.s * (F.s - 1) / 2;
+    Tiles<MAXT> T;
+    for (int64_t t = blockIdx.x; t < F.ntasks; t += gridDim.x) {
+        const int64_t code = F.tasks[t];
+        const int k = (int)(code / F.T);
+        const int j = (int)(code - (int64_t)k * F.T);
+        const double* Jk = F.J[k];
+        const int dpos = F.diag[j];
+        const bool keep_d = F.keep[dpos] != 0;
+        // D = fl(alpha*J_jj) + fl(coef*M_j)  (build_stage_matrix, precond.py:48-54)
+        for (int e = threadIdx.x; e < F.nbp4 * ld; e += blockDim.x) S.D[e] = 0.0;
+        __syncthreads();
+        if (keep_d) {
+            const int P = (nb + 1) >> 1;
+            const double2* Jd = reinterpret_cast<const double2*>(Jk + (int64_t)dpos * bsz);
+            const double2* Md = F.M ? reinterpret_cast<const double2*>(F.M + (int64_t)j * bsz) : nullptr;
+            for (int e = threadIdx.x; e < nb * P; e += blockDim.x) {
+                const int p = e / nb, a = e - p * nb;
+                const double2 v = Jd[e];
+                double x0 = __dmul_rn(F.alpha, v.x), x1 = __dmul_rn(F.alpha, v.y);
+                if (Md) {
+                    const double2 m = Md[e];
+                    x0 = __dadd_rn(x0, __dmul_rn(F.coef[k], m.x));
+                    x1 = __dadd_rn(x1, __dmul_rn(F.coef[k], m.y));
+                }
+                S.D[a * ld + 2 * p] = x0;
+                if (2 * p + 1 < nb) S.D[a * ld + 2 * p + 1] = x1;
+            }
+        }
+        __syncthreads();
+        if (F.coupled) {
+            // cross-stage Schur updates from earlier stages l < k (numba_backend.py:117-124)
+            for (int l = 0; l < k; ++l) {
+                const double* clo;
+                double slo;
+                if (F.Cexp) { clo = F.Cexp + (((int64_t)k * F.s + l) * F.T + j) * bsz; slo = 1.0; }
+                else { clo = F.M + (int64_t)j * bsz; slo = F.cmix[k * F.s + l]; }
+                gemm_global<MAXT>(T, clo, slo, F.Dinv + ((int64_t)j * F.s + l) * bsz, 1.0, S, F);
+                store_L<MAXT>(T, F.G + ((int64_t)j * npairs + pair_index(k, l)) * bsz, S, F);
+                const double* cup;
+                double sup;
+                if (F.literal) { cup = F.Dst + ((int64_t)j * F.s + l) * bsz; sup = 1.0; }
+                else if (F.Cexp) { cup = F.Cexp + (((int64_t)l * F.s + k) * F.T + j) * bsz; sup = 1.0; }
+                else { cup = F.M + (int64_t)j * bsz; sup = F.cmix[l * F.s + k]; }
+                gemm_lt<MAXT>(T, cup, sup, S, F);
+                sub_into_D<MAXT>(T, S, F);
+            }
+        }
+        // within-stage updates from kept lower neighbours, ascending
+        const int q0 = F.indptr[j];
+        const int lq0 = F.lptr[j];
+        for (int q = q0; q < dpos; ++q) {
+            const int i = F.indices[q];
+            const int tq = F.tpos[q];   // (i, j) block in row i
+            const bool keep_lo = F.keep[q] != 0;
+            const bool keep_up = tq >= 0 && F.keep[tq] != 0;
+            double* Lout = F.L + ((int64_t)(lq0 + (q - q0)) * F.s + k) * bsz;
+            if (!keep_up) {
+                // reference never touches this block: it stays B_ji (or 0 if dropped)
+                for (int e = threadIdx.x; e < nb * nb; e += blockDim.x) {
+                    const int a = e / nb, b = e - a * nb;
+                    Lout[lay(a, b, nb)] = keep_lo ? F.alpha * Jk[(int64_t)q * bsz + lay(a, b, nb)] : 0.0;
+                }
+                __syncthreads();
+                continue;
+            }
+            gemm_global<MAXT>(T, keep_lo ? Jk + (int64_t)q * bsz : nullptr, F.alpha,
+                              F.Dinv + ((int64_t)i * F.s + k) * bsz, 1.0, S, F);
+            store_L<MAXT>(T, Lout, S, F);
+            if (!keep_lo) continue;   // L == 0: D unchanged
+            const double* Ub;
+            double su;
+            if (F.U) { Ub = F.U + ((int64_t)(F.uptr[i] + (tq - F.diag[i] - 1)) * F.s + k) * bsz; su = 1.0; }
+            else { Ub = Jk + (int64_t)tq * bsz; su = F.alpha; }
+            gemm_lt<MAXT>(T, Ub, su, S, F);
+            sub_into_D<MAXT>(T, S, F);
+            if (!F.simplified) {
+                // fill-limited updates U_jk2 -= L U_ik2 (numba_backend.py:64-71)
+                for (int kik = F.indptr[i]; kik < F.indptr[i + 1]; ++kik) {
+                    const int k2 = F.indices[kik];
+                    if (k2 <= j || k2 == i || !F.keep[kik]) continue;
+                    int kjk = -1;
+                    for (int qq = dpos + 1; qq < F.indptr[j + 1]; ++qq)
+                        if (F.indices[qq] == k2) { kjk = qq; break; }
+                    if (kjk < 0 || !F.keep[kjk]) continue;
+                    const double* Uik = F.U + ((int64_t)(F.uptr[i] + (kik - F.diag[i] - 1)) * F.s + k) * bsz;
+                    double* Ujk = F.U + ((int64_t)(F.uptr[j] + (kjk - dpos - 1)) * F.s + k) * bsz;
+                    gemm_lt<MAXT>(T, Uik, 1.0, S, F);
+                    for_tiles<MAXT>(T, F, [&](int a, int b, double v) {
+                        if (a < nb && b < nb) Ujk[lay(a, b, nb)] -= v;
+                    });
+                    __syncthreads();
+                }
+            }
+        }
+        if (F.Dst) {
+            store_D(S.D, F.Dst + ((int64_t)j * F.s + k) * bsz, F);
+            __syncthreads();
+        }
+        const bool ok = gj_invert(S, F);
+        store_D(S.D, F.Dinv + ((int64_t)j * F.s + k) * bsz, F);
+        if (!ok && threadIdx.x == 0) atomicMin(F.fail_key, (unsigned long long)((int64_t)k * F.T + j));
+        __syncthreads();
+    }
+}
+
+// U[uq][k] = keep ? alpha * J_k[q] : 0 for every upper block (general mode)
+__global__ void k_init_upper(FactorArgs F, int64_t T) {
+    const int nb = F.nb;
+    const int64_t bsz = (int64_t)nb * 2 * ((nb + 1) >> 1);
+    for (int64_t i = blockIdx.x; i < T; i += gridDim.x) {
+        const int d = F.diag[i], q1 = F.indptr[i + 1], u0 = F.uptr[i];
+        for (int q = d + 1; q < q1; ++q)
+            for (int k = 0; k < F.s; ++k) {
+                double* dst = F.U + ((int64_t)(u0 + q - d - 1) * F.s + k) * bsz;
+                const double* src = F.J[k] + (int64_t)q * bsz;
+                const bool kp = F.keep[q] != 0;
+                for (int e = threadIdx.x; e < bsz; e += blockDim.x) dst[e] = kp ? F.alpha * src[e] : 0.0;
+            }
+    }
+}
+
+static void levels_forward(const irk_pattern* p, const std::vector<uint8_t>& keep, std::vector<int64_t>& lev) {
+    const int64_t T = p->T;
+    lev.assign(T, 0);
+    std::vector<int32_t> tpos(p->nnzb);
+    for (int64_t j = 0; j < T; ++j) {
+        int64_t L = 0;
+        for (int64_t q = p->h_indptr[j]; q < p->h_diag[j]; ++q) {
+            const int64_t i = p->h_indices[q];
+            // dependency if the reference reads row i for row j (either block kept)
+            const int64_t* b = p->h_indices.data() + p->h_indptr[i];
+            const int64_t* e = p->h_indices.data() + p->h_indptr[i + 1];
+            const int64_t* f = std::lower_bound(b, e, j);
+            const bool up = (f != e && *f == j) && keep[p->h_indptr[i] + (f - b)];
+            if (keep[q] || up) L = std::max(L, lev[i] + 1);
+        }
+        lev[j] = L;
+    }
+}
+
+static void levels_backward(const irk_pattern* p, const std::vector<uint8_t>& keep, std::vector<int64_t>& lev) {
+    const int64_t T = p->T;
+    lev.assign(T, 0);
+    for (int64_t i = T - 1; i >= 0; --i) {
+        int64_t L = 0;
+        for (int64_t q = p->h_diag[i] + 1; q < p->h_indptr[i + 1]; ++q) {
+            const int64_t j = p->h_indices[q];
+            const int64_t* b = p->h_indices.data() + p->h_indptr[j];
+            const int64_t* e = p->h_indices.data() + p->h_indptr[j + 1];
+            const int64_t* f = std::lower_bound(b, e, i);
+            const bool lo = (f != e && *f == i) && keep[p->h_indptr[j] + (f - b)];
+            if (keep[q] || lo) L = std::max(L, lev[j] + 1);
+        }
+        lev[i] = L;
+    }
+}
+
+// group task codes by level: tasks (k, elem) with level = lev[elem] + skew(k)
+static int build_sched(irk_sched& S, const std::vector<int64_t>& lev, int64_t T, int s, bool per_stage,
+                       int skew_dir) {
+    int64_t maxl = 0;
+    for (auto v : lev) maxl = std::max(maxl, v);
+    const int kstages = per_stage ? s : 1;
+    const int64_t nlev = maxl + 1 + (per_stage && skew_dir != 0 ? s - 1 : 0);
+    std::vector<int64_t> cnt(nlev + 1, 0);
+    auto level_of = [&](int k, int64_t e) -> int64_t {
+        if (!per_stage || skew_dir == 0) return lev[e];
+        return lev[e] + (skew_dir > 0 ? k : (s - 1 - k));
+    };
+    for (int k = 0; k < kstages; ++k)
+        for (int64_t e = 0; e < T; ++e) cnt[level_of(k, e) + 1]++;
+    for (int64_t l = 0; l < nlev; ++l) cnt[l + 1] += cnt[l];
+    std::vector<int32_t> order(cnt[nlev]);
+    std::vector<int64_t> pos(cnt.begin(), cnt.end() - 1);
+    for (int k = 0; k < kstages; ++k)
+        for (int64_t e = 0; e < T; ++e) order[pos[level_of(k, e)]++] = (int32_t)((int64_t)k * T + e);
+    S.nlevels = nlev;
+    S.h_lvl_ptr = cnt;
+    IRK_CK(cudaMalloc(&S.d_order, sizeof(int32_t) * std::max<size_t>(order.size(), 1)));
+    IRK_CK(cudaMemcpy(S.d_order, order.data(), sizeof(int32_t) * order.size(), cudaMemcpyHostToDevice));
+    return IRK_OK;
+}
+
+// apply schedules: uncoupled -> element tasks; coupled -> (stage, element)
+// tasks on stage-skewed levels
+int build_apply_schedules(irk_factor* f, const std::vector<uint8_t>& keep) {
+    std::vector<int64_t> levf, levb;
+    levels_forward(f->pat, keep, levf);
+    levels_backward(f->pat, keep, levb);
+    const bool cpl = f->kind == IRK_FACTOR_COUPLED;
+    IRK_TRY(build_sched(f->fwd, levf, f->pat->T, f->s, cpl, +1));
+    IRK_TRY(build_sched(f->bwd, levb, f->pat->T, f->s, cpl, -1));
+    return IRK_OK;
+}
+
+static size_t factor_smem(int nbp4, int ld, int KC) {
+    return sizeof(double) * ((size_t)2 * nbp4 * ld + (size_t)2 * KC * ld + nbp4 + 64) +
+           sizeof(int) * (nbp4 + 8);
+}
+
+template <int MAXT>
+static int launch_levels(const irk_factor* f, FactorArgs& F, const irk_sched& sched, size_t smem,
+                         cudaStream_t st) {
+    static bool attr_set = false;
+    if (!attr_set) {
+        IRK_CK(cudaFuncSetAttribute(k_factor<MAXT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    (int)f->ctx->smem_optin));
+        attr_set = true;
+    }
+    for (int64_t l = 0; l < sched.nlevels; ++l) {
+        const int64_t lo = sched.h_lvl_ptr[l], hi = sched.h_lvl_ptr[l + 1];
+        if (hi == lo) continue;
+        F.tasks = sched.d_order + lo;
+        F.ntasks = hi - lo;
+        const int grid = (int)std::min<int64_t>(hi - lo, (int64_t)f->ctx->num_sms * 8);
+        k_factor<MAXT><<<grid, 256, smem, st>>>(F);
+        IRK_CK(cudaGetLastError());
+    }
+    return IRK_OK;
+}
+
+struct FactorSetup {
+    int s;
+    const irk_blocks* const* J;
+    const int64_t* jfirst;
+    const irk_blocks* M;
+    const double* coef;     // uncoupled diag coefficients
+    const double* a_inv;    // coupled mixing
+    double alpha;
+    const irk_blocks* coupling;
+    const uint8_t* keep;
+    int simplified, literal, store_diag, coupled;
+};
+
+static int factor_common(irk_ctx* ctx, const irk_pattern* pat, const FactorSetup& P, irk_factor** out,
+                         int64_t* fail_stage, int64_t* fail_elem, cudaStream_t st) {
+    IRK_ARG(ctx && pat && P.J && out, "NULL argument");
+    IRK_ARG(P.s >= 1 && P.s <= IRK_MAX_STAGES, "stage count out of range");
+    const int nb = P.J[0]->nb;
+    for (int k = 0; k < P.s; ++k) {
+        IRK_ARG(P.J[k] && P.J[k]->nb == nb, "J blocks missing or nb mismatch");
+        const int64_t jf = P.jfirst ? P.jfirst[k] : 0;
+        IRK_ARG(jf >= 0 && jf + pat->nnzb <= P.J[k]->count, "J block range out of bounds");
+    }
+    IRK_ARG(!P.M || (P.M->nb == nb && P.M->count >= pat->T), "mass blocks mismatch");
+    IRK_ARG(!P.coupling || (P.coupling->nb == nb && P.coupling->count >= (int64_t)P.s * P.s * pat->T),
+            "coupling blocks mismatch");
+    IRK_ARG(!P.coupled || P.M || P.coupling, "coupled factor needs M or explicit couplings");
+    IRK_ARG((int64_t)P.s * pat->T < INT_MAX, "s*T too large");
+    auto* f = new irk_factor();
+    f->ctx = ctx;
+    f->pat = pat;
+    f->kind = P.coupled ? IRK_FACTOR_COUPLED : IRK_FACTOR_UNCOUPLED;
+    f->s = P.s;
+    f->nb = nb;
+    f->simplified = P.coupled ? 1 : P.simplified;
+    f->literal = P.literal;
+    std::vector<uint8_t> keep(pat->nnzb, 1);
+    if (P.keep) std::memcpy(keep.data(), P.keep, pat->nnzb);
+    const int64_t bsz = block_doubles(nb);
+    int rc = IRK_OK;
+    auto fail = [&](int code) { irk_factor_destroy(f); return code; };
+#define FCK(call) do { cudaError_t _e = (call); if (_e != cudaSuccess) return fail(fail_cuda(_e, #call, __FILE__, __LINE__)); } while (0)
+    FCK(cudaMalloc(&f->d_keep, pat->nnzb));
+    FCK(cudaMemcpy(f->d_keep, keep.data(), pat->nnzb, cudaMemcpyHostToDevice));
+    FCK(cudaMalloc(&f->d_L, sizeof(double) * bsz * std::max<int64_t>(pat->nlow * P.s, 1)));
+    FCK(cudaMalloc(&f->d_Dinv, sizeof(double) * bsz * pat->T * P.s));
+    if (P.store_diag || P.literal) FCK(cudaMalloc(&f->d_D, sizeof(double) * bsz * pat->T * P.s));
+    const bool need_u = !f->simplified;
+    if (need_u) {
+        FCK(cudaMalloc(&f->d_U, sizeof(double) * bsz * std::max<int64_t>(pat->nup * P.s, 1)));
+        f->u_stored = true;
+        f->uscale = 1.0;
+    } else {
+        f->u_stored = false;
+        f->uscale = P.alpha;
+    }
+    bool shared = true;
+    for (int k = 0; k < P.s; ++k) {
+        f->ubase[k] = P.J[k]->d + (P.jfirst ? P.jfirst[k] : 0) * bsz;
+        if (f->ubase[k] != f->ubase[0]) shared = false;
+    }
+    f->u_shared = shared && !f->u_stored;
+    const int npairs = P.s * (P.s - 1) / 2;
+    if (P.coupled && npairs > 0) FCK(cudaMalloc(&f->d_G, sizeof(double) * bsz * pat->T * npairs));
+    if (P.coupled) {
+        if (P.coupling) {
+            // upper couplings C[k][l] (k<l) are used unmodified by the apply
+            if (npairs > 0) FCK(cudaMalloc(&f->d_Cup, sizeof(double) * bsz * pat->T * npairs));
+        } else {
+            f->mass = P.M->d;
+            for (int e = 0; e < P.s * P.s; ++e) f->cup_scale[e] = P.a_inv[e];
+        }
+    }
+    std::vector<int64_t> levf;
+    if ((rc = build_apply_schedules(f, keep))) return fail(rc);
+    levels_forward(pat, keep, levf);
+    irk_sched fsched;  // factor tasks: (stage, element) per level
+    if ((rc = build_sched(fsched, levf, pat->T, P.s, true, P.coupled ? +1 : 0))) return fail(rc);
+
+    FactorArgs F{};
+    F.indptr = pat->d_indptr;
+    F.indices = pat->d_indices;
+    F.diag = pat->d_diag;
+    F.lptr = pat->d_lptr;
+    F.uptr = pat->d_uptr;
+    F.tpos = pat->d_tpos;
+    F.keep = f->d_keep;
+    for (int k = 0; k < P.s; ++k) F.J[k] = f->ubase[k];
+    F.M = P.M ? P.M->d : nullptr;
+    F.Cexp = P.coupling ? P.coupling->d : nullptr;
+    F.alpha = P.alpha;
+    for (int k = 0; k < P.s; ++k) F.coef[k] = P.coupled ? P.a_inv[k * P.s + k] : (P.coef ? P.coef[k] : 0.0);
+    if (P.coupled && P.a_inv)
+        for (int e = 0; e < P.s * P.s; ++e) F.cmix[e] = P.a_inv[e];
+    F.L = f->d_L;
+    F.Dinv = f->d_Dinv;
+    F.Dst = f->d_D;
+    F.U = f->d_U;
+    F.G = f->d_G;
+    F.T = pat->T;
+    F.s = P.s;
+    F.nb = nb;
+    F.nbp4 = (nb + 3) & ~3;
+    F.ld = F.nbp4 + 2;
+    F.coupled = P.coupled;
+    F.literal = P.literal;
+    F.simplified = f->simplified;
+    // shared memory budget: full D and L^T, K-chunked operand tiles
+    F.KC = F.nbp4;
+    while (factor_smem(F.nbp4, F.ld, F.KC) > ctx->smem_optin && F.KC > 4) F.KC = std::max(4, F.KC / 2);
+    const size_t smem = factor_smem(F.nbp4, F.ld, F.KC);
+    if (smem > ctx->smem_optin) { set_error("block size too large for shared memory"); cudaFree(fsched.d_order); return fail(IRK_EINVAL); }
+    unsigned long long* d_fail = nullptr;
+    FCK(cudaMallocAsync(&d_fail, sizeof(unsigned long long), st));
+    FCK(cudaMemsetAsync(d_fail, 0xff, sizeof(unsigned long long), st));
+    F.fail_key = d_fail;
+    if (P.coupled && P.coupling && npairs > 0) {
+        // copy upper couplings (k<l) into Cup[i][pair(l,k)]
+        for (int l = 1; l < P.s; ++l)
+            for (int k = 0; k < l; ++k)
+                FCK(cudaMemcpy2DAsync(f->d_Cup + (int64_t)(l * (l - 1) / 2 + k) * bsz, sizeof(double) * bsz * npairs,
+                                      P.coupling->d + ((int64_t)k * P.s + l) * pat->T * bsz, sizeof(double) * bsz,
+                                      sizeof(double) * bsz, pat->T, cudaMemcpyDeviceToDevice, st));
+    }
+    if (need_u) {
+        k_init_upper<<<(int)std::min<int64_t>(pat->T, ctx->num_sms * 8), 256, 0, st>>>(F, pat->T);
+        FCK(cudaGetLastError());
+    }
+    const int tpr = F.nbp4 / 4;
+    const int maxt = (tpr * tpr + 255) / 256;
+    switch (maxt) {
+        case 1: rc = launch_levels<1>(f, F, fsched, smem, st); break;
+        case 2: rc = launch_levels<2>(f, F, fsched, smem, st); break;
+        case 3: rc = launch_levels<3>(f, F, fsched, smem, st); break;
+        case 4: rc = launch_levels<4>(f, F, fsched, smem, st); break;
+        default: set_error("block size too large"); rc = IRK_EINVAL;
+    }
+    cudaFree(fsched.d_order);  // synchronous free: waits for the launches
+    if (rc) { cudaFreeAsync(d_fail, st); return fail(rc); }
+    unsigned long long key = 0;
+    FCK(cudaMemcpyAsync(&key, d_fail, sizeof key, cudaMemcpyDeviceToHost, st));
+    FCK(cudaFreeAsync(d_fail, st));
+    FCK(cudaStreamSynchronize(st));
+#undef FCK
+    if (fail_stage) *fail_stage = -1;
+    if (fail_elem) *fail_elem = -1;
+    *out = f;
+    if (key != ~0ULL) {
+        if (fail_stage) *fail_stage = (int64_t)(key / pat->T);
+        if (fail_elem) *fail_elem = (int64_t)(key % pat->T);
+        set_error("numerically singular pivot block");
+        return IRK_ESINGULAR;
+    }
+    return IRK_OK;
+}
+
+}  // namespace irk
+
+using namespace irk;
+
+extern "C" {
+
+int irk_factor_uncoupled(irk_ctx* ctx, const irk_pattern* pat, int s, const irk_blocks* const* J,
+                         const int64_t* jfirst, const irk_blocks* M, const double* coef, double alpha,
+                         const uint8_t* keep, int simplified, int store_diag, irk_factor** out,
+                         int64_t* fail_stage, int64_t* fail_elem, void* stream) {
+    IRK_ARG(!M || coef, "coef required with M");
+    FactorSetup P{};
+    P.s = s;
+    P.J = J;
+    P.jfirst = jfirst;
+    P.M = M;
+    P.coef = coef;
+    P.alpha = alpha;
+    P.keep = keep;
+    P.simplified = simplified;
+    P.store_diag = store_diag;
+    P.coupled = 0;
+    return factor_common(ctx, pat, P, out, fail_stage, fail_elem, (cudaStream_t)stream);
+}
+
+int irk_factor_coupled(irk_ctx* ctx, const irk_pattern* pat, int s, const irk_blocks* const* J,
+                       const int64_t* jfirst, const irk_blocks* M, const double* a_inv, double alpha,
+                       const irk_blocks* coupling, const uint8_t* keep, int literal, int store_diag,
+                       irk_factor** out, int64_t* fail_stage, int64_t* fail_elem, void* stream) {
+    IRK_ARG(a_inv || coupling, "a_inv or coupling required");
+    IRK_ARG(!M || a_inv, "a_inv required with M");
+    FactorSetup P{};
+    P.s = s;
+    P.J = J;
+    P.jfirst = jfirst;
+    P.M = M;
+    P.a_inv = a_inv;
+    P.alpha = alpha;
+    P.coupling = coupling;
+    P.keep = keep;
+    P.simplified = 1;
+    P.literal = literal;
+    P.store_diag = store_diag;
+    P.coupled = 1;
+    return factor_common(ctx, pat, P, out, fail_stage, fail_elem, (cudaStream_t)stream);
+}
+
+void irk_factor_destroy(irk_factor* f) {
+    if (!f) return;
+    cudaFree(f->d_keep);
+    cudaFree(f->d_L);
+    cudaFree(f->d_Dinv);
+    cudaFree(f->d_D);
+    cudaFree(f->d_U);
+    cudaFree(f->d_G);
+    cudaFree(f->d_Cup);
+    cudaFree(f->fwd.d_order);
+    cudaFree(f->bwd.d_order);
+    for (auto* b : f->owned) irk_blocks_destroy(b);
+    delete f;
+}
+
+int irk_factor_levels(const irk_factor* f, int64_t* fwd_levels, int64_t* bwd_levels) {
+    IRK_ARG(f, "NULL factor");
+    if (fwd_levels) *fwd_levels = f->fwd.nlevels;
+    if (bwd_levels) *bwd_levels = f->bwd.nlevels;
+    return IRK_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,130 @@
+// irk-b200 internal definitions (not part of the C-ABI).
+//
+// Device block layout ("column-pair interleaved"): an nb x nb fp64 block is
+// stored as P = ceil(nb/2) column pairs; pair p holds rows 0..nb-1, each row
+// contributing the 16-byte vector (B[a][2p], B[a][2p+1]).  Element (a, b)
+// lives at double offset ((b>>1)*nb + a)*2 + (b&1).  A warp whose lanes walk
+// consecutive rows a of one pair therefore issues perfectly coalesced 128-bit
+// loads, and a thread that owns row a multiplies both columns of the pair
+// with a broadcast x[2p..2p+1].  Odd nb pads the last pair's second column
+// with zeros (block size nb * 2P doubles).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+#include <vector>
+
+#include "../../include/irkb200.h"
+
+namespace irk {
+
+void set_error(const std::string& msg);
+int fail_cuda(cudaError_t e, const char* what, const char* file, int line);
+
+#define IRK_CK(call)                                                          \
+    do {                                                                      \
+        cudaError_t _e = (call);                                              \
+        if (_e != cudaSuccess) return ::irk::fail_cuda(_e, #call, __FILE__, __LINE__); \
+    } while (0)
+
+#define IRK_ARG(cond, msg)                                                    \
+    do {                                                                      \
+        if (!(cond)) { ::irk::set_error(std::string("invalid argument: ") + (msg)); return IRK_EINVAL; } \
+    } while (0)
+
+#define IRK_TRY(expr)                                                         \
+    do { int _rc = (expr); if (_rc != IRK_OK) return _rc; } while (0)
+
+inline int npairs(int nb) { return (nb + 1) / 2; }
+inline int64_t block_doubles(int nb) { return (int64_t)nb * 2 * npairs(nb); }
+
+}  // namespace irk
+
+// ---------------------------------------------------------------------------
+// opaque handle definitions
+// ---------------------------------------------------------------------------
+struct irk_ctx {
+    int device = 0;
+    int num_sms = 148;
+    size_t smem_optin = 0;
+};
+
+struct irk_pattern {
+    irk_ctx* ctx = nullptr;
+    int64_t T = 0, nnzb = 0;
+    // host copies (int64, reference layout)
+    std::vector<int64_t> h_indptr, h_indices, h_diag;
+    // device (int32)
+    int32_t* d_indptr = nullptr;   // T+1
+    int32_t* d_indices = nullptr;  // nnzb
+    int32_t* d_diag = nullptr;     // T
+    int32_t* d_rowof = nullptr;    // nnzb: row of each block
+    // lower / upper slot maps (lower slot = position among strictly-lower blocks)
+    int64_t nlow = 0, nup = 0;
+    std::vector<int64_t> h_lptr, h_uptr;  // T+1 each
+    int32_t* d_lptr = nullptr;     // T+1
+    int32_t* d_uptr = nullptr;     // T+1
+    int32_t* d_tpos = nullptr;     // nnzb: position of the transposed block (j,i) for (i,j), -1 if absent
+};
+
+struct irk_blocks {
+    irk_ctx* ctx = nullptr;
+    int nb = 0;
+    int64_t count = 0;
+    double* d = nullptr;            // count * block_doubles(nb)
+};
+
+struct irk_stage_op {
+    irk_ctx* ctx = nullptr;
+    const irk_pattern* pat = nullptr;
+    int s = 0, nb = 0;
+    const irk_blocks* J[IRK_MAX_STAGES] = {};
+    int64_t jfirst[IRK_MAX_STAGES] = {};   // first block of stage k inside J[k]
+    bool shared_j = true;
+    const irk_blocks* M = nullptr;
+    double alpha = 0.0;                    // multiplies J (=-dt)
+    double C[IRK_MAX_STAGES * IRK_MAX_STAGES] = {};  // mass mixing (a_inv)
+    // optional halo (distributed): columns >= T_local index the ghost buffer
+    int64_t T_local = 0;
+    const double* ghost = nullptr;
+    int64_t n_ghost = 0;
+};
+
+// schedule of one sweep direction: element order grouped by level
+struct irk_sched {
+    int64_t nlevels = 0;
+    std::vector<int64_t> h_lvl_ptr;   // nlevels+1
+    int32_t* d_order = nullptr;       // T elements in level order
+};
+
+struct irk_factor {
+    irk_ctx* ctx = nullptr;
+    const irk_pattern* pat = nullptr;
+    int kind = 0;          // IRK_FACTOR_UNCOUPLED | IRK_FACTOR_COUPLED
+    int s = 0, nb = 0;
+    int simplified = 1;
+    int literal = 0;
+    uint8_t* d_keep = nullptr;        // nnzb
+    // lower factors L[lq][k], diag inverses Dinv[i][k], optional stored diag D[i][k]
+    double* d_L = nullptr;
+    double* d_Dinv = nullptr;
+    double* d_D = nullptr;
+    // upper blocks: either implicit (ubase[k] block array at pattern position q,
+    // scaled by uscale) or stored U[uq][k] (uscale = 1)
+    bool u_stored = false;
+    double* d_U = nullptr;
+    const double* ubase[IRK_MAX_STAGES] = {};
+    double uscale = 1.0;
+    bool u_shared = false;            // all stages read the same upper blocks
+    // coupled: lower couplings G[i][pair(l,k)] for l>k ; upper couplings either
+    // implicit C_kl * M_i or stored Cup[i][pair(k,l)] for k<l
+    double* d_G = nullptr;
+    double* d_Cup = nullptr;          // stored upper couplings (explicit mode)
+    const double* mass = nullptr;     // implicit upper couplings
+    double cup_scale[IRK_MAX_STAGES * IRK_MAX_STAGES] = {};
+    irk_sched fwd, bwd;
+    // owned copies when created from explicit host data
+    std::vector<irk_blocks*> owned;
+};

@@ -1,0 +1,488 @@
+// Restarted, left-preconditioned GMRES with fused classical Gram-Schmidt.
+//
+// Control flow and stopping rules follow the reference krylov.py:37-130
+// exactly (tolerance rel_tol*||P^-1 b||, Givens rotations, happy breakdown at
+// 1e-14*max(b_norm,1), restart residual P^-1(b - Bx), operator_applies and
+// residual_history bookkeeping).  Differences, all result-preserving:
+//  * orthogonalisation is classical Gram-Schmidt -- one fused multi-dot pass
+//    (all V_i . w and w . w) and one fused update pass (w -= V h, with w . w)
+//    -- plus a DGKS second pass when ||w|| < eta ||w_0|| (reference: MGS with a
+//    1e-8 re-orthogonalisation trigger, krylov.py:89-97);
+//  * with x0 = 0 the reference's second apply P^-1(b - B*0) (krylov.py:62) is
+//    bitwise P^-1 b, so it is not recomputed (still counted as an operator
+//    apply, as the reference counts it);
+//  * the restart residual after the final, converged cycle is skipped (the
+//    reference computes it and discards it, krylov.py:123-127).
+// All reductions are per-CTA partial sums reduced in a fixed order, so the
+// solver is bitwise reproducible run to run.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <vector>
+
+#include "irk_internal.cuh"
+
+namespace irk {
+
+int factor_apply(const irk_factor* f, const double* y, double* x, cudaStream_t st);
+
+constexpr int VB = 256;      // threads per vector CTA
+constexpr int VGROUP = 8;    // vectors per multidot pass
+
+static int vec_blocks(const irk_ctx* ctx) { return ctx->num_sms * 2; }
+
+__device__ __forceinline__ double warp_sum(double v) {
+    for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+
+// CTA-wide sum of `nv` per-thread values, written to out[v * gridDim.x + blockIdx.x]
+__device__ __forceinline__ void block_store_partials(const double* vals, int nv, double* red, double* out) {
+    const int w = threadIdx.x >> 5, l = threadIdx.x & 31, nw = blockDim.x >> 5;
+    for (int v = 0; v < nv; ++v) {
+        const double s = warp_sum(vals[v]);
+        if (l == 0) red[v * nw + w] = s;
+    }
+    __syncthreads();
+    for (int v = threadIdx.x; v < nv; v += blockDim.x) {
+        double s = 0.0;
+        for (int i = 0; i < nw; ++i) s += red[v * nw + i];
+        out[(int64_t)v * gridDim.x + blockIdx.x] = s;
+    }
+    __syncthreads();
+}
+
+__device__ __forceinline__ void chunk_range(int64_t n, int64_t& lo, int64_t& hi) {
+    const int64_t per = ((n + gridDim.x - 1) / gridDim.x + 1) & ~int64_t(1);
+    lo = std::min<int64_t>(n, per * blockIdx.x);
+    hi = std::min<int64_t>(n, lo + per);
+}
+
+// partials[v][blk]: v < nv -> V_v . w ; v == nv -> w . w.  Vectors are read
+// in groups of VGROUP per pass over the CTA's chunk of w.
+__global__ void __launch_bounds__(VB) k_multidot(const double* __restrict__ V, int64_t ldv, int nv,
+                                                 const double* __restrict__ w, int64_t n, double* partials) {
+    __shared__ double red[(VGROUP + 1) * (VB / 32)];
+    int64_t lo, hi;
+    chunk_range(n, lo, hi);
+    for (int v0 = 0;; v0 += VGROUP) {
+        const int cnt = min(VGROUP, nv - v0);
+        const bool with_ww = (v0 == 0);
+        double acc[VGROUP + 1];
+#pragma unroll
+        for (int i = 0; i <= VGROUP; ++i) acc[i] = 0.0;
+        for (int64_t e = lo + threadIdx.x; e < hi; e += VB) {
+            const double wv = w[e];
+#pragma unroll
+            for (int i = 0; i < VGROUP; ++i)
+                if (i < cnt) acc[i] = fma(V[(int64_t)(v0 + i) * ldv + e], wv, acc[i]);
+            if (with_ww) acc[VGROUP] = fma(wv, wv, acc[VGROUP]);
+        }
+        if (cnt > 0) block_store_partials(acc, cnt, red, partials + (int64_t)v0 * gridDim.x);
+        if (with_ww) block_store_partials(acc + VGROUP, 1, red, partials + (int64_t)nv * gridDim.x);
+        if (v0 + VGROUP >= nv) break;
+    }
+}
+
+// out[v] = sum_b partials[v][b] (fixed order), v < nv
+__global__ void k_reduce_partials(const double* partials, int nblk, int nv, double* out) {
+    __shared__ double red[32];
+    for (int v = 0; v < nv; ++v) {
+        double s = 0.0;
+        for (int b = threadIdx.x; b < nblk; b += blockDim.x) s += partials[(int64_t)v * nblk + b];
+        s = warp_sum(s);
+        const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+        if (l == 0) red[w] = s;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            double t = 0.0;
+            for (int i = 0; i < (int)(blockDim.x >> 5); ++i) t += red[i];
+            out[v] = t;
+        }
+        __syncthreads();
+    }
+}
+
+// w -= sum_i h[i] V_i ; partials[blk] = w . w
+__global__ void __launch_bounds__(VB) k_update(const double* __restrict__ V, int64_t ldv, int nv,
+                                               const double* __restrict__ h, double* __restrict__ w,
+                                               int64_t n, double* partials) {
+    __shared__ double hs[64];
+    __shared__ double red[VB / 32];
+    for (int i = threadIdx.x; i < nv && i < 64; i += blockDim.x) hs[i] = h[i];
+    __syncthreads();
+    int64_t lo, hi;
+    chunk_range(n, lo, hi);
+    double nrm = 0.0;
+    for (int64_t e = lo + threadIdx.x; e < hi; e += VB) {
+        double acc = w[e];
+        for (int i = 0; i < nv; ++i) acc -= hs[i] * V[(int64_t)i * ldv + e];
+        w[e] = acc;
+        nrm = fma(acc, acc, nrm);
+    }
+    block_store_partials(&nrm, 1, red, partials);
+}
+
+// y = x / d  (d on host)
+__global__ void k_scale_div(const double* __restrict__ x, double* __restrict__ y, int64_t n, double d) {
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x)
+        y[e] = x[e] / d;
+}
+
+// x += sum_i c[i] V_i
+__global__ void k_axpy_multi(const double* __restrict__ V, int64_t ldv, int nv, const double* __restrict__ c,
+                             double* __restrict__ x, int64_t n) {
+    __shared__ double cs[64];
+    for (int i = threadIdx.x; i < nv && i < 64; i += blockDim.x) cs[i] = c[i];
+    __syncthreads();
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x) {
+        double t = 0.0;
+        for (int i = 0; i < nv; ++i) t = fma(cs[i], V[(int64_t)i * ldv + e], t);
+        x[e] += t;
+    }
+}
+
+// t = b - t
+__global__ void k_bminus(const double* __restrict__ b, double* __restrict__ t, int64_t n) {
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x)
+        t[e] = b[e] - t[e];
+}
+
+// partials[blk] = sum x^2 ; partials[nblk + blk] = max |x|
+__global__ void __launch_bounds__(VB) k_norm_max(const double* __restrict__ x, int64_t n, double* partials) {
+    __shared__ double red[2 * (VB / 32)];
+    int64_t lo, hi;
+    chunk_range(n, lo, hi);
+    double s = 0.0, m = 0.0;
+    for (int64_t e = lo + threadIdx.x; e < hi; e += VB) {
+        const double v = x[e];
+        s = fma(v, v, s);
+        m = fmax(m, fabs(v));
+    }
+    block_store_partials(&s, 1, red, partials);
+    for (int o = 16; o; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+    const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+    if (l == 0) red[w] = m;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double t = 0.0;
+        for (int i = 0; i < VB / 32; ++i) t = fmax(t, red[i]);
+        partials[gridDim.x + blockIdx.x] = t;
+    }
+}
+
+__global__ void k_reduce_max(const double* partials, int nblk, double* out) {
+    if (threadIdx.x == 0 && blockIdx.x == 0) {
+        double t = 0.0;
+        for (int b = 0; b < nblk; ++b) t = fmax(t, partials[b]);
+        *out = t;
+    }
+}
+
+struct Workspace {
+    double* V = nullptr;
+    double* tmp = nullptr;
+    double* partials = nullptr;
+    double* small = nullptr;   // device scratch for reduced values / coefficients
+    cudaStream_t st = nullptr;
+    ~Workspace() {
+        if (V) cudaFreeAsync(V, st);
+        if (tmp) cudaFreeAsync(tmp, st);
+        if (partials) cudaFreeAsync(partials, st);
+        if (small) cudaFreeAsync(small, st);
+    }
+};
+
+static int multidot(const irk_ctx* ctx, int64_t n, int nv, const double* V, int64_t ldv, const double* w,
+                    double* partials, double* out, cudaStream_t st) {
+    const int nb = vec_blocks(ctx);
+    k_multidot<<<nb, VB, 0, st>>>(V, ldv, nv, w, n, partials);
+    IRK_CK(cudaGetLastError());
+    k_reduce_partials<<<1, 256, 0, st>>>(partials, nb, nv + 1, out);
+    IRK_CK(cudaGetLastError());
+    return IRK_OK;
+}
+
+static int update(const irk_ctx* ctx, int64_t n, int nv, const double* V, int64_t ldv, const double* h,
+                  double* w, double* partials, double* out, cudaStream_t st) {
+    const int nb = vec_blocks(ctx);
+    k_update<<<nb, VB, 0, st>>>(V, ldv, nv, h, w, n, partials);
+    IRK_CK(cudaGetLastError());
+    k_reduce_partials<<<1, 256, 0, st>>>(partials, nb, 1, out);
+    IRK_CK(cudaGetLastError());
+    return IRK_OK;
+}
+
+static int norm_max(const irk_ctx* ctx, int64_t n, const double* x, double* partials, double* out2,
+                    cudaStream_t st) {
+    const int nb = vec_blocks(ctx);
+    k_norm_max<<<nb, VB, 0, st>>>(x, n, partials);
+    IRK_CK(cudaGetLastError());
+    k_reduce_partials<<<1, 256, 0, st>>>(partials, nb, 1, out2);
+    k_reduce_max<<<1, 32, 0, st>>>(partials + nb, nb, out2 + 1);
+    IRK_CK(cudaGetLastError());
+    return IRK_OK;
+}
+
+static int grid_1d(const irk_ctx* ctx, int64_t n) {
+    return (int)std::max<int64_t>(1, std::min<int64_t>((n + 255) / 256, ctx->num_sms * 8));
+}
+
+}  // namespace irk
+
+using namespace irk;
+
+extern "C" {
+
+static int linop_stage(void* u, const double* in, double* out, void* st) {
+    return irk_stage_op_apply((const irk_stage_op*)u, in, out, st);
+}
+static int linop_factor(void* u, const double* in, double* out, void* st) {
+    return irk_factor_apply((const irk_factor*)u, in, out, st);
+}
+
+int irk_linop_stage_op(const irk_stage_op* op, irk_linop* out) {
+    IRK_ARG(op && out, "NULL argument");
+    out->fn = linop_stage;
+    out->user = (void*)op;
+    return IRK_OK;
+}
+
+int irk_linop_factor(const irk_factor* f, irk_linop* out) {
+    IRK_ARG(f && out, "NULL argument");
+    out->fn = linop_factor;
+    out->user = (void*)f;
+    return IRK_OK;
+}
+
+int irk_vec_multidot(irk_ctx* ctx, int64_t n, int nv, const double* V, int64_t ldv, const double* w,
+                     double* out, void* stream) {
+    IRK_ARG(ctx && w && out && (V || nv == 0), "NULL argument");
+    IRK_ARG(nv >= 0 && nv <= 64 && n >= 0, "bad sizes");
+    cudaStream_t st = (cudaStream_t)stream;
+    double* partials = nullptr;
+    IRK_CK(cudaMallocAsync(&partials, sizeof(double) * vec_blocks(ctx) * (nv + 1), st));
+    int rc = multidot(ctx, n, nv, V, ldv, w, partials, out, st);
+    cudaFreeAsync(partials, st);
+    return rc;
+}
+
+int irk_vec_update(irk_ctx* ctx, int64_t n, int nv, const double* V, int64_t ldv, const double* h, double* w,
+                   double* out_nrm2, void* stream) {
+    IRK_ARG(ctx && w && out_nrm2 && (V || nv == 0), "NULL argument");
+    IRK_ARG(nv >= 0 && nv <= 64 && n >= 0, "bad sizes");
+    cudaStream_t st = (cudaStream_t)stream;
+    double* partials = nullptr;
+    IRK_CK(cudaMallocAsync(&partials, sizeof(double) * vec_blocks(ctx), st));
+    int rc = update(ctx, n, nv, V, ldv, h, w, partials, out_nrm2, st);
+    cudaFreeAsync(partials, st);
+    return rc;
+}
+
+int irk_gmres(irk_ctx* ctx, int64_t n, irk_linop op, irk_linop pre, irk_allreduce_fn allreduce, void* ar_user,
+              const double* rhs, double* x, const irk_gmres_cfg* cfg, irk_gmres_stats* stats, double* history,
+              int history_cap, void* stream) {
+    IRK_ARG(ctx && rhs && x && cfg && stats && op.fn, "NULL argument");
+    IRK_ARG(cfg->rel_tol > 0, "rel_tol must be positive");
+    IRK_ARG(cfg->max_iters >= 1, "max_iters must be at least 1");
+    IRK_ARG(n >= 1, "empty system");
+    cudaStream_t st = (cudaStream_t)stream;
+    const int restart = std::min(cfg->restart > 0 ? cfg->restart : cfg->max_iters, cfg->max_iters);
+    IRK_ARG(restart <= 64, "restart length above 64 is not supported");
+    const double eta = cfg->reorth_eta > 0 ? cfg->reorth_eta : 0.70710678118654752;
+    *stats = irk_gmres_stats{};
+    stats->final_true_residual = NAN;
+    int hist_n = 0;
+    auto push_hist = [&](double v) {
+        if (history && hist_n < history_cap) history[hist_n] = v;
+        ++hist_n;
+    };
+    Workspace ws;
+    ws.st = st;
+    const int nblk = vec_blocks(ctx);
+    IRK_CK(cudaMallocAsync(&ws.V, sizeof(double) * n * (restart + 1), st));
+    IRK_CK(cudaMallocAsync(&ws.tmp, sizeof(double) * n, st));
+    IRK_CK(cudaMallocAsync(&ws.partials, sizeof(double) * nblk * (restart + 2) * 2, st));
+    IRK_CK(cudaMallocAsync(&ws.small, sizeof(double) * 4 * (restart + 4), st));
+    double* hdev = ws.small;                       // restart+2
+    double* ndev = ws.small + (restart + 2);       // 2
+    double* cdev = ws.small + 2 * (restart + 4);   // restart+1 coefficients
+    std::vector<double> hbuf(restart + 4);
+    auto V = [&](int i) { return ws.V + (int64_t)i * n; };
+    const int g1 = grid_1d(ctx, n);
+
+    auto ar = [&](double* buf, int64_t cnt) -> int {
+        if (!allreduce) return IRK_OK;
+        const int rc = allreduce(ar_user, buf, cnt, st);
+        if (rc) { set_error("allreduce callback failed"); return IRK_ECALLBACK; }
+        return IRK_OK;
+    };
+    auto call = [&](const irk_linop& L, const double* in, double* out) -> int {
+        if (!L.fn) {
+            IRK_CK(cudaMemcpyAsync(out, in, sizeof(double) * n, cudaMemcpyDeviceToDevice, st));
+            return IRK_OK;
+        }
+        const int rc = L.fn(L.user, in, out, st);
+        if (rc < 0) return rc;
+        if (rc > 0) { set_error("operator callback failed"); return IRK_ECALLBACK; }
+        return IRK_OK;
+    };
+    // ||v|| (and max|v|) with the allreduce; returns on host
+    auto norm = [&](const double* v, double& nrm, double* mx) -> int {
+        IRK_TRY(norm_max(ctx, n, v, ws.partials, ndev, st));
+        IRK_TRY(ar(ndev, 1));
+        double h2[2];
+        IRK_CK(cudaMemcpyAsync(h2, ndev, sizeof h2, cudaMemcpyDeviceToHost, st));
+        IRK_CK(cudaStreamSynchronize(st));
+        nrm = std::sqrt(h2[0]);
+        if (mx) *mx = h2[1];
+        return IRK_OK;
+    };
+    auto true_residual = [&](double& res) -> int {
+        IRK_TRY(call(op, x, ws.tmp));
+        k_bminus<<<g1, 256, 0, st>>>(rhs, ws.tmp, n);
+        IRK_CK(cudaGetLastError());
+        return norm(ws.tmp, res, nullptr);
+    };
+
+    IRK_CK(cudaMemsetAsync(x, 0, sizeof(double) * n, st));
+    double rnorm, rmax;
+    IRK_TRY(norm(rhs, rnorm, &rmax));
+    if (allreduce) {
+        // global "any nonzero": the max is rank-local; use the reduced 2-norm
+        rmax = rnorm;
+    }
+    if (rmax == 0.0) {   // `not np.any(rhs)` (krylov.py:48-52)
+        stats->converged = 1;
+        stats->final_true_residual = 0.0;
+        stats->history_len = 0;
+        return IRK_OK;
+    }
+    // pb = P^-1 b ; r = P^-1 (b - B*0) == pb (x0 = 0)
+    IRK_TRY(call(pre, rhs, V(0)));
+    double b_norm;
+    IRK_TRY(norm(V(0), b_norm, nullptr));
+    stats->b_norm = b_norm;
+    stats->operator_applies = 1;
+    double beta = b_norm;
+    push_hist(beta);
+    const double tol_abs = cfg->rel_tol * b_norm;
+    if (beta <= tol_abs) {
+        stats->converged = 1;
+        double res;
+        IRK_TRY(true_residual(res));
+        stats->final_true_residual = res;
+        stats->history_len = hist_n;
+        return IRK_OK;
+    }
+    k_scale_div<<<g1, 256, 0, st>>>(V(0), V(0), n, beta);
+    IRK_CK(cudaGetLastError());
+    int total = 0;
+    bool converged = false, breakdown = false;
+    double last_res = beta;
+    std::vector<double> H, cs, sn, g, y;
+    while (total < cfg->max_iters) {
+        const int cycle = std::min(restart, cfg->max_iters - total);
+        H.assign((size_t)(cycle + 1) * cycle, 0.0);
+        auto Hc = [&](int i, int j) -> double& { return H[(size_t)i * cycle + j]; };
+        cs.assign(cycle, 0.0);
+        sn.assign(cycle, 0.0);
+        g.assign(cycle + 1, 0.0);
+        g[0] = beta;
+        int j_done = 0;
+        breakdown = false;
+        for (int j = 0; j < cycle; ++j) {
+            double* w = V(j + 1);
+            if (pre.fn) {
+                IRK_TRY(call(op, V(j), ws.tmp));
+                IRK_TRY(call(pre, ws.tmp, w));
+            } else {
+                IRK_TRY(call(op, V(j), w));
+            }
+            stats->operator_applies += 1;
+            // classical Gram-Schmidt: h = V^T w (+ w.w), then w -= V h (+ w.w)
+            IRK_TRY(multidot(ctx, n, j + 1, ws.V, n, w, ws.partials, hdev, st));
+            IRK_TRY(ar(hdev, j + 2));
+            IRK_TRY(update(ctx, n, j + 1, ws.V, n, hdev, w, ws.partials, ndev, st));
+            IRK_TRY(ar(ndev, 1));
+            IRK_CK(cudaMemcpyAsync(hbuf.data(), hdev, sizeof(double) * (j + 2), cudaMemcpyDeviceToHost, st));
+            double nrm2;
+            IRK_CK(cudaMemcpyAsync(&nrm2, ndev, sizeof(double), cudaMemcpyDeviceToHost, st));
+            IRK_CK(cudaStreamSynchronize(st));
+            const double norm_before = std::sqrt(hbuf[j + 1]);
+            for (int i = 0; i <= j; ++i) Hc(i, j) = hbuf[i];
+            double nw = std::sqrt(nrm2);
+            if (nw < eta * norm_before) {
+                // DGKS second pass
+                IRK_TRY(multidot(ctx, n, j + 1, ws.V, n, w, ws.partials, hdev, st));
+                IRK_TRY(ar(hdev, j + 2));
+                IRK_TRY(update(ctx, n, j + 1, ws.V, n, hdev, w, ws.partials, ndev, st));
+                IRK_TRY(ar(ndev, 1));
+                IRK_CK(cudaMemcpyAsync(hbuf.data(), hdev, sizeof(double) * (j + 2), cudaMemcpyDeviceToHost, st));
+                IRK_CK(cudaMemcpyAsync(&nrm2, ndev, sizeof(double), cudaMemcpyDeviceToHost, st));
+                IRK_CK(cudaStreamSynchronize(st));
+                for (int i = 0; i <= j; ++i) Hc(i, j) += hbuf[i];
+                nw = std::sqrt(nrm2);
+                stats->reorth_passes += 1;
+            }
+            Hc(j + 1, j) = nw;
+            if (nw > 1e-14 * std::max(b_norm, 1.0)) {
+                k_scale_div<<<g1, 256, 0, st>>>(w, w, n, nw);
+                IRK_CK(cudaGetLastError());
+            } else {
+                breakdown = true;
+            }
+            for (int i = 0; i < j; ++i) {
+                const double t = cs[i] * Hc(i, j) + sn[i] * Hc(i + 1, j);
+                Hc(i + 1, j) = -sn[i] * Hc(i, j) + cs[i] * Hc(i + 1, j);
+                Hc(i, j) = t;
+            }
+            const double denom = std::hypot(Hc(j, j), Hc(j + 1, j));
+            cs[j] = denom != 0.0 ? Hc(j, j) / denom : 1.0;
+            sn[j] = denom != 0.0 ? Hc(j + 1, j) / denom : 0.0;
+            Hc(j, j) = denom;
+            Hc(j + 1, j) = 0.0;
+            g[j + 1] = -sn[j] * g[j];
+            g[j] = cs[j] * g[j];
+            total += 1;
+            j_done = j + 1;
+            last_res = std::fabs(g[j + 1]);
+            push_hist(last_res);
+            if (last_res <= tol_abs || breakdown || total >= cfg->max_iters) break;
+        }
+        // y = triu(H)^-1 g ; x += V^T y
+        y.assign(j_done, 0.0);
+        for (int i = j_done - 1; i >= 0; --i) {
+            double acc = g[i];
+            for (int c = i + 1; c < j_done; ++c) acc -= Hc(i, c) * y[c];
+            y[i] = acc / Hc(i, i);
+        }
+        IRK_CK(cudaMemcpyAsync(cdev, y.data(), sizeof(double) * j_done, cudaMemcpyHostToDevice, st));
+        k_axpy_multi<<<g1, 256, 0, st>>>(ws.V, n, j_done, cdev, x, n);
+        IRK_CK(cudaGetLastError());
+        if (last_res <= tol_abs || breakdown) {
+            converged = true;
+            break;
+        }
+        if (total >= cfg->max_iters) break;
+        // restart residual r = P^-1 (b - B x)
+        IRK_TRY(call(op, x, ws.tmp));
+        k_bminus<<<g1, 256, 0, st>>>(rhs, ws.tmp, n);
+        IRK_CK(cudaGetLastError());
+        IRK_TRY(call(pre, ws.tmp, V(0)));
+        IRK_TRY(norm(V(0), beta, nullptr));
+        k_scale_div<<<g1, 256, 0, st>>>(V(0), V(0), n, beta);
+        IRK_CK(cudaGetLastError());
+    }
+    stats->iterations = total;
+    stats->converged = converged ? 1 : 0;
+    stats->breakdown = breakdown ? 1 : 0;
+    double res;
+    IRK_TRY(true_residual(res));
+    stats->final_true_residual = res;
+    stats->history_len = hist_n;
+    return IRK_OK;
+}
+
+}  // extern "C"

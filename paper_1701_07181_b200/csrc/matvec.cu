@@ -1,0 +1,210 @@
+// Fused transformed stage operator:
+//   y_k = alpha * J_k w_k + sum_l mix[k][l] * (M w_l),   k = 0..s-1
+// (reference StageOperator.matvec, stage_system.py:52-70, which does s
+// Jacobian sweeps plus s^2 mass sweeps; here every J block and every M block
+// is read from HBM exactly once per call and applied to all s stage vectors,
+// and the s x s mixing is fused into the epilogue).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+
+#include "blockops.cuh"
+#include "irk_internal.cuh"
+
+namespace irk {
+
+int choose_groups(int nb, int max_threads);  // defined below
+
+struct MixParams {
+    double c[IRK_MAX_STAGES * IRK_MAX_STAGES];
+};
+
+struct MatvecArgs {
+    const int32_t* indptr;
+    const int32_t* indices;
+    const double* J[IRK_MAX_STAGES];   // per-stage block base (already offset by jfirst)
+    const double* M;                   // NULL: no mass term
+    const double* w;
+    double* y;
+    const double* ghost;               // halo values (s, n_ghost, nb) or NULL
+    const int32_t* rows;               // row subset or NULL (all rows)
+    int64_t nrows;
+    int64_t n;                         // T_local * nb (stage stride of w, y)
+    int64_t T_local;
+    int64_t n_ghost;
+    double alpha;
+    int nb, G;
+};
+
+template <int S, bool SHARED, bool EVEN>
+__global__ void __launch_bounds__(512) k_stage_matvec(MatvecArgs A, MixParams C) {
+    extern __shared__ double red[];
+    const Geo q = make_geo(A.nb, A.G);
+    const int64_t bsz = (int64_t)A.nb * 2 * q.P;
+    for (int64_t t = blockIdx.x; t < A.nrows; t += gridDim.x) {
+        const int64_t i = A.rows ? A.rows[t] : t;
+        double part[2 * S];
+#pragma unroll
+        for (int v = 0; v < 2 * S; ++v) part[v] = 0.0;
+        if (q.active) {
+            const int q0 = A.indptr[i], q1 = A.indptr[i + 1];
+            for (int qq = q0; qq < q1; ++qq) {
+                const int64_t col = A.indices[qq];
+                const double* xs[S];
+#pragma unroll
+                for (int r = 0; r < S; ++r)
+                    xs[r] = col < A.T_local ? A.w + r * A.n + col * A.nb
+                                            : A.ghost + (r * A.n_ghost + (col - A.T_local)) * A.nb;
+                if (SHARED) {
+                    gemv_shared<S, EVEN, false>(A.J[0] + qq * bsz, xs, q, part);
+                } else {
+#pragma unroll
+                    for (int r = 0; r < S; ++r)
+                        part[r] = gemv1<EVEN, false>(A.J[r] + qq * bsz, xs[r], q, part[r]);
+                }
+            }
+            if (A.M) {
+                const double* xs[S];
+#pragma unroll
+                for (int r = 0; r < S; ++r) xs[r] = A.w + r * A.n + i * A.nb;
+                gemv_shared<S, EVEN, false>(A.M + i * bsz, xs, q, part + S);
+            }
+        }
+        double tot[2 * S];
+        group_reduce(red, part, 2 * S, q, tot);
+        if (q.active && q.g == 0) {
+#pragma unroll
+            for (int k = 0; k < S; ++k) {
+                double acc = A.alpha * tot[k];
+                if (A.M) {
+#pragma unroll
+                    for (int l = 0; l < S; ++l) acc += C.c[k * S + l] * tot[S + l];
+                }
+                A.y[k * A.n + i * A.nb + q.a] = acc;
+            }
+        }
+    }
+}
+
+int choose_groups(int nb, int max_threads) {
+    const int P = (nb + 1) / 2;
+    int best = 1;
+    double best_eff = -1.0;
+    for (int G = 1; G <= P && G * nb <= max_threads; ++G) {
+        const int thr = G * nb;
+        const int warps = (thr + 31) / 32;
+        const double e1 = (double)thr / (warps * 32);
+        const int per = (P + G - 1) / G;
+        const double e2 = (double)P / (G * per);
+        // prefer more threads when efficiency ties (more memory parallelism)
+        const double eff = e1 * e2 + 1e-4 * G;
+        if (eff > best_eff) { best_eff = eff; best = G; }
+    }
+    return best;
+}
+
+template <int S, bool SHARED, bool EVEN>
+static int launch_t(const irk_stage_op* op, MatvecArgs& A, const MixParams& C, cudaStream_t st) {
+    const int threads = ((A.G * A.nb + 31) / 32) * 32;
+    const size_t smem = sizeof(double) * A.G * 2 * S * A.nb;
+    const int64_t grid = std::min<int64_t>(A.nrows, (int64_t)op->ctx->num_sms * 16);
+    if (grid <= 0) return IRK_OK;
+    k_stage_matvec<S, SHARED, EVEN><<<(int)grid, threads, smem, st>>>(A, C);
+    IRK_CK(cudaGetLastError());
+    return IRK_OK;
+}
+
+template <int S>
+static int launch_s(const irk_stage_op* op, MatvecArgs& A, const MixParams& C, cudaStream_t st) {
+    const bool even = (A.nb % 2) == 0;
+    if (op->shared_j) return even ? launch_t<S, true, true>(op, A, C, st) : launch_t<S, true, false>(op, A, C, st);
+    return even ? launch_t<S, false, true>(op, A, C, st) : launch_t<S, false, false>(op, A, C, st);
+}
+
+int stage_op_apply_rows(const irk_stage_op* op, const double* w, double* y, const int32_t* rows,
+                        int64_t nrows, cudaStream_t st) {
+    MatvecArgs A{};
+    A.indptr = op->pat->d_indptr;
+    A.indices = op->pat->d_indices;
+    for (int k = 0; k < op->s; ++k) A.J[k] = op->J[k]->d + op->jfirst[k] * block_doubles(op->nb);
+    A.M = op->M ? op->M->d : nullptr;
+    A.w = w;
+    A.y = y;
+    A.ghost = op->ghost;
+    A.rows = rows;
+    A.nrows = nrows;
+    A.T_local = op->T_local;
+    A.n = op->T_local * op->nb;
+    A.n_ghost = op->n_ghost;
+    A.alpha = op->alpha;
+    A.nb = op->nb;
+    A.G = choose_groups(op->nb, 256);
+    MixParams C{};
+    for (int e = 0; e < op->s * op->s; ++e) C.c[e] = op->C[e];
+    switch (op->s) {
+        case 1: return launch_s<1>(op, A, C, st);
+        case 2: return launch_s<2>(op, A, C, st);
+        case 3: return launch_s<3>(op, A, C, st);
+        case 4: return launch_s<4>(op, A, C, st);
+        case 5: return launch_s<5>(op, A, C, st);
+        default: set_error("stage count > 5 not supported by the fused matvec"); return IRK_EINVAL;
+    }
+}
+
+}  // namespace irk
+
+using namespace irk;
+
+extern "C" {
+
+int irk_stage_op_create(irk_ctx* ctx, const irk_pattern* pat, int s, const irk_blocks* const* J,
+                        const int64_t* jfirst, const irk_blocks* M, const double* mix,
+                        double alpha, irk_stage_op** out) {
+    IRK_ARG(ctx && pat && J && out, "NULL argument");
+    IRK_ARG(s >= 1 && s <= 5, "stage count must be in [1, 5]");
+    auto* op = new irk_stage_op();
+    op->ctx = ctx;
+    op->pat = pat;
+    op->s = s;
+    op->nb = J[0]->nb;
+    op->alpha = alpha;
+    op->shared_j = true;
+    for (int k = 0; k < s; ++k) {
+        if (!J[k] || J[k]->nb != op->nb) { delete op; set_error("J blocks missing or nb mismatch"); return IRK_EINVAL; }
+        op->J[k] = J[k];
+        op->jfirst[k] = jfirst ? jfirst[k] : 0;
+        if (op->jfirst[k] < 0 || op->jfirst[k] + pat->nnzb > J[k]->count) {
+            delete op; set_error("J block range out of bounds"); return IRK_EINVAL;
+        }
+        if (J[k] != J[0] || op->jfirst[k] != op->jfirst[0]) op->shared_j = false;
+    }
+    op->M = M;
+    if (M && (M->nb != op->nb || M->count < pat->T)) { delete op; set_error("mass blocks mismatch"); return IRK_EINVAL; }
+    if (M) {
+        if (!mix) { delete op; set_error("mix coefficients required with M"); return IRK_EINVAL; }
+        for (int e = 0; e < s * s; ++e) op->C[e] = mix[e];
+    }
+    op->T_local = pat->T;
+    *out = op;
+    return IRK_OK;
+}
+
+void irk_stage_op_destroy(irk_stage_op* op) { delete op; }
+
+int irk_stage_op_set_halo(irk_stage_op* op, int64_t T_local, const double* ghost, int64_t n_ghost) {
+    IRK_ARG(op, "NULL op");
+    IRK_ARG(T_local >= 1 && T_local <= op->pat->T, "T_local out of range");
+    IRK_ARG(n_ghost >= 0 && (n_ghost == 0 || ghost), "ghost buffer missing");
+    IRK_ARG(!op->M || op->M->count >= T_local, "mass blocks mismatch");
+    op->T_local = T_local;
+    op->ghost = ghost;
+    op->n_ghost = n_ghost;
+    return IRK_OK;
+}
+
+int irk_stage_op_apply(const irk_stage_op* op, const double* w, double* y, void* stream) {
+    IRK_ARG(op && w && y, "NULL argument");
+    return stage_op_apply_rows(op, w, y, nullptr, op->T_local, (cudaStream_t)stream);
+}
+
+}  // extern "C"

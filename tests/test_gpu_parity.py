@@ -1,0 +1,276 @@
+"""GPU parity: the CUDA path (through the C ABI) vs the reference golden
+vectors and the CPU oracle.
+
+Bars (BASELINE north star): matvec and preconditioner apply within 1e-12
+relative; factor blocks within 1e-12; GMRES iteration counts within +-1 and
+the stage solution within 1e-10 relative at equal iteration counts; the
+singular-pivot decision (element, stage) identical.
+"""
+
+import numpy as np
+import pytest
+
+import oracle as O
+from paper_1701_07181_b200 import workloads as W
+from paper_1701_07181_b200.meshes import line_mesh, partition
+from paper_1701_07181_b200.tableau import builtin_tableau, derive
+from tests.helpers import load_golden, pattern_of, rel, sha
+
+pytestmark = pytest.mark.gpu
+TOL = 1e-12
+
+
+@pytest.fixture(scope="module")
+def ks():
+    return load_golden("kernels_small")
+
+
+@pytest.fixture(scope="module")
+def be():
+    from paper_1701_07181_b200 import backend
+    return backend
+
+
+def line(T, periodic=True):
+    return pattern_of(line_mesh(T, periodic=periodic).adjacency)
+
+
+# ---------------------------------------------------------------------------
+# backend protocol (kernels/numba_backend.py) vs reference golden vectors
+# ---------------------------------------------------------------------------
+
+def test_protocol_bsr_matvec(ks, be):
+    ip, ix, _ = line(10)
+    assert rel(be.bsr_matvec(ip, ix, ks["line_data"], ks["line_x"]), ks["line_matvec"]) < TOL
+
+
+@pytest.mark.parametrize("tag,keep_key", [("", None), ("4", "line_keep4")])
+def test_protocol_ilu0(ks, be, tag, keep_key):
+    ip, ix, dp = line(10)
+    keep = np.ones(len(ix), bool) if keep_key is None else ks[keep_key]
+    data = ks["line_data"].copy()
+    f, d, fail = be.ilu0_factor(ip, ix, dp, data, keep, True)
+    np.testing.assert_array_equal(data, ks["line_data"])  # inputs never mutated
+    assert fail == -1
+    assert rel(f, ks[f"line_f{tag}"]) < TOL
+    assert rel(d, ks[f"line_dinv{tag}"]) < TOL
+    x = be.ilu0_solve(ip, ix, dp, ks[f"line_f{tag}"], ks[f"line_dinv{tag}"], keep, ks["line_x"])
+    assert rel(x, ks[f"line_solve{tag}"]) < TOL
+
+
+def test_protocol_general_triangle(ks, be):
+    ip, ix, dp = pattern_of([[1, 2], [0, 2], [0, 1]])
+    keep = np.ones(len(ix), bool)
+    f, d, fail = be.ilu0_factor(ip, ix, dp, ks["tri_data"], keep, False)
+    assert fail == -1
+    assert rel(f, ks["tri_f"]) < TOL
+    assert rel(d, ks["tri_dinv"]) < TOL
+    assert rel(be.ilu0_solve(ip, ix, dp, f, d, keep, ks["tri_y"]), ks["tri_solve"]) < TOL
+
+
+@pytest.mark.parametrize("which", ["0", "2"])
+def test_protocol_singular_pivot(ks, be, which):
+    ip, ix, dp = line(4, periodic=False)
+    _, _, fail = be.ilu0_factor(ip, ix, dp, ks[f"sing_data{which}"], np.ones(len(ix), bool), True)
+    assert fail == int(ks[f"sing_fail{which}"])
+
+
+@pytest.mark.parametrize("lit", [False, True])
+def test_protocol_coupled(ks, be, lit):
+    ip, ix, dp = line(8)
+    der = derive(builtin_tableau("RADAU35"))
+    s, T = 3, 8
+    jac = list(ks["cpl_J"])
+    stage_data = np.stack([O.build_stage_matrix(der.a_inv[k, k], ks["cpl_M"], jac[k], dp, 0.08)
+                           for k in range(s)])
+    coupling = np.zeros((s, s, T, 3, 3))
+    for k in range(s):
+        for l in range(s):
+            if k != l:
+                coupling[k, l] = der.a_inv[k, l] * ks["cpl_M"]
+    keep = np.ones(len(ix), bool)
+    f, g, d, fs, fe = be.coupled_factor(ip, ix, dp, stage_data, coupling, keep, lit)
+    tag = "lit" if lit else "std"
+    assert (fs, fe) == (-1, -1)
+    assert rel(f, ks[f"cpl_{tag}_fstage"]) < TOL
+    assert rel(g, ks[f"cpl_{tag}_fcoupling"]) < TOL
+    assert rel(d, ks[f"cpl_{tag}_dinv"]) < TOL
+    x = be.coupled_solve(ip, ix, dp, ks[f"cpl_{tag}_fstage"], ks[f"cpl_{tag}_fcoupling"],
+                         ks[f"cpl_{tag}_dinv"], keep, ks["cpl_w"])
+    assert rel(x, ks[f"cpl_{tag}_apply"]) < TOL
+
+
+# ---------------------------------------------------------------------------
+# device-resident operator / preconditioners / GMRES vs reference
+# ---------------------------------------------------------------------------
+
+class _Der:
+    def __init__(self, a_inv):
+        self.a_inv = a_inv
+
+
+def _device_setup(ks, shared=False):
+    from paper_1701_07181_b200.blocks import BlockDiagonalMatrix, BlockSparseMatrix
+    from paper_1701_07181_b200.stage_system import StageOperator
+    g = line_mesh(8, periodic=True)
+    der = derive(builtin_tableau("RADAU35"))
+    jacs = [BlockSparseMatrix.from_host(g, j) for j in ks["cpl_J"]]
+    if shared:
+        jacs = [jacs[0]] * 3
+    op = StageOperator(der, 0.08, BlockDiagonalMatrix(ks["cpl_M"]), jacs)
+    return der, op
+
+
+def test_stage_operator_distinct_j(ks):
+    _, op = _device_setup(ks)
+    assert rel(op.matvec(ks["cpl_w"]), ks["cpl_matvec"]) < TOL
+
+
+def test_stage_operator_counters(ks):
+    from paper_1701_07181_b200.blocks import OpCounter
+    _, op = _device_setup(ks)
+    c = OpCounter()
+    op.matvec(np.zeros(op.total_dim), c)
+    assert c.jacobian_multiplies == 3 * 24 and c.mass_multiplies == 9 * 8
+    with pytest.raises(ValueError):
+        op.matvec(np.zeros(op.total_dim + 1))
+
+
+def test_device_preconditioners(ks):
+    from paper_1701_07181_b200 import precond as P
+    from paper_1701_07181_b200.blocks import OpCounter
+    der, op = _device_setup(ks)
+    w = ks["cpl_w"]
+    for lit in (False, True):
+        fac = P.stage_coupled_factorize(op, literal_update=lit)
+        assert rel(fac.apply(w), ks[f"cpl_{'lit' if lit else 'std'}_apply"]) < TOL
+    unc = P.stage_uncoupled_factorize(op, der.shifts)
+    assert rel(unc.apply(w), ks["unc_apply"]) < TOL
+    assert rel(P.stage_uncoupled_factorize(op, None).apply(w), ks["unc0_apply"]) < TOL
+    bj = P.stage_uncoupled_factorize(op, der.shifts, partition_of=np.arange(8))
+    assert rel(bj.apply(w), ks["bj_apply"]) < TOL
+    cp4 = P.stage_coupled_factorize(op, partition_of=np.repeat(np.arange(4), 2))
+    assert rel(cp4.apply(w), ks["cpl4_apply"]) < TOL
+    # counters (tests/test_precond.py:238-255): s=3, T=8, r=2
+    c = OpCounter()
+    P.stage_coupled_factorize(op, c)
+    assert c.block_factorizations == 24 and c.block_multiplies == 3 * 2 * 8 + 6 * 8
+    c = OpCounter()
+    unc.apply(np.zeros(op.total_dim), c)
+    assert c.block_multiplies == 3 * 3 * 8
+
+
+def test_device_gmres_vs_reference(ks):
+    from paper_1701_07181_b200 import precond as P
+    from paper_1701_07181_b200.krylov import GmresConfig, gmres
+    der, op = _device_setup(ks)
+    for tag, fac in (("cpl", P.stage_coupled_factorize(op)),
+                     ("unc", P.stage_uncoupled_factorize(op, der.shifts))):
+        x, st = gmres(op.matvec, fac.apply, ks["gm_rhs"], GmresConfig(rel_tol=1e-8))
+        ref_it = int(ks[f"gm_{tag}_iters"])
+        assert abs(st.iterations - ref_it) <= 1
+        if st.iterations == ref_it:
+            assert rel(x, ks[f"gm_{tag}_x"]) < 1e-10
+        # python-callback path (lambdas, as irksolve.stepper passes them)
+        x2, st2 = gmres(lambda v: op.matvec(v), lambda v: fac.apply(v), ks["gm_rhs"],
+                        GmresConfig(rel_tol=1e-8))
+        assert st2.iterations == st.iterations
+        np.testing.assert_array_equal(x2, x)
+        xr, str_ = gmres(op.matvec, fac.apply, ks["gm_rhs"], GmresConfig(rel_tol=1e-10, restart=3))
+        assert abs(str_.iterations - int(ks[f"gm_{tag}_rst_iters"])) <= 1
+        assert rel(xr, ks[f"gm_{tag}_rst_x"]) < 1e-8
+
+
+def test_singular_pivot_error_device():
+    from paper_1701_07181_b200 import SingularPivotError
+    from paper_1701_07181_b200 import precond as P
+    from paper_1701_07181_b200.blocks import BlockSparseMatrix
+    from tests.helpers import random_blocks
+    g = line_mesh(4)
+    data = random_blocks(g.adjacency, 2, seed=8)
+    ip, ix, dp = pattern_of(g.adjacency)
+    data[dp[0]] = 0.0
+    with pytest.raises(SingularPivotError) as exc:
+        P.ilu0_factorize(BlockSparseMatrix.from_host(g, data))
+    assert exc.value.element == 0 and exc.value.stage is None
+
+
+# ---------------------------------------------------------------------------
+# workload-level: same cases the oracle is pinned on (tests/test_oracle_golden.py)
+# ---------------------------------------------------------------------------
+
+from tests.test_oracle_golden import CASES  # noqa: E402
+
+
+def _solver_for(name):
+    from paper_1701_07181_b200.blocks import DevicePattern
+    from paper_1701_07181_b200.krylov import GmresConfig
+    from paper_1701_07181_b200.meshes import partition_bounds
+    from paper_1701_07181_b200.solver import StageSolver
+    cfg, kind, opts = CASES[name]
+    g = load_golden(name)
+    wl = W.make_workload(cfg)
+    assert sha(wl.J, wl.M, wl.rhs) == str(g["input_sha"])
+    dt = float(g["dt"])
+    part = None
+    if opts.get("partitions"):
+        b = partition_bounds(wl.pattern.T, opts["partitions"])
+        part = np.repeat(np.arange(opts["partitions"]), np.diff(b))
+    p = wl.pattern
+    solver = StageSolver(DevicePattern(p.indptr, p.indices, p.diag_pos), wl.J, wl.M, wl.a_inv, dt,
+                         kind=kind or cfg.precond, shifts=wl.shifts, partition_of=part,
+                         gmres_cfg=GmresConfig(rel_tol=cfg.rtol, restart=cfg.restart,
+                                               max_iters=opts.get("max_iters", 500)))
+    return cfg, g, wl, solver
+
+
+@pytest.mark.parametrize("name", list(CASES))
+def test_workload_parity(name):
+    import torch
+    cfg, g, wl, solver = _solver_for(name)
+    assert rel(solver.op.matvec(g["w"]), g["matvec"]) < TOL
+    solver.factorize()
+    assert rel(solver.fac.apply(g["w"]), g["apply"]) < TOL
+    x, st = solver.solve(torch.from_numpy(wl.rhs).cuda())
+    xr = x.cpu().numpy()
+    ref_it = int(g["iterations"])
+    assert abs(st.iterations - ref_it) <= 1, (st.iterations, ref_it)
+    if st.iterations == ref_it:
+        assert rel(xr, g["x"]) < 1e-10
+    assert st.converged == bool(g["converged"]) or abs(st.iterations - ref_it) <= 1
+
+
+def test_solve_is_deterministic():
+    import torch
+    cfg, g, wl, solver = _solver_for("cfg1_n8")
+    solver.factorize()
+    rhs = torch.from_numpy(wl.rhs).cuda()
+    x1, s1 = solver.solve(rhs)
+    x2, s2 = solver.solve(rhs)
+    assert torch.equal(x1, x2) and s1.residual_history == s2.residual_history
+
+
+def test_medium_vs_oracle():
+    """Config-1 shape on a 32x32 quad mesh (T=2048): matvec, apply and solve
+    vs the oracle on identical inputs."""
+    import torch
+    from paper_1701_07181_b200.blocks import DevicePattern
+    from paper_1701_07181_b200.krylov import GmresConfig
+    from paper_1701_07181_b200.solver import StageSolver
+    cfg = W.CONFIGS[1].scaled(N=32)
+    wl = W.make_workload(cfg, norm_iters=30)
+    p = wl.pattern
+    solver = StageSolver(DevicePattern(p.indptr, p.indices, p.diag_pos), wl.J, wl.M, wl.a_inv,
+                         wl.dt, kind="uncoupled", shifts=wl.shifts,
+                         gmres_cfg=GmresConfig(rel_tol=1e-8, restart=40))
+    prob = O.problem_from_workload(wl)
+    w = np.random.default_rng(5).standard_normal(prob.s * prob.T * prob.m)
+    assert rel(solver.op.matvec(w), prob.matvec(w)) < TOL
+    solver.factorize()
+    ofac = O.make_preconditioner(prob, "uncoupled", wl.shifts, workers=3)
+    assert rel(solver.fac.apply(w), ofac.apply(w)) < TOL
+    x, st = solver.solve(torch.from_numpy(wl.rhs).cuda())
+    xo, so = O.gmres(prob.matvec, ofac.apply, wl.rhs, O.GmresConfig(rel_tol=1e-8, restart=40))
+    assert abs(st.iterations - so.iterations) <= 1
+    if st.iterations == so.iterations:
+        assert rel(x.cpu().numpy(), xo) < 1e-10
