@@ -1,0 +1,465 @@
+#!/usr/bin/env python
+"""Benchmark of the irk-b200 hot path (driver contract: one JSON line on rank 0).
+
+Metric (BASELINE.json): IRK stage-solves/s; also BSR-matvec and ILU-apply GB/s
+against the measured B200 HBM peak.  A *step* = one stage-solve = build the
+shifted stage-uncoupled block ILU(0) of B = A^-1 (x) M - dt blkdiag(J) and run
+GMRES(40) to rtol 1e-8, all on device-resident inputs (BASELINE config 1:
+periodic 128x128 quad grid -> T=32768 triangles, nb=40, Radau IIA s=3,
+dt*||J||_2 = 100).  Synthetic seeded inputs (no dataset exists); J entries
+N(0, (1/nb)^2) (SURVEY 8d reading).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
+
+N>1 (torchrun): each rank runs its own replica of the workload (the single
+config-1 system does not need partitioning; the partitioned solve lives in
+paper_1701_07181_b200.distributed), timed with a barrier and the max over
+ranks.  --impl reference times the CPU oracle (C restatement of the
+reference kernels + its GMRES) on the host cores.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+REPO = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, REPO)
+
+MEASURED = os.path.join(REPO, "MEASURED_PEAKS.json")
+FALLBACK_HBM = 6650.0
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--config", type=int, default=1)
+    ap.add_argument("--N", type=int, default=None, help="override mesh cells per side")
+    ap.add_argument("--ordering", default="natural", choices=["natural", "color"])
+    ap.add_argument("--cpu-N", type=int, default=64, help="CPU sample mesh (cells per side)")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--profile", action="store_true", help="timed steps only (for ncu)")
+    return ap.parse_args()
+
+
+def dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+def hbm_peak():
+    try:
+        with open(MEASURED) as fh:
+            return float(json.load(fh)["hbm_gbs"]), "measured"
+    except Exception:
+        return FALLBACK_HBM, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 8:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx.append(float(parts[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[4:8]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# ---------------------------------------------------------------------------
+# algorithmic bytes (Bk = 8 nb^2, v = 8 T nb, int32 indices)
+# ---------------------------------------------------------------------------
+
+def bytes_matvec(T, r, nb, s):
+    nnzb = T * (r + 1)
+    Bk, v = 8 * nb * nb, 8 * T * nb
+    return nnzb * Bk + T * Bk + 2 * s * v + 4 * (nnzb + T + 1)
+
+
+def bytes_apply_uncoupled_shared(T, r, nb, s):
+    """L and D^-1 per stage, U = -dt J upper read once for all stages."""
+    Bk, v = 8 * nb * nb, 8 * T * nb
+    up = T * r // 2
+    return up * Bk + s * (up + T) * Bk + 2 * s * v
+
+
+def make_config(args):
+    from paper_1701_07181_b200 import workloads as W
+    cfg = W.CONFIGS[args.config]
+    kw = {"ordering": args.ordering}
+    if args.N:
+        kw["N"] = args.N
+    return cfg.scaled(**kw)
+
+
+def jnorm_device(pattern, J, iters=60, seed=7):
+    """||J||_2 by power iteration on J^T J with the library's BSR matvec."""
+    import torch
+    from paper_1701_07181_b200.blocks import BlockSparseMatrix, DeviceBlocks
+    p = pattern
+    rows = np.repeat(np.arange(p.T), np.diff(p.indptr))
+    # transposed pattern is the same (symmetric adjacency); block (i,j) of J^T = J_ji^T
+    order = np.lexsort((rows, p.indices))          # sort by (col, row)
+    JT = np.ascontiguousarray(J[order].transpose(0, 2, 1))
+    from paper_1701_07181_b200.blocks import DevicePattern
+    dp = DevicePattern(p.indptr, p.indices, p.diag_pos)
+    A = BlockSparseMatrix(dp, DeviceBlocks.from_host(J))
+    At = BlockSparseMatrix(dp, DeviceBlocks.from_host(JT))
+    g = torch.Generator(device="cpu").manual_seed(seed)
+    v = torch.randn(p.T * J.shape[1], generator=g, dtype=torch.float64).cuda()
+    v /= torch.linalg.vector_norm(v)
+    lam = 0.0
+    for _ in range(iters):
+        w = At.matvec(A.matvec(v))
+        lam = float(torch.linalg.vector_norm(w))
+        v = w / lam
+    return float(np.sqrt(lam))
+
+
+def cpu_sample(args, reps=1):
+    """CPU oracle (C restatement of the reference) on a bounded sample:
+    the config-1 problem shape on a cpu_N x cpu_N quad sub-mesh; the
+    stage-solve rate is scaled by T_sample / T_config."""
+    import oracle as O
+    from paper_1701_07181_b200 import workloads as W
+    cfg = make_config(args)
+    scfg = cfg.scaled(N=args.cpu_N)
+    wl = W.make_workload(scfg, norm_iters=30)
+    prob = O.problem_from_workload(wl)
+    times = []
+    iters = None
+    for _ in range(reps):
+        t0 = time.perf_counter()
+        fac = O.make_preconditioner(prob, scfg.precond, wl.shifts, workers=scfg.s)
+        x, st = O.gmres(prob.matvec, fac.apply, wl.rhs,
+                        O.GmresConfig(rel_tol=scfg.rtol, restart=scfg.restart))
+        times.append(time.perf_counter() - t0)
+        iters = st.iterations
+    t = min(times)
+    scale = wl.pattern.T / cfg.T
+    threads = os.cpu_count()
+    return {
+        "value": scale / t, "unit": "stage-solves/s", "cores": threads, "kind": "port",
+        "sample": (f"oracle/irk_oracle.c (C restatement of the reference numba kernels, OpenMP "
+                   f"rows + {scfg.s} stage threads) + numpy MGS GMRES: one stage-solve of the "
+                   f"config-{args.config} shape on a {args.cpu_N}x{args.cpu_N}-quad sub-mesh "
+                   f"(T={wl.pattern.T}), {t:.2f} s, {iters} GMRES iterations; rate scaled by "
+                   f"T_sample/T = {scale:.4f}"),
+    }
+
+
+def run_reference(args):
+    world, rank, _ = dist_env()
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("gloo")
+        if rank != 0:
+            dist.barrier()
+            return
+    os.environ.setdefault("OMP_NUM_THREADS", str(os.cpu_count()))
+    cfg = make_config(args)
+    import oracle as O
+    from paper_1701_07181_b200 import workloads as W
+    scfg = cfg.scaled(N=args.cpu_N)
+    wl = W.make_workload(scfg, norm_iters=30)
+    prob = O.problem_from_workload(wl)
+
+    def step():
+        fac = O.make_preconditioner(prob, scfg.precond, wl.shifts, workers=scfg.s)
+        return O.gmres(prob.matvec, fac.apply, wl.rhs, O.GmresConfig(rel_tol=scfg.rtol, restart=scfg.restart))
+
+    for _ in range(min(args.warmup, 1)):
+        step()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        _, st = step()
+    t = time.perf_counter() - t0
+    scale = wl.pattern.T / cfg.T
+    value = args.steps * scale / t
+    line = {
+        "impl": "reference", "metric": "IRK stage-solves/sec", "value": value,
+        "unit": "stage-solves/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1e3 * t / args.steps / scale, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": config_dict(cfg, args),
+        "cpu_baseline": {"value": value, "unit": "stage-solves/s", "cores": os.cpu_count(),
+                         "kind": "port",
+                         "sample": (f"each step: one stage-solve of the config-{args.config} shape on "
+                                    f"a {args.cpu_N}x{args.cpu_N}-quad sub-mesh (T={wl.pattern.T}) "
+                                    f"with the C oracle (OpenMP) + MGS GMRES, {st.iterations} "
+                                    f"iterations; rate scaled by {scale:.4f}; warm-up capped at 1")},
+        "e2e": {"value": value, "unit": "stage-solves/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+
+
+def config_dict(cfg, args):
+    return {
+        "workload": (f"cfg{args.config}: periodic {cfg.N}x{cfg.N} quads -> {cfg.T} triangles, "
+                     f"nb={cfg.nb}, {cfg.scheme} (s={cfg.s}), {cfg.precond} block ILU(0) "
+                     f"({cfg.ordering} numbering), GMRES({cfg.restart}) rtol {cfg.rtol}, "
+                     f"dt*||J||2={cfg.dt_norm}, J std 1/nb"),
+        "T": cfg.T, "nb": cfg.nb, "s": cfg.s, "precond": cfg.precond, "restart": cfg.restart,
+        "rtol": cfg.rtol, "ordering": cfg.ordering,
+        "l2": "inputs larger than L2 (J alone is %.2f GB > 126 MB)" % (cfg.T * 4 * 8 * cfg.nb ** 2 / 1e9),
+        "parallelism": f"replicas x{args.gpus}" if args.gpus > 1 else "single GPU",
+    }
+
+
+def run_b200(args):
+    import torch
+    world, rank, local = dist_env()
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    from paper_1701_07181_b200 import _lib as L
+    from paper_1701_07181_b200 import workloads as W
+    from paper_1701_07181_b200.blocks import DeviceBlocks, DevicePattern
+    from paper_1701_07181_b200.krylov import GmresConfig
+    from paper_1701_07181_b200.solver import StageSolver
+    from paper_1701_07181_b200.tableau import builtin_tableau, derive
+
+    cfg = make_config(args)
+    s = cfg.s
+    table = W.mesh_table(cfg.mesh, cfg.N, cfg.ordering)
+    pat = W.Pattern.from_table(table)
+    J = W.jacobian_blocks(pat, cfg.nb, cfg.seed, cfg.jstd)
+    M = W.mass_blocks(pat.T, cfg.nb, cfg.seed)
+    rhs_h = W.rhs_vector(s, pat.T, cfg.nb, cfg.seed)
+    der = derive(builtin_tableau(cfg.scheme))
+    log(f'workload generated T={pat.T}')
+    jnorm = jnorm_device(pat, J)
+    log(f'jnorm {jnorm:.4f}')
+    dt = cfg.dt_norm / jnorm
+    dpat = DevicePattern(pat.indptr, pat.indices, pat.diag_pos)
+    gcfg = GmresConfig(rel_tol=cfg.rtol, restart=cfg.restart, max_iters=cfg.max_iters)
+    solver = StageSolver(dpat, J, M, der.a_inv, dt, kind=cfg.precond, shifts=der.shifts,
+                         gmres_cfg=gcfg)
+    log('solver ready')
+    rhs = torch.from_numpy(rhs_h).cuda()
+    x = torch.empty_like(rhs)
+    stream = torch.cuda.current_stream()
+
+    def step():
+        solver.factorize()
+        _, st = solver.solve(rhs, x=x)
+        return st
+
+    for _ in range(max(args.warmup, 0)):
+        st = step()
+        log(f'warmup step: {st.iterations} iterations')
+    torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    clk = ClockSampler(local)
+    clk.start()
+    time.sleep(0.3)
+    launches0 = L.lib().irk_launch_count()
+    torch.cuda.synchronize()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ev0.record(stream)
+    iters = []
+    for _ in range(args.steps):
+        st = step()
+        iters.append(st.iterations)
+    ev1.record(stream)
+    torch.cuda.synchronize()
+    launches = L.lib().irk_launch_count() - launches0
+    log('timed region done')
+    clocks = clk.stop()
+    t_local = ev0.elapsed_time(ev1) / 1e3
+    t = t_local
+    if dist:
+        tt = torch.tensor([t_local], device="cuda")
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        t = float(tt)
+        dist.barrier()
+    value = world * args.steps / t
+    if args.profile:
+        if rank == 0:
+            print(json.dumps({"metric": "IRK stage-solves/sec", "value": value, "profile": True}))
+        return
+
+    # ---- component timings (outside the timed region) -------------------
+    T, r, nb = cfg.T, 3 if cfg.mesh == "tri2d" else 4, cfg.nb
+    w = torch.randn(s * T * nb, dtype=torch.float64, device="cuda")
+    y = torch.empty_like(w)
+
+    def timed(fn, reps):
+        fn()
+        torch.cuda.synchronize()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        for _ in range(reps):
+            fn()
+        b.record(stream)
+        torch.cuda.synchronize()
+        return a.elapsed_time(b) / 1e3 / reps
+
+    t_mv = timed(lambda: solver.op.apply_device(w, y), 20)
+    log('components timed')
+    t_ap = timed(lambda: solver.fac.apply_device(w, y), 10)
+    t_fac = timed(lambda: solver.factorize(), 3)
+    t_sol = timed(lambda: solver.solve(rhs, x=x), 3)
+    peak, peak_src = hbm_peak()
+    bm = bytes_matvec(T, r, nb, s)
+    ba = bytes_apply_uncoupled_shared(T, r, nb, s) if cfg.precond.startswith("uncoupled") else None
+    ms_step = 1e3 * t / args.steps
+    it_mean = float(np.mean(iters))
+    # operator applications per stage-solve: 1 (P^-1 b) + iters (+ restarts) applies,
+    # iters + 1 (true residual) matvecs
+    share_ap = (it_mean + 1) * t_ap / (t / args.steps)
+    share_mv = (it_mean + 1) * t_mv / (t / args.steps)
+    if ba is not None and share_ap >= share_mv:
+        dom = {"name": "ilu0_apply (fwd+bwd sweeps, all stages)", "bytes": ba, "t": t_ap, "share": share_ap}
+    else:
+        dom = {"name": "stage_matvec (fused)", "bytes": bm, "t": t_mv, "share": share_mv}
+    achieved = dom["bytes"] / dom["t"] / 1e9
+    roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                "frac": achieved / peak, "traffic": None, "kernel": dom["name"],
+                "algorithmic_bytes_per_launch": dom["bytes"], "avg_launch_ms": 1e3 * dom["t"],
+                "share_of_step": dom["share"], "peak_source": peak_src}
+    components = {
+        "matvec_ms": 1e3 * t_mv, "matvec_GBps": bm / t_mv / 1e9, "matvec_frac": bm / t_mv / 1e9 / peak,
+        "apply_ms": 1e3 * t_ap,
+        "apply_GBps": (ba / t_ap / 1e9) if ba else None,
+        "apply_frac": (ba / t_ap / 1e9 / peak) if ba else None,
+        "factor_ms": 1e3 * t_fac, "gmres_ms": 1e3 * t_sol, "gmres_iterations": iters[-1],
+        "levels_fwd_bwd": list(solver.fac.levels()) if solver.fac is not None else None,
+        "jnorm2": jnorm, "dt": dt,
+    }
+
+    # ---- end to end through host buffers (pinned), C-ABI upload path ------
+    e2e = None
+    if not args.no_e2e:
+        Jp = torch.from_numpy(J).pin_memory()
+        Mp = torch.from_numpy(M).pin_memory()
+        rp = torch.from_numpy(rhs_h).pin_memory()
+        xp = torch.empty_like(rp).pin_memory()
+        jb = solver.op.jacobians[0].blocks
+        mb = solver.op.mass.device
+
+        def e2e_step():
+            jb.upload(Jp.numpy())
+            mb.upload(Mp.numpy())
+            rhs.copy_(rp, non_blocking=True)
+            solver.factorize()
+            solver.solve(rhs, x=x)
+            xp.copy_(x, non_blocking=True)
+            torch.cuda.synchronize()
+
+        e2e_step()
+        ne = max(1, min(args.steps, 3))
+        if dist:
+            dist.barrier()
+        t0 = time.perf_counter()
+        for _ in range(ne):
+            e2e_step()
+        te = time.perf_counter() - t0
+        if dist:
+            tt = torch.tensor([te], device="cuda")
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            te = float(tt)
+        e2e = {"value": world * ne / te, "unit": "stage-solves/s",
+               "h2d_bytes_per_step": int(J.nbytes + M.nbytes + rhs_h.nbytes),
+               "d2h_bytes_per_step": int(rhs_h.nbytes),
+               "note": "pinned host J, M, rhs -> irk_blocks_upload / H2D, factorise + GMRES, "
+                       "solution D2H, per step"}
+    if rank != 0:
+        return
+    log('e2e done')
+    cpu = None if args.no_cpu else cpu_sample(args)
+    line = {
+        "metric": "IRK stage-solves/sec", "value": value, "unit": "stage-solves/s",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded generators, no dataset; J std 1/nb)",
+        "config": config_dict(cfg, args), "gmres_iterations_mean": it_mean,
+        "roofline": roofline, "components": components, "cpu_baseline": cpu, "e2e": e2e,
+        "gpu_launches": int(launches), "clocks": clocks,
+    }
+    print(json.dumps(line), flush=True)
+
+
+def log(msg):
+    if os.environ.get("BENCH_QUIET") != "1":
+        print(f"[bench {time.strftime('%H:%M:%S')}] {msg}", file=sys.stderr, flush=True)
+
+
+def main():
+    import faulthandler
+    faulthandler.enable()
+    if os.environ.get("BENCH_HANG_DUMP"):
+        faulthandler.dump_traceback_later(float(os.environ["BENCH_HANG_DUMP"]), exit=True)
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_b200(args)
+
+
+if __name__ == "__main__":
+    main()

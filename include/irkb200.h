@@ -61,6 +61,8 @@ typedef struct irk_factor irk_factor;
 /* ---- library / context ------------------------------------------------ */
 IRK_API int irk_version(void);
 IRK_API const char *irk_last_error(void);
+/* number of CUDA kernels this library has launched in the process */
+IRK_API int64_t irk_launch_count(void);
 IRK_API int irk_ctx_create(int device, irk_ctx **out);
 IRK_API void irk_ctx_destroy(irk_ctx *ctx);
 

@@ -63,6 +63,7 @@ class GmresStatsC(ctypes.Structure):
 _SIGS = {
     "irk_version": (c_int, []),
     "irk_last_error": (ctypes.c_char_p, []),
+    "irk_launch_count": (c_i64, []),
     "irk_ctx_create": (c_int, [c_int, P(c_vp)]),
     "irk_ctx_destroy": (None, [c_vp]),
     "irk_pattern_create": (c_int, [c_vp, c_i64, c_vp, c_vp, c_vp, P(c_vp)]),
@@ -103,7 +104,7 @@ _SIGS = {
 EXPORTED = tuple(_SIGS)
 
 _lib = None
-_lock = threading.Lock()
+_lock = threading.RLock()
 
 
 def load(path: str = LIB_PATH):

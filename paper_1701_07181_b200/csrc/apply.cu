@@ -219,7 +219,7 @@ static int run_levels(const irk_factor* f, K kernel, ApplyArgs& A, const irk_sch
         A.ntasks = hi - lo;
         const int grid = (int)std::min<int64_t>(hi - lo, (int64_t)f->ctx->num_sms * 16);
         kernel<<<grid, threads, smem, st>>>(A);
-        IRK_CK(cudaGetLastError());
+        IRK_LAUNCHED();
     }
     return IRK_OK;
 }
@@ -312,7 +312,7 @@ int copy_blocks(const double* src, const std::vector<int64_t>& sidx, double* dst
     IRK_CK(cudaMemcpyAsync(d, sidx.data(), sizeof(int64_t) * n, cudaMemcpyHostToDevice, st));
     IRK_CK(cudaMemcpyAsync(d + n, didx.data(), sizeof(int64_t) * n, cudaMemcpyHostToDevice, st));
     k_copy_blocks<<<(int)std::min<int64_t>(n, 148 * 16), 128, 0, st>>>(src, d, dst, d + n, n, bsz, scale);
-    IRK_CK(cudaGetLastError());
+    IRK_LAUNCHED();
     IRK_CK(cudaStreamSynchronize(st));  // host index vectors go out of scope
     IRK_CK(cudaFreeAsync(d, st));
     return IRK_OK;

@@ -5,6 +5,7 @@
 #include <algorithm>
 #include <cstdio>
 #include <cstring>
+#include <atomic>
 #include <mutex>
 #include <string>
 
@@ -13,6 +14,9 @@
 namespace irk {
 
 static thread_local std::string g_err;
+static std::atomic<long long> g_launches{0};
+
+void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
 
 void set_error(const std::string& msg) { g_err = msg; }
 
@@ -80,7 +84,7 @@ int permute_in(const double* src_dev, double* dst_dev, int nb, int64_t count, cu
     });
     const int grid = (int)std::min<int64_t>(count, 148 * 16);
     k_rowmajor_to_layout<<<grid, 256, smem, st>>>(src_dev, dst_dev, nb, count);
-    IRK_CK(cudaGetLastError());
+    IRK_LAUNCHED();
     return IRK_OK;
 }
 
@@ -90,7 +94,7 @@ int permute_out(const double* src_dev, double* dst_dev, int nb, int64_t count, c
     const size_t smem = sizeof(double) * nb * nb;
     const int grid = (int)std::min<int64_t>(count, 148 * 16);
     k_layout_to_rowmajor<<<grid, 256, smem, st>>>(src_dev, dst_dev, nb, count);
-    IRK_CK(cudaGetLastError());
+    IRK_LAUNCHED();
     return IRK_OK;
 }
 
@@ -101,6 +105,8 @@ using namespace irk;
 extern "C" {
 
 int irk_version(void) { return 10000; }
+
+int64_t irk_launch_count(void) { return (int64_t)g_launches.load(); }
 
 const char* irk_last_error(void) { return g_err.c_str(); }
 

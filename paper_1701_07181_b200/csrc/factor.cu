@@ -564,7 +564,7 @@ static int launch_levels(const irk_factor* f, FactorArgs& F, const irk_sched& sc
         F.ntasks = hi - lo;
         const int grid = (int)std::min<int64_t>(hi - lo, (int64_t)f->ctx->num_sms * 8);
         k_factor<MAXT><<<grid, 256, smem, st>>>(F);
-        IRK_CK(cudaGetLastError());
+        IRK_LAUNCHED();
     }
     return IRK_OK;
 }
@@ -695,6 +695,7 @@ static int factor_common(irk_ctx* ctx, const irk_pattern* pat, const FactorSetup
     }
     if (need_u) {
         k_init_upper<<<(int)std::min<int64_t>(pat->T, ctx->num_sms * 8), 256, 0, st>>>(F, pat->T);
+        count_launch();
         FCK(cudaGetLastError());
     }
     const int tpr = F.nbp4 / 4;

@@ -29,6 +29,14 @@ int fail_cuda(cudaError_t e, const char* what, const char* file, int line);
         if (_e != cudaSuccess) return ::irk::fail_cuda(_e, #call, __FILE__, __LINE__); \
     } while (0)
 
+void count_launch();
+// after every kernel launch: count it (irk_launch_count) and check the launch
+#define IRK_LAUNCHED()                                                        \
+    do {                                                                      \
+        ::irk::count_launch();                                                \
+        IRK_CK(cudaGetLastError());                                           \
+    } while (0)
+
 #define IRK_ARG(cond, msg)                                                    \
     do {                                                                      \
         if (!(cond)) { ::irk::set_error(std::string("invalid argument: ") + (msg)); return IRK_EINVAL; } \

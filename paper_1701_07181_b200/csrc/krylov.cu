@@ -108,9 +108,9 @@ __global__ void k_reduce_partials(const double* partials, int nblk, int nv, doub
 __global__ void __launch_bounds__(VB) k_update(const double* __restrict__ V, int64_t ldv, int nv,
                                                const double* __restrict__ h, double* __restrict__ w,
                                                int64_t n, double* partials) {
-    __shared__ double hs[64];
+    extern __shared__ double hs[];   // nv coefficients
     __shared__ double red[VB / 32];
-    for (int i = threadIdx.x; i < nv && i < 64; i += blockDim.x) hs[i] = h[i];
+    for (int i = threadIdx.x; i < nv; i += blockDim.x) hs[i] = h[i];
     __syncthreads();
     int64_t lo, hi;
     chunk_range(n, lo, hi);
@@ -133,8 +133,8 @@ __global__ void k_scale_div(const double* __restrict__ x, double* __restrict__ y
 // x += sum_i c[i] V_i
 __global__ void k_axpy_multi(const double* __restrict__ V, int64_t ldv, int nv, const double* __restrict__ c,
                              double* __restrict__ x, int64_t n) {
-    __shared__ double cs[64];
-    for (int i = threadIdx.x; i < nv && i < 64; i += blockDim.x) cs[i] = c[i];
+    extern __shared__ double cs[];   // nv coefficients
+    for (int i = threadIdx.x; i < nv; i += blockDim.x) cs[i] = c[i];
     __syncthreads();
     for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x) {
         double t = 0.0;
@@ -198,19 +198,19 @@ static int multidot(const irk_ctx* ctx, int64_t n, int nv, const double* V, int6
                     double* partials, double* out, cudaStream_t st) {
     const int nb = vec_blocks(ctx);
     k_multidot<<<nb, VB, 0, st>>>(V, ldv, nv, w, n, partials);
-    IRK_CK(cudaGetLastError());
+    IRK_LAUNCHED();
     k_reduce_partials<<<1, 256, 0, st>>>(partials, nb, nv + 1, out);
-    IRK_CK(cudaGetLastError());
+    IRK_LAUNCHED();
     return IRK_OK;
 }
 
 static int update(const irk_ctx* ctx, int64_t n, int nv, const double* V, int64_t ldv, const double* h,
                   double* w, double* partials, double* out, cudaStream_t st) {
     const int nb = vec_blocks(ctx);
-    k_update<<<nb, VB, 0, st>>>(V, ldv, nv, h, w, n, partials);
-    IRK_CK(cudaGetLastError());
+    k_update<<<nb, VB, sizeof(double) * std::max(nv, 1), st>>>(V, ldv, nv, h, w, n, partials);
+    IRK_LAUNCHED();
     k_reduce_partials<<<1, 256, 0, st>>>(partials, nb, 1, out);
-    IRK_CK(cudaGetLastError());
+    IRK_LAUNCHED();
     return IRK_OK;
 }
 
@@ -218,10 +218,11 @@ static int norm_max(const irk_ctx* ctx, int64_t n, const double* x, double* part
                     cudaStream_t st) {
     const int nb = vec_blocks(ctx);
     k_norm_max<<<nb, VB, 0, st>>>(x, n, partials);
-    IRK_CK(cudaGetLastError());
+    IRK_LAUNCHED();
     k_reduce_partials<<<1, 256, 0, st>>>(partials, nb, 1, out2);
+    IRK_LAUNCHED();
     k_reduce_max<<<1, 32, 0, st>>>(partials + nb, nb, out2 + 1);
-    IRK_CK(cudaGetLastError());
+    IRK_LAUNCHED();
     return IRK_OK;
 }
 
@@ -259,7 +260,7 @@ int irk_linop_factor(const irk_factor* f, irk_linop* out) {
 int irk_vec_multidot(irk_ctx* ctx, int64_t n, int nv, const double* V, int64_t ldv, const double* w,
                      double* out, void* stream) {
     IRK_ARG(ctx && w && out && (V || nv == 0), "NULL argument");
-    IRK_ARG(nv >= 0 && nv <= 64 && n >= 0, "bad sizes");
+    IRK_ARG(nv >= 0 && nv <= 4096 && n >= 0, "bad sizes");
     cudaStream_t st = (cudaStream_t)stream;
     double* partials = nullptr;
     IRK_CK(cudaMallocAsync(&partials, sizeof(double) * vec_blocks(ctx) * (nv + 1), st));
@@ -271,7 +272,7 @@ int irk_vec_multidot(irk_ctx* ctx, int64_t n, int nv, const double* V, int64_t l
 int irk_vec_update(irk_ctx* ctx, int64_t n, int nv, const double* V, int64_t ldv, const double* h, double* w,
                    double* out_nrm2, void* stream) {
     IRK_ARG(ctx && w && out_nrm2 && (V || nv == 0), "NULL argument");
-    IRK_ARG(nv >= 0 && nv <= 64 && n >= 0, "bad sizes");
+    IRK_ARG(nv >= 0 && nv <= 4096 && n >= 0, "bad sizes");
     cudaStream_t st = (cudaStream_t)stream;
     double* partials = nullptr;
     IRK_CK(cudaMallocAsync(&partials, sizeof(double) * vec_blocks(ctx), st));
@@ -289,7 +290,7 @@ int irk_gmres(irk_ctx* ctx, int64_t n, irk_linop op, irk_linop pre, irk_allreduc
     IRK_ARG(n >= 1, "empty system");
     cudaStream_t st = (cudaStream_t)stream;
     const int restart = std::min(cfg->restart > 0 ? cfg->restart : cfg->max_iters, cfg->max_iters);
-    IRK_ARG(restart <= 64, "restart length above 64 is not supported");
+    IRK_ARG(restart <= 4096, "restart length above 4096 is not supported");
     const double eta = cfg->reorth_eta > 0 ? cfg->reorth_eta : 0.70710678118654752;
     *stats = irk_gmres_stats{};
     stats->final_true_residual = NAN;
@@ -342,7 +343,7 @@ int irk_gmres(irk_ctx* ctx, int64_t n, irk_linop op, irk_linop pre, irk_allreduc
     auto true_residual = [&](double& res) -> int {
         IRK_TRY(call(op, x, ws.tmp));
         k_bminus<<<g1, 256, 0, st>>>(rhs, ws.tmp, n);
-        IRK_CK(cudaGetLastError());
+        IRK_LAUNCHED();
         return norm(ws.tmp, res, nullptr);
     };
 
@@ -377,7 +378,7 @@ int irk_gmres(irk_ctx* ctx, int64_t n, irk_linop op, irk_linop pre, irk_allreduc
         return IRK_OK;
     }
     k_scale_div<<<g1, 256, 0, st>>>(V(0), V(0), n, beta);
-    IRK_CK(cudaGetLastError());
+    IRK_LAUNCHED();
     int total = 0;
     bool converged = false, breakdown = false;
     double last_res = beta;
@@ -429,7 +430,7 @@ int irk_gmres(irk_ctx* ctx, int64_t n, irk_linop op, irk_linop pre, irk_allreduc
             Hc(j + 1, j) = nw;
             if (nw > 1e-14 * std::max(b_norm, 1.0)) {
                 k_scale_div<<<g1, 256, 0, st>>>(w, w, n, nw);
-                IRK_CK(cudaGetLastError());
+                IRK_LAUNCHED();
             } else {
                 breakdown = true;
             }
@@ -459,8 +460,8 @@ int irk_gmres(irk_ctx* ctx, int64_t n, irk_linop op, irk_linop pre, irk_allreduc
             y[i] = acc / Hc(i, i);
         }
         IRK_CK(cudaMemcpyAsync(cdev, y.data(), sizeof(double) * j_done, cudaMemcpyHostToDevice, st));
-        k_axpy_multi<<<g1, 256, 0, st>>>(ws.V, n, j_done, cdev, x, n);
-        IRK_CK(cudaGetLastError());
+        k_axpy_multi<<<g1, 256, sizeof(double) * std::max(j_done, 1), st>>>(ws.V, n, j_done, cdev, x, n);
+        IRK_LAUNCHED();
         if (last_res <= tol_abs || breakdown) {
             converged = true;
             break;
@@ -469,11 +470,11 @@ int irk_gmres(irk_ctx* ctx, int64_t n, irk_linop op, irk_linop pre, irk_allreduc
         // restart residual r = P^-1 (b - B x)
         IRK_TRY(call(op, x, ws.tmp));
         k_bminus<<<g1, 256, 0, st>>>(rhs, ws.tmp, n);
-        IRK_CK(cudaGetLastError());
+        IRK_LAUNCHED();
         IRK_TRY(call(pre, ws.tmp, V(0)));
         IRK_TRY(norm(V(0), beta, nullptr));
         k_scale_div<<<g1, 256, 0, st>>>(V(0), V(0), n, beta);
-        IRK_CK(cudaGetLastError());
+        IRK_LAUNCHED();
     }
     stats->iterations = total;
     stats->converged = converged ? 1 : 0;

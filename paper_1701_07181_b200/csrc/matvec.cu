@@ -110,7 +110,7 @@ static int launch_t(const irk_stage_op* op, MatvecArgs& A, const MixParams& C, c
     const int64_t grid = std::min<int64_t>(A.nrows, (int64_t)op->ctx->num_sms * 16);
     if (grid <= 0) return IRK_OK;
     k_stage_matvec<S, SHARED, EVEN><<<(int)grid, threads, smem, st>>>(A, C);
-    IRK_CK(cudaGetLastError());
+    IRK_LAUNCHED();
     return IRK_OK;
 }
 

@@ -55,7 +55,8 @@ class StageOperator:
         for J in jacobians[1:]:
             if J.graph is not graph or J.m != m:
                 raise ValueError("all stage Jacobians must share one graph and block size")
-        if mass.T_elems != graph.num_elements or mass.m != m:
+        T = len(jacobians[0].indptr) - 1
+        if mass.T_elems != T or mass.m != m:
             raise ValueError("mass matrix dimensions do not match the Jacobians")
         self.derived = derived
         self.dt = float(dt)
