@@ -46,7 +46,9 @@ def parse():
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--config", type=int, default=1)
     ap.add_argument("--N", type=int, default=None, help="override mesh cells per side")
-    ap.add_argument("--ordering", default="natural", choices=["natural", "color"])
+    ap.add_argument("--ordering", default="color", choices=["natural", "color"],
+                    help="element numbering (color: colour-major, the mesh-colouring level schedule)")
+    ap.add_argument("--no-alt", action="store_true", help="skip the other-ordering measurement")
     ap.add_argument("--cpu-N", type=int, default=64, help="CPU sample mesh (cells per side)")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
@@ -284,11 +286,8 @@ def run_b200(args):
 
     cfg = make_config(args)
     s = cfg.s
-    table = W.mesh_table(cfg.mesh, cfg.N, cfg.ordering)
-    pat = W.Pattern.from_table(table)
-    J = W.jacobian_blocks(pat, cfg.nb, cfg.seed, cfg.jstd)
-    M = W.mass_blocks(pat.T, cfg.nb, cfg.seed)
-    rhs_h = W.rhs_vector(s, pat.T, cfg.nb, cfg.seed)
+    wl = W.make_workload(cfg, jnorm=1.0)     # host arrays; dt comes from the GPU norm below
+    pat, J, M, rhs_h = wl.pattern, wl.J, wl.M, wl.rhs
     der = derive(builtin_tableau(cfg.scheme))
     log(f'workload generated T={pat.T}')
     jnorm = jnorm_device(pat, J)

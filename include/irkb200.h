@@ -120,6 +120,14 @@ IRK_API int irk_factor_coupled(irk_ctx *ctx, const irk_pattern *pat, int s, cons
                        double alpha, const irk_blocks *coupling, const uint8_t *keep,
                        int literal, int store_diag, irk_factor **out, int64_t *fail_stage,
                        int64_t *fail_elem, void *stream);
+/* Re-factorise in place with new numeric values on the same structure
+ * (pattern, keep mask, kind, stage count, explicit/implicit couplings):
+ * coef = per-stage diagonal coefficients (uncoupled) or a_inv (coupled).
+ * Reuses all device buffers and schedules (one Newton iteration's factor). */
+IRK_API int irk_factor_refactor(irk_factor *f, const irk_blocks *const *J, const int64_t *jfirst,
+                                const irk_blocks *M, const double *coef, double alpha,
+                                const irk_blocks *coupling, int64_t *fail_stage, int64_t *fail_elem,
+                                void *stream);
 IRK_API void irk_factor_destroy(irk_factor *f);
 /* x = P^-1 y for all s stages, (s,T,nb) device vectors (BlockIlu0.apply /
  * StageUncoupledIlu0.apply / StageCoupledIlu0.apply, precond.py:79-87,

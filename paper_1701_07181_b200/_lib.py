@@ -80,6 +80,8 @@ _SIGS = {
                                      c_int, c_int, P(c_vp), P(c_i64), P(c_i64), c_vp]),
     "irk_factor_coupled": (c_int, [c_vp, c_vp, c_int, c_vp, c_vp, c_vp, c_vp, c_dbl, c_vp, c_vp,
                                    c_int, c_int, P(c_vp), P(c_i64), P(c_i64), c_vp]),
+    "irk_factor_refactor": (c_int, [c_vp, c_vp, c_vp, c_vp, c_vp, c_dbl, c_vp, P(c_i64), P(c_i64),
+                                    c_vp]),
     "irk_factor_destroy": (None, [c_vp]),
     "irk_factor_apply": (c_int, [c_vp, c_vp, c_vp, c_vp]),
     "irk_factor_export": (c_int, [c_vp, c_vp, c_vp, c_vp, c_vp]),

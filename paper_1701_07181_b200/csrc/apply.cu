@@ -37,33 +37,76 @@ struct ApplyArgs {
     double cup_scale[IRK_MAX_STAGES * IRK_MAX_STAGES];
     const double* y;
     double* x;
-    const int32_t* tasks;
+    // persistent sweep: tasks in topological (level) order, claimed by ticket;
+    // a task publishes flags[task] = epoch when its output is in memory
+    const int32_t* order;
     int64_t ntasks;
+    unsigned* flags;
+    int* ticket;
+    unsigned epoch;
     int64_t T, n;
     int s, nb, G_;
 };
 
 __device__ __forceinline__ int pidx(int hi, int lo) { return hi * (hi - 1) / 2 + lo; }
 
+__device__ __forceinline__ unsigned ld_acquire(const unsigned* p) {
+    unsigned v;
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+
+__device__ __forceinline__ void st_release(unsigned* p, unsigned v) {
+    asm volatile("st.release.gpu.global.u32 [%0], %1;" :: "l"(p), "r"(v) : "memory");
+}
+
+__device__ __forceinline__ void wait_flag(const unsigned* f, unsigned epoch) {
+    while ((int)(ld_acquire(f) - epoch) < 0) __nanosleep(20);
+}
+
+// claim the next task (CTA-uniform); returns -1 when the sweep is done
+__device__ __forceinline__ int64_t claim(const ApplyArgs& A, int* s_task) {
+    if (threadIdx.x == 0) *s_task = atomicAdd(A.ticket, 1);
+    __syncthreads();
+    const int64_t t = *s_task;
+    return t < A.ntasks ? t : -1;
+}
+
+// all writes of the CTA for this task are done -> publish the flag
+__device__ __forceinline__ void publish(unsigned* f, unsigned epoch) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence();
+        st_release(f, epoch);
+    }
+}
+
+// ---- uncoupled: one task = one element, all S stages ------------------------
 template <int S, bool EVEN>
-__global__ void __launch_bounds__(512) k_unc_fwd(ApplyArgs A) {
+__global__ void __launch_bounds__(256) k_unc_fwd(ApplyArgs A) {
     extern __shared__ double red[];
+    __shared__ int s_task;
     const Geo q = make_geo(A.nb, A.G_);
     const int64_t bsz = (int64_t)A.nb * 2 * q.P;
-    for (int64_t t = blockIdx.x; t < A.ntasks; t += gridDim.x) {
-        const int64_t i = A.tasks[t];
+    for (;;) {
+        const int64_t t = claim(A, &s_task);
+        if (t < 0) break;
+        const int64_t i = A.order[t];
+        const int q0 = A.indptr[i], d = A.diag[i], l0 = A.lptr[i];
+        if ((int)threadIdx.x < d - q0 && A.keep[q0 + threadIdx.x])
+            wait_flag(A.flags + A.indices[q0 + threadIdx.x], A.epoch);
+        __syncthreads();
         double part[S];
 #pragma unroll
         for (int k = 0; k < S; ++k) part[k] = 0.0;
         if (q.active) {
-            const int q0 = A.indptr[i], d = A.diag[i], l0 = A.lptr[i];
             for (int qq = q0; qq < d; ++qq) {
                 if (!A.keep[qq]) continue;
                 const int64_t col = A.indices[qq];
                 const double* Lb = A.L + (int64_t)(l0 + qq - q0) * S * bsz;
 #pragma unroll
                 for (int k = 0; k < S; ++k)
-                    part[k] = gemv1<EVEN, false>(Lb + k * bsz, A.x + k * A.n + col * A.nb, q, part[k]);
+                    part[k] = gemv1<EVEN, true>(Lb + k * bsz, A.x + k * A.n + col * A.nb, q, part[k]);
             }
         }
         double tot[S];
@@ -75,22 +118,29 @@ __global__ void __launch_bounds__(512) k_unc_fwd(ApplyArgs A) {
                 A.x[o] = A.y[o] - tot[k];
             }
         }
+        publish(A.flags + i, A.epoch);
     }
 }
 
 template <int S, bool EVEN>
-__global__ void __launch_bounds__(512) k_unc_bwd(ApplyArgs A) {
+__global__ void __launch_bounds__(256) k_unc_bwd(ApplyArgs A) {
     extern __shared__ double red[];
+    __shared__ int s_task;
     double* tv = red + (int64_t)A.G_ * S * A.nb;   // [S][nb]
     const Geo q = make_geo(A.nb, A.G_);
     const int64_t bsz = (int64_t)A.nb * 2 * q.P;
-    for (int64_t t = blockIdx.x; t < A.ntasks; t += gridDim.x) {
-        const int64_t i = A.tasks[t];
+    for (;;) {
+        const int64_t t = claim(A, &s_task);
+        if (t < 0) break;
+        const int64_t i = A.order[t];
+        const int d = A.diag[i], q1 = A.indptr[i + 1], u0 = A.uptr[i];
+        if ((int)threadIdx.x < q1 - d - 1 && A.keep[d + 1 + threadIdx.x])
+            wait_flag(A.flags + A.indices[d + 1 + threadIdx.x], A.epoch);
+        __syncthreads();
         double part[S];
 #pragma unroll
         for (int k = 0; k < S; ++k) part[k] = 0.0;
         if (q.active) {
-            const int d = A.diag[i], q1 = A.indptr[i + 1], u0 = A.uptr[i];
             for (int qq = d + 1; qq < q1; ++qq) {
                 if (!A.keep[qq]) continue;
                 const int64_t col = A.indices[qq];
@@ -98,15 +148,15 @@ __global__ void __launch_bounds__(512) k_unc_bwd(ApplyArgs A) {
 #pragma unroll
                 for (int k = 0; k < S; ++k) xs[k] = A.x + k * A.n + col * A.nb;
                 if (A.u_shared) {
-                    gemv_shared<S, EVEN, false>(A.ubase[0] + qq * bsz, xs, q, part);
+                    gemv_shared<S, EVEN, true>(A.ubase[0] + qq * bsz, xs, q, part);
                 } else if (A.U) {
                     const double* Ub = A.U + (int64_t)(u0 + qq - d - 1) * S * bsz;
 #pragma unroll
-                    for (int k = 0; k < S; ++k) part[k] = gemv1<EVEN, false>(Ub + k * bsz, xs[k], q, part[k]);
+                    for (int k = 0; k < S; ++k) part[k] = gemv1<EVEN, true>(Ub + k * bsz, xs[k], q, part[k]);
                 } else {
 #pragma unroll
                     for (int k = 0; k < S; ++k)
-                        part[k] = gemv1<EVEN, false>(A.ubase[k] + qq * bsz, xs[k], q, part[k]);
+                        part[k] = gemv1<EVEN, true>(A.ubase[k] + qq * bsz, xs[k], q, part[k]);
                 }
             }
         }
@@ -114,7 +164,8 @@ __global__ void __launch_bounds__(512) k_unc_bwd(ApplyArgs A) {
         group_reduce(red, part, S, q, tot);
         if (q.active && q.g == 0) {
 #pragma unroll
-            for (int k = 0; k < S; ++k) tv[k * A.nb + q.a] = A.x[k * A.n + i * A.nb + q.a] - A.uscale * tot[k];
+            for (int k = 0; k < S; ++k)
+                tv[k * A.nb + q.a] = ld_cg(A.x + k * A.n + i * A.nb + q.a) - A.uscale * tot[k];
         }
         __syncthreads();
 #pragma unroll
@@ -129,30 +180,43 @@ __global__ void __launch_bounds__(512) k_unc_bwd(ApplyArgs A) {
 #pragma unroll
             for (int k = 0; k < S; ++k) A.x[k * A.n + i * A.nb + q.a] = tot[k];
         }
+        publish(A.flags + i, A.epoch);
     }
 }
 
+// ---- coupled: one task = (stage k, element i); flags indexed k*T + i --------
 template <bool EVEN>
-__global__ void __launch_bounds__(512) k_cpl_fwd(ApplyArgs A) {
+__global__ void __launch_bounds__(256) k_cpl_fwd(ApplyArgs A) {
     extern __shared__ double red[];
+    __shared__ int s_task;
     const Geo q = make_geo(A.nb, A.G_);
     const int64_t bsz = (int64_t)A.nb * 2 * q.P;
     const int npairs = A.s * (A.s - 1) / 2;
-    for (int64_t t = blockIdx.x; t < A.ntasks; t += gridDim.x) {
-        const int64_t code = A.tasks[t];
+    for (;;) {
+        const int64_t t = claim(A, &s_task);
+        if (t < 0) break;
+        const int64_t code = A.order[t];
         const int k = (int)(code / A.T);
         const int64_t i = code - (int64_t)k * A.T;
+        const int q0 = A.indptr[i], d = A.diag[i], l0 = A.lptr[i];
+        const int nlo = d - q0;
+        const int w = threadIdx.x;
+        if (w < nlo) {
+            if (A.keep[q0 + w]) wait_flag(A.flags + (int64_t)k * A.T + A.indices[q0 + w], A.epoch);
+        } else if (w < nlo + k) {
+            wait_flag(A.flags + (int64_t)(w - nlo) * A.T + i, A.epoch);
+        }
+        __syncthreads();
         double part = 0.0;
         if (q.active) {
-            const int q0 = A.indptr[i], d = A.diag[i], l0 = A.lptr[i];
             for (int qq = q0; qq < d; ++qq) {
                 if (!A.keep[qq]) continue;
                 const int64_t col = A.indices[qq];
-                part = gemv1<EVEN, false>(A.L + ((int64_t)(l0 + qq - q0) * A.s + k) * bsz,
-                                          A.x + k * A.n + col * A.nb, q, part);
+                part = gemv1<EVEN, true>(A.L + ((int64_t)(l0 + qq - q0) * A.s + k) * bsz,
+                                         A.x + k * A.n + col * A.nb, q, part);
             }
             for (int l = 0; l < k; ++l)
-                part = gemv1<EVEN, false>(A.G + (i * npairs + pidx(k, l)) * bsz, A.x + l * A.n + i * A.nb, q, part);
+                part = gemv1<EVEN, true>(A.G + (i * npairs + pidx(k, l)) * bsz, A.x + l * A.n + i * A.nb, q, part);
         }
         double tot;
         group_reduce(red, &part, 1, q, &tot);
@@ -160,36 +224,48 @@ __global__ void __launch_bounds__(512) k_cpl_fwd(ApplyArgs A) {
             const int64_t o = k * A.n + i * A.nb + q.a;
             A.x[o] = A.y[o] - tot;
         }
+        publish(A.flags + code, A.epoch);
     }
 }
 
 template <bool EVEN>
-__global__ void __launch_bounds__(512) k_cpl_bwd(ApplyArgs A) {
+__global__ void __launch_bounds__(256) k_cpl_bwd(ApplyArgs A) {
     extern __shared__ double red[];
+    __shared__ int s_task;
     double* tv = red + (int64_t)A.G_ * 2 * A.nb;
     const Geo q = make_geo(A.nb, A.G_);
     const int64_t bsz = (int64_t)A.nb * 2 * q.P;
     const int npairs = A.s * (A.s - 1) / 2;
-    for (int64_t t = blockIdx.x; t < A.ntasks; t += gridDim.x) {
-        const int64_t code = A.tasks[t];
+    for (;;) {
+        const int64_t t = claim(A, &s_task);
+        if (t < 0) break;
+        const int64_t code = A.order[t];
         const int k = (int)(code / A.T);
         const int64_t i = code - (int64_t)k * A.T;
+        const int d = A.diag[i], q1 = A.indptr[i + 1], u0 = A.uptr[i];
+        const int nup = q1 - d - 1;
+        const int w = threadIdx.x;
+        if (w < nup) {
+            if (A.keep[d + 1 + w]) wait_flag(A.flags + (int64_t)k * A.T + A.indices[d + 1 + w], A.epoch);
+        } else if (w < nup + (A.s - 1 - k)) {
+            wait_flag(A.flags + (int64_t)(k + 1 + w - nup) * A.T + i, A.epoch);
+        }
+        __syncthreads();
         double part[2] = {0.0, 0.0};
         if (q.active) {
-            const int d = A.diag[i], q1 = A.indptr[i + 1], u0 = A.uptr[i];
             for (int qq = d + 1; qq < q1; ++qq) {
                 if (!A.keep[qq]) continue;
                 const int64_t col = A.indices[qq];
                 const double* Ub = A.U ? A.U + ((int64_t)(u0 + qq - d - 1) * A.s + k) * bsz
                                        : A.ubase[k] + qq * bsz;
-                part[0] = gemv1<EVEN, false>(Ub, A.x + k * A.n + col * A.nb, q, part[0]);
+                part[0] = gemv1<EVEN, true>(Ub, A.x + k * A.n + col * A.nb, q, part[0]);
             }
             for (int l = k + 1; l < A.s; ++l) {
                 const double* xl = A.x + l * A.n + i * A.nb;
                 if (A.Cup) {
-                    part[1] = gemv1<EVEN, false>(A.Cup + (i * npairs + pidx(l, k)) * bsz, xl, q, part[1]);
+                    part[1] = gemv1<EVEN, true>(A.Cup + (i * npairs + pidx(l, k)) * bsz, xl, q, part[1]);
                 } else {
-                    const double v = gemv1<EVEN, false>(A.mass + i * bsz, xl, q, 0.0);
+                    const double v = gemv1<EVEN, true>(A.mass + i * bsz, xl, q, 0.0);
                     part[1] = fma(A.cup_scale[k * A.s + l], v, part[1]);
                 }
             }
@@ -198,7 +274,7 @@ __global__ void __launch_bounds__(512) k_cpl_bwd(ApplyArgs A) {
         group_reduce(red, part, 2, q, tot);
         if (q.active && q.g == 0) {
             const double* xi = A.x + k * A.n + i * A.nb;
-            tv[q.a] = xi[q.a] - (A.uscale * tot[0] + tot[1]);
+            tv[q.a] = ld_cg(xi + q.a) - (A.uscale * tot[0] + tot[1]);
         }
         __syncthreads();
         double p2 = 0.0;
@@ -206,21 +282,24 @@ __global__ void __launch_bounds__(512) k_cpl_bwd(ApplyArgs A) {
         double t2;
         group_reduce(red, &p2, 1, q, &t2);
         if (q.active && q.g == 0) A.x[k * A.n + i * A.nb + q.a] = t2;
+        publish(A.flags + code, A.epoch);
     }
 }
 
+// one persistent launch per sweep direction
 template <typename K>
-static int run_levels(const irk_factor* f, K kernel, ApplyArgs& A, const irk_sched& S, int threads,
-                      size_t smem, cudaStream_t st) {
-    for (int64_t l = 0; l < S.nlevels; ++l) {
-        const int64_t lo = S.h_lvl_ptr[l], hi = S.h_lvl_ptr[l + 1];
-        if (hi == lo) continue;
-        A.tasks = S.d_order + lo;
-        A.ntasks = hi - lo;
-        const int grid = (int)std::min<int64_t>(hi - lo, (int64_t)f->ctx->num_sms * 16);
-        kernel<<<grid, threads, smem, st>>>(A);
-        IRK_LAUNCHED();
-    }
+static int run_sweep(const irk_factor* f, K kernel, ApplyArgs& A, const irk_sched& S, unsigned* flags,
+                     int* ticket, int threads, size_t smem, cudaStream_t st) {
+    A.order = S.d_order;
+    A.ntasks = S.h_lvl_ptr.empty() ? 0 : S.h_lvl_ptr.back();
+    A.flags = flags;
+    A.ticket = ticket;
+    IRK_CK(cudaMemsetAsync(ticket, 0, sizeof(int), st));
+    int per_sm = 0;
+    IRK_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, threads, smem));
+    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(A.ntasks, (int64_t)f->ctx->num_sms * std::max(per_sm, 1)));
+    kernel<<<grid, threads, smem, st>>>(A);
+    IRK_LAUNCHED();
     return IRK_OK;
 }
 
@@ -229,8 +308,9 @@ static int unc_apply(const irk_factor* f, ApplyArgs& A, cudaStream_t st) {
     const int threads = ((A.G_ * A.nb + 31) / 32) * 32;
     const size_t smem_f = sizeof(double) * A.G_ * S * A.nb;
     const size_t smem_b = smem_f + sizeof(double) * S * A.nb;
-    IRK_TRY(run_levels(f, k_unc_fwd<S, EVEN>, A, f->fwd, threads, smem_f, st));
-    IRK_TRY(run_levels(f, k_unc_bwd<S, EVEN>, A, f->bwd, threads, smem_b, st));
+    const int64_t nf = (int64_t)f->pat->T;
+    IRK_TRY(run_sweep(f, k_unc_fwd<S, EVEN>, A, f->fwd, f->d_flags, f->d_ticket, threads, smem_f, st));
+    IRK_TRY(run_sweep(f, k_unc_bwd<S, EVEN>, A, f->bwd, f->d_flags + nf, f->d_ticket + 1, threads, smem_b, st));
     return IRK_OK;
 }
 
@@ -239,8 +319,9 @@ static int cpl_apply(const irk_factor* f, ApplyArgs& A, cudaStream_t st) {
     const int threads = ((A.G_ * A.nb + 31) / 32) * 32;
     const size_t smem_f = sizeof(double) * A.G_ * A.nb;
     const size_t smem_b = sizeof(double) * (A.G_ * 2 * A.nb + A.nb);
-    IRK_TRY(run_levels(f, k_cpl_fwd<EVEN>, A, f->fwd, threads, smem_f, st));
-    IRK_TRY(run_levels(f, k_cpl_bwd<EVEN>, A, f->bwd, threads, smem_b, st));
+    const int64_t nf = (int64_t)f->s * f->pat->T;
+    IRK_TRY(run_sweep(f, k_cpl_fwd<EVEN>, A, f->fwd, f->d_flags, f->d_ticket, threads, smem_f, st));
+    IRK_TRY(run_sweep(f, k_cpl_bwd<EVEN>, A, f->bwd, f->d_flags + nf, f->d_ticket + 1, threads, smem_b, st));
     return IRK_OK;
 }
 
@@ -274,6 +355,7 @@ int factor_apply(const irk_factor* f, const double* y, double* x, cudaStream_t s
     fill_args(f, A);
     A.y = y;
     A.x = x;
+    A.epoch = ++f->epoch;
     const bool even = (f->nb % 2) == 0;
     if (f->kind == IRK_FACTOR_COUPLED) return even ? cpl_apply<true>(f, A, st) : cpl_apply<false>(f, A, st);
     switch (f->s) {

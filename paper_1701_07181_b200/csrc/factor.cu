@@ -266,70 +266,91 @@ __device__ double block_norm1(const double* D, Smem& S, const FactorArgs& F) {
     return r;
 }
 
-// In-place Gauss-Jordan inverse of S.D (nb x nb) with partial pivoting.
-// Returns (in all threads) whether the pivot is acceptable.
-__device__ bool gj_invert(Smem& S, const FactorArgs& F) {
+// Gauss-Jordan inverse of S.D (nb x nb) with partial pivoting (row
+// interchanges, the pivot rows LAPACK getrf would pick: first max |a_rk|).
+// One CTA barrier per pivot step: every warp finds the pivot redundantly from
+// the current buffer, every thread writes its elements of the next buffer
+// (S.D <-> S.Lt, Lt is free here); the column un-permutation is folded into
+// the final store.  The inverse is written to `dst` (device layout).
+// Returns (in all threads) whether the pivot passed the reference checks
+// (numba_backend.py:33-40,53-55: det = exp(sum log|u_kk|) nonzero and finite,
+// cond_1 <= 1e14).
+__device__ bool gj_invert(Smem& S, const FactorArgs& F, double* dst) {
     const int nb = F.nb, ld = F.ld;
-    double* D = S.D;
-    const double n1 = block_norm1(D, S, F);
+    const int lane = threadIdx.x & 31;
+    const int nthr = blockDim.x;
+    const int dr = nthr / nb, dc = nthr - (nthr / nb) * nb;   // stride of the flat (r,c) walk
+    const int r0 = threadIdx.x / nb, c0 = threadIdx.x - (threadIdx.x / nb) * nb;
+    const int tot = nb * nb;
+    double* A = S.D;
+    double* B = S.Lt;
+    const double n1 = block_norm1(A, S, F);
     double logdet = 0.0;
     int zero = 0;
     for (int k = 0; k < nb; ++k) {
-        if (threadIdx.x < 32) {
-            double best = -1.0;
-            int bi = k;
-            for (int r = k + threadIdx.x; r < nb; r += 32) {
-                const double v = fabs(D[r * ld + k]);
-                if (v > best) { best = v; bi = r; }
-            }
-            for (int o = 16; o; o >>= 1) {
-                const double ob = __shfl_xor_sync(0xffffffffu, best, o);
-                const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
-                if (ob > best || (ob == best && oi < bi)) { best = ob; bi = oi; }
-            }
-            if (threadIdx.x == 0) { S.misc[0] = bi; S.piv[k] = bi; }
+        double best = -1.0;
+        int bi = k;
+        for (int r = k + lane; r < nb; r += 32) {
+            const double v = fabs(A[r * ld + k]);
+            if (v > best) { best = v; bi = r; }
         }
-        __syncthreads();
-        const int p = S.misc[0];
-        if (p != k)
-            for (int b = threadIdx.x; b < nb; b += blockDim.x) {
-                const double t = D[k * ld + b];
-                D[k * ld + b] = D[p * ld + b];
-                D[p * ld + b] = t;
-            }
-        __syncthreads();
-        const double piv = D[k * ld + k];
+#pragma unroll
+        for (int o = 16; o; o >>= 1) {
+            const double ob = __shfl_xor_sync(0xffffffffu, best, o);
+            const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+            if (ob > best || (ob == best && oi < bi)) { best = ob; bi = oi; }
+        }
+        const int p = bi;
+        const double piv = A[p * ld + k];
+        const double inv = 1.0 / piv;
         if (threadIdx.x == 0) {
+            S.piv[k] = p;
             logdet += log(fabs(piv));
             if (piv == 0.0) zero = 1;
         }
-        for (int r = threadIdx.x; r < nb; r += blockDim.x) S.colk[r] = D[r * ld + k];
-        __syncthreads();
-        for (int b = threadIdx.x; b < nb; b += blockDim.x)
-            D[k * ld + b] = (b == k) ? 1.0 / piv : D[k * ld + b] / piv;
-        __syncthreads();
-        const int tot = nb * nb;
-        for (int e = threadIdx.x; e < tot; e += blockDim.x) {
-            const int r = e / nb, b = e - r * nb;
-            if (r == k) continue;
-            const double f = S.colk[r];
-            if (b == k) D[r * ld + k] = -f * D[k * ld + k];
-            else D[r * ld + b] -= f * D[k * ld + b];
-        }
-        __syncthreads();
-    }
-    for (int k = nb - 1; k >= 0; --k) {
-        const int p = S.piv[k];
-        if (p != k) {
-            for (int r = threadIdx.x; r < nb; r += blockDim.x) {
-                const double t = D[r * ld + k];
-                D[r * ld + k] = D[r * ld + p];
-                D[r * ld + p] = t;
+        const double* P = A + p * ld;
+        int r = r0, c = c0;
+        for (int e = threadIdx.x; e < tot; e += nthr) {
+            double v;
+            if (r == k) {
+                v = (c == k) ? inv : P[c] * inv;
+            } else {
+                const int src = (r == p) ? k : r;   // row p receives the old row k
+                const double f = A[src * ld + k];
+                v = (c == k) ? -f * inv : fma(-f, P[c] * inv, A[src * ld + c]);
             }
-            __syncthreads();
+            B[r * ld + c] = v;
+            c += dc;
+            r += dr;
+            if (c >= nb) { c -= nb; r += 1; }
+        }
+        __syncthreads();
+        double* t = A;
+        A = B;
+        B = t;
+    }
+    // column un-permutation: Y = X S_{n-1} ... S_0  ->  Y[:, c] = X[:, idx[c]]
+    int* idx = S.misc + 8;
+    if (threadIdx.x == 0) {
+        for (int c = 0; c < nb; ++c) idx[c] = c;
+        for (int k = nb - 1; k >= 0; --k) {
+            const int p = S.piv[k];
+            const int tmp = idx[k];
+            idx[k] = idx[p];
+            idx[p] = tmp;
         }
     }
-    const double n2 = block_norm1(D, S, F);
+    const double n2 = block_norm1(A, S, F);   // permutation invariant; has barriers
+    {
+        const int P2 = (nb + 1) >> 1;
+        for (int e = threadIdx.x; e < nb * P2; e += nthr) {
+            const int pp = e / nb, a = e - pp * nb;
+            double2 v;
+            v.x = A[a * ld + idx[2 * pp]];
+            v.y = (2 * pp + 1 < nb) ? A[a * ld + idx[2 * pp + 1]] : 0.0;
+            reinterpret_cast<double2*>(dst)[e] = v;
+        }
+    }
     if (threadIdx.x == 0) {
         const double det = exp(logdet);
         const double cond = n1 * n2;
@@ -446,8 +467,7 @@ __global__ void __launch_bounds__(256) k_factor(FactorArgs F) {
             store_D(S.D, F.Dst + ((int64_t)j * F.s + k) * bsz, F);
             __syncthreads();
         }
-        const bool ok = gj_invert(S, F);
-        store_D(S.D, F.Dinv + ((int64_t)j * F.s + k) * bsz, F);
+        const bool ok = gj_invert(S, F, F.Dinv + ((int64_t)j * F.s + k) * bsz);
         if (!ok && threadIdx.x == 0) atomicMin(F.fail_key, (unsigned long long)((int64_t)k * F.T + j));
         __syncthreads();
     }
@@ -540,12 +560,16 @@ int build_apply_schedules(irk_factor* f, const std::vector<uint8_t>& keep) {
     const bool cpl = f->kind == IRK_FACTOR_COUPLED;
     IRK_TRY(build_sched(f->fwd, levf, f->pat->T, f->s, cpl, +1));
     IRK_TRY(build_sched(f->bwd, levb, f->pat->T, f->s, cpl, -1));
+    const int64_t nflags = 2 * (cpl ? (int64_t)f->s : 1) * f->pat->T;
+    IRK_CK(cudaMalloc(&f->d_flags, sizeof(unsigned) * nflags));
+    IRK_CK(cudaMemset(f->d_flags, 0, sizeof(unsigned) * nflags));
+    IRK_CK(cudaMalloc(&f->d_ticket, sizeof(int) * 2));
     return IRK_OK;
 }
 
 static size_t factor_smem(int nbp4, int ld, int KC) {
     return sizeof(double) * ((size_t)2 * nbp4 * ld + (size_t)2 * KC * ld + nbp4 + 64) +
-           sizeof(int) * (nbp4 + 8);
+           sizeof(int) * (2 * nbp4 + 16);
 }
 
 template <int MAXT>
@@ -582,11 +606,12 @@ struct FactorSetup {
     int simplified, literal, store_diag, coupled;
 };
 
-static int factor_common(irk_ctx* ctx, const irk_pattern* pat, const FactorSetup& P, irk_factor** out,
-                         int64_t* fail_stage, int64_t* fail_elem, cudaStream_t st) {
-    IRK_ARG(ctx && pat && P.J && out, "NULL argument");
-    IRK_ARG(P.s >= 1 && P.s <= IRK_MAX_STAGES, "stage count out of range");
-    const int nb = P.J[0]->nb;
+// numeric values of a factorisation: operator sources and scalars (the
+// structure -- pattern, keep, schedules, buffers -- is fixed at creation)
+static int set_sources(irk_factor* f, const FactorSetup& P) {
+    const irk_pattern* pat = f->pat;
+    const int nb = f->nb;
+    IRK_ARG(P.s == f->s, "stage count differs from the factor's");
     for (int k = 0; k < P.s; ++k) {
         IRK_ARG(P.J[k] && P.J[k]->nb == nb, "J blocks missing or nb mismatch");
         const int64_t jf = P.jfirst ? P.jfirst[k] : 0;
@@ -595,8 +620,83 @@ static int factor_common(irk_ctx* ctx, const irk_pattern* pat, const FactorSetup
     IRK_ARG(!P.M || (P.M->nb == nb && P.M->count >= pat->T), "mass blocks mismatch");
     IRK_ARG(!P.coupling || (P.coupling->nb == nb && P.coupling->count >= (int64_t)P.s * P.s * pat->T),
             "coupling blocks mismatch");
-    IRK_ARG(!P.coupled || P.M || P.coupling, "coupled factor needs M or explicit couplings");
+    IRK_ARG(f->kind != IRK_FACTOR_COUPLED || P.M || P.coupling, "coupled factor needs M or explicit couplings");
+    IRK_ARG(f->kind != IRK_FACTOR_COUPLED || f->s < 2 || (f->d_Cup != nullptr) == (P.coupling != nullptr),
+            "explicit/implicit coupling mode differs from the factor's");
+    const int64_t bsz = block_doubles(nb);
+    FactorArgs& F = *static_cast<FactorArgs*>(f->fargs);
+    bool shared = true;
+    for (int k = 0; k < P.s; ++k) {
+        f->ubase[k] = P.J[k]->d + (P.jfirst ? P.jfirst[k] : 0) * bsz;
+        if (f->ubase[k] != f->ubase[0]) shared = false;
+        F.J[k] = f->ubase[k];
+    }
+    f->u_shared = shared && !f->u_stored;
+    f->uscale = f->u_stored ? 1.0 : P.alpha;
+    F.M = P.M ? P.M->d : nullptr;
+    F.Cexp = P.coupling ? P.coupling->d : nullptr;
+    f->cpl_src = P.coupling ? P.coupling->d : nullptr;
+    F.alpha = P.alpha;
+    for (int k = 0; k < P.s; ++k)
+        F.coef[k] = f->kind == IRK_FACTOR_COUPLED ? (P.a_inv ? P.a_inv[k * P.s + k] : 0.0)
+                                                  : (P.coef ? P.coef[k] : 0.0);
+    if (P.a_inv)
+        for (int e = 0; e < P.s * P.s; ++e) F.cmix[e] = P.a_inv[e];
+    if (f->kind == IRK_FACTOR_COUPLED && !P.coupling) {
+        f->mass = P.M->d;
+        for (int e = 0; e < P.s * P.s; ++e) f->cup_scale[e] = P.a_inv[e];
+    }
+    return IRK_OK;
+}
+
+static int factor_numeric(irk_factor* f, int64_t* fail_stage, int64_t* fail_elem, cudaStream_t st) {
+    FactorArgs& F = *static_cast<FactorArgs*>(f->fargs);
+    const irk_pattern* pat = f->pat;
+    const int64_t bsz = block_doubles(f->nb);
+    const int npairs = f->s * (f->s - 1) / 2;
+    IRK_CK(cudaMemsetAsync(f->d_fail, 0xff, sizeof(unsigned long long), st));
+    F.fail_key = f->d_fail;
+    if (f->cpl_src && npairs > 0) {
+        // explicit upper couplings C[k][l] (k<l) -> Cup[i][pair(l,k)], used unmodified by the apply
+        for (int l = 1; l < f->s; ++l)
+            for (int k = 0; k < l; ++k)
+                IRK_CK(cudaMemcpy2DAsync(f->d_Cup + (int64_t)(l * (l - 1) / 2 + k) * bsz, sizeof(double) * bsz * npairs,
+                                         f->cpl_src + ((int64_t)k * f->s + l) * pat->T * bsz, sizeof(double) * bsz,
+                                         sizeof(double) * bsz, pat->T, cudaMemcpyDeviceToDevice, st));
+    }
+    if (f->u_stored) {
+        k_init_upper<<<(int)std::min<int64_t>(pat->T, f->ctx->num_sms * 8), 256, 0, st>>>(F, pat->T);
+        IRK_LAUNCHED();
+    }
+    int rc = IRK_OK;
+    switch (f->maxt) {
+        case 1: rc = launch_levels<1>(f, F, f->fsched, f->fsmem, st); break;
+        case 2: rc = launch_levels<2>(f, F, f->fsched, f->fsmem, st); break;
+        case 3: rc = launch_levels<3>(f, F, f->fsched, f->fsmem, st); break;
+        case 4: rc = launch_levels<4>(f, F, f->fsched, f->fsmem, st); break;
+        default: set_error("block size too large"); rc = IRK_EINVAL;
+    }
+    if (rc) return rc;
+    unsigned long long key = 0;
+    IRK_CK(cudaMemcpyAsync(&key, f->d_fail, sizeof key, cudaMemcpyDeviceToHost, st));
+    IRK_CK(cudaStreamSynchronize(st));
+    if (fail_stage) *fail_stage = -1;
+    if (fail_elem) *fail_elem = -1;
+    if (key != ~0ULL) {
+        if (fail_stage) *fail_stage = (int64_t)(key / pat->T);
+        if (fail_elem) *fail_elem = (int64_t)(key % pat->T);
+        set_error("numerically singular pivot block");
+        return IRK_ESINGULAR;
+    }
+    return IRK_OK;
+}
+
+static int factor_common(irk_ctx* ctx, const irk_pattern* pat, const FactorSetup& P, irk_factor** out,
+                         int64_t* fail_stage, int64_t* fail_elem, cudaStream_t st) {
+    IRK_ARG(ctx && pat && P.J && P.J[0] && out, "NULL argument");
+    IRK_ARG(P.s >= 1 && P.s <= IRK_MAX_STAGES, "stage count out of range");
     IRK_ARG((int64_t)P.s * pat->T < INT_MAX, "s*T too large");
+    const int nb = P.J[0]->nb;
     auto* f = new irk_factor();
     f->ctx = ctx;
     f->pat = pat;
@@ -605,50 +705,32 @@ static int factor_common(irk_ctx* ctx, const irk_pattern* pat, const FactorSetup
     f->nb = nb;
     f->simplified = P.coupled ? 1 : P.simplified;
     f->literal = P.literal;
+    f->fargs = new FactorArgs{};
     std::vector<uint8_t> keep(pat->nnzb, 1);
     if (P.keep) std::memcpy(keep.data(), P.keep, pat->nnzb);
     const int64_t bsz = block_doubles(nb);
     int rc = IRK_OK;
     auto fail = [&](int code) { irk_factor_destroy(f); return code; };
 #define FCK(call) do { cudaError_t _e = (call); if (_e != cudaSuccess) return fail(fail_cuda(_e, #call, __FILE__, __LINE__)); } while (0)
+    f->u_stored = !f->simplified;
+    const int npairs = P.s * (P.s - 1) / 2;
     FCK(cudaMalloc(&f->d_keep, pat->nnzb));
     FCK(cudaMemcpy(f->d_keep, keep.data(), pat->nnzb, cudaMemcpyHostToDevice));
     FCK(cudaMalloc(&f->d_L, sizeof(double) * bsz * std::max<int64_t>(pat->nlow * P.s, 1)));
     FCK(cudaMalloc(&f->d_Dinv, sizeof(double) * bsz * pat->T * P.s));
     if (P.store_diag || P.literal) FCK(cudaMalloc(&f->d_D, sizeof(double) * bsz * pat->T * P.s));
-    const bool need_u = !f->simplified;
-    if (need_u) {
-        FCK(cudaMalloc(&f->d_U, sizeof(double) * bsz * std::max<int64_t>(pat->nup * P.s, 1)));
-        f->u_stored = true;
-        f->uscale = 1.0;
-    } else {
-        f->u_stored = false;
-        f->uscale = P.alpha;
-    }
-    bool shared = true;
-    for (int k = 0; k < P.s; ++k) {
-        f->ubase[k] = P.J[k]->d + (P.jfirst ? P.jfirst[k] : 0) * bsz;
-        if (f->ubase[k] != f->ubase[0]) shared = false;
-    }
-    f->u_shared = shared && !f->u_stored;
-    const int npairs = P.s * (P.s - 1) / 2;
+    if (f->u_stored) FCK(cudaMalloc(&f->d_U, sizeof(double) * bsz * std::max<int64_t>(pat->nup * P.s, 1)));
     if (P.coupled && npairs > 0) FCK(cudaMalloc(&f->d_G, sizeof(double) * bsz * pat->T * npairs));
-    if (P.coupled) {
-        if (P.coupling) {
-            // upper couplings C[k][l] (k<l) are used unmodified by the apply
-            if (npairs > 0) FCK(cudaMalloc(&f->d_Cup, sizeof(double) * bsz * pat->T * npairs));
-        } else {
-            f->mass = P.M->d;
-            for (int e = 0; e < P.s * P.s; ++e) f->cup_scale[e] = P.a_inv[e];
-        }
-    }
+    if (P.coupled && P.coupling && npairs > 0) FCK(cudaMalloc(&f->d_Cup, sizeof(double) * bsz * pat->T * npairs));
+    FCK(cudaMalloc(&f->d_fail, sizeof(unsigned long long)));
+    if ((rc = set_sources(f, P))) return fail(rc);
     std::vector<int64_t> levf;
     if ((rc = build_apply_schedules(f, keep))) return fail(rc);
     levels_forward(pat, keep, levf);
-    irk_sched fsched;  // factor tasks: (stage, element) per level
-    if ((rc = build_sched(fsched, levf, pat->T, P.s, true, P.coupled ? +1 : 0))) return fail(rc);
+    // factor tasks: (stage, element) per level
+    if ((rc = build_sched(f->fsched, levf, pat->T, P.s, true, P.coupled ? +1 : 0))) return fail(rc);
 
-    FactorArgs F{};
+    FactorArgs& F = *static_cast<FactorArgs*>(f->fargs);
     F.indptr = pat->d_indptr;
     F.indices = pat->d_indices;
     F.diag = pat->d_diag;
@@ -656,13 +738,6 @@ static int factor_common(irk_ctx* ctx, const irk_pattern* pat, const FactorSetup
     F.uptr = pat->d_uptr;
     F.tpos = pat->d_tpos;
     F.keep = f->d_keep;
-    for (int k = 0; k < P.s; ++k) F.J[k] = f->ubase[k];
-    F.M = P.M ? P.M->d : nullptr;
-    F.Cexp = P.coupling ? P.coupling->d : nullptr;
-    F.alpha = P.alpha;
-    for (int k = 0; k < P.s; ++k) F.coef[k] = P.coupled ? P.a_inv[k * P.s + k] : (P.coef ? P.coef[k] : 0.0);
-    if (P.coupled && P.a_inv)
-        for (int e = 0; e < P.s * P.s; ++e) F.cmix[e] = P.a_inv[e];
     F.L = f->d_L;
     F.Dinv = f->d_Dinv;
     F.Dst = f->d_D;
@@ -679,51 +754,15 @@ static int factor_common(irk_ctx* ctx, const irk_pattern* pat, const FactorSetup
     // shared memory budget: full D and L^T, K-chunked operand tiles
     F.KC = F.nbp4;
     while (factor_smem(F.nbp4, F.ld, F.KC) > ctx->smem_optin && F.KC > 4) F.KC = std::max(4, F.KC / 2);
-    const size_t smem = factor_smem(F.nbp4, F.ld, F.KC);
-    if (smem > ctx->smem_optin) { set_error("block size too large for shared memory"); cudaFree(fsched.d_order); return fail(IRK_EINVAL); }
-    unsigned long long* d_fail = nullptr;
-    FCK(cudaMallocAsync(&d_fail, sizeof(unsigned long long), st));
-    FCK(cudaMemsetAsync(d_fail, 0xff, sizeof(unsigned long long), st));
-    F.fail_key = d_fail;
-    if (P.coupled && P.coupling && npairs > 0) {
-        // copy upper couplings (k<l) into Cup[i][pair(l,k)]
-        for (int l = 1; l < P.s; ++l)
-            for (int k = 0; k < l; ++k)
-                FCK(cudaMemcpy2DAsync(f->d_Cup + (int64_t)(l * (l - 1) / 2 + k) * bsz, sizeof(double) * bsz * npairs,
-                                      P.coupling->d + ((int64_t)k * P.s + l) * pat->T * bsz, sizeof(double) * bsz,
-                                      sizeof(double) * bsz, pat->T, cudaMemcpyDeviceToDevice, st));
-    }
-    if (need_u) {
-        k_init_upper<<<(int)std::min<int64_t>(pat->T, ctx->num_sms * 8), 256, 0, st>>>(F, pat->T);
-        count_launch();
-        FCK(cudaGetLastError());
-    }
+    f->fsmem = factor_smem(F.nbp4, F.ld, F.KC);
+    if (f->fsmem > ctx->smem_optin) { set_error("block size too large for shared memory"); return fail(IRK_EINVAL); }
     const int tpr = F.nbp4 / 4;
-    const int maxt = (tpr * tpr + 255) / 256;
-    switch (maxt) {
-        case 1: rc = launch_levels<1>(f, F, fsched, smem, st); break;
-        case 2: rc = launch_levels<2>(f, F, fsched, smem, st); break;
-        case 3: rc = launch_levels<3>(f, F, fsched, smem, st); break;
-        case 4: rc = launch_levels<4>(f, F, fsched, smem, st); break;
-        default: set_error("block size too large"); rc = IRK_EINVAL;
-    }
-    cudaFree(fsched.d_order);  // synchronous free: waits for the launches
-    if (rc) { cudaFreeAsync(d_fail, st); return fail(rc); }
-    unsigned long long key = 0;
-    FCK(cudaMemcpyAsync(&key, d_fail, sizeof key, cudaMemcpyDeviceToHost, st));
-    FCK(cudaFreeAsync(d_fail, st));
-    FCK(cudaStreamSynchronize(st));
+    f->maxt = (tpr * tpr + 255) / 256;
 #undef FCK
-    if (fail_stage) *fail_stage = -1;
-    if (fail_elem) *fail_elem = -1;
+    rc = factor_numeric(f, fail_stage, fail_elem, st);
+    if (rc < 0) return fail(rc);
     *out = f;
-    if (key != ~0ULL) {
-        if (fail_stage) *fail_stage = (int64_t)(key / pat->T);
-        if (fail_elem) *fail_elem = (int64_t)(key % pat->T);
-        set_error("numerically singular pivot block");
-        return IRK_ESINGULAR;
-    }
-    return IRK_OK;
+    return rc;
 }
 
 }  // namespace irk
@@ -773,6 +812,24 @@ int irk_factor_coupled(irk_ctx* ctx, const irk_pattern* pat, int s, const irk_bl
     return factor_common(ctx, pat, P, out, fail_stage, fail_elem, (cudaStream_t)stream);
 }
 
+int irk_factor_refactor(irk_factor* f, const irk_blocks* const* J, const int64_t* jfirst, const irk_blocks* M,
+                        const double* coef, double alpha, const irk_blocks* coupling, int64_t* fail_stage,
+                        int64_t* fail_elem, void* stream) {
+    IRK_ARG(f && J, "NULL argument");
+    IRK_ARG(f->kind == IRK_FACTOR_COUPLED || !M || coef, "coef required with M");
+    FactorSetup P{};
+    P.s = f->s;
+    P.J = J;
+    P.jfirst = jfirst;
+    P.M = M;
+    if (f->kind == IRK_FACTOR_COUPLED) P.a_inv = coef;
+    else P.coef = coef;
+    P.alpha = alpha;
+    P.coupling = coupling;
+    IRK_TRY(set_sources(f, P));
+    return factor_numeric(f, fail_stage, fail_elem, (cudaStream_t)stream);
+}
+
 void irk_factor_destroy(irk_factor* f) {
     if (!f) return;
     cudaFree(f->d_keep);
@@ -784,6 +841,11 @@ void irk_factor_destroy(irk_factor* f) {
     cudaFree(f->d_Cup);
     cudaFree(f->fwd.d_order);
     cudaFree(f->bwd.d_order);
+    cudaFree(f->d_flags);
+    cudaFree(f->d_ticket);
+    cudaFree(f->d_fail);
+    cudaFree(f->fsched.d_order);
+    delete static_cast<FactorArgs*>(f->fargs);
     for (auto* b : f->owned) irk_blocks_destroy(b);
     delete f;
 }

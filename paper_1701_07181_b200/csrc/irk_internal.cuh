@@ -133,6 +133,17 @@ struct irk_factor {
     const double* mass = nullptr;     // implicit upper couplings
     double cup_scale[IRK_MAX_STAGES * IRK_MAX_STAGES] = {};
     irk_sched fwd, bwd;
+    // persistent-sweep synchronisation: per-task flags (fwd, bwd) + tickets
+    unsigned* d_flags = nullptr;
+    int* d_ticket = nullptr;
+    mutable unsigned epoch = 0;
+    // numeric factorisation state (re-run by irk_factor_refactor)
+    void* fargs = nullptr;            // FactorArgs (factor.cu)
+    irk_sched fsched;                 // factor tasks by level
+    unsigned long long* d_fail = nullptr;
+    size_t fsmem = 0;
+    int maxt = 1;
+    const double* cpl_src = nullptr;  // explicit couplings (s*s*T blocks)
     // owned copies when created from explicit host data
     std::vector<irk_blocks*> owned;
 };

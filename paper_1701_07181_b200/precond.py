@@ -192,6 +192,22 @@ class _Factor:
 
     _coupled = False
 
+    def _refactor(self, jblocks, jfirst, mass, coef, alpha, staged):
+        s = len(jblocks)
+        jarr = (ctypes.c_void_p * s)(*[b.handle for b in jblocks])
+        jf = (ctypes.c_int64 * s)(*[int(v) for v in jfirst])
+        carr = None if coef is None else np.ascontiguousarray(coef, dtype=np.float64)
+        fs, fe = ctypes.c_int64(-1), ctypes.c_int64(-1)
+        rc = L.lib().irk_factor_refactor(self.handle, jarr, jf,
+                                         None if mass is None else mass.handle, L.ptr(carr),
+                                         float(alpha), None, ctypes.byref(fs), ctypes.byref(fe),
+                                         L.stream_ptr())
+        L.check(rc, "irk_factor_refactor")
+        self.keepalive = (self.keepalive[0], jblocks, mass, carr, self.keepalive[4], jarr, jf)
+        if rc == L.IRK_ESINGULAR:
+            raise SingularPivotError(fe.value, stage=fs.value if staged else None)
+        return self
+
 
 def _call_factor(fn, *args):
     h = ctypes.c_void_p()
@@ -285,6 +301,14 @@ class StageUncoupledIlu0(_Factor):
     def memory_blocks(self) -> int:
         return self.s * len(self.keep)
 
+    def refactor(self, op: StageOperator, shifts=None) -> "StageUncoupledIlu0":
+        """Re-factorise for a new operator with the same structure, in place
+        (no device allocation; one Newton iteration's preconditioner)."""
+        shifts = self.shifts if shifts is None else np.asarray(shifts, dtype=np.float64)
+        jb, jf = _stage_sources(op.jacobians)
+        self.shifts = shifts
+        return self._refactor(jb, jf, op.mass.device, np.diag(op.a_inv) + shifts, -op.dt, True)
+
     def apply(self, y, counter: OpCounter | None = None):
         x = self._apply(y, self.s * self.n)
         if counter is not None:
@@ -337,6 +361,10 @@ class StageCoupledIlu0(_Factor):
 
     def memory_blocks(self) -> int:
         return self.s * len(self.keep) + self.num_coupling_blocks
+
+    def refactor(self, op: StageOperator) -> "StageCoupledIlu0":
+        jb, jf = _stage_sources(op.jacobians)
+        return self._refactor(jb, jf, op.mass.device, np.ascontiguousarray(op.a_inv), -op.dt, True)
 
     def apply(self, y, counter: OpCounter | None = None):
         x = self._apply(y, self.n_total)

@@ -60,8 +60,16 @@ class StageSolver:
         return self.op.total_dim
 
     def factorize(self):
+        """(Re)build the preconditioner; an existing factor of the same kind is
+        re-factorised in place (no allocation)."""
         k = self.kind
         op = self.op
+        if self.fac is not None and k in ("coupled", "coupled-literal"):
+            return self.fac.refactor(op)
+        if self.fac is not None and k == "uncoupled":
+            return self.fac.refactor(op, self.shifts)
+        if self.fac is not None and k in ("block-jacobi", "uncoupled-unshifted"):
+            return self.fac.refactor(op, self.fac.shifts)
         if k == "none":
             self.fac = None
         elif k in ("coupled", "coupled-literal"):

@@ -207,10 +207,36 @@ class Workload:
                             periodic=True, validate=False)
 
 
+def relabel(table: np.ndarray, J: np.ndarray, M: np.ndarray, rhs: np.ndarray, s: int,
+            new_of_old: np.ndarray):
+    """The same block system under an element renumbering: returns the new
+    neighbour table, pattern and (J, M, rhs) with block (i', j') = old block
+    (old(i'), old(j')).  Numbering changes the ILU(0) factors, not B."""
+    from .meshes import renumber_table
+    T = table.shape[0]
+    old_pat = Pattern.from_table(table)
+    new_table = np.sort(renumber_table(table, new_of_old), axis=1)
+    new_pat = Pattern.from_table(new_table)
+    old_of_new = np.empty(T, dtype=np.int64)
+    old_of_new[new_of_old] = np.arange(T)
+    old_rows = np.repeat(np.arange(T), np.diff(old_pat.indptr))
+    old_keys = old_rows * T + old_pat.indices
+    new_rows = np.repeat(np.arange(T), np.diff(new_pat.indptr))
+    want = old_of_new[new_rows] * T + old_of_new[new_pat.indices]
+    pos = np.searchsorted(old_keys, want)
+    assert np.array_equal(old_keys[pos], want)
+    nb = J.shape[1]
+    rhs_new = rhs.reshape(s, T, nb)[:, old_of_new].reshape(-1)
+    return new_table, new_pat, J[pos], M[old_of_new], rhs_new
+
+
 def make_workload(cfg: SolveConfig, jnorm: float | None = None,
                   norm_iters: int = 60) -> Workload:
-    """Full single-process workload on the host (small/medium sizes)."""
-    table = mesh_table(cfg.mesh, cfg.N, cfg.ordering)
+    """Full single-process workload on the host (small/medium sizes).  Values
+    are drawn in natural element order; ``ordering="color"`` relabels the same
+    system colour-major."""
+    from .meshes import color_major_permutation
+    table = mesh_table(cfg.mesh, cfg.N, "natural")
     pat = Pattern.from_table(table)
     J = jacobian_blocks(pat, cfg.nb, cfg.seed, cfg.jstd)
     M = mass_blocks(pat.T, cfg.nb, cfg.seed)
@@ -218,6 +244,10 @@ def make_workload(cfg: SolveConfig, jnorm: float | None = None,
     der = derive(tab)
     s = tab.s
     rhs = rhs_vector(s, pat.T, cfg.nb, cfg.seed)
+    if cfg.ordering == "color":
+        table, pat, J, M, rhs = relabel(table, J, M, rhs, s, color_major_permutation(table))
+    elif cfg.ordering != "natural":
+        raise ValueError(f"unknown ordering {cfg.ordering!r}")
     if jnorm is None:
         jnorm = norm2_power_cpu(pat, J, iters=norm_iters)
     dt = cfg.dt_norm / jnorm

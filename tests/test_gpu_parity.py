@@ -274,3 +274,26 @@ def test_medium_vs_oracle():
     assert abs(st.iterations - so.iterations) <= 1
     if st.iterations == so.iterations:
         assert rel(x.cpu().numpy(), xo) < 1e-10
+
+
+def test_refactor_in_place_matches_fresh():
+    """irk_factor_refactor on new values == a freshly created factor."""
+    import torch
+    from paper_1701_07181_b200.blocks import DevicePattern
+    from paper_1701_07181_b200.krylov import GmresConfig
+    from paper_1701_07181_b200.solver import StageSolver
+    for kind in ("uncoupled", "coupled"):
+        cfg = W.CONFIGS[1].scaled(N=8, scheme="RADAU23" if kind == "coupled" else "RADAU35")
+        wl = W.make_workload(cfg)
+        p = wl.pattern
+        dp = DevicePattern(p.indptr, p.indices, p.diag_pos)
+        mk = lambda dt: StageSolver(dp, wl.J, wl.M, wl.a_inv, dt, kind=kind, shifts=wl.shifts,  # noqa: E731
+                                    gmres_cfg=GmresConfig(rel_tol=1e-8, restart=40))
+        a = mk(wl.dt)
+        a.factorize()
+        b = mk(0.5 * wl.dt)
+        b.factorize()
+        a.op = b.op            # same structure, new values (dt halved)
+        a.factorize()          # refactor in place
+        w = np.random.default_rng(1).standard_normal(a.n)
+        np.testing.assert_array_equal(a.fac.apply(w), b.fac.apply(w))
