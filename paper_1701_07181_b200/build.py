@@ -17,7 +17,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 REPO = os.path.dirname(HERE)
 OUT = os.path.join(CSRC, "libirkb200.so")
-SOURCES = ["common.cu", "matvec.cu", "factor.cu", "apply.cu", "krylov.cu", "refshim.cu"]
+SOURCES = ["common.cu", "matvec.cu", "factor.cu", "inverse.cu", "apply.cu", "krylov.cu", "refshim.cu"]
 HEADERS = ["irk_internal.cuh", "blockops.cuh"]
 
 

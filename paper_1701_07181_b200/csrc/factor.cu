@@ -363,7 +363,9 @@ __device__ bool gj_invert(Smem& S, const FactorArgs& F, double* dst) {
     return ok;
 }
 
-template <int MAXT>
+// INVERT=false: Schur updates only; the updated pivot block goes to F.Dst and
+// is inverted by the batched warp kernel (inverse.cu).
+template <int MAXT, bool INVERT>
 __global__ void __launch_bounds__(256) k_factor(FactorArgs F) {
     Smem S = carve(F);
     const int nb = F.nb, ld = F.ld;
@@ -467,9 +469,11 @@ __global__ void __launch_bounds__(256) k_factor(FactorArgs F) {
             store_D(S.D, F.Dst + ((int64_t)j * F.s + k) * bsz, F);
             __syncthreads();
         }
-        const bool ok = gj_invert(S, F, F.Dinv + ((int64_t)j * F.s + k) * bsz);
-        if (!ok && threadIdx.x == 0) atomicMin(F.fail_key, (unsigned long long)((int64_t)k * F.T + j));
-        __syncthreads();
+        if (INVERT) {
+            const bool ok = gj_invert(S, F, F.Dinv + ((int64_t)j * F.s + k) * bsz);
+            if (!ok && threadIdx.x == 0) atomicMin(F.fail_key, (unsigned long long)((int64_t)k * F.T + j));
+            __syncthreads();
+        }
     }
 }
 
@@ -572,23 +576,36 @@ static size_t factor_smem(int nbp4, int ld, int KC) {
            sizeof(int) * (2 * nbp4 + 16);
 }
 
+int launch_inverse(const irk_ctx* ctx, const int32_t* tasks, int64_t ntasks, int64_t T, int s, int nb,
+                   const double* D, double* Dinv, unsigned long long* fail_key, cudaStream_t st);
+
 template <int MAXT>
 static int launch_levels(const irk_factor* f, FactorArgs& F, const irk_sched& sched, size_t smem,
                          cudaStream_t st) {
     static bool attr_set = false;
     if (!attr_set) {
-        IRK_CK(cudaFuncSetAttribute(k_factor<MAXT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        IRK_CK(cudaFuncSetAttribute(k_factor<MAXT, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    (int)f->ctx->smem_optin));
+        IRK_CK(cudaFuncSetAttribute(k_factor<MAXT, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     (int)f->ctx->smem_optin));
         attr_set = true;
     }
+    // batched warp inversion when nb has a specialisation (nb <= 64)
+    const bool split = F.nb <= 64 && F.Dst != nullptr;
     for (int64_t l = 0; l < sched.nlevels; ++l) {
         const int64_t lo = sched.h_lvl_ptr[l], hi = sched.h_lvl_ptr[l + 1];
         if (hi == lo) continue;
         F.tasks = sched.d_order + lo;
         F.ntasks = hi - lo;
         const int grid = (int)std::min<int64_t>(hi - lo, (int64_t)f->ctx->num_sms * 8);
-        k_factor<MAXT><<<grid, 256, smem, st>>>(F);
-        IRK_LAUNCHED();
+        if (split) {
+            k_factor<MAXT, false><<<grid, 256, smem, st>>>(F);
+            IRK_LAUNCHED();
+            IRK_TRY(launch_inverse(f->ctx, F.tasks, F.ntasks, F.T, F.s, F.nb, F.Dst, F.Dinv, F.fail_key, st));
+        } else {
+            k_factor<MAXT, true><<<grid, 256, smem, st>>>(F);
+            IRK_LAUNCHED();
+        }
     }
     return IRK_OK;
 }
@@ -718,7 +735,8 @@ static int factor_common(irk_ctx* ctx, const irk_pattern* pat, const FactorSetup
     FCK(cudaMemcpy(f->d_keep, keep.data(), pat->nnzb, cudaMemcpyHostToDevice));
     FCK(cudaMalloc(&f->d_L, sizeof(double) * bsz * std::max<int64_t>(pat->nlow * P.s, 1)));
     FCK(cudaMalloc(&f->d_Dinv, sizeof(double) * bsz * pat->T * P.s));
-    if (P.store_diag || P.literal) FCK(cudaMalloc(&f->d_D, sizeof(double) * bsz * pat->T * P.s));
+    // pivot blocks: needed for export/literal, and as the hand-off to the batched inverse
+    if (P.store_diag || P.literal || nb <= 64) FCK(cudaMalloc(&f->d_D, sizeof(double) * bsz * pat->T * P.s));
     if (f->u_stored) FCK(cudaMalloc(&f->d_U, sizeof(double) * bsz * std::max<int64_t>(pat->nup * P.s, 1)));
     if (P.coupled && npairs > 0) FCK(cudaMalloc(&f->d_G, sizeof(double) * bsz * pat->T * npairs));
     if (P.coupled && P.coupling && npairs > 0) FCK(cudaMalloc(&f->d_Cup, sizeof(double) * bsz * pat->T * npairs));

@@ -297,3 +297,24 @@ def test_refactor_in_place_matches_fresh():
         a.factorize()          # refactor in place
         w = np.random.default_rng(1).standard_normal(a.n)
         np.testing.assert_array_equal(a.fac.apply(w), b.fac.apply(w))
+
+
+@pytest.mark.parametrize("nb", [5, 24, 33, 40, 50, 70])
+def test_block_sizes_vs_oracle(nb):
+    """Every inverse specialisation (warp-register GJ for nb<=64, CTA fallback
+    above) and odd block sizes, through the protocol shims and the device API."""
+    from paper_1701_07181_b200 import backend as be
+    mesh = W.CONFIGS[1].scaled(N=3, nb=nb)
+    wl = W.make_workload(mesh, norm_iters=20)
+    p = wl.pattern
+    keep = np.ones(p.nnzb, bool)
+    mat = O.build_stage_matrix(1.3, wl.M, wl.J, p.diag_pos, wl.dt)
+    f, d, fail = be.ilu0_factor(p.indptr, p.indices, p.diag_pos, mat, keep, True)
+    fo, do, failo = O.ilu0_factor(p.indptr, p.indices, p.diag_pos, mat, keep, True)
+    assert fail == failo == -1
+    assert rel(f, fo) < TOL and rel(d, do) < TOL
+    y = np.random.default_rng(nb).standard_normal(p.T * nb)
+    assert rel(be.ilu0_solve(p.indptr, p.indices, p.diag_pos, fo, do, keep, y),
+               O.ilu0_solve(p.indptr, p.indices, p.diag_pos, fo, do, keep, y)) < TOL
+    x = np.random.default_rng(nb + 1).standard_normal(p.T * nb)
+    assert rel(be.bsr_matvec(p.indptr, p.indices, wl.J, x), O.bsr_matvec(p.indptr, p.indices, wl.J, x)) < TOL
