@@ -18,7 +18,7 @@ CSRC = os.path.join(HERE, "csrc")
 REPO = os.path.dirname(HERE)
 OUT = os.path.join(CSRC, "libirkb200.so")
 SOURCES = ["common.cu", "matvec.cu", "factor.cu", "inverse.cu", "apply.cu", "krylov.cu", "refshim.cu"]
-HEADERS = ["irk_internal.cuh", "blockops.cuh"]
+HEADERS = ["irk_internal.cuh", "blockops.cuh", "pipeline.cuh"]
 
 
 def nvcc() -> str:

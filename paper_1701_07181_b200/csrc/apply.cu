@@ -15,6 +15,7 @@
 
 #include "blockops.cuh"
 #include "irk_internal.cuh"
+#include "pipeline.cuh"
 
 namespace irk {
 
@@ -286,6 +287,583 @@ __global__ void __launch_bounds__(256) k_cpl_bwd(ApplyArgs A) {
     }
 }
 
+// ---------------------------------------------------------------------------
+// Bulk-copy pipelined persistent sweeps (uncoupled, nb even).
+// Warp 0 lane 0 (producer) claims tasks in topological order.  For each task
+// it (1) waits until the task's x double-buffer slot is free, (2) streams the
+// task's factor blocks (fwd: L[lq][k]; bwd: U blocks then Dinv[i][k]) into the
+// block ring with cp.async.bulk -- no dependency needed, so the next task's
+// blocks are prefetched while the previous task finishes -- then (3) waits for
+// the task's dependency flags (ld.acquire.gpu), issues fence.proxy.async and
+// (4) bulk-copies the x segments the task multiplies into the x slot.
+// Consumer warps take blocks in FIFO order, read x from the slot, reduce and
+// store the task's output, publish its flag and free the x slot.
+// Deadlock-free: tasks enter every ring in ticket order, dependencies have
+// smaller tickets, and a task's x is loaded only after its dependencies.
+// ---------------------------------------------------------------------------
+enum { PD_FIRST = 1, PD_LAST = 2, PD_END = 4, PD_USH = 8, PD_U = 16, PD_DINV = 32, PD_L = 64 };
+
+struct PipeCfg {
+    int nst;
+    int stage_bytes;
+    int block_bytes;
+    int maxdeg;        // max lower/upper neighbours of a row
+    int xslot_doubles; // (maxdeg + 1) * S * nb
+};
+
+struct PipeSmem {
+    unsigned char* stages;
+    uint64_t* full;
+    uint64_t* empty;
+    uint64_t* xfull;   // [2]
+    uint64_t* xempty;  // [2]
+    int4* desc;
+    double* xs;        // [2][xslot]
+    double* red;       // [G][S][nb]
+    double* tv;        // [S][nb]
+};
+
+template <int S>
+__device__ __forceinline__ PipeSmem pipe_carve(unsigned char* raw, const PipeCfg& PC, int G, int nb) {
+    PipeSmem P;
+    P.stages = raw;
+    P.full = reinterpret_cast<uint64_t*>(raw + (size_t)PC.nst * PC.stage_bytes);
+    P.empty = P.full + PC.nst;
+    P.xfull = P.empty + PC.nst;
+    P.xempty = P.xfull + 2;
+    P.desc = reinterpret_cast<int4*>(P.xempty + 2);
+    P.xs = reinterpret_cast<double*>(P.desc + PC.nst);
+    P.red = P.xs + 2 * (size_t)PC.xslot_doubles;
+    P.tv = P.red + (size_t)G * S * nb;
+    return P;
+}
+
+__device__ __forceinline__ void pipe_init(PipeSmem& P, int nst, int ncons_warps) {
+    if (threadIdx.x == 0) {
+        for (int i = 0; i < nst; ++i) {
+            mbar_init(P.full + i, 1);
+            mbar_init(P.empty + i, ncons_warps);
+        }
+        for (int b = 0; b < 2; ++b) {
+            mbar_init(P.xfull + b, 1);
+            mbar_init(P.xempty + b, ncons_warps);
+        }
+        fence_mbar_init();
+    }
+    __syncthreads();
+}
+
+__device__ __forceinline__ void fence_proxy_async_global() {
+    asm volatile("fence.proxy.async.global;" ::: "memory");
+}
+
+struct Producer {
+    PipeSmem* P;
+    const PipeCfg* PC;
+    int st = 0;
+    uint32_t ph = 0;
+    int xb = 0;          // x slot of the current task
+    uint32_t xph = 0;    // phase of slot xb
+    __device__ void push(int4 d, const double* blk) {
+        mbar_wait(P->empty + st, ph ^ 1);
+        P->desc[st] = d;
+        if (blk) {
+            mbar_expect_tx(P->full + st, PC->block_bytes);
+            bulk_g2s(P->stages + (size_t)st * PC->stage_bytes, blk, PC->block_bytes, P->full + st);
+        } else {
+            mbar_expect_tx(P->full + st, 0);
+        }
+        if (++st == PC->nst) { st = 0; ph ^= 1; }
+    }
+    __device__ double* x_acquire() {   // wait for the task's x slot to be free
+        mbar_wait(P->xempty + xb, xph ^ 1);
+        return P->xs + (size_t)xb * PC->xslot_doubles;
+    }
+    __device__ void x_commit(uint32_t bytes) { mbar_expect_tx(P->xfull + xb, bytes); }
+    __device__ void x_next() { xb ^= 1; if (xb == 0) xph ^= 1; }
+};
+
+struct Consumer {
+    PipeSmem* P;
+    const PipeCfg* PC;
+    int st = 0;
+    uint32_t ph = 0;
+    int xb = 0;
+    uint32_t xph = 0;
+    __device__ int4 take() {
+        mbar_wait(P->full + st, ph);
+        return P->desc[st];
+    }
+    __device__ const double2* block() const {
+        return reinterpret_cast<const double2*>(P->stages + (size_t)st * PC->stage_bytes);
+    }
+    __device__ void release() {
+        __syncwarp();
+        if ((threadIdx.x & 31) == 0) mbar_arrive(P->empty + st);
+        if (++st == PC->nst) { st = 0; ph ^= 1; }
+    }
+    __device__ const double* x_wait() {
+        mbar_wait(P->xfull + xb, xph);
+        return P->xs + (size_t)xb * PC->xslot_doubles;
+    }
+    __device__ void x_release() {
+        __syncwarp();
+        if ((threadIdx.x & 31) == 0) mbar_arrive(P->xempty + xb);
+        xb ^= 1;
+        if (xb == 0) xph ^= 1;
+    }
+};
+
+// acc += rows of a staged block times an x segment (smem); caller checks q.active
+__device__ __forceinline__ double smem_gemv(const double2* B, const double* x, const Geo& q, double acc) {
+    for (int p = q.g; p < q.P; p += q.G) {
+        const double2 b = B[p * q.nb + q.a];
+        const double2 v = *reinterpret_cast<const double2*>(x + 2 * p);
+        acc = fma(b.x, v.x, acc);
+        acc = fma(b.y, v.y, acc);
+    }
+    return acc;
+}
+
+constexpr int MAXD = 8;   // neighbour metadata held in registers per task
+
+// Task ranges: DEPS (persistent, many levels) -> batches of 32 tickets;
+// !DEPS (one launch per level) -> a static contiguous slice per CTA.
+template <bool DEPS>
+__device__ __forceinline__ bool next_batch(const ApplyArgs& A, int& tb, int& tend, int& cur, int hi) {
+    const int lane = threadIdx.x & 31;
+    if (DEPS) {
+        // one ticket at a time: consecutive tickets are mostly independent tasks
+        // of one level, which must spread over CTAs for the wavefront to flow
+        int v = 0;
+        if (lane == 0) v = atomicAdd(A.ticket, 1);
+        tb = __shfl_sync(0xffffffffu, v, 0);
+        tend = min((int)A.ntasks, tb + 1);
+    } else {
+        tb = cur;
+        cur += 32;
+        tend = hi;
+    }
+    return tb < tend;
+}
+
+template <int S, bool DEPS>
+__global__ void __launch_bounds__(288) k_unc_fwd_pipe(ApplyArgs A, PipeCfg PC) {
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    const int nb = A.nb;
+    PipeSmem P = pipe_carve<S>(smem_raw, PC, A.G_, nb);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int ncons_warps = (blockDim.x >> 5) - 1, ncons = ncons_warps * 32;
+    pipe_init(P, PC.nst, ncons_warps);
+    const int64_t bsz = (int64_t)PC.block_bytes / 8;
+    const uint32_t seg = (uint32_t)nb * 8;
+    if (warp == 0) {
+        Producer pr{&P, &PC};
+        int cur = (int)(A.ntasks * blockIdx.x / gridDim.x);
+        const int hi = (int)(A.ntasks * (blockIdx.x + 1) / gridDim.x);
+        int tb, tend;
+        while (next_batch<DEPS>(A, tb, tend, cur, hi)) {
+            // warp-parallel metadata prefetch: lane l <-> task tb + l
+            const int tl = tb + lane;
+            const bool valid = tl < tend;
+            const int64_t il = valid ? A.order[tl] : 0;
+            const int q0l = valid ? A.indptr[il] : 0, dl = valid ? A.diag[il] : 0, l0l = valid ? A.lptr[il] : 0;
+            const int nnl = dl - q0l;
+            int coll[MAXD];
+            unsigned kml = 0;
+#pragma unroll
+            for (int m = 0; m < MAXD; ++m) {
+                coll[m] = 0;
+                if (m < nnl) { coll[m] = A.indices[q0l + m]; kml |= (A.keep[q0l + m] ? 1u : 0u) << m; }
+            }
+            for (int bt = 0; bt < 32 && tb + bt < tend; ++bt) {
+                const int t = tb + bt;
+                const int64_t i = __shfl_sync(0xffffffffu, il, bt);
+                const int q0 = __shfl_sync(0xffffffffu, q0l, bt), nn = __shfl_sync(0xffffffffu, nnl, bt);
+                const int l0 = __shfl_sync(0xffffffffu, l0l, bt);
+                unsigned km = __shfl_sync(0xffffffffu, kml, bt);
+                int col[MAXD];
+#pragma unroll
+                for (int m = 0; m < MAXD; ++m) col[m] = __shfl_sync(0xffffffffu, coll[m], bt);
+                if (nn > MAXD) {   // rare: wide rows, read directly
+                    km = 0;
+                    for (int m = 0; m < nn && m < 32; ++m) km |= (A.keep[q0 + m] ? 1u : 0u) << m;
+                }
+                auto colm = [&](int m) -> int64_t {
+                    if (m < MAXD) {
+                        int v = 0;
+#pragma unroll
+                        for (int mm = 0; mm < MAXD; ++mm) v = (mm == m) ? col[mm] : v;
+                        return v;
+                    }
+                    return A.indices[q0 + m];
+                };
+                auto kept = [&](int m) -> bool { return m < 32 ? ((km >> m) & 1u) : A.keep[q0 + m] != 0; };
+                // item n of the task: (kept neighbour, stage) in order
+                int nitems = 0;
+                for (int m = 0; m < nn; ++m) nitems += kept(m) ? S : 0;
+                auto push_items = [&](int from, int to) {
+                    if (nitems == 0) {
+                        if (from == 0 && to > 0) pr.push(make_int4(t, -1, PD_FIRST | PD_LAST, 0), nullptr);
+                        return;
+                    }
+                    int n = 0;
+                    for (int m = 0; m < nn; ++m) {
+                        if (!kept(m)) continue;
+                        for (int k = 0; k < S; ++k, ++n) {
+                            if (n < from || n >= to) continue;
+                            const int fl = PD_L | (n == 0 ? PD_FIRST : 0) | (n == nitems - 1 ? PD_LAST : 0);
+                            pr.push(make_int4(t, m * S + k, fl, 0), A.L + ((int64_t)(l0 + m) * S + k) * bsz);
+                        }
+                    }
+                };
+                const int ntot = nitems > 0 ? nitems : 1;
+                // blocks pushed before x is committed: consumers block on x at the
+                // task's first item, so at most nst - 1 may precede the commit
+                const int npre = DEPS ? min(ntot, PC.nst - 1) : 0;
+                double* xs = nullptr;
+                int xb = 0;
+                if (lane == 0) {
+                    xs = pr.x_acquire();
+                    xb = pr.xb;
+                    push_items(0, npre);
+                }
+                // dependencies (one lane per neighbour), then the x segments z_{k,j}
+                if (DEPS)
+                    for (int m = lane; m < nn; m += 32)
+                        if (kept(m)) wait_flag(A.flags + colm(m), A.epoch);
+                __syncwarp();
+                uint32_t bytes = 0;
+                for (int m = 0; m < nn; ++m) bytes += kept(m) ? S * seg : 0;
+                if (lane == 0) {
+                    if (DEPS) fence_proxy_async_global();
+                    pr.x_commit(bytes);
+                }
+                xs = reinterpret_cast<double*>(__shfl_sync(0xffffffffu, reinterpret_cast<uintptr_t>(xs), 0));
+                xb = __shfl_sync(0xffffffffu, xb, 0);
+                __syncwarp();
+                for (int e = lane; e < nn * S; e += 32) {
+                    const int m = e / S, k = e - m * S;
+                    if (kept(m)) bulk_g2s(xs + e * nb, A.x + k * A.n + colm(m) * nb, seg, P.xfull + xb);
+                }
+                if (lane == 0) push_items(npre, ntot);
+                if (lane == 0) pr.x_next();
+            }
+        }
+        if (lane == 0) pr.push(make_int4(-1, 0, PD_END, 0), nullptr);
+        return;
+    }
+    const int c = threadIdx.x - 32;
+    Geo q;
+    q.nb = nb; q.P = (nb + 1) >> 1; q.G = A.G_; q.g = c / nb; q.a = c - q.g * nb; q.active = q.g < q.G;
+    Consumer cs{&P, &PC};
+    double part[S];
+    const double* xs = nullptr;
+    for (;;) {
+        const int4 dsc = cs.take();
+        if (dsc.z & PD_END) break;
+        const int64_t i = A.order[dsc.x];
+        if (dsc.z & PD_FIRST) {
+#pragma unroll
+            for (int k = 0; k < S; ++k) part[k] = 0.0;
+            xs = cs.x_wait();
+        }
+        if (dsc.y >= 0 && q.active) {
+            const int m = dsc.y / S, kk = dsc.y - m * S;
+            const double2* B = cs.block();
+            const double* xv = xs + (m * S + kk) * nb;
+#pragma unroll
+            for (int k = 0; k < S; ++k)
+                if (k == kk) part[k] = smem_gemv(B, xv, q, part[k]);
+        }
+        cs.release();
+        if (dsc.z & PD_LAST) {
+            if (dsc.y < 0) {
+                // no kept lower neighbour: z_i = y_i, no reduction
+                if (q.active && q.g == 0)
+#pragma unroll
+                    for (int k = 0; k < S; ++k) {
+                        const int64_t o = k * A.n + i * nb + q.a;
+                        A.x[o] = A.y[o];
+                    }
+                cs.x_release();
+                if (DEPS) {
+                    consumer_sync(1, ncons);
+                    if (c == 0) { __threadfence(); st_release(A.flags + i, A.epoch); }
+                }
+                continue;
+            }
+            if (q.active)
+#pragma unroll
+                for (int k = 0; k < S; ++k) P.red[(q.g * S + k) * nb + q.a] = part[k];
+            consumer_sync(1, ncons);
+            if (q.active && q.g == 0) {
+#pragma unroll
+                for (int k = 0; k < S; ++k) {
+                    double sum = 0.0;
+                    for (int gg = 0; gg < q.G; ++gg) sum += P.red[(gg * S + k) * nb + q.a];
+                    const int64_t o = k * A.n + i * nb + q.a;
+                    A.x[o] = A.y[o] - sum;
+                }
+            }
+            cs.x_release();
+            consumer_sync(1, ncons);
+            if (DEPS && c == 0) {
+                __threadfence();
+                st_release(A.flags + i, A.epoch);
+            }
+        }
+    }
+}
+
+template <int S, bool DEPS>
+__global__ void __launch_bounds__(288) k_unc_bwd_pipe(ApplyArgs A, PipeCfg PC) {
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    const int nb = A.nb;
+    PipeSmem P = pipe_carve<S>(smem_raw, PC, A.G_, nb);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int ncons_warps = (blockDim.x >> 5) - 1, ncons = ncons_warps * 32;
+    pipe_init(P, PC.nst, ncons_warps);
+    const int64_t bsz = (int64_t)PC.block_bytes / 8;
+    const uint32_t seg = (uint32_t)nb * 8;
+    if (warp == 0) {
+        Producer pr{&P, &PC};
+        int cur = (int)(A.ntasks * blockIdx.x / gridDim.x);
+        const int hi = (int)(A.ntasks * (blockIdx.x + 1) / gridDim.x);
+        int tb, tend;
+        while (next_batch<DEPS>(A, tb, tend, cur, hi)) {
+            const int tl = tb + lane;
+            const bool valid = tl < tend;
+            const int64_t il = valid ? A.order[tl] : 0;
+            const int dl = valid ? A.diag[il] : 0, q1l = valid ? A.indptr[il + 1] : 0, u0l = valid ? A.uptr[il] : 0;
+            const int nnl = valid ? q1l - dl - 1 : 0;
+            int coll[MAXD];
+            unsigned kml = 0;
+#pragma unroll
+            for (int m = 0; m < MAXD; ++m) {
+                coll[m] = 0;
+                if (m < nnl) { coll[m] = A.indices[dl + 1 + m]; kml |= (A.keep[dl + 1 + m] ? 1u : 0u) << m; }
+            }
+            for (int bt = 0; bt < 32 && tb + bt < tend; ++bt) {
+                const int t = tb + bt;
+                const int64_t i = __shfl_sync(0xffffffffu, il, bt);
+                const int d = __shfl_sync(0xffffffffu, dl, bt), nn = __shfl_sync(0xffffffffu, nnl, bt);
+                const int u0 = __shfl_sync(0xffffffffu, u0l, bt);
+                unsigned km = __shfl_sync(0xffffffffu, kml, bt);
+                int col[MAXD];
+#pragma unroll
+                for (int m = 0; m < MAXD; ++m) col[m] = __shfl_sync(0xffffffffu, coll[m], bt);
+                if (nn > MAXD) {
+                    km = 0;
+                    for (int m = 0; m < nn && m < 32; ++m) km |= (A.keep[d + 1 + m] ? 1u : 0u) << m;
+                }
+                auto colm = [&](int m) -> int64_t {
+                    if (m < MAXD) {
+                        int v = 0;
+#pragma unroll
+                        for (int mm = 0; mm < MAXD; ++mm) v = (mm == m) ? col[mm] : v;
+                        return v;
+                    }
+                    return A.indices[d + 1 + m];
+                };
+                auto kept = [&](int m) -> bool { return m < 32 ? ((km >> m) & 1u) : A.keep[d + 1 + m] != 0; };
+                int nu = 0;
+                for (int m = 0; m < nn; ++m) nu += kept(m) ? (A.u_shared ? 1 : S) : 0;
+                const int ntot = nu + S;
+                auto push_items = [&](int from, int to) {
+                    int n = 0;
+                    for (int m = 0; m < nn; ++m) {
+                        if (!kept(m)) continue;
+                        const int qq = d + 1 + m;
+                        if (A.u_shared) {
+                            if (n >= from && n < to)
+                                pr.push(make_int4(t, m * S, PD_USH | (n == 0 ? PD_FIRST : 0), 0), A.ubase[0] + qq * bsz);
+                            ++n;
+                        } else {
+                            for (int k = 0; k < S; ++k, ++n) {
+                                if (n < from || n >= to) continue;
+                                const double* ub = A.U ? A.U + ((int64_t)(u0 + m) * S + k) * bsz : A.ubase[k] + qq * bsz;
+                                pr.push(make_int4(t, m * S + k, PD_U | (n == 0 ? PD_FIRST : 0), 0), ub);
+                            }
+                        }
+                    }
+                    for (int k = 0; k < S; ++k, ++n) {
+                        if (n < from || n >= to) continue;
+                        const int fl = PD_DINV | (n == 0 ? PD_FIRST : 0) | (k == S - 1 ? PD_LAST : 0);
+                        pr.push(make_int4(t, k, fl, nu == 0 ? 1 : 0), A.Dinv + (i * S + k) * bsz);
+                    }
+                };
+                const int npre = DEPS ? min(ntot, PC.nst - 1) : 0;
+                double* xs = nullptr;
+                int xb = 0;
+                if (lane == 0) {
+                    xs = pr.x_acquire();
+                    xb = pr.xb;
+                    push_items(0, npre);
+                }
+                if (DEPS)
+                    for (int m = lane; m < nn; m += 32)
+                        if (kept(m)) wait_flag(A.flags + colm(m), A.epoch);
+                __syncwarp();
+                uint32_t bytes = S * seg;
+                for (int m = 0; m < nn; ++m) bytes += kept(m) ? S * seg : 0;
+                if (lane == 0) {
+                    if (DEPS) fence_proxy_async_global();
+                    pr.x_commit(bytes);
+                }
+                xs = reinterpret_cast<double*>(__shfl_sync(0xffffffffu, reinterpret_cast<uintptr_t>(xs), 0));
+                xb = __shfl_sync(0xffffffffu, xb, 0);
+                __syncwarp();
+                for (int e = lane; e < (nn + 1) * S; e += 32) {
+                    const int m = e / S, k = e - m * S;
+                    if (m == nn) bulk_g2s(xs + e * nb, A.x + k * A.n + i * nb, seg, P.xfull + xb);
+                    else if (kept(m)) bulk_g2s(xs + e * nb, A.x + k * A.n + colm(m) * nb, seg, P.xfull + xb);
+                }
+                if (lane == 0) push_items(npre, ntot);
+                if (lane == 0) pr.x_next();
+            }
+        }
+        if (lane == 0) pr.push(make_int4(-1, 0, PD_END, 0), nullptr);
+        return;
+    }
+    const int c = threadIdx.x - 32;
+    Geo q;
+    q.nb = nb; q.P = (nb + 1) >> 1; q.G = A.G_; q.g = c / nb; q.a = c - q.g * nb; q.active = q.g < q.G;
+    Consumer cs{&P, &PC};
+    double part[S];
+    const double* xs = nullptr;
+    for (;;) {
+        const int4 dsc = cs.take();
+        if (dsc.z & PD_END) break;
+        const int64_t i = A.order[dsc.x];
+        const int nup = A.indptr[i + 1] - A.diag[i] - 1;
+        if (dsc.z & PD_FIRST) {
+#pragma unroll
+            for (int k = 0; k < S; ++k) part[k] = 0.0;
+            xs = cs.x_wait();
+        }
+        const double2* B = cs.block();
+        if (dsc.z & PD_USH) {
+            if (q.active) {
+                const int m = dsc.y / S;
+#pragma unroll
+                for (int k = 0; k < S; ++k) part[k] = smem_gemv(B, xs + (m * S + k) * nb, q, part[k]);
+            }
+        } else if (dsc.z & PD_U) {
+            if (q.active) {
+                const int m = dsc.y / S, kk = dsc.y - m * S;
+#pragma unroll
+                for (int k = 0; k < S; ++k)
+                    if (k == kk) part[k] = smem_gemv(B, xs + (m * S + k) * nb, q, part[k]);
+            }
+        } else {  // Dinv item k
+            const int kk = dsc.y;
+            const bool no_upper = (dsc.z & PD_FIRST) || (dsc.w & 1);
+            if (kk == 0 && no_upper) {
+                // no kept upper neighbour: t = z_i, read straight from the x slot
+#pragma unroll
+                for (int k = 0; k < S; ++k) part[k] = 0.0;
+            } else if (kk == 0) {
+                // t_k = z_{i,k} - uscale * sum_j U_ij x_{j,k}  (all stages)
+                if (q.active)
+#pragma unroll
+                    for (int k = 0; k < S; ++k) P.red[(q.g * S + k) * nb + q.a] = part[k];
+                consumer_sync(1, ncons);
+                if (q.active && q.g == 0) {
+#pragma unroll
+                    for (int k = 0; k < S; ++k) {
+                        double sum = 0.0;
+                        for (int gg = 0; gg < q.G; ++gg) sum += P.red[(gg * S + k) * nb + q.a];
+                        P.tv[k * nb + q.a] = xs[(nup * S + k) * nb + q.a] - A.uscale * sum;
+                    }
+                }
+                consumer_sync(1, ncons);
+#pragma unroll
+                for (int k = 0; k < S; ++k) part[k] = 0.0;
+            }
+            if (q.active) {
+                const bool direct = (dsc.w & 1) != 0;
+#pragma unroll
+                for (int k = 0; k < S; ++k)
+                    if (k == kk)
+                        part[k] = smem_gemv(B, direct ? xs + (nup * S + k) * nb : P.tv + k * nb, q, part[k]);
+            }
+        }
+        cs.release();
+        if (dsc.z & PD_LAST) {
+            if (q.active)
+#pragma unroll
+                for (int k = 0; k < S; ++k) P.red[(q.g * S + k) * nb + q.a] = part[k];
+            consumer_sync(1, ncons);
+            if (q.active && q.g == 0) {
+#pragma unroll
+                for (int k = 0; k < S; ++k) {
+                    double sum = 0.0;
+                    for (int gg = 0; gg < q.G; ++gg) sum += P.red[(gg * S + k) * nb + q.a];
+                    A.x[k * A.n + i * nb + q.a] = sum;
+                }
+            }
+            cs.x_release();
+            consumer_sync(1, ncons);
+            if (DEPS && c == 0) {
+                __threadfence();
+                st_release(A.flags + i, A.epoch);
+            }
+        }
+    }
+}
+
+// Few levels (mesh-colouring schedule): one launch per level, static task
+// slices, no flags.  Many levels (e.g. natural numbering): one persistent
+// launch with tickets and dependency flags.
+constexpr int64_t LEVEL_LAUNCH_MAX = 16;
+
+template <typename K1, typename K2>
+static int run_pipe(const irk_factor* f, K1 kernel_deps, K2 kernel_level, ApplyArgs& A, const irk_sched& S,
+                    unsigned* flags, int* ticket, int s, cudaStream_t st) {
+    A.flags = flags;
+    A.ticket = ticket;
+    const int nb = A.nb;
+    PipeCfg PC;
+    PC.block_bytes = (int)(block_doubles(nb) * 8);
+    PC.stage_bytes = (PC.block_bytes + 127) & ~127;
+    PC.maxdeg = f->maxdeg;
+    PC.xslot_doubles = (((PC.maxdeg + 1) * s * nb) + 15) & ~15;
+    const int threads = 32 + ((A.G_ * nb + 31) / 32) * 32;
+    const size_t fixed = sizeof(double) * (2 * (size_t)PC.xslot_doubles + (size_t)A.G_ * s * nb + (size_t)s * nb) +
+                         4 * sizeof(uint64_t);
+    const size_t budget = 104 * 1024;
+    const size_t per_stage = PC.stage_bytes + 2 * sizeof(uint64_t) + sizeof(int4);
+    PC.nst = (int)std::max<size_t>(2, std::min<size_t>(24, (budget - std::min(budget / 2, fixed)) / per_stage));
+    const size_t smem = (size_t)PC.nst * per_stage + fixed;
+    const bool level_mode = S.nlevels <= LEVEL_LAUNCH_MAX;
+    int per_sm = 1;
+    if (level_mode) {
+        IRK_CK(cudaFuncSetAttribute(kernel_level, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)f->ctx->smem_optin));
+        IRK_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel_level, threads, smem));
+        for (int64_t l = 0; l < S.nlevels; ++l) {
+            const int64_t lo = S.h_lvl_ptr[l], hi = S.h_lvl_ptr[l + 1];
+            if (hi == lo) continue;
+            A.order = S.d_order + lo;
+            A.ntasks = hi - lo;
+            const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((A.ntasks + 1) / 2,
+                                                                        (int64_t)f->ctx->num_sms * std::max(per_sm, 1)));
+            kernel_level<<<grid, threads, smem, st>>>(A, PC);
+            IRK_LAUNCHED();
+        }
+        return IRK_OK;
+    }
+    A.order = S.d_order;
+    A.ntasks = S.h_lvl_ptr.empty() ? 0 : S.h_lvl_ptr.back();
+    IRK_CK(cudaFuncSetAttribute(kernel_deps, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)f->ctx->smem_optin));
+    IRK_CK(cudaMemsetAsync(ticket, 0, sizeof(int), st));
+    IRK_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel_deps, threads, smem));
+    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(A.ntasks, (int64_t)f->ctx->num_sms * std::max(per_sm, 1)));
+    kernel_deps<<<grid, threads, smem, st>>>(A, PC);
+    IRK_LAUNCHED();
+    return IRK_OK;
+}
+
 // one persistent launch per sweep direction
 template <typename K>
 static int run_sweep(const irk_factor* f, K kernel, ApplyArgs& A, const irk_sched& S, unsigned* flags,
@@ -305,6 +883,13 @@ static int run_sweep(const irk_factor* f, K kernel, ApplyArgs& A, const irk_sche
 
 template <int S, bool EVEN>
 static int unc_apply(const irk_factor* f, ApplyArgs& A, cudaStream_t st) {
+    if (EVEN && S <= 4 && A.G_ * A.nb <= 256) {
+        const int64_t nf = (int64_t)f->pat->T;
+        IRK_TRY(run_pipe(f, k_unc_fwd_pipe<S, true>, k_unc_fwd_pipe<S, false>, A, f->fwd, f->d_flags, f->d_ticket, S, st));
+        IRK_TRY(run_pipe(f, k_unc_bwd_pipe<S, true>, k_unc_bwd_pipe<S, false>, A, f->bwd, f->d_flags + nf,
+                         f->d_ticket + 1, S, st));
+        return IRK_OK;
+    }
     const int threads = ((A.G_ * A.nb + 31) / 32) * 32;
     const size_t smem_f = sizeof(double) * A.G_ * S * A.nb;
     const size_t smem_b = smem_f + sizeof(double) * S * A.nb;

@@ -559,6 +559,15 @@ static int build_sched(irk_sched& S, const std::vector<int64_t>& lev, int64_t T,
 // tasks on stage-skewed levels
 int build_apply_schedules(irk_factor* f, const std::vector<uint8_t>& keep) {
     std::vector<int64_t> levf, levb;
+    {
+        const irk_pattern* p = f->pat;
+        int md = 0;
+        for (int64_t i = 0; i < p->T; ++i) {
+            md = std::max<int>(md, (int)(p->h_diag[i] - p->h_indptr[i]));
+            md = std::max<int>(md, (int)(p->h_indptr[i + 1] - p->h_diag[i] - 1));
+        }
+        f->maxdeg = md;
+    }
     levels_forward(f->pat, keep, levf);
     levels_backward(f->pat, keep, levb);
     const bool cpl = f->kind == IRK_FACTOR_COUPLED;

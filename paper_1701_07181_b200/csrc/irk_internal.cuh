@@ -137,6 +137,7 @@ struct irk_factor {
     unsigned* d_flags = nullptr;
     int* d_ticket = nullptr;
     mutable unsigned epoch = 0;
+    int maxdeg = 0;                   // max lower/upper neighbours of a row
     // numeric factorisation state (re-run by irk_factor_refactor)
     void* fargs = nullptr;            // FactorArgs (factor.cu)
     irk_sched fsched;                 // factor tasks by level

@@ -10,6 +10,7 @@
 
 #include "blockops.cuh"
 #include "irk_internal.cuh"
+#include "pipeline.cuh"
 
 namespace irk {
 
@@ -86,6 +87,205 @@ __global__ void __launch_bounds__(512) k_stage_matvec(MatvecArgs A, MixParams C)
     }
 }
 
+// ---------------------------------------------------------------------------
+// Warp-specialised bulk-copy pipeline version (nb even, all rows).
+// Warp 0 lane 0 is the producer: for the CTA's contiguous row range it streams
+// every block of the row (J blocks in pattern order, then M_i) together with
+// the x segments that block multiplies (s segments of nb doubles) into a ring
+// of shared-memory stages with cp.async.bulk, completing on the stage's full
+// mbarrier.  Warps 1.. are consumers: thread (g, a) multiplies row a of the
+// staged block with the staged x pairs of its column pairs p = g (mod G) --
+// 128-bit conflict-free LDS for the block, broadcast LDS for x -- and releases
+// the stage on its empty mbarrier.  Row ends reduce the G groups through
+// shared memory under a consumer-only named barrier.
+// ---------------------------------------------------------------------------
+struct PipeGeom {
+    int nst;            // stages
+    int stage_bytes;    // block + x segments, 128-B aligned
+    int block_bytes;
+    int seg_bytes;      // nb * 8
+    int nseg;           // x segments per item (S shared, 1 distinct)
+};
+
+template <int S, bool SHARED>
+__global__ void __launch_bounds__(288) k_stage_matvec_pipe(MatvecArgs A, MixParams C, PipeGeom PG) {
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    unsigned char* stages = smem_raw;
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem_raw + (size_t)PG.nst * PG.stage_bytes);
+    uint64_t* empty = full + PG.nst;
+    double* red = reinterpret_cast<double*>(empty + PG.nst);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int ncons_warps = (blockDim.x >> 5) - 1;
+    const int64_t T = A.T_local;
+    const int64_t r0 = T * blockIdx.x / gridDim.x, r1 = T * (blockIdx.x + 1) / gridDim.x;
+    if (threadIdx.x == 0) {
+        for (int i = 0; i < PG.nst; ++i) {
+            mbar_init(full + i, 1);
+            mbar_init(empty + i, ncons_warps);
+        }
+        fence_mbar_init();
+    }
+    __syncthreads();
+    const int nb = A.nb;
+    const int64_t bsz = (int64_t)PG.block_bytes / 8;
+    if (warp == 0) {
+        if (lane == 0) {
+            int st = 0;
+            uint32_t ph = 0;
+            auto push = [&](const double* blk, const double* const* segs, int nseg) {
+                mbar_wait(empty + st, ph ^ 1);
+                unsigned char* dst = stages + (size_t)st * PG.stage_bytes;
+                mbar_expect_tx(full + st, PG.block_bytes + nseg * PG.seg_bytes);
+                bulk_g2s(dst, blk, PG.block_bytes, full + st);
+                for (int r = 0; r < nseg; ++r)
+                    bulk_g2s(dst + PG.block_bytes + r * PG.seg_bytes, segs[r], PG.seg_bytes, full + st);
+                if (++st == PG.nst) { st = 0; ph ^= 1; }
+            };
+            for (int64_t i = r0; i < r1; ++i) {
+                const int q0 = A.indptr[i], q1 = A.indptr[i + 1];
+                for (int qq = q0; qq < q1; ++qq) {
+                    const int64_t col = A.indices[qq];
+                    const double* xs[S];
+#pragma unroll
+                    for (int r = 0; r < S; ++r)
+                        xs[r] = col < A.T_local ? A.w + r * A.n + col * nb
+                                                : A.ghost + (r * A.n_ghost + (col - A.T_local)) * nb;
+                    if (SHARED) {
+                        push(A.J[0] + qq * bsz, xs, S);
+                    } else {
+#pragma unroll
+                        for (int r = 0; r < S; ++r) push(A.J[r] + qq * bsz, xs + r, 1);
+                    }
+                }
+                if (A.M) {
+                    const double* xs[S];
+#pragma unroll
+                    for (int r = 0; r < S; ++r) xs[r] = A.w + r * A.n + i * nb;
+                    push(A.M + i * bsz, xs, S);
+                }
+            }
+        }
+        return;
+    }
+    // ---- consumers
+    const int c = threadIdx.x - 32;
+    Geo q;
+    q.nb = nb;
+    q.P = (nb + 1) >> 1;
+    q.G = A.G;
+    q.g = c / nb;
+    q.a = c - q.g * nb;
+    q.active = q.g < q.G;
+    const int ncons = ncons_warps * 32;
+    int st = 0;
+    uint32_t ph = 0;
+    auto consume = [&](auto&& fn) {
+        mbar_wait(full + st, ph);
+        const unsigned char* base = stages + (size_t)st * PG.stage_bytes;
+        if (q.active) fn(reinterpret_cast<const double2*>(base),
+                         reinterpret_cast<const double*>(base + PG.block_bytes));
+        __syncwarp();
+        if (lane == 0) mbar_arrive(empty + st);
+        if (++st == PG.nst) { st = 0; ph ^= 1; }
+    };
+    for (int64_t i = r0; i < r1; ++i) {
+        double part[2 * S];
+#pragma unroll
+        for (int v = 0; v < 2 * S; ++v) part[v] = 0.0;
+        const int q0 = A.indptr[i], q1 = A.indptr[i + 1];
+        for (int qq = q0; qq < q1; ++qq) {
+            if (SHARED) {
+                consume([&](const double2* B, const double* X) {
+                    for (int p = q.g; p < q.P; p += q.G) {
+                        const double2 b = B[p * nb + q.a];
+#pragma unroll
+                        for (int r = 0; r < S; ++r) {
+                            const double2 x = *reinterpret_cast<const double2*>(X + r * nb + 2 * p);
+                            part[r] = fma(b.x, x.x, part[r]);
+                            part[r] = fma(b.y, x.y, part[r]);
+                        }
+                    }
+                });
+            } else {
+#pragma unroll
+                for (int r = 0; r < S; ++r)
+                    consume([&](const double2* B, const double* X) {
+                        for (int p = q.g; p < q.P; p += q.G) {
+                            const double2 b = B[p * nb + q.a];
+                            const double2 x = *reinterpret_cast<const double2*>(X + 2 * p);
+                            part[r] = fma(b.x, x.x, part[r]);
+                            part[r] = fma(b.y, x.y, part[r]);
+                        }
+                    });
+            }
+        }
+        if (A.M)
+            consume([&](const double2* B, const double* X) {
+                for (int p = q.g; p < q.P; p += q.G) {
+                    const double2 b = B[p * nb + q.a];
+#pragma unroll
+                    for (int r = 0; r < S; ++r) {
+                        const double2 x = *reinterpret_cast<const double2*>(X + r * nb + 2 * p);
+                        part[S + r] = fma(b.x, x.x, part[S + r]);
+                        part[S + r] = fma(b.y, x.y, part[S + r]);
+                    }
+                }
+            });
+        // reduce the G groups (consumer-only named barrier 1)
+        if (q.active)
+#pragma unroll
+            for (int v = 0; v < 2 * S; ++v) red[(q.g * 2 * S + v) * nb + q.a] = part[v];
+        consumer_sync(1, ncons);
+        if (q.active && q.g == 0) {
+            double tot[2 * S];
+#pragma unroll
+            for (int v = 0; v < 2 * S; ++v) {
+                double sum = 0.0;
+                for (int gg = 0; gg < q.G; ++gg) sum += red[(gg * 2 * S + v) * nb + q.a];
+                tot[v] = sum;
+            }
+#pragma unroll
+            for (int k = 0; k < S; ++k) {
+                double acc = A.alpha * tot[k];
+                if (A.M) {
+#pragma unroll
+                    for (int l = 0; l < S; ++l) acc += C.c[k * S + l] * tot[S + l];
+                }
+                A.y[k * A.n + i * nb + q.a] = acc;
+            }
+        }
+        consumer_sync(1, ncons);
+    }
+}
+
+template <int S, bool SHARED>
+static int launch_pipe(const irk_stage_op* op, MatvecArgs& A, const MixParams& C, cudaStream_t st) {
+    const int nb = A.nb;
+    PipeGeom PG;
+    PG.block_bytes = (int)(block_doubles(nb) * 8);
+    PG.seg_bytes = nb * 8;
+    PG.nseg = SHARED ? S : 1;
+    PG.stage_bytes = ((PG.block_bytes + PG.nseg * PG.seg_bytes) + 127) & ~127;
+    const int cons_threads = ((A.G * nb + 31) / 32) * 32;
+    const int threads = 32 + cons_threads;
+    const size_t red_bytes = sizeof(double) * A.G * 2 * S * nb;
+    const size_t budget = 100 * 1024;
+    PG.nst = (int)std::max<size_t>(2, std::min<size_t>(16, (budget - red_bytes) / PG.stage_bytes));
+    const size_t smem = (size_t)PG.nst * PG.stage_bytes + 2 * sizeof(uint64_t) * PG.nst + red_bytes;
+    static bool attr = false;
+    if (!attr) {
+        IRK_CK(cudaFuncSetAttribute(k_stage_matvec_pipe<S, SHARED>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    (int)std::min<size_t>(op->ctx->smem_optin, 200 * 1024)));
+        attr = true;
+    }
+    int per_sm = 1;
+    IRK_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_stage_matvec_pipe<S, SHARED>, threads, smem));
+    const int64_t grid = std::max<int64_t>(1, std::min<int64_t>(A.T_local, (int64_t)op->ctx->num_sms * std::max(per_sm, 1)));
+    k_stage_matvec_pipe<S, SHARED><<<(int)grid, threads, smem, st>>>(A, C, PG);
+    IRK_LAUNCHED();
+    return IRK_OK;
+}
+
 int choose_groups(int nb, int max_threads) {
     const int P = (nb + 1) / 2;
     int best = 1;
@@ -117,6 +317,8 @@ static int launch_t(const irk_stage_op* op, MatvecArgs& A, const MixParams& C, c
 template <int S>
 static int launch_s(const irk_stage_op* op, MatvecArgs& A, const MixParams& C, cudaStream_t st) {
     const bool even = (A.nb % 2) == 0;
+    if (even && A.rows == nullptr && S <= 4 && A.G * A.nb <= 256)
+        return op->shared_j ? launch_pipe<S, true>(op, A, C, st) : launch_pipe<S, false>(op, A, C, st);
     if (op->shared_j) return even ? launch_t<S, true, true>(op, A, C, st) : launch_t<S, true, false>(op, A, C, st);
     return even ? launch_t<S, false, true>(op, A, C, st) : launch_t<S, false, false>(op, A, C, st);
 }
