@@ -97,44 +97,44 @@ __device__ void load_Bs(double* Bs, const double* __restrict__ B, double scale, 
     }
 }
 
+// Block products on the FP64 tensor cores: mma.sync.m8n8k4.f64 (DMMA).
+// The padded block (F.nbp4, a multiple of 8) is cut into 8x8 output tiles;
+// warp w owns tiles w, w+8, ... (MAXT per warp).  Fragment layout of
+// m8n8k4.f64: A[r=lane/4][k=lane%4], B[k=lane%4][c=lane/4],
+// C[r=lane/4][c=2*(lane%4)+{0,1}].
 template <int MAXT>
 struct Tiles {
-    double acc[MAXT][4][4];
+    double acc[MAXT][2];
     __device__ void zero() {
 #pragma unroll
-        for (int t = 0; t < MAXT; ++t)
-#pragma unroll
-            for (int x = 0; x < 4; ++x)
-#pragma unroll
-                for (int y = 0; y < 4; ++y) acc[t][x][y] = 0.0;
+        for (int t = 0; t < MAXT; ++t) acc[t][0] = acc[t][1] = 0.0;
     }
 };
 
-// acc(tile) += At[c][a0..a0+3] (x) Bs[c][b0..b0+3] for c < kc.
-// AT points at row 0 of the A operand's k-range (k-major, ld).
+__device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b) {
+    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
+                 : "+d"(c0), "+d"(c1) : "d"(a), "d"(b));
+}
+
+// acc(tile) += A(tile rows, k) B(k, tile cols) for k < kc (kc % 4 == 0);
+// AT / BS are k-major with leading dimension ld.
 template <int MAXT>
 __device__ __forceinline__ void mma_chunk(Tiles<MAXT>& T, const double* AT, const double* BS,
                                           int kc, const FactorArgs& F) {
-    const int tpr = F.nbp4 >> 2;  // tiles per row
+    const int tpr = F.nbp4 >> 3;
     const int ntile = tpr * tpr;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int nw = blockDim.x >> 5;
+    const int fr = lane >> 2, fk = lane & 3;
 #pragma unroll
     for (int t = 0; t < MAXT; ++t) {
-        const int tile = threadIdx.x + t * blockDim.x;
+        const int tile = warp + t * nw;
         if (tile >= ntile) break;
-        const int a0 = (tile / tpr) * 4, b0 = (tile % tpr) * 4;
-#pragma unroll 4
-        for (int c = 0; c < kc; ++c) {
-            const double2 a01 = *reinterpret_cast<const double2*>(AT + c * F.ld + a0);
-            const double2 a23 = *reinterpret_cast<const double2*>(AT + c * F.ld + a0 + 2);
-            const double2 b01 = *reinterpret_cast<const double2*>(BS + c * F.ld + b0);
-            const double2 b23 = *reinterpret_cast<const double2*>(BS + c * F.ld + b0 + 2);
-            const double av[4] = {a01.x, a01.y, a23.x, a23.y};
-            const double bv[4] = {b01.x, b01.y, b23.x, b23.y};
-#pragma unroll
-            for (int x = 0; x < 4; ++x)
-#pragma unroll
-                for (int y = 0; y < 4; ++y) T.acc[t][x][y] = fma(av[x], bv[y], T.acc[t][x][y]);
-        }
+        const int r0 = (tile / tpr) * 8, c0 = (tile % tpr) * 8;
+        const double* ap = AT + fk * F.ld + r0 + fr;
+        const double* bp = BS + fk * F.ld + c0 + fr;
+#pragma unroll 5
+        for (int k = 0; k < kc; k += 4) dmma(T.acc[t][0], T.acc[t][1], ap[k * F.ld], bp[k * F.ld]);
     }
 }
 
@@ -194,17 +194,17 @@ __device__ void gemm_lt(Tiles<MAXT>& T, const double* B, double sb, Smem& S, con
 
 template <int MAXT, typename Fn>
 __device__ __forceinline__ void for_tiles(Tiles<MAXT>& T, const FactorArgs& F, Fn fn) {
-    const int tpr = F.nbp4 >> 2;
+    const int tpr = F.nbp4 >> 3;
     const int ntile = tpr * tpr;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int nw = blockDim.x >> 5;
 #pragma unroll
     for (int t = 0; t < MAXT; ++t) {
-        const int tile = threadIdx.x + t * blockDim.x;
+        const int tile = warp + t * nw;
         if (tile >= ntile) break;
-        const int a0 = (tile / tpr) * 4, b0 = (tile % tpr) * 4;
-#pragma unroll
-        for (int x = 0; x < 4; ++x)
-#pragma unroll
-            for (int y = 0; y < 4; ++y) fn(a0 + x, b0 + y, T.acc[t][x][y]);
+        const int r = (tile / tpr) * 8 + (lane >> 2), c = (tile % tpr) * 8 + 2 * (lane & 3);
+        fn(r, c, T.acc[t][0]);
+        fn(r, c + 1, T.acc[t][1]);
     }
 }
 
@@ -696,10 +696,11 @@ static int factor_numeric(irk_factor* f, int64_t* fail_stage, int64_t* fail_elem
     }
     int rc = IRK_OK;
     switch (f->maxt) {
-        case 1: rc = launch_levels<1>(f, F, f->fsched, f->fsmem, st); break;
         case 2: rc = launch_levels<2>(f, F, f->fsched, f->fsmem, st); break;
-        case 3: rc = launch_levels<3>(f, F, f->fsched, f->fsmem, st); break;
         case 4: rc = launch_levels<4>(f, F, f->fsched, f->fsmem, st); break;
+        case 8: rc = launch_levels<8>(f, F, f->fsched, f->fsmem, st); break;
+        case 16: rc = launch_levels<16>(f, F, f->fsched, f->fsmem, st); break;
+        case 32: rc = launch_levels<32>(f, F, f->fsched, f->fsmem, st); break;
         default: set_error("block size too large"); rc = IRK_EINVAL;
     }
     if (rc) return rc;
@@ -773,18 +774,19 @@ static int factor_common(irk_ctx* ctx, const irk_pattern* pat, const FactorSetup
     F.T = pat->T;
     F.s = P.s;
     F.nb = nb;
-    F.nbp4 = (nb + 3) & ~3;
-    F.ld = F.nbp4 + 2;
+    F.nbp4 = (nb + 7) & ~7;                        // padded to the 8x8 DMMA tile
+    F.ld = F.nbp4 + ((F.nbp4 % 16 == 0) ? 8 : 0);  // ld = 8 (mod 16): conflict-free fragments
     F.coupled = P.coupled;
     F.literal = P.literal;
     F.simplified = f->simplified;
     // shared memory budget: full D and L^T, K-chunked operand tiles
     F.KC = F.nbp4;
-    while (factor_smem(F.nbp4, F.ld, F.KC) > ctx->smem_optin && F.KC > 4) F.KC = std::max(4, F.KC / 2);
+    while (factor_smem(F.nbp4, F.ld, F.KC) > ctx->smem_optin && F.KC > 8) F.KC = std::max(8, ((F.KC / 2) + 7) & ~7);
     f->fsmem = factor_smem(F.nbp4, F.ld, F.KC);
     if (f->fsmem > ctx->smem_optin) { set_error("block size too large for shared memory"); return fail(IRK_EINVAL); }
-    const int tpr = F.nbp4 / 4;
-    f->maxt = (tpr * tpr + 255) / 256;
+    const int tpr = F.nbp4 / 8;
+    const int tiles_per_warp = (tpr * tpr + 7) / 8;
+    f->maxt = tiles_per_warp <= 2 ? 2 : tiles_per_warp <= 4 ? 4 : tiles_per_warp <= 8 ? 8 : tiles_per_warp <= 16 ? 16 : 32;
 #undef FCK
     rc = factor_numeric(f, fail_stage, fail_elem, st);
     if (rc < 0) return fail(rc);

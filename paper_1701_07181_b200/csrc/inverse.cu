@@ -31,7 +31,9 @@ struct InvArgs {
     unsigned long long* fail_key;
 };
 
-template <int NBT>
+// EXACT: nb == NBT -- the pivot loop is fully unrolled, so every register
+// index (column k, pivot column extraction) is a compile-time constant.
+template <int NBT, bool EXACT>
 __global__ void __launch_bounds__(128) k_inverse(InvArgs A) {
     constexpr int ROWS = (NBT + 31) / 32;
     constexpr int LDX = NBT + 1;
@@ -43,7 +45,7 @@ __global__ void __launch_bounds__(128) k_inverse(InvArgs A) {
     int* ibuf = reinterpret_cast<int*>(sm + (size_t)wpb * (NBT * LDX + NBT)) + warp * 2 * NBT;
     int* piv = ibuf;                                // pivot row of each step
     int* invp = ibuf + NBT;                         // inverse permutation
-    const int nb = A.nb;
+    const int nb = EXACT ? NBT : A.nb;
     const int P = (nb + 1) >> 1;
     const int64_t bsz = (int64_t)nb * 2 * P;
 
@@ -103,6 +105,7 @@ __global__ void __launch_bounds__(128) k_inverse(InvArgs A) {
         for (int s = 0; s < ROWS; ++s) { used[s] = (lane + 32 * s) >= nb; pstep[s] = -1; }
         double logdet = 0.0;
         int zero = 0;
+#pragma unroll(EXACT ? NBT : 1)
         for (int k = 0; k < nb; ++k) {
             // own entries of column k
             double ck[ROWS];
@@ -210,20 +213,20 @@ size_t inverse_smem(int nbt, int warps) {
     return (size_t)warps * (sizeof(double) * (nbt * (nbt + 1) + nbt) + sizeof(int) * 2 * nbt);
 }
 
-template <int NBT>
+template <int NBT, bool EXACT>
 static int launch_t(const irk_ctx* ctx, const InvArgs& A, cudaStream_t st) {
     const int warps = 4;
     const size_t smem = inverse_smem(NBT, warps);
     static bool attr = false;
     if (!attr) {
-        IRK_CK(cudaFuncSetAttribute(k_inverse<NBT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        IRK_CK(cudaFuncSetAttribute(k_inverse<NBT, EXACT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         attr = true;
     }
     int per_sm = 1;
-    IRK_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_inverse<NBT>, warps * 32, smem));
+    IRK_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_inverse<NBT, EXACT>, warps * 32, smem));
     const int64_t need = (A.ntasks + warps - 1) / warps;
     const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(need, (int64_t)ctx->num_sms * std::max(per_sm, 1)));
-    k_inverse<NBT><<<grid, warps * 32, smem, st>>>(A);
+    k_inverse<NBT, EXACT><<<grid, warps * 32, smem, st>>>(A);
     IRK_LAUNCHED();
     return IRK_OK;
 }
@@ -233,12 +236,12 @@ int launch_inverse(const irk_ctx* ctx, const int32_t* tasks, int64_t ntasks, int
                    const double* D, double* Dinv, unsigned long long* fail_key, cudaStream_t st) {
     if (ntasks <= 0) return IRK_OK;
     InvArgs A{tasks, ntasks, T, s, nb, D, Dinv, fail_key};
-    if (nb == 24) return launch_t<24>(ctx, A, st);
-    if (nb == 40) return launch_t<40>(ctx, A, st);
-    if (nb == 50) return launch_t<50>(ctx, A, st);
-    if (nb <= 16) return launch_t<16>(ctx, A, st);
-    if (nb <= 32) return launch_t<32>(ctx, A, st);
-    if (nb <= 64) return launch_t<64>(ctx, A, st);
+    if (nb == 24) return launch_t<24, true>(ctx, A, st);
+    if (nb == 40) return launch_t<40, true>(ctx, A, st);
+    if (nb == 50) return launch_t<50, true>(ctx, A, st);
+    if (nb <= 16) return launch_t<16, false>(ctx, A, st);
+    if (nb <= 32) return launch_t<32, false>(ctx, A, st);
+    if (nb <= 64) return launch_t<64, false>(ctx, A, st);
     return IRK_EINVAL;
 }
 
