@@ -16,10 +16,21 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <type_traits>
+#include <utility>
 
 #include "irk_internal.cuh"
 
 namespace irk {
+
+template <int K>
+__host__ __device__ constexpr int kval(std::integral_constant<int, K>) { return K; }
+__host__ __device__ constexpr int kval(int k) { return k; }
+
+template <class F, int... K>
+__device__ __forceinline__ void static_for(F&& f, std::integer_sequence<int, K...>) {
+    (f(std::integral_constant<int, K>{}), ...);
+}
 
 struct InvArgs {
     const int32_t* tasks;     // task codes k*T + j
@@ -105,8 +116,8 @@ __global__ void __launch_bounds__(128) k_inverse(InvArgs A) {
         for (int s = 0; s < ROWS; ++s) { used[s] = (lane + 32 * s) >= nb; pstep[s] = -1; }
         double logdet = 0.0;
         int zero = 0;
-#pragma unroll(EXACT ? NBT : 1)
-        for (int k = 0; k < nb; ++k) {
+        auto gj_step = [&](auto kc) {
+            const int k = kval(kc);
             // own entries of column k
             double ck[ROWS];
 #pragma unroll
@@ -156,22 +167,45 @@ __global__ void __launch_bounds__(128) k_inverse(InvArgs A) {
                 const bool is_p = (r == p);
                 if (is_p) { used[s] = 1; pstep[s] = k; }
                 const double f = ck[s];
+                if (EXACT) {
+                    // uniform row update new = a*P + g*old (no per-element select):
+                    // pivot row a = 1/p, g = 0; other rows a = -f/p, g = 1;
+                    // column k (static after unrolling) becomes a
+                    const double a = is_p ? inv : -f * inv;
+                    const double g = is_p ? 0.0 : 1.0;
 #pragma unroll
-                for (int c = 0; c < NBT; c += 2) {
-                    const double2 pc2 = *reinterpret_cast<const double2*>(prow + c);
-                    const double pcs[2] = {pc2.x, pc2.y};
+                    for (int c = 0; c < NBT; c += 2) {
+                        const double2 pc2 = *reinterpret_cast<const double2*>(prow + c);
+                        const double pcs[2] = {pc2.x, pc2.y};
 #pragma unroll
-                    for (int e = 0; e < 2 && c + e < NBT; ++e) {
-                        const int cc = c + e;
-                        const double sc = pcs[e] * inv;
-                        double v;
-                        if (is_p) v = (cc == k) ? inv : sc;
-                        else v = (cc == k) ? -f * inv : fma(-f, sc, d[s][cc]);
-                        d[s][cc] = v;
+                        for (int e = 0; e < 2 && c + e < NBT; ++e) {
+                            const int cc = c + e;
+                            d[s][cc] = (cc == k) ? a : fma(a, pcs[e], g * d[s][cc]);
+                        }
+                    }
+                } else {
+#pragma unroll
+                    for (int c = 0; c < NBT; c += 2) {
+                        const double2 pc2 = *reinterpret_cast<const double2*>(prow + c);
+                        const double pcs[2] = {pc2.x, pc2.y};
+#pragma unroll
+                        for (int e = 0; e < 2 && c + e < NBT; ++e) {
+                            const int cc = c + e;
+                            const double sc = pcs[e] * inv;
+                            double v;
+                            if (is_p) v = (cc == k) ? inv : sc;
+                            else v = (cc == k) ? -f * inv : fma(-f, sc, d[s][cc]);
+                            d[s][cc] = v;
+                        }
                     }
                 }
             }
             __syncwarp();
+        };
+        if constexpr (EXACT) {
+            static_for(gj_step, std::make_integer_sequence<int, NBT>{});   // k is a constant per step
+        } else {
+            for (int k = 0; k < nb; ++k) gj_step(k);
         }
         // ---- stage rows at their pivot step, then store inv(D)[k][c] = X[p_k][invp[c]]
 #pragma unroll
@@ -209,6 +243,213 @@ __global__ void __launch_bounds__(128) k_inverse(InvArgs A) {
     }
 }
 
+// ---------------------------------------------------------------------------
+// 32 < nb <= 64: one row per lane.  A CTA inverts G = 32 / (nb-32) blocks with
+// G "main" warps (rows 0..31 of block m in warp m) and one "extra" warp whose
+// lane l holds row 32 + l % E of block l / E (E = nb - 32).  Each pivot step
+// needs one CTA barrier: before it, every warp stages its best candidate row
+// (per block) in a double-buffered shared slot; after it, every lane picks the
+// winning candidate and reads the pivot row from the slot.  k is a compile-time
+// constant in every step (fully unrolled), so all register indices are static.
+// ---------------------------------------------------------------------------
+template <int NB>
+struct Inv2Cfg {
+    static constexpr int E = NB - 32;
+    static constexpr int G = (32 / E) < 4 ? (32 / E) : 4;
+    static constexpr int LDX = NB + 1;
+};
+
+template <int NB>
+__global__ void __launch_bounds__(32 * (Inv2Cfg<NB>::G + 1)) k_inverse2(InvArgs A) {
+    using C = Inv2Cfg<NB>;
+    constexpr int E = C::E, G = C::G, LDX = C::LDX;
+    constexpr int NBP = (NB + 1) & ~1;
+    extern __shared__ __align__(16) double sm2[];
+    // layout: cand[2 bufs][G blocks][2 owners][NBP] | Xs[G][NB][LDX] | cval,cidx[2][G][2] | piv/invp ints
+    double* cand = sm2;
+    double* Xs = cand + 2 * G * 2 * NBP;
+    double* cval = Xs + (size_t)G * NB * LDX;
+    int* cidx = reinterpret_cast<int*>(cval + 2 * G * 2);
+    int* pivs = cidx + 2 * G * 2;                     // [G][NB]
+    int* invp = pivs + G * NB;                        // [G][NB]
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const bool extra = warp == G;
+    // my block and row
+    const int blk = extra ? (lane / E) : warp;
+    const int row = extra ? (32 + lane % E) : lane;
+    const bool live = extra ? (lane < G * E) : true;
+    const int P = NB / 2;
+    const int64_t bsz = (int64_t)NB * 2 * ((NB + 1) / 2);
+    for (int64_t base = (int64_t)blockIdx.x * G; base < A.ntasks; base += (int64_t)gridDim.x * G) {
+        const int64_t t = base + blk;
+        const bool valid = live && t < A.ntasks;
+        int64_t code = 0, j = 0;
+        int k_st = 0;
+        if (valid) {
+            code = A.tasks[t];
+            k_st = (int)(code / A.T);
+            j = code - (int64_t)k_st * A.T;
+        }
+        double d[NB];
+        {
+            const double2* src = reinterpret_cast<const double2*>(A.D + (j * A.s + k_st) * bsz);
+#pragma unroll
+            for (int p = 0; p < (NB + 1) / 2; ++p) {
+                double2 v = make_double2(0.0, 0.0);
+                if (valid) v = src[(int64_t)p * NB + row];
+                d[2 * p] = v.x;
+                if (2 * p + 1 < NB) d[2 * p + 1] = v.y;
+            }
+        }
+        double* X = Xs + (size_t)blk * NB * LDX;
+        // |D|_1 via shared memory: every row stored, main-warp lanes sum columns
+        auto colnorm = [&](double* out_norm) {
+            if (live)
+#pragma unroll
+                for (int c = 0; c < NB; ++c) X[row * LDX + c] = fabs(d[c]);
+            __syncthreads();
+            if (!extra) {
+                double mx = -1.0;
+                int nan = 0;
+                for (int c = lane; c < NB; c += 32) {
+                    double sum = 0.0;
+                    for (int r = 0; r < NB; ++r) sum += X[r * LDX + c];
+                    if (sum != sum) nan = 1;
+                    mx = fmax(mx, sum);
+                }
+#pragma unroll
+                for (int o = 16; o; o >>= 1) {
+                    mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+                    nan |= __shfl_xor_sync(0xffffffffu, nan, o);
+                }
+                *out_norm = nan ? __longlong_as_double(0x7ff8000000000000LL) : mx;
+            }
+            __syncthreads();
+        };
+        double n1 = 0.0;
+        colnorm(&n1);
+        int used = live ? 0 : 1;
+        int pstep = -1;
+        double logdet = 0.0;
+        int zero = 0;
+        int* piv = pivs + blk * NB;
+        auto step = [&](auto kc) {
+            constexpr int k = decltype(kc)::value;
+            const int buf = k & 1;
+            // candidate of this warp for its block(s): max |d[k]| over unused rows
+            double best = used ? -1.0 : fabs(d[k]);
+            int br = used ? 0x7fffffff : row;
+            if (!extra) {
+#pragma unroll
+                for (int o = 16; o; o >>= 1) {
+                    const double ob = __shfl_xor_sync(0xffffffffu, best, o);
+                    const int orr = __shfl_xor_sync(0xffffffffu, br, o);
+                    if (ob > best || (ob == best && orr < br)) { best = ob; br = orr; }
+                }
+            } else {
+                // segmented reduction over the E lanes of each block (E-lane groups)
+#pragma unroll
+                for (int o = 16; o; o >>= 1) {
+                    const double ob = __shfl_xor_sync(0xffffffffu, best, o);
+                    const int orr = __shfl_xor_sync(0xffffffffu, br, o);
+                    const int ol = lane ^ o;
+                    const bool same = (ol / E == lane / E) && ol < G * E;
+                    if (same && (ob > best || (ob == best && orr < br))) { best = ob; br = orr; }
+                }
+                // the group leader holds the complete result (E need not be a power of 2)
+                const int leader = (lane / E) * E;
+                best = __shfl_sync(0xffffffffu, best, leader);
+                br = __shfl_sync(0xffffffffu, br, leader);
+            }
+            const int owner_slot = extra ? 1 : 0;
+            if (live && br == row) {   // I hold this warp's candidate row for my block
+                double* cr = cand + ((buf * G + blk) * 2 + owner_slot) * NBP;
+#pragma unroll
+                for (int c = 0; c < NB; c += 2)
+                    *reinterpret_cast<double2*>(cr + c) = make_double2(d[c], c + 1 < NB ? d[c + 1] : 0.0);
+            }
+            if (live && (extra ? (lane % E == 0) : (lane == 0))) {
+                cval[(buf * G + blk) * 2 + owner_slot] = best;
+                cidx[(buf * G + blk) * 2 + owner_slot] = br;
+            }
+            __syncthreads();
+            // winner: main rows have smaller indices, so ties go to the main candidate
+            const double v0 = cval[(buf * G + blk) * 2 + 0], v1 = cval[(buf * G + blk) * 2 + 1];
+            const int i0 = cidx[(buf * G + blk) * 2 + 0], i1 = cidx[(buf * G + blk) * 2 + 1];
+            const bool take1 = v1 > v0 || (v1 == v0 && i1 < i0);
+            int p = take1 ? i1 : i0;
+            if (p == 0x7fffffff) p = k;
+            const double* pr = cand + ((buf * G + blk) * 2 + (take1 ? 1 : 0)) * NBP;
+            const double pv = pr[k];
+            const double inv = 1.0 / pv;
+            if (!extra && lane == 0) {
+                logdet += log(fabs(pv));
+                if (pv == 0.0) zero = 1;
+                piv[k] = p;
+            }
+            const bool is_p = (row == p) && live;
+            if (is_p) { used = 1; pstep = k; }
+            const double a = is_p ? inv : -d[k] * inv;
+            const double g = is_p ? 0.0 : 1.0;
+#pragma unroll
+            for (int c = 0; c < NB; c += 2) {
+                const double2 pc = *reinterpret_cast<const double2*>(pr + c);
+                if (c == k) d[c] = a;
+                else d[c] = fma(a, pc.x, g * d[c]);
+                if (c + 1 < NB) {
+                    if (c + 1 == k) d[c + 1] = a;
+                    else d[c + 1] = fma(a, pc.y, g * d[c + 1]);
+                }
+            }
+        };
+        static_for(step, std::make_integer_sequence<int, NB>{});
+        __syncthreads();
+        // stage rows at their pivot step; inverse permutation; coalesced store
+        if (live && pstep >= 0)
+#pragma unroll
+            for (int c = 0; c < NB; ++c) X[pstep * LDX + c] = d[c];
+        if (!extra)
+            for (int m = lane; m < NB; m += 32) invp[blk * NB + piv[m]] = m;
+        __syncthreads();
+        if (valid) {
+            double2* dst = reinterpret_cast<double2*>(A.Dinv + (j * A.s + k_st) * bsz);
+            const int* ip = invp + blk * NB;
+            for (int p = 0; p < P; ++p)
+                dst[(int64_t)p * NB + row] = make_double2(X[row * LDX + ip[2 * p]], X[row * LDX + ip[2 * p + 1]]);
+        }
+        __syncthreads();
+        double n2 = 0.0;
+        colnorm(&n2);   // |inv|_1: column sums of the row-permuted X
+        if (!extra && lane == 0 && base + blk < A.ntasks) {
+            const double det = exp(logdet);
+            const double cond = n1 * n2;
+            const bool bad = zero || det == 0.0 || !isfinite(det) || !(cond <= 1e14);
+            if (bad) atomicMin(A.fail_key, (unsigned long long)A.tasks[base + blk]);
+        }
+    }
+}
+
+template <int NB>
+static int launch2(const irk_ctx* ctx, const InvArgs& A, cudaStream_t st) {
+    using C = Inv2Cfg<NB>;
+    constexpr int NBP = (NB + 1) & ~1;
+    const size_t smem = sizeof(double) * (2 * C::G * 2 * NBP + (size_t)C::G * NB * C::LDX + 2 * C::G * 2) +
+                        sizeof(int) * (2 * C::G * 2 + 2 * C::G * NB);
+    static bool attr = false;
+    if (!attr) {
+        IRK_CK(cudaFuncSetAttribute(k_inverse2<NB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        attr = true;
+    }
+    const int threads = 32 * (C::G + 1);
+    int per_sm = 1;
+    IRK_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_inverse2<NB>, threads, smem));
+    const int64_t need = (A.ntasks + C::G - 1) / C::G;
+    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(need, (int64_t)ctx->num_sms * std::max(per_sm, 1)));
+    k_inverse2<NB><<<grid, threads, smem, st>>>(A);
+    IRK_LAUNCHED();
+    return IRK_OK;
+}
+
 size_t inverse_smem(int nbt, int warps) {
     return (size_t)warps * (sizeof(double) * (nbt * (nbt + 1) + nbt) + sizeof(int) * 2 * nbt);
 }
@@ -237,8 +478,8 @@ int launch_inverse(const irk_ctx* ctx, const int32_t* tasks, int64_t ntasks, int
     if (ntasks <= 0) return IRK_OK;
     InvArgs A{tasks, ntasks, T, s, nb, D, Dinv, fail_key};
     if (nb == 24) return launch_t<24, true>(ctx, A, st);
-    if (nb == 40) return launch_t<40, true>(ctx, A, st);
-    if (nb == 50) return launch_t<50, true>(ctx, A, st);
+    if (nb == 40) return launch2<40>(ctx, A, st);
+    if (nb == 50) return launch2<50>(ctx, A, st);
     if (nb <= 16) return launch_t<16, false>(ctx, A, st);
     if (nb <= 32) return launch_t<32, false>(ctx, A, st);
     if (nb <= 64) return launch_t<64, false>(ctx, A, st);
