@@ -813,6 +813,21 @@ __global__ void __launch_bounds__(288) k_unc_bwd_pipe(ApplyArgs A, PipeCfg PC) {
     }
 }
 
+// x[k][i] = y[k][i] for the elements of a level with no kept lower neighbour
+// (forward sweep: z_i = y_i) -- a plain vectorised row copy.
+__global__ void k_copy_rows(const int32_t* __restrict__ rows, int64_t nrows, const double* __restrict__ y,
+                            double* __restrict__ x, int s, int nb, int64_t n) {
+    const int P = nb >> 1;   // nb even
+    const int64_t tot = (int64_t)s * nrows * P;
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < tot; e += (int64_t)gridDim.x * blockDim.x) {
+        const int p = (int)(e % P);
+        const int64_t rr = (e / P) % nrows;
+        const int k = (int)(e / ((int64_t)P * nrows));
+        const int64_t o = k * n + (int64_t)rows[rr] * nb + 2 * p;
+        *reinterpret_cast<double2*>(x + o) = *reinterpret_cast<const double2*>(y + o);
+    }
+}
+
 // Few levels (mesh-colouring schedule): one launch per level, static task
 // slices, no flags.  Many levels (e.g. natural numbering): one persistent
 // launch with tickets and dependency flags.
@@ -846,6 +861,13 @@ static int run_pipe(const irk_factor* f, K1 kernel_deps, K2 kernel_level, ApplyA
             if (hi == lo) continue;
             A.order = S.d_order + lo;
             A.ntasks = hi - lo;
+            if (l < (int64_t)S.h_trivial.size() && S.h_trivial[l]) {
+                const int64_t tot = (int64_t)s * A.ntasks * (nb / 2);
+                const int g = (int)std::max<int64_t>(1, std::min<int64_t>((tot + 255) / 256, (int64_t)f->ctx->num_sms * 16));
+                k_copy_rows<<<g, 256, 0, st>>>(A.order, A.ntasks, A.y, A.x, s, nb, A.n);
+                IRK_LAUNCHED();
+                continue;
+            }
             const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((A.ntasks + 1) / 2,
                                                                         (int64_t)f->ctx->num_sms * std::max(per_sm, 1)));
             kernel_level<<<grid, threads, smem, st>>>(A, PC);

@@ -573,6 +573,16 @@ int build_apply_schedules(irk_factor* f, const std::vector<uint8_t>& keep) {
     const bool cpl = f->kind == IRK_FACTOR_COUPLED;
     IRK_TRY(build_sched(f->fwd, levf, f->pat->T, f->s, cpl, +1));
     IRK_TRY(build_sched(f->bwd, levb, f->pat->T, f->s, cpl, -1));
+    if (!cpl) {
+        // forward levels whose elements have no kept lower block: z_i = y_i
+        const irk_pattern* p = f->pat;
+        std::vector<char> has(f->fwd.nlevels, 0);
+        for (int64_t i = 0; i < p->T; ++i)
+            for (int64_t q = p->h_indptr[i]; q < p->h_diag[i]; ++q)
+                if (keep[q]) has[levf[i]] = 1;
+        f->fwd.h_trivial.assign(f->fwd.nlevels, 0);
+        for (int64_t l = 0; l < f->fwd.nlevels; ++l) f->fwd.h_trivial[l] = !has[l];
+    }
     const int64_t nflags = 2 * (cpl ? (int64_t)f->s : 1) * f->pat->T;
     IRK_CK(cudaMalloc(&f->d_flags, sizeof(unsigned) * nflags));
     IRK_CK(cudaMemset(f->d_flags, 0, sizeof(unsigned) * nflags));

@@ -105,6 +105,7 @@ struct irk_sched {
     int64_t nlevels = 0;
     std::vector<int64_t> h_lvl_ptr;   // nlevels+1
     int32_t* d_order = nullptr;       // T elements in level order
+    std::vector<char> h_trivial;      // level has no kept off-diagonal dependency (fwd: z = y)
 };
 
 struct irk_factor {
