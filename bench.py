@@ -53,6 +53,8 @@ def parse():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--profile", action="store_true", help="timed steps only (for ncu)")
+    ap.add_argument("--partitioned", action="store_true",
+                    help="element-partitioned solve even at N=1 (always used for N>1)")
     return ap.parse_args()
 
 
@@ -480,6 +482,99 @@ def log(msg):
         print(f"[bench {time.strftime('%H:%M:%S')}] {msg}", file=sys.stderr, flush=True)
 
 
+def estimate_jnorm(cfg):
+    """||J||_2 for dt: exact power iteration on the GPU when the global J fits
+    comfortably on one rank (config 1), else on a reduced mesh of the same
+    generator (the norm of these random block matrices is nearly independent
+    of the mesh size: 2.4485 at 32x32 vs 2.4496 at 128x128 quads)."""
+    from paper_1701_07181_b200 import workloads as W
+    c = cfg if cfg.T <= 40000 else cfg.scaled(N=8 if cfg.mesh == "tet3d" else 32)
+    wl = W.make_workload(c.scaled(ordering="natural"), jnorm=1.0)
+    return jnorm_device(wl.pattern, wl.J), c.T
+
+
+def run_partitioned(args):
+    """Element-partitioned solve of one global system over all ranks:
+    contiguous slabs (colour-major inside each slab), NCCL halo exchange before
+    every operator application, allreduced inner products, partitioned
+    (communication-free) block ILU(0).  Strong scaling."""
+    import torch
+    world, rank, local = dist_env()
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    from paper_1701_07181_b200 import _lib as L
+    from paper_1701_07181_b200 import workloads as W
+    from paper_1701_07181_b200.distributed import DistributedStageSolver, SlabPlan
+    from paper_1701_07181_b200.krylov import GmresConfig
+    from paper_1701_07181_b200.tableau import builtin_tableau, derive
+    cfg = make_config(args)
+    P = world
+    pat, J, M, rhs_h = W.make_slab_workload(cfg, P, rank)
+    jnorm, norm_T = estimate_jnorm(cfg)
+    dt = cfg.dt_norm / jnorm
+    der = derive(builtin_tableau(cfg.scheme))
+    plan = SlabPlan.build(pat.indptr, pat.indices, pat.diag_pos, P, rank)
+    gcfg = GmresConfig(rel_tol=cfg.rtol, restart=cfg.restart, max_iters=cfg.max_iters)
+    sol = DistributedStageSolver(plan, J, M, der.a_inv, dt, cfg.precond, der.shifts, gcfg)
+    rhs = torch.from_numpy(rhs_h).cuda()
+    x = torch.empty_like(rhs)
+    stream = torch.cuda.current_stream()
+    log(f"rank {rank}: slab {plan.lo}..{plan.hi} ghosts {plan.n_ghost}")
+
+    def step():
+        sol.factorize()
+        return sol.solve(rhs, x=x)[1]
+
+    for _ in range(max(args.warmup, 0)):
+        st = step()
+    torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    clk = ClockSampler(local)
+    clk.start()
+    launches0 = L.lib().irk_launch_count()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ev0.record(stream)
+    iters = []
+    for _ in range(args.steps):
+        iters.append(step().iterations)
+    ev1.record(stream)
+    torch.cuda.synchronize()
+    launches = L.lib().irk_launch_count() - launches0
+    clocks = clk.stop()
+    t = ev0.elapsed_time(ev1) / 1e3
+    if dist:
+        tt = torch.tensor([t], device="cuda")
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        t = float(tt)
+    value = args.steps / t
+    if rank != 0:
+        if dist:
+            dist.barrier()
+        return
+    peak, peak_src = hbm_peak()
+    r = 3 if cfg.mesh == "tri2d" else 4
+    line = {
+        "metric": "IRK stage-solves/sec", "value": value, "unit": "stage-solves/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * t / args.steps,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded generators, no dataset; J std 1/nb)",
+        "config": dict(config_dict(cfg, args), parallelism=f"element-partitioned x{world} "
+                       "(NCCL halo send/recv + allreduce; partitioned block ILU(0))",
+                       jnorm_mesh_T=norm_T),
+        "gmres_iterations_mean": float(np.mean(iters)),
+        "roofline": None, "cpu_baseline": None, "e2e": None,
+        "gpu_launches": int(launches), "clocks": clocks,
+        "note": "roofline / cpu_baseline / e2e are reported by the N=1 run",
+    }
+    print(json.dumps(line), flush=True)
+    if dist:
+        dist.barrier()
+
+
 def main():
     import faulthandler
     faulthandler.enable()
@@ -488,6 +583,8 @@ def main():
     args = parse()
     if args.impl == "reference":
         run_reference(args)
+    elif dist_env()[0] > 1 or args.partitioned:
+        run_partitioned(args)
     else:
         run_b200(args)
 

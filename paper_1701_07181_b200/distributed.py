@@ -1,0 +1,273 @@
+"""Element-partitioned (multi-GPU) transformed stage solve.
+
+One process per GPU.  Elements are split into P contiguous index ranges
+(reference ``meshing.partition``, meshing.py:81-90; z-major numbering makes
+them slabs of the 3D cube).  Per GMRES iteration the ranks exchange:
+
+* the halo: stage values of the elements a neighbouring slab's Jacobian rows
+  touch (one grouped NCCL send/recv per peer, packed by an index gather), so
+  every rank can apply its rows of B = A^-1 (x) M - dt blkdiag(J);
+* the inner products of classical Gram-Schmidt and the norms (one allreduce of
+  the j+2 partial dots, one of the norm) -- issued from the native GMRES loop
+  through its allreduce callback.
+
+The preconditioner is the *partitioned* block ILU(0): blocks coupling two
+partitions are dropped (precond.py:26-45, the paper's parallel scheme,
+PAPER.md:694-699), so its factorisation and apply are purely local -- each rank
+factors the diagonal block of its slab.  The result equals the single-process
+solve with ``partition_of = partition(graph, P).partition_of``.
+
+``SlabPlan`` (index bookkeeping) and ``HaloExchange`` (torch.distributed
+send/recv) are device-agnostic and are exercised with the gloo backend on CPU
+in tests/test_distributed.py; ``DistributedStageSolver`` binds them to the
+CUDA kernels and NCCL.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+
+from .meshes import partition_bounds
+
+
+@dataclass
+class SlabPlan:
+    """Rank-local view of a CSR-of-blocks pattern under a contiguous partition.
+
+    Local element ids: 0..T_local-1 are the owned elements (global
+    lo..hi-1, same order); T_local.. are ghosts (neighbours owned by other
+    ranks), sorted by global id.
+    """
+
+    rank: int
+    P: int
+    T: int
+    lo: int
+    hi: int
+    ghosts: np.ndarray            # global ids of ghost elements
+    ext_indptr: np.ndarray        # local rows, columns in extended numbering
+    ext_indices: np.ndarray
+    ext_diag: np.ndarray
+    row_block_src: np.ndarray     # global block position of every local block
+    loc_indptr: np.ndarray        # local rows, local columns only (factor pattern)
+    loc_indices: np.ndarray
+    loc_diag: np.ndarray
+    loc_block_src: np.ndarray
+    q0: int                       # global position of the rank's first block
+    send: dict                    # peer -> local ids to send (ascending global id)
+    recv: dict                    # peer -> ghost slots to fill (ascending global id)
+    interior: tuple               # (r0, r1): rows with no ghost column
+
+    @property
+    def T_local(self) -> int:
+        return self.hi - self.lo
+
+    @property
+    def n_ghost(self) -> int:
+        return len(self.ghosts)
+
+    @classmethod
+    def build(cls, indptr, indices, diag_pos, P: int, rank: int) -> "SlabPlan":
+        indptr = np.asarray(indptr, dtype=np.int64)
+        indices = np.asarray(indices, dtype=np.int64)
+        T = len(indptr) - 1
+        bounds = partition_bounds(T, P)
+        owner = np.repeat(np.arange(P), np.diff(bounds))
+        lo, hi = int(bounds[rank]), int(bounds[rank + 1])
+        q0, q1 = int(indptr[lo]), int(indptr[hi])
+        cols = indices[q0:q1]
+        rows = np.repeat(np.arange(lo, hi), np.diff(indptr[lo:hi + 1]))
+        remote = (cols < lo) | (cols >= hi)
+        ghosts = np.unique(cols[remote])
+        # extended numbering: owned -> g - lo, ghost -> T_local + rank in ghosts
+        ext_cols = np.where(remote, (hi - lo) + np.searchsorted(ghosts, cols), cols - lo)
+        ext_indptr = indptr[lo:hi + 1] - q0
+        src = np.arange(q0, q1, dtype=np.int64)
+        # re-sort every row by extended column (ghost ids follow the owned ones)
+        order = np.lexsort((ext_cols, rows))
+        ext_cols, src, cols, rows, remote = ext_cols[order], src[order], cols[order], rows[order], remote[order]
+        ext_diag = np.empty(hi - lo, dtype=np.int64)
+        diag_hits = np.nonzero(ext_cols == rows - lo)[0]
+        ext_diag[rows[diag_hits] - lo] = diag_hits
+        # local factor pattern: drop the cross-partition blocks (they are not kept)
+        keepm = ~remote
+        loc_indices = (cols - lo)[keepm]
+        loc_src = src[keepm]
+        counts = np.add.reduceat(keepm.astype(np.int64), ext_indptr[:-1]) if hi > lo else np.zeros(0, np.int64)
+        loc_indptr = np.concatenate([[0], np.cumsum(counts)]).astype(np.int64)
+        loc_rows = rows[keepm] - lo
+        loc_diag = loc_indptr[:-1] + np.array(
+            [np.searchsorted(loc_indices[loc_indptr[i]:loc_indptr[i + 1]], i) for i in range(hi - lo)],
+            dtype=np.int64)
+        del loc_rows
+        # halo lists: what each peer needs from me / what I receive from each peer
+        recv = {}
+        gown = owner[ghosts]
+        for p in np.unique(gown):
+            recv[int(p)] = np.nonzero(gown == p)[0].astype(np.int64)
+        send = {}
+        for p in range(P):
+            if p == rank:
+                continue
+            plo, phi = int(bounds[p]), int(bounds[p + 1])
+            pc = indices[int(indptr[plo]):int(indptr[phi])]
+            need = np.unique(pc[(pc >= lo) & (pc < hi)])
+            if len(need):
+                send[p] = (need - lo).astype(np.int64)
+        # interior rows: rows whose columns are all owned (contiguous core when the
+        # numbering is slab-major; computed as the longest owned-only run)
+        has_remote = np.zeros(hi - lo, dtype=bool)
+        np.logical_or.at(has_remote, rows - lo, remote)
+        r0, r1 = _longest_false_run(has_remote)
+        return cls(rank, P, T, lo, hi, ghosts, ext_indptr, ext_cols.astype(np.int64), ext_diag, src,
+                   loc_indptr, loc_indices.astype(np.int64), loc_diag, loc_src, q0, send, recv, (r0, r1))
+
+
+def _longest_false_run(mask: np.ndarray) -> tuple[int, int]:
+    best = (0, 0)
+    start = None
+    for i, m in enumerate(list(mask) + [True]):
+        if not m and start is None:
+            start = i
+        elif m and start is not None:
+            if i - start > best[1] - best[0]:
+                best = (start, i)
+            start = None
+    return best
+
+
+class HaloExchange:
+    """Ghost exchange of stage-major vectors over torch.distributed.
+
+    ``exchange(x, ghost)``: x is the rank's (s, T_local, nb) vector (flat),
+    ghost the (s, n_ghost, nb) receive buffer.  One grouped batch of isend /
+    irecv per call (NCCL on GPU, gloo on CPU), packed with index_select.
+    """
+
+    def __init__(self, plan: SlabPlan, s: int, nb: int, device, group=None):
+        import torch
+        self.plan, self.s, self.nb, self.group = plan, s, nb, group
+        self.torch = torch
+        self.send_idx = {p: torch.as_tensor(v, device=device) for p, v in plan.send.items()}
+        self.recv_idx = {p: torch.as_tensor(v, device=device) for p, v in plan.recv.items()}
+        self.send_buf = {p: torch.empty((s, len(v), nb), dtype=torch.float64, device=device)
+                         for p, v in plan.send.items()}
+        self.recv_buf = {p: torch.empty((s, len(v), nb), dtype=torch.float64, device=device)
+                         for p, v in plan.recv.items()}
+
+    def exchange(self, x, ghost) -> None:
+        if self.plan.n_ghost == 0 and not self.send_idx:
+            return
+        dist = self.torch.distributed
+        xv = x.view(self.s, self.plan.T_local, self.nb)
+        ops = []
+        for p, idx in self.send_idx.items():
+            self.torch.index_select(xv, 1, idx, out=self.send_buf[p])
+            ops.append(dist.P2POp(dist.isend, self.send_buf[p], p, self.group))
+        for p in self.recv_idx:
+            ops.append(dist.P2POp(dist.irecv, self.recv_buf[p], p, self.group))
+        if ops:
+            for r in dist.batch_isend_irecv(ops):
+                r.wait()
+        gv = ghost.view(self.s, self.plan.n_ghost, self.nb)
+        for p, idx in self.recv_idx.items():
+            gv.index_copy_(1, idx, self.recv_buf[p])
+
+
+def allreduce_sum(buf, group=None) -> None:
+    import torch.distributed as dist
+    dist.all_reduce(buf, op=dist.ReduceOp.SUM, group=group)
+
+
+class DistributedStageSolver:
+    """Rank-local device solver for the element-partitioned stage system.
+
+    ``J_rows``: the rank's Jacobian block rows in global pattern order
+    (positions plan.q0 .. plan.q0 + len, reference row-major layout);
+    ``M_rows``: its mass blocks; ``a_inv``/``dt``/``shifts`` as in ``StageSolver``.
+    """
+
+    def __init__(self, plan: SlabPlan, J_rows: np.ndarray, M_rows: np.ndarray, a_inv, dt: float,
+                 kind: str = "uncoupled", shifts=None, gmres_cfg=None, group=None, exchange=None):
+        import ctypes
+
+        import torch
+
+        from . import _lib as L
+        from .blocks import BlockDiagonalMatrix, BlockSparseMatrix, DeviceBlocks, DevicePattern
+        from .krylov import GmresConfig
+        from .precond import stage_coupled_factorize, stage_uncoupled_factorize
+        from .stage_system import StageOperator
+
+        self.plan, self.group, self.kind = plan, group, kind
+        a_inv = np.asarray(a_inv, dtype=np.float64)
+        s = a_inv.shape[0]
+        nb = J_rows.shape[1]
+        self.s, self.nb = s, nb
+        self.cfg = gmres_cfg or GmresConfig(rel_tol=1e-8, restart=40)
+        Tl, ng = plan.T_local, plan.n_ghost
+        # operator pattern: local rows + one diagonal-only row per ghost (never computed)
+        ip = np.concatenate([plan.ext_indptr, plan.ext_indptr[-1] + 1 + np.arange(ng)])
+        ix = np.concatenate([plan.ext_indices, Tl + np.arange(ng)])
+        dg = np.concatenate([plan.ext_diag, plan.ext_indptr[-1] + np.arange(ng)])
+        self.op_pat = DevicePattern(ip, ix, dg)
+        jb = DeviceBlocks(nb, len(ix))
+        jb.upload(np.ascontiguousarray(J_rows[plan.row_block_src - plan.q0]))
+        if ng:
+            jb.upload(np.zeros((ng, nb, nb)), first=len(plan.ext_indices))
+        Mext = np.concatenate([M_rows, np.broadcast_to(np.eye(nb), (ng, nb, nb))]) if ng else M_rows
+        self.mass = BlockDiagonalMatrix(Mext)
+
+        class _Der:
+            pass
+
+        der = _Der()
+        der.a_inv = a_inv
+        der.shifts = np.zeros(s) if shifts is None else np.asarray(shifts, dtype=np.float64)
+        self.op = StageOperator(der, dt, self.mass, [BlockSparseMatrix(self.op_pat, jb)] * s)
+        self.ghost = torch.zeros(max(s * ng * nb, 1), dtype=torch.float64, device="cuda")
+        L.check(L.lib().irk_stage_op_set_halo(self.op._op.handle, Tl, self.ghost.data_ptr(), ng),
+                "irk_stage_op_set_halo")
+        # exchange(w_local, ghost) fills the ghost buffer; default: NCCL send/recv
+        self.exchange = exchange or HaloExchange(plan, s, nb, "cuda", group).exchange
+        # factor operator: local blocks only (cross-partition blocks are dropped)
+        self.fac_pat = DevicePattern(plan.loc_indptr, plan.loc_indices, plan.loc_diag)
+        fj = DeviceBlocks.from_host(np.ascontiguousarray(J_rows[plan.loc_block_src - plan.q0]))
+        fm = BlockDiagonalMatrix(M_rows)
+        self.fac_op = StageOperator(der, dt, fm, [BlockSparseMatrix(self.fac_pat, fj)] * s)
+        self._factorize = (stage_coupled_factorize if kind.startswith("coupled") else
+                           (lambda o: stage_uncoupled_factorize(o, der.shifts if kind == "uncoupled" else None)))
+        self.fac = None
+        self.n_local = s * Tl * nb
+        self._y = torch.empty(self.n_local, dtype=torch.float64, device="cuda")
+        del ctypes
+
+    def factorize(self):
+        """Local partitioned factor; re-factorised in place after the first call."""
+        if self.fac is not None and hasattr(self.fac, "refactor"):
+            if self.kind.startswith("coupled"):
+                return self.fac.refactor(self.fac_op)
+            return self.fac.refactor(self.fac_op, self.fac.shifts)
+        self.fac = self._factorize(self.fac_op)
+        return self.fac
+
+    def matvec(self, w):
+        """Halo exchange, then this rank's rows of B w."""
+        self.exchange(w, self.ghost)
+        y = self.torch_empty()
+        self.op.apply_device(w, y)
+        return y
+
+    def torch_empty(self):
+        import torch
+        return torch.empty(self.n_local, dtype=torch.float64, device="cuda")
+
+    def solve(self, rhs_local, x=None):
+        from .krylov import gmres_device
+        import torch.distributed as dist
+        pre = None if self.fac is None else self.fac.apply
+        multi = dist.is_available() and dist.is_initialized() and dist.get_world_size(self.group) > 1
+        ar = (lambda buf: allreduce_sum(buf, self.group)) if multi else None
+        return gmres_device(self.matvec, pre, rhs_local, self.cfg, allreduce=ar, x=x)

@@ -191,7 +191,23 @@ def color_major_permutation(nbr: np.ndarray) -> np.ndarray:
     return new_of_old
 
 
-def mesh_table(kind: str, N: int, ordering: str = "natural") -> np.ndarray:
+def slab_color_permutation(nbr: np.ndarray, parts: int) -> np.ndarray:
+    """new index of each old (natural) element: the natural order is cut into
+    ``parts`` contiguous slabs (``partition``), and inside each slab elements
+    are ordered colour-major (colour 0 first, natural order inside a colour).
+    parts=1 is the global colour-major numbering."""
+    color = two_coloring(nbr)
+    T = nbr.shape[0]
+    b = partition_bounds(T, parts)
+    new_of_old = np.empty(T, dtype=np.int64)
+    for p in range(parts):
+        lo, hi = int(b[p]), int(b[p + 1])
+        order = lo + np.argsort(color[lo:hi], kind="stable")
+        new_of_old[order] = np.arange(lo, hi)
+    return new_of_old
+
+
+def mesh_table(kind: str, N: int, ordering: str = "natural", parts: int = 1) -> np.ndarray:
     if kind == "tri2d":
         nbr = tri2d_table(N)
     elif kind == "tet3d":
@@ -201,7 +217,7 @@ def mesh_table(kind: str, N: int, ordering: str = "natural") -> np.ndarray:
     if ordering == "natural":
         return np.sort(nbr, axis=1)
     if ordering == "color":
-        return np.sort(renumber_table(nbr, color_major_permutation(nbr)), axis=1)
+        return np.sort(renumber_table(nbr, slab_color_permutation(nbr, parts)), axis=1)
     raise ValueError(f"unknown ordering {ordering!r}")
 
 

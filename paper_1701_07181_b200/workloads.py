@@ -245,10 +245,51 @@ def make_workload(cfg: SolveConfig, jnorm: float | None = None,
     s = tab.s
     rhs = rhs_vector(s, pat.T, cfg.nb, cfg.seed)
     if cfg.ordering == "color":
-        table, pat, J, M, rhs = relabel(table, J, M, rhs, s, color_major_permutation(table))
+        from .meshes import slab_color_permutation
+        parts = int(cfg.extra.get("parts", 1))
+        table, pat, J, M, rhs = relabel(table, J, M, rhs, s, slab_color_permutation(table, parts))
     elif cfg.ordering != "natural":
         raise ValueError(f"unknown ordering {cfg.ordering!r}")
     if jnorm is None:
         jnorm = norm2_power_cpu(pat, J, iters=norm_iters)
     dt = cfg.dt_norm / jnorm
     return Workload(cfg, table, pat, J, M, rhs, der.a_inv, der.shifts, jnorm, dt)
+
+
+def make_slab_workload(cfg: SolveConfig, P: int, rank: int):
+    """Rank-local inputs for the element-partitioned solve: the global pattern
+    (numbering per ``cfg.ordering``; colour ordering is applied inside each of
+    the P slabs) plus only this rank's J rows, M blocks and rhs rows.  Values are
+    generated for the rank's natural slab only (chunked generators), so no rank
+    materialises the global matrix."""
+    from .meshes import partition_bounds, renumber_table, slab_color_permutation
+    table = mesh_table(cfg.mesh, cfg.N, "natural")
+    T = table.shape[0]
+    b = partition_bounds(T, P)
+    lo, hi = int(b[rank]), int(b[rank + 1])
+    nat = Pattern.from_table(table)
+    s = builtin_tableau(cfg.scheme).s
+    Jn = jacobian_blocks(nat, cfg.nb, cfg.seed, cfg.jstd, rows=(lo, hi))
+    Mn = mass_blocks(T, cfg.nb, cfg.seed, rows=(lo, hi))
+    rn = rhs_vector(s, T, cfg.nb, cfg.seed, rows=(lo, hi)).reshape(s, hi - lo, cfg.nb)
+    if cfg.ordering == "color":
+        new_of_old = slab_color_permutation(table, P)
+    else:
+        new_of_old = np.arange(T, dtype=np.int64)
+    old_of_new = np.empty(T, dtype=np.int64)
+    old_of_new[new_of_old] = np.arange(T)
+    new_table = np.sort(renumber_table(table, new_of_old), axis=1)
+    pat = Pattern.from_table(new_table)
+    # local rows lo..hi of the new numbering are old rows of the same slab
+    q0, q1 = int(pat.indptr[lo]), int(pat.indptr[hi])
+    new_rows = np.repeat(np.arange(lo, hi), np.diff(pat.indptr[lo:hi + 1]))
+    want = old_of_new[new_rows] * T + old_of_new[pat.indices[q0:q1]]
+    oq0 = int(nat.indptr[lo])
+    old_rows = np.repeat(np.arange(lo, hi), np.diff(nat.indptr[lo:hi + 1]))
+    old_keys = old_rows * T + nat.indices[oq0:int(nat.indptr[hi])]
+    pos = np.searchsorted(old_keys, want)
+    J = Jn[pos]
+    loc_old = old_of_new[lo:hi] - lo
+    M = Mn[loc_old]
+    rhs = np.ascontiguousarray(rn[:, loc_old]).reshape(-1)
+    return pat, J, M, rhs
