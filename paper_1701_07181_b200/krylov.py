@@ -115,7 +115,8 @@ def gmres_device(apply_operator, apply_precond, rhs, cfg: GmresConfig, allreduce
     if x is None:
         x = t.empty(n, dtype=t.float64, device="cuda")
     restart = cfg.restart or cfg.max_iters
-    ccfg = L.GmresCfg(cfg.rel_tol, cfg.max_iters, min(restart, cfg.max_iters), cfg.reorth_eta)
+    eta = getattr(cfg, "reorth_eta", 0.7071067811865476)   # reference GmresConfig has none
+    ccfg = L.GmresCfg(cfg.rel_tol, cfg.max_iters, min(restart, cfg.max_iters), eta)
     st = L.GmresStatsC()
     hist = np.zeros(cfg.max_iters + 2)
     ar_fn, ar_user = None, None
@@ -153,9 +154,10 @@ def gmres(apply_operator, apply_precond, rhs, cfg: GmresConfig | None = None):
     cfg = cfg or GmresConfig()
     rd, was_np = to_device(rhs)
     rd = rd.reshape(-1)
-    if not cfg.left_precondition:
+    if not getattr(cfg, "left_precondition", True):
         inner = GmresConfig(rel_tol=cfg.rel_tol, max_iters=cfg.max_iters, restart=cfg.restart,
-                            left_precondition=True, reorth_eta=cfg.reorth_eta)
+                            left_precondition=True,
+                            reorth_eta=getattr(cfg, "reorth_eta", 0.7071067811865476))
         pre = apply_precond if apply_precond is not None else (lambda v: v)
         u, stats = gmres_device(lambda v: apply_operator(pre(v)), None, rd, inner)
         x, _ = to_device(pre(u))
