@@ -53,6 +53,8 @@ def parse():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--profile", action="store_true", help="timed steps only (for ncu)")
+    ap.add_argument("--jnorm", type=float, default=None,
+                    help="use this ||J||_2 instead of the power iteration (profiling runs)")
     ap.add_argument("--partitioned", action="store_true",
                     help="element-partitioned solve even at N=1 (always used for N>1)")
     return ap.parse_args()
@@ -292,7 +294,7 @@ def run_b200(args):
     pat, J, M, rhs_h = wl.pattern, wl.J, wl.M, wl.rhs
     der = derive(builtin_tableau(cfg.scheme))
     log(f'workload generated T={pat.T}')
-    jnorm = jnorm_device(pat, J)
+    jnorm = args.jnorm if args.jnorm else jnorm_device(pat, J)
     log(f'jnorm {jnorm:.4f}')
     dt = cfg.dt_norm / jnorm
     dpat = DevicePattern(pat.indptr, pat.indices, pat.diag_pos)
@@ -379,8 +381,15 @@ def run_b200(args):
     else:
         dom = {"name": "stage_matvec (fused)", "bytes": bm, "t": t_mv, "share": share_mv}
     achieved = dom["bytes"] / dom["t"] / 1e9
+    traffic = None
+    try:   # DRAM bytes per launch from the committed ncu --set full capture (profiles/)
+        with open(os.path.join(REPO, "profiles", "r1_traffic.json")) as fh:
+            tj = json.load(fh)
+        traffic = tj["ilu0_apply" if dom["name"].startswith("ilu0") else "stage_matvec"]
+    except Exception:
+        pass
     roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                "frac": achieved / peak, "traffic": None, "kernel": dom["name"],
+                "frac": achieved / peak, "traffic": traffic, "kernel": dom["name"],
                 "algorithmic_bytes_per_launch": dom["bytes"], "avg_launch_ms": 1e3 * dom["t"],
                 "share_of_step": dom["share"], "peak_source": peak_src}
     components = {

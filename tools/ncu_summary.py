@@ -1,0 +1,114 @@
+"""Summarise ncu CSV exports into profiles/ (run in the build container).
+
+  python tools/ncu_summary.py gpurun_out/launches_r1.csv gpurun_out/raw_g.csv gpurun_out/raw_f.csv \
+      --out profiles/r1
+
+Writes <out>_ncu_summary.md (per-kernel launch list shares of one timed step,
+dram traffic per launch vs algorithmic bytes, key --set full metrics) and
+<out>_traffic.json (dram bytes per launch, read by bench.py for roofline.traffic).
+"""
+import argparse
+import collections
+import csv
+import json
+
+
+def read_launches(path):
+    rows = list(csv.reader(open(path)))
+    hi = [i for i, r in enumerate(rows) if "Kernel Name" in r][0]
+    h = rows[hi]
+    ki, mi, vi, ui, idi = (h.index("Kernel Name"), h.index("Metric Name"), h.index("Metric Value"),
+                           h.index("Metric Unit"), h.index("ID"))
+    launches = collections.OrderedDict()
+    for r in rows[hi + 1:]:
+        if len(r) <= vi:
+            continue
+        v = float(r[vi].replace(",", ""))
+        u = r[ui]
+        if r[mi] == "gpu__time_duration.sum":
+            v = {"nsecond": 1e-3, "ns": 1e-3, "usecond": 1.0, "us": 1.0, "msecond": 1e3, "ms": 1e3}.get(u, 1.0) * v  # -> us
+        elif u in ("Kbyte", "KB"):
+            v *= 1e3
+        elif u in ("Mbyte", "MB"):
+            v *= 1e6
+        elif u in ("Gbyte", "GB"):
+            v *= 1e9
+        d = launches.setdefault(r[idi], {"name": r[ki].split("(")[0].replace("void ", "")})
+        d[r[mi]] = v
+    return list(launches.values())
+
+
+def read_raw(path, want):
+    rows = list(csv.reader(open(path)))
+    h = rows[0]
+    out = []
+    for r in rows[2:]:
+        if len(r) < len(h):
+            continue
+        d = dict(zip(h, r))
+        out.append({"name": d.get("Kernel Name", "").split("(")[0], **{w: d.get(w, "") for w in want}})
+    return out
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("launches")
+    ap.add_argument("raw", nargs="*")
+    ap.add_argument("--out", required=True)
+    a = ap.parse_args()
+    L = read_launches(a.launches)
+    # the timed step: from the second k_factor launch pair on
+    fidx = [i for i, d in enumerate(L) if "k_factor" in d["name"]]
+    start = fidx[len(fidx) // 2] if len(fidx) >= 2 else 0
+    step = L[start:]
+    agg = collections.OrderedDict()
+    for d in step:
+        g = agg.setdefault(d["name"], {"n": 0, "us": 0.0, "dram": 0.0})
+        g["n"] += 1
+        g["us"] += d.get("gpu__time_duration.sum", 0.0)
+        g["dram"] += d.get("dram__bytes_read.sum", 0.0) + d.get("dram__bytes_write.sum", 0.0)
+    tot = sum(g["us"] for g in agg.values())
+    lines = ["# ncu summary (one timed stage-solve, config 1, colour ordering)", "",
+             "Launch list: `ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum "
+             "--clock-control none` over `bench.py --steps 1 --warmup 1 --profile` (serialised, cold "
+             "caches: compare shares, not absolute times).", "",
+             f"Step total (serialised): {tot/1e3:.3f} ms", "",
+             "| kernel | launches | time (ms) | share | DRAM bytes / launch (GB) |",
+             "|---|---|---|---|---|"]
+    for name, g in sorted(agg.items(), key=lambda kv: -kv[1]["us"]):
+        lines.append(f"| `{name}` | {g['n']} | {g['us']/1e3:.3f} | {100*g['us']/tot:.1f}% | "
+                     f"{g['dram']/g['n']/1e9:.4f} |")
+    # traffic per operation (apply = copy + fwd + bwd launches of one apply)
+    traffic = {}
+    for key, names in (("stage_matvec", ("k_stage_matvec_pipe",)),
+                       ("ilu0_apply", ("k_copy_rows", "k_unc_fwd_pipe", "k_unc_bwd_pipe"))):
+        per = [agg[n]["dram"] / agg[n]["n"] for n in agg if any(k in n for k in names)]
+        cnt = [agg[n]["n"] for n in agg if any(k in n for k in names)]
+        if key == "ilu0_apply":
+            # launches per apply: one copy + one fwd + two bwd levels; scale to one apply
+            napply = next((agg[n]["n"] for n in agg if "k_copy_rows" in n), 1)
+            val = sum(agg[n]["dram"] for n in agg if any(k in n for k in names)) / max(napply, 1)
+        else:
+            val = per[0] if per else None
+        traffic[key] = val
+    lines += ["", "DRAM traffic per operation (bytes):", "",
+              f"* stage matvec: {traffic['stage_matvec']:.4e} (algorithmic 2.161e9)",
+              f"* ILU apply (all launches of one apply): {traffic['ilu0_apply']:.4e} (algorithmic 3.838e9)"]
+    want = ["gpu__time_duration.sum", "dram__throughput.avg.pct_of_peak_sustained_elapsed",
+            "sm__throughput.avg.pct_of_peak_sustained_elapsed", "sm__warps_active.avg.pct_of_peak_sustained_active",
+            "launch__registers_per_thread", "dram__bytes_read.sum", "dram__bytes_write.sum",
+            "sm__inst_executed_pipe_fp64.avg.pct_of_peak_sustained_active",
+            "smsp__average_warps_issue_stalled_barrier_per_issue_active.ratio"]
+    for p in a.raw:
+        lines += ["", f"## --set full metrics ({p.split('/')[-1]})", "",
+                  "| kernel | " + " | ".join(w.split(".")[0] if len(w) < 40 else w[:38] for w in want) + " |",
+                  "|" + "---|" * (len(want) + 1)]
+        for d in read_raw(p, want):
+            lines.append(f"| `{d['name']}` | " + " | ".join(d[w] for w in want) + " |")
+    open(a.out + "_ncu_summary.md", "w").write("\n".join(lines) + "\n")
+    json.dump(traffic, open(a.out + "_traffic.json", "w"), indent=1)
+    print("\n".join(lines[:30]))
+
+
+if __name__ == "__main__":
+    main()
