@@ -504,7 +504,7 @@ __global__ void __launch_bounds__(288) k_unc_fwd_pipe(ApplyArgs A, PipeCfg PC) {
                 for (int m = 0; m < nn; ++m) nitems += kept(m) ? S : 0;
                 auto push_items = [&](int from, int to) {
                     if (nitems == 0) {
-                        if (from == 0 && to > 0) pr.push(make_int4(t, -1, PD_FIRST | PD_LAST, 0), nullptr);
+                        if (from == 0 && to > 0) pr.push(make_int4((int)i, -1, PD_FIRST | PD_LAST, 0), nullptr);
                         return;
                     }
                     int n = 0;
@@ -513,7 +513,7 @@ __global__ void __launch_bounds__(288) k_unc_fwd_pipe(ApplyArgs A, PipeCfg PC) {
                         for (int k = 0; k < S; ++k, ++n) {
                             if (n < from || n >= to) continue;
                             const int fl = PD_L | (n == 0 ? PD_FIRST : 0) | (n == nitems - 1 ? PD_LAST : 0);
-                            pr.push(make_int4(t, m * S + k, fl, 0), A.L + ((int64_t)(l0 + m) * S + k) * bsz);
+                            pr.push(make_int4((int)i, m * S + k, fl, 0), A.L + ((int64_t)(l0 + m) * S + k) * bsz);
                         }
                     }
                 };
@@ -562,7 +562,7 @@ __global__ void __launch_bounds__(288) k_unc_fwd_pipe(ApplyArgs A, PipeCfg PC) {
     for (;;) {
         const int4 dsc = cs.take();
         if (dsc.z & PD_END) break;
-        const int64_t i = A.order[dsc.x];
+        const int64_t i = dsc.x;   // element id (descriptor)
         if (dsc.z & PD_FIRST) {
 #pragma unroll
             for (int k = 0; k < S; ++k) part[k] = 0.0;
@@ -677,20 +677,20 @@ __global__ void __launch_bounds__(288) k_unc_bwd_pipe(ApplyArgs A, PipeCfg PC) {
                         const int qq = d + 1 + m;
                         if (A.u_shared) {
                             if (n >= from && n < to)
-                                pr.push(make_int4(t, m * S, PD_USH | (n == 0 ? PD_FIRST : 0), 0), A.ubase[0] + qq * bsz);
+                                pr.push(make_int4((int)i, m * S, PD_USH | (n == 0 ? PD_FIRST : 0), nn << 1), A.ubase[0] + qq * bsz);
                             ++n;
                         } else {
                             for (int k = 0; k < S; ++k, ++n) {
                                 if (n < from || n >= to) continue;
                                 const double* ub = A.U ? A.U + ((int64_t)(u0 + m) * S + k) * bsz : A.ubase[k] + qq * bsz;
-                                pr.push(make_int4(t, m * S + k, PD_U | (n == 0 ? PD_FIRST : 0), 0), ub);
+                                pr.push(make_int4((int)i, m * S + k, PD_U | (n == 0 ? PD_FIRST : 0), nn << 1), ub);
                             }
                         }
                     }
                     for (int k = 0; k < S; ++k, ++n) {
                         if (n < from || n >= to) continue;
                         const int fl = PD_DINV | (n == 0 ? PD_FIRST : 0) | (k == S - 1 ? PD_LAST : 0);
-                        pr.push(make_int4(t, k, fl, nu == 0 ? 1 : 0), A.Dinv + (i * S + k) * bsz);
+                        pr.push(make_int4((int)i, k, fl, (nn << 1) | (nu == 0 ? 1 : 0)), A.Dinv + (i * S + k) * bsz);
                     }
                 };
                 const int npre = DEPS ? min(ntot, PC.nst - 1) : 0;
@@ -735,8 +735,8 @@ __global__ void __launch_bounds__(288) k_unc_bwd_pipe(ApplyArgs A, PipeCfg PC) {
     for (;;) {
         const int4 dsc = cs.take();
         if (dsc.z & PD_END) break;
-        const int64_t i = A.order[dsc.x];
-        const int nup = A.indptr[i + 1] - A.diag[i] - 1;
+        const int64_t i = dsc.x;     // element id and upper-neighbour count from the descriptor
+        const int nup = dsc.w >> 1;
         if (dsc.z & PD_FIRST) {
 #pragma unroll
             for (int k = 0; k < S; ++k) part[k] = 0.0;
