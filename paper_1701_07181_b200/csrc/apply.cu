@@ -319,7 +319,7 @@ struct PipeSmem {
     uint64_t* xempty;  // [2]
     int4* desc;
     double* xs;        // [2][xslot]
-    double* red;       // [G][S][nb]
+    double* red;       // [2][G][S][nb] (task parity)
     double* tv;        // [S][nb]
 };
 
@@ -334,7 +334,7 @@ __device__ __forceinline__ PipeSmem pipe_carve(unsigned char* raw, const PipeCfg
     P.desc = reinterpret_cast<int4*>(P.xempty + 2);
     P.xs = reinterpret_cast<double*>(P.desc + PC.nst);
     P.red = P.xs + 2 * (size_t)PC.xslot_doubles;
-    P.tv = P.red + (size_t)G * S * nb;
+    P.tv = P.red + 2 * (size_t)G * S * nb;
     return P;
 }
 
@@ -504,7 +504,7 @@ __global__ void __launch_bounds__(288) k_unc_fwd_pipe(ApplyArgs A, PipeCfg PC) {
                 for (int m = 0; m < nn; ++m) nitems += kept(m) ? S : 0;
                 auto push_items = [&](int from, int to) {
                     if (nitems == 0) {
-                        if (from == 0 && to > 0) pr.push(make_int4((int)i, -1, PD_FIRST | PD_LAST, 0), nullptr);
+                        if (from == 0 && to > 0) pr.push(make_int4((int)i, -1, PD_FIRST | PD_LAST, nn), nullptr);
                         return;
                     }
                     int n = 0;
@@ -513,7 +513,7 @@ __global__ void __launch_bounds__(288) k_unc_fwd_pipe(ApplyArgs A, PipeCfg PC) {
                         for (int k = 0; k < S; ++k, ++n) {
                             if (n < from || n >= to) continue;
                             const int fl = PD_L | (n == 0 ? PD_FIRST : 0) | (n == nitems - 1 ? PD_LAST : 0);
-                            pr.push(make_int4((int)i, m * S + k, fl, 0), A.L + ((int64_t)(l0 + m) * S + k) * bsz);
+                            pr.push(make_int4((int)i, m * S + k, fl, nn), A.L + ((int64_t)(l0 + m) * S + k) * bsz);
                         }
                     }
                 };
@@ -533,7 +533,7 @@ __global__ void __launch_bounds__(288) k_unc_fwd_pipe(ApplyArgs A, PipeCfg PC) {
                     for (int m = lane; m < nn; m += 32)
                         if (kept(m)) wait_flag(A.flags + colm(m), A.epoch);
                 __syncwarp();
-                uint32_t bytes = 0;
+                uint32_t bytes = S * seg;   // y_i (segments nn*S + k)
                 for (int m = 0; m < nn; ++m) bytes += kept(m) ? S * seg : 0;
                 if (lane == 0) {
                     if (DEPS) fence_proxy_async_global();
@@ -542,9 +542,10 @@ __global__ void __launch_bounds__(288) k_unc_fwd_pipe(ApplyArgs A, PipeCfg PC) {
                 xs = reinterpret_cast<double*>(__shfl_sync(0xffffffffu, reinterpret_cast<uintptr_t>(xs), 0));
                 xb = __shfl_sync(0xffffffffu, xb, 0);
                 __syncwarp();
-                for (int e = lane; e < nn * S; e += 32) {
+                for (int e = lane; e < (nn + 1) * S; e += 32) {
                     const int m = e / S, k = e - m * S;
-                    if (kept(m)) bulk_g2s(xs + e * nb, A.x + k * A.n + colm(m) * nb, seg, P.xfull + xb);
+                    if (m == nn) bulk_g2s(xs + e * nb, A.y + k * A.n + i * nb, seg, P.xfull + xb);
+                    else if (kept(m)) bulk_g2s(xs + e * nb, A.x + k * A.n + colm(m) * nb, seg, P.xfull + xb);
                 }
                 if (lane == 0) push_items(npre, ntot);
                 if (lane == 0) pr.x_next();
@@ -559,10 +560,12 @@ __global__ void __launch_bounds__(288) k_unc_fwd_pipe(ApplyArgs A, PipeCfg PC) {
     Consumer cs{&P, &PC};
     double part[S];
     const double* xs = nullptr;
+    int par = 0;   // reduction buffer of the current task
     for (;;) {
         const int4 dsc = cs.take();
         if (dsc.z & PD_END) break;
         const int64_t i = dsc.x;   // element id (descriptor)
+        const int nn = dsc.w;      // lower neighbours: y_i sits at x-slot segment nn*S + k
         if (dsc.z & PD_FIRST) {
 #pragma unroll
             for (int k = 0; k < S; ++k) part[k] = 0.0;
@@ -582,10 +585,7 @@ __global__ void __launch_bounds__(288) k_unc_fwd_pipe(ApplyArgs A, PipeCfg PC) {
                 // no kept lower neighbour: z_i = y_i, no reduction
                 if (q.active && q.g == 0)
 #pragma unroll
-                    for (int k = 0; k < S; ++k) {
-                        const int64_t o = k * A.n + i * nb + q.a;
-                        A.x[o] = A.y[o];
-                    }
+                    for (int k = 0; k < S; ++k) A.x[k * A.n + i * nb + q.a] = xs[(nn * S + k) * nb + q.a];
                 cs.x_release();
                 if (DEPS) {
                     consumer_sync(1, ncons);
@@ -593,24 +593,26 @@ __global__ void __launch_bounds__(288) k_unc_fwd_pipe(ApplyArgs A, PipeCfg PC) {
                 }
                 continue;
             }
+            // one barrier per task: the reduction buffer alternates with the task
+            // parity, and the next barrier orders the reads before its reuse
+            double* red = P.red + (size_t)par * q.G * S * nb;
+            par ^= 1;
             if (q.active)
 #pragma unroll
-                for (int k = 0; k < S; ++k) P.red[(q.g * S + k) * nb + q.a] = part[k];
+                for (int k = 0; k < S; ++k) red[(q.g * S + k) * nb + q.a] = part[k];
             consumer_sync(1, ncons);
             if (q.active && q.g == 0) {
 #pragma unroll
                 for (int k = 0; k < S; ++k) {
                     double sum = 0.0;
-                    for (int gg = 0; gg < q.G; ++gg) sum += P.red[(gg * S + k) * nb + q.a];
-                    const int64_t o = k * A.n + i * nb + q.a;
-                    A.x[o] = A.y[o] - sum;
+                    for (int gg = 0; gg < q.G; ++gg) sum += red[(gg * S + k) * nb + q.a];
+                    A.x[k * A.n + i * nb + q.a] = xs[(nn * S + k) * nb + q.a] - sum;
                 }
             }
             cs.x_release();
-            consumer_sync(1, ncons);
-            if (DEPS && c == 0) {
-                __threadfence();
-                st_release(A.flags + i, A.epoch);
+            if (DEPS) {
+                consumer_sync(1, ncons);
+                if (c == 0) { __threadfence(); st_release(A.flags + i, A.epoch); }
             }
         }
     }
@@ -732,10 +734,12 @@ __global__ void __launch_bounds__(288) k_unc_bwd_pipe(ApplyArgs A, PipeCfg PC) {
     Consumer cs{&P, &PC};
     double part[S];
     const double* xs = nullptr;
+    int par = 0;
     for (;;) {
         const int4 dsc = cs.take();
         if (dsc.z & PD_END) break;
         const int64_t i = dsc.x;     // element id and upper-neighbour count from the descriptor
+        double* red = P.red + (size_t)par * q.G * S * nb;
         const int nup = dsc.w >> 1;
         if (dsc.z & PD_FIRST) {
 #pragma unroll
@@ -767,13 +771,13 @@ __global__ void __launch_bounds__(288) k_unc_bwd_pipe(ApplyArgs A, PipeCfg PC) {
                 // t_k = z_{i,k} - uscale * sum_j U_ij x_{j,k}  (all stages)
                 if (q.active)
 #pragma unroll
-                    for (int k = 0; k < S; ++k) P.red[(q.g * S + k) * nb + q.a] = part[k];
+                    for (int k = 0; k < S; ++k) red[(q.g * S + k) * nb + q.a] = part[k];
                 consumer_sync(1, ncons);
                 if (q.active && q.g == 0) {
 #pragma unroll
                     for (int k = 0; k < S; ++k) {
                         double sum = 0.0;
-                        for (int gg = 0; gg < q.G; ++gg) sum += P.red[(gg * S + k) * nb + q.a];
+                        for (int gg = 0; gg < q.G; ++gg) sum += red[(gg * S + k) * nb + q.a];
                         P.tv[k * nb + q.a] = xs[(nup * S + k) * nb + q.a] - A.uscale * sum;
                     }
                 }
@@ -791,23 +795,23 @@ __global__ void __launch_bounds__(288) k_unc_bwd_pipe(ApplyArgs A, PipeCfg PC) {
         }
         cs.release();
         if (dsc.z & PD_LAST) {
+            par ^= 1;
             if (q.active)
 #pragma unroll
-                for (int k = 0; k < S; ++k) P.red[(q.g * S + k) * nb + q.a] = part[k];
+                for (int k = 0; k < S; ++k) red[(q.g * S + k) * nb + q.a] = part[k];
             consumer_sync(1, ncons);
             if (q.active && q.g == 0) {
 #pragma unroll
                 for (int k = 0; k < S; ++k) {
                     double sum = 0.0;
-                    for (int gg = 0; gg < q.G; ++gg) sum += P.red[(gg * S + k) * nb + q.a];
+                    for (int gg = 0; gg < q.G; ++gg) sum += red[(gg * S + k) * nb + q.a];
                     A.x[k * A.n + i * nb + q.a] = sum;
                 }
             }
             cs.x_release();
-            consumer_sync(1, ncons);
-            if (DEPS && c == 0) {
-                __threadfence();
-                st_release(A.flags + i, A.epoch);
+            if (DEPS) {
+                consumer_sync(1, ncons);
+                if (c == 0) { __threadfence(); st_release(A.flags + i, A.epoch); }
             }
         }
     }
@@ -845,11 +849,17 @@ static int run_pipe(const irk_factor* f, K1 kernel_deps, K2 kernel_level, ApplyA
     PC.maxdeg = f->maxdeg;
     PC.xslot_doubles = (((PC.maxdeg + 1) * s * nb) + 15) & ~15;
     const int threads = 32 + ((A.G_ * nb + 31) / 32) * 32;
-    const size_t fixed = sizeof(double) * (2 * (size_t)PC.xslot_doubles + (size_t)A.G_ * s * nb + (size_t)s * nb) +
+    const size_t fixed = sizeof(double) * (2 * (size_t)PC.xslot_doubles + 2 * (size_t)A.G_ * s * nb + (size_t)s * nb) +
                          4 * sizeof(uint64_t);
-    const size_t budget = 104 * 1024;
+    // Each task is a short serial chain (x gather -> 3..12 blocks -> reduction),
+    // so throughput comes from tasks in flight per SM, not ring depth: size the
+    // ring so that >= 4 CTAs fit on an SM (tools/tune_apply.py: 2-3 stages of a
+    // 40x40 block at 4-5 CTAs/SM run at 84% of HBM peak, 7 stages at 2 CTAs/SM
+    // at 59%).  IRK_APPLY_NST overrides.
     const size_t per_stage = PC.stage_bytes + 2 * sizeof(uint64_t) + sizeof(int4);
-    PC.nst = (int)std::max<size_t>(2, std::min<size_t>(24, (budget - std::min(budget / 2, fixed)) / per_stage));
+    const size_t per_cta = (size_t)f->ctx->smem_per_sm / 4 - 1024;
+    PC.nst = (int)std::max<size_t>(2, std::min<size_t>(24, per_cta > fixed ? (per_cta - fixed) / per_stage : 0));
+    if (const char* ns = getenv("IRK_APPLY_NST")) PC.nst = std::max(2, atoi(ns));
     const size_t smem = (size_t)PC.nst * per_stage + fixed;
     const bool level_mode = S.nlevels <= LEVEL_LAUNCH_MAX;
     int per_sm = 1;
@@ -955,6 +965,7 @@ static void fill_args(const irk_factor* f, ApplyArgs& A) {
     A.s = f->s;
     A.nb = f->nb;
     A.G_ = choose_groups(f->nb, 256);
+    if (const char* g = getenv("IRK_APPLY_G")) A.G_ = std::max(1, std::min(atoi(g), (f->nb + 1) / 2));
 }
 
 int factor_apply(const irk_factor* f, const double* y, double* x, cudaStream_t st) {

@@ -122,6 +122,7 @@ int irk_ctx_create(int device, irk_ctx** out) {
     IRK_CK(cudaGetDeviceProperties(&prop, device));
     c->num_sms = prop.multiProcessorCount;
     c->smem_optin = prop.sharedMemPerBlockOptin;
+    c->smem_per_sm = prop.sharedMemPerMultiprocessor;
     // keep stream-ordered allocations cached between calls
     cudaMemPool_t pool;
     if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {

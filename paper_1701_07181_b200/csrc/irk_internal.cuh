@@ -57,6 +57,7 @@ struct irk_ctx {
     int device = 0;
     int num_sms = 148;
     size_t smem_optin = 0;
+    size_t smem_per_sm = 0;
 };
 
 struct irk_pattern {
