@@ -249,32 +249,47 @@ __global__ void __launch_bounds__(128) k_inverse(InvArgs A) {
 // lane l holds row 32 + l % E of block l / E (E = nb - 32).  Each pivot step
 // needs one CTA barrier: before it, every warp stages its best candidate row
 // (per block) in a double-buffered shared slot; after it, every lane picks the
-// winning candidate and reads the pivot row from the slot.  k is a compile-time
-// constant in every step (fully unrolled), so all register indices are static.
+// winning candidate and reads the pivot row from the slot.
+//
+// Code size: a fully unrolled nb-step elimination is ~0.5 MB of SASS and
+// thrashes the instruction cache.  Instead the row registers are rotated: the
+// pivot steps run in chunks of 8 (unrolled), and after each chunk the row is
+// rotated left by 8 columns, so the column eliminated in sub-step u always sits
+// in register u (a compile-time index) and the loop body is one 8-step chunk.
+// Rows are padded to NBR = ceil8(nb) zero columns; after NBR/8 chunks the
+// rotation is back to the identity.
 // ---------------------------------------------------------------------------
 template <int NB>
 struct Inv2Cfg {
     static constexpr int E = NB - 32;
     static constexpr int G = (32 / E) < 4 ? (32 / E) : 4;
     static constexpr int LDX = NB + 1;
+    static constexpr int NBR = (NB + 7) & ~7;
 };
 
 template <int NB>
-__global__ void __launch_bounds__(32 * (Inv2Cfg<NB>::G + 1)) k_inverse2(InvArgs A) {
+__host__ __device__ constexpr size_t inv2_smem_bytes() {
     using C = Inv2Cfg<NB>;
-    constexpr int E = C::E, G = C::G, LDX = C::LDX;
-    constexpr int NBP = (NB + 1) & ~1;
+    return sizeof(double) * (2 * C::G * 2 * C::NBR + (size_t)C::G * NB * C::LDX + 2 * C::G * 2 + (size_t)C::G * NB) +
+           sizeof(int) * (2 * C::G * 2 + 2 * C::G * NB);
+}
+
+template <int NB>
+__global__ void __launch_bounds__(32 * (Inv2Cfg<NB>::G + 1), 2) k_inverse2(InvArgs A) {
+    using C = Inv2Cfg<NB>;
+    constexpr int E = C::E, G = C::G, LDX = C::LDX, NBR = C::NBR;
     extern __shared__ __align__(16) double sm2[];
-    // layout: cand[2 bufs][G blocks][2 owners][NBP] | Xs[G][NB][LDX] | cval,cidx[2][G][2] | piv/invp ints
+    // layout: cand[2 bufs][G blocks][2 owners][NBR] | Xs[G][NB][LDX] | cval[2][G][2] | pvals[G][NB]
+    //         | cidx[2][G][2] | piv[G][NB] | invp[G][NB]
     double* cand = sm2;
-    double* Xs = cand + 2 * G * 2 * NBP;
+    double* Xs = cand + 2 * G * 2 * NBR;
     double* cval = Xs + (size_t)G * NB * LDX;
-    int* cidx = reinterpret_cast<int*>(cval + 2 * G * 2);
-    int* pivs = cidx + 2 * G * 2;                     // [G][NB]
-    int* invp = pivs + G * NB;                        // [G][NB]
+    double* pvals = cval + 2 * G * 2;
+    int* cidx = reinterpret_cast<int*>(pvals + G * NB);
+    int* pivs = cidx + 2 * G * 2;
+    int* invp = pivs + G * NB;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const bool extra = warp == G;
-    // my block and row
     const int blk = extra ? (lane / E) : warp;
     const int row = extra ? (32 + lane % E) : lane;
     const bool live = extra ? (lane < G * E) : true;
@@ -290,15 +305,15 @@ __global__ void __launch_bounds__(32 * (Inv2Cfg<NB>::G + 1)) k_inverse2(InvArgs 
             k_st = (int)(code / A.T);
             j = code - (int64_t)k_st * A.T;
         }
-        double d[NB];
+        double d[NBR];
         {
             const double2* src = reinterpret_cast<const double2*>(A.D + (j * A.s + k_st) * bsz);
 #pragma unroll
-            for (int p = 0; p < (NB + 1) / 2; ++p) {
+            for (int p = 0; p < NBR / 2; ++p) {
                 double2 v = make_double2(0.0, 0.0);
-                if (valid) v = src[(int64_t)p * NB + row];
+                if (valid && p < (NB + 1) / 2) v = src[(int64_t)p * NB + row];
                 d[2 * p] = v.x;
-                if (2 * p + 1 < NB) d[2 * p + 1] = v.y;
+                d[2 * p + 1] = (2 * p + 1 < NB) ? v.y : 0.0;
             }
         }
         double* X = Xs + (size_t)blk * NB * LDX;
@@ -330,43 +345,35 @@ __global__ void __launch_bounds__(32 * (Inv2Cfg<NB>::G + 1)) k_inverse2(InvArgs 
         colnorm(&n1);
         int used = live ? 0 : 1;
         int pstep = -1;
-        double logdet = 0.0;
-        int zero = 0;
         int* piv = pivs + blk * NB;
-        auto step = [&](auto kc) {
-            constexpr int k = decltype(kc)::value;
+        double* pvb = pvals + blk * NB;
+        const int owner_slot = extra ? 1 : 0;
+        // sub-step u of chunk ch eliminates column k = 8 ch + u, held in d[u]
+        auto step = [&](int k, auto uc) {
+            constexpr int u = decltype(uc)::value;
             const int buf = k & 1;
-            // candidate of this warp for its block(s): max |d[k]| over unused rows
-            double best = used ? -1.0 : fabs(d[k]);
+            double best = used ? -1.0 : fabs(d[u]);
             int br = used ? 0x7fffffff : row;
-            if (!extra) {
+            // one branch-free butterfly for both warp kinds: main warps reduce over
+            // all 32 lanes, the extra warp over its E-lane groups (then the group
+            // leader's result is broadcast; E need not be a power of 2)
 #pragma unroll
-                for (int o = 16; o; o >>= 1) {
-                    const double ob = __shfl_xor_sync(0xffffffffu, best, o);
-                    const int orr = __shfl_xor_sync(0xffffffffu, br, o);
-                    if (ob > best || (ob == best && orr < br)) { best = ob; br = orr; }
-                }
-            } else {
-                // segmented reduction over the E lanes of each block (E-lane groups)
-#pragma unroll
-                for (int o = 16; o; o >>= 1) {
-                    const double ob = __shfl_xor_sync(0xffffffffu, best, o);
-                    const int orr = __shfl_xor_sync(0xffffffffu, br, o);
-                    const int ol = lane ^ o;
-                    const bool same = (ol / E == lane / E) && ol < G * E;
-                    if (same && (ob > best || (ob == best && orr < br))) { best = ob; br = orr; }
-                }
-                // the group leader holds the complete result (E need not be a power of 2)
-                const int leader = (lane / E) * E;
+            for (int o = 16; o; o >>= 1) {
+                const double ob = __shfl_xor_sync(0xffffffffu, best, o);
+                const int orr = __shfl_xor_sync(0xffffffffu, br, o);
+                const int ol = lane ^ o;
+                const bool same = !extra || ((ol / E == lane / E) && ol < G * E);
+                if (same && (ob > best || (ob == best && orr < br))) { best = ob; br = orr; }
+            }
+            {
+                const int leader = extra ? (lane / E) * E : lane;
                 best = __shfl_sync(0xffffffffu, best, leader);
                 br = __shfl_sync(0xffffffffu, br, leader);
             }
-            const int owner_slot = extra ? 1 : 0;
             if (live && br == row) {   // I hold this warp's candidate row for my block
-                double* cr = cand + ((buf * G + blk) * 2 + owner_slot) * NBP;
+                double* cr = cand + ((buf * G + blk) * 2 + owner_slot) * NBR;
 #pragma unroll
-                for (int c = 0; c < NB; c += 2)
-                    *reinterpret_cast<double2*>(cr + c) = make_double2(d[c], c + 1 < NB ? d[c + 1] : 0.0);
+                for (int c = 0; c < NBR; c += 2) *reinterpret_cast<double2*>(cr + c) = make_double2(d[c], d[c + 1]);
             }
             if (live && (extra ? (lane % E == 0) : (lane == 0))) {
                 cval[(buf * G + blk) * 2 + owner_slot] = best;
@@ -379,30 +386,63 @@ __global__ void __launch_bounds__(32 * (Inv2Cfg<NB>::G + 1)) k_inverse2(InvArgs 
             const bool take1 = v1 > v0 || (v1 == v0 && i1 < i0);
             int p = take1 ? i1 : i0;
             if (p == 0x7fffffff) p = k;
-            const double* pr = cand + ((buf * G + blk) * 2 + (take1 ? 1 : 0)) * NBP;
-            const double pv = pr[k];
+            const double* pr = cand + ((buf * G + blk) * 2 + (take1 ? 1 : 0)) * NBR;
+            const double pv = pr[u];
             const double inv = 1.0 / pv;
             if (!extra && lane == 0) {
-                logdet += log(fabs(pv));
-                if (pv == 0.0) zero = 1;
+                pvb[k] = pv;
                 piv[k] = p;
             }
             const bool is_p = (row == p) && live;
             if (is_p) { used = 1; pstep = k; }
-            const double a = is_p ? inv : -d[k] * inv;
+            // pivot row: a * P; other rows: d + a * P; column k becomes a
+            const double a = is_p ? inv : -d[u] * inv;
             const double g = is_p ? 0.0 : 1.0;
 #pragma unroll
-            for (int c = 0; c < NB; c += 2) {
+            for (int c = 0; c < NBR; c += 2) {
                 const double2 pc = *reinterpret_cast<const double2*>(pr + c);
-                if (c == k) d[c] = a;
-                else d[c] = fma(a, pc.x, g * d[c]);
-                if (c + 1 < NB) {
-                    if (c + 1 == k) d[c + 1] = a;
-                    else d[c + 1] = fma(a, pc.y, g * d[c + 1]);
-                }
+                d[c] = (c == u) ? a : fma(a, pc.x, g * d[c]);
+                d[c + 1] = (c + 1 == u) ? a : fma(a, pc.y, g * d[c + 1]);
             }
         };
-        static_for(step, std::make_integer_sequence<int, NB>{});
+        // rotate left by 8: column 8(ch+1)+u moves to register u
+        auto rotate8 = [&]() {
+            double tmp[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) tmp[u] = d[u];
+#pragma unroll
+            for (int c = 0; c < NBR - 8; ++c) d[c] = d[c + 8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) d[NBR - 8 + u] = tmp[u];
+        };
+        // full chunks (no per-step guard: shuffles stay in provably converged code)
+#pragma unroll 1
+        for (int ch = 0; ch < NB / 8; ++ch) {
+            static_for([&](auto uc) { step(ch * 8 + decltype(uc)::value, uc); },
+                       std::make_integer_sequence<int, 8>{});
+            rotate8();
+        }
+        if constexpr (NB % 8 != 0) {   // tail chunk: NB % 8 steps, then the last rotation
+            static_for([&](auto uc) { step((NB / 8) * 8 + decltype(uc)::value, uc); },
+                       std::make_integer_sequence<int, NB % 8>{});
+            rotate8();
+        }
+        __syncthreads();
+        // det = exp(sum_k log|pivot_k|) as slogdet: logs in parallel, summed in step order
+        double logdet = 0.0;
+        int zero = 0;
+        if (!extra) {
+            for (int m = lane; m < NB; m += 32) {
+                const double pv = pvb[m];
+                X[m] = log(fabs(pv));   // X is free until the rows are staged below
+            }
+            __syncwarp();
+            if (lane == 0)
+                for (int m = 0; m < NB; ++m) {
+                    logdet += X[m];
+                    if (pvb[m] == 0.0) zero = 1;
+                }
+        }
         __syncthreads();
         // stage rows at their pivot step; inverse permutation; coalesced store
         if (live && pstep >= 0)
@@ -432,9 +472,7 @@ __global__ void __launch_bounds__(32 * (Inv2Cfg<NB>::G + 1)) k_inverse2(InvArgs 
 template <int NB>
 static int launch2(const irk_ctx* ctx, const InvArgs& A, cudaStream_t st) {
     using C = Inv2Cfg<NB>;
-    constexpr int NBP = (NB + 1) & ~1;
-    const size_t smem = sizeof(double) * (2 * C::G * 2 * NBP + (size_t)C::G * NB * C::LDX + 2 * C::G * 2) +
-                        sizeof(int) * (2 * C::G * 2 + 2 * C::G * NB);
+    const size_t smem = inv2_smem_bytes<NB>();
     static bool attr = false;
     if (!attr) {
         IRK_CK(cudaFuncSetAttribute(k_inverse2<NB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
