@@ -16,6 +16,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <type_traits>
 #include <utility>
 
@@ -30,6 +31,21 @@ __host__ __device__ constexpr int kval(int k) { return k; }
 template <class F, int... K>
 __device__ __forceinline__ void static_for(F&& f, std::integer_sequence<int, K...>) {
     (f(std::integral_constant<int, K>{}), ...);
+}
+
+// Warp argmax for partial pivoting: the largest |v| over lanes with a
+// candidate, smallest row index on ties (the getrf rule).  For |v| >= 0 the
+// IEEE bit pattern is monotonic, so three redux.sync reductions (high word,
+// low word among the high-word winners, then row index) replace a 5-round
+// shuffle butterfly.  Returns INT_MAX when no lane has a candidate.
+__device__ __forceinline__ int warp_pivot(bool has, double absval, int row) {
+    const unsigned hk = has ? (unsigned)__double2hiint(absval) + 1u : 0u;
+    const unsigned lk = has ? (unsigned)__double2loint(absval) : 0u;
+    const unsigned m1 = __reduce_max_sync(0xffffffffu, hk);
+    const bool c1 = has && hk == m1;
+    const unsigned m2 = __reduce_max_sync(0xffffffffu, c1 ? lk : 0u);
+    const bool c2 = c1 && lk == m2;
+    return (int)__reduce_min_sync(0xffffffffu, c2 ? (unsigned)row : 0x7fffffffu);
 }
 
 struct InvArgs {
@@ -395,14 +411,18 @@ __global__ void __launch_bounds__(32 * (Inv2Cfg<NB>::G + 1), 2) k_inverse2(InvAr
             }
             const bool is_p = (row == p) && live;
             if (is_p) { used = 1; pstep = k; }
-            // pivot row: a * P; other rows: d + a * P; column k becomes a
-            const double a = is_p ? inv : -d[u] * inv;
-            const double g = is_p ? 0.0 : 1.0;
+            // Unscaled pivot rows: the pivot row keeps its values (column k := 1)
+            // and is scaled by 1/pivot once, when the rows are staged at the end;
+            // every other row gets d + a * P with a = -d[k] / pivot (column k := a).
+            // Rows that were pivots earlier carry their scale in f = d[k], so the
+            // update is the scaled Gauss-Jordan step, one DFMA per element.
+            const double a = is_p ? 0.0 : -d[u] * inv;
+            const double ck = is_p ? 1.0 : a;
 #pragma unroll
             for (int c = 0; c < NBR; c += 2) {
                 const double2 pc = *reinterpret_cast<const double2*>(pr + c);
-                d[c] = (c == u) ? a : fma(a, pc.x, g * d[c]);
-                d[c + 1] = (c + 1 == u) ? a : fma(a, pc.y, g * d[c + 1]);
+                d[c] = (c == u) ? ck : fma(a, pc.x, d[c]);
+                d[c + 1] = (c + 1 == u) ? ck : fma(a, pc.y, d[c + 1]);
             }
         };
         // rotate left by 8: column 8(ch+1)+u moves to register u
@@ -444,10 +464,12 @@ __global__ void __launch_bounds__(32 * (Inv2Cfg<NB>::G + 1), 2) k_inverse2(InvAr
                 }
         }
         __syncthreads();
-        // stage rows at their pivot step; inverse permutation; coalesced store
-        if (live && pstep >= 0)
+        // stage rows at their pivot step (scaled by 1/pivot); inverse permutation; coalesced store
+        if (live && pstep >= 0) {
+            const double rs = 1.0 / pvb[pstep];
 #pragma unroll
-            for (int c = 0; c < NB; ++c) X[pstep * LDX + c] = d[c];
+            for (int c = 0; c < NB; ++c) X[pstep * LDX + c] = d[c] * rs;
+        }
         if (!extra)
             for (int m = lane; m < NB; m += 32) invp[blk * NB + piv[m]] = m;
         __syncthreads();
@@ -466,6 +488,475 @@ __global__ void __launch_bounds__(32 * (Inv2Cfg<NB>::G + 1), 2) k_inverse2(InvAr
             const bool bad = zero || det == 0.0 || !isfinite(det) || !(cond <= 1e14);
             if (bad) atomicMin(A.fail_key, (unsigned long long)A.tasks[base + blk]);
         }
+    }
+}
+
+// ---------------------------------------------------------------------------
+// nb <= 40 (NBR = ceil8(nb) <= 40): one warp per block, no CTA barriers.
+// Lane l holds rows l and l + 32 (ROWS = ceil(NBR/32) slots); the block is
+// padded to NBR x NBR with an identity block, so the padded pivot steps pick
+// their own padded row (pivot 1, zero multipliers) and change nothing -- the
+// 8-step chunks need no runtime guard.  Same register rotation, unscaled pivot
+// rows and pivot rule as k_inverse2; the pivot row is broadcast through a
+// double-buffered per-warp shared row.
+// ---------------------------------------------------------------------------
+template <int NBR>
+struct Inv3Cfg {
+    static constexpr int ROWS = (NBR + 31) / 32;
+    static constexpr int LDX = NBR + 1;
+    static constexpr int WARPS = 4;
+    // per warp: prow[2][NBR] | X[NBR][LDX] | pvals[NBR] doubles, piv/invp[NBR] ints
+    static constexpr size_t warp_doubles = 2 * NBR + (size_t)NBR * LDX + NBR;
+    static constexpr size_t smem = WARPS * (warp_doubles * sizeof(double) + 2 * NBR * sizeof(int));
+};
+
+template <int NBR>
+__global__ void __launch_bounds__(32 * Inv3Cfg<NBR>::WARPS) k_inverse3(InvArgs A) {
+    using C = Inv3Cfg<NBR>;
+    constexpr int ROWS = C::ROWS, LDX = C::LDX;
+    extern __shared__ __align__(16) double sm3[];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    double* prow = sm3 + (size_t)warp * C::warp_doubles;
+    double* X = prow + 2 * NBR;
+    double* pvb = X + (size_t)NBR * LDX;
+    int* piv = reinterpret_cast<int*>(sm3 + (size_t)C::WARPS * C::warp_doubles) + warp * 2 * NBR;
+    int* invp = piv + NBR;
+    const int nb = A.nb;
+    const int P = (nb + 1) >> 1;
+    const int64_t bsz = (int64_t)nb * 2 * P;
+    for (int64_t t = (int64_t)blockIdx.x * C::WARPS + warp; t < A.ntasks; t += (int64_t)gridDim.x * C::WARPS) {
+        const int64_t code = A.tasks[t];
+        const int k_st = (int)(code / A.T);
+        const int64_t j = code - (int64_t)k_st * A.T;
+        double d[ROWS][NBR];
+        int used[ROWS], pstep[ROWS];
+        {
+            const double2* src = reinterpret_cast<const double2*>(A.D + (j * A.s + k_st) * bsz);
+#pragma unroll
+            for (int s = 0; s < ROWS; ++s) {
+                const int r = lane + 32 * s;
+                used[s] = r >= NBR;   // rows past the padded block never pivot
+                pstep[s] = -1;
+#pragma unroll
+                for (int p = 0; p < NBR / 2; ++p) {
+                    double2 v = make_double2(0.0, 0.0);
+                    if (r < nb && p < P) v = src[(int64_t)p * nb + r];
+                    if (2 * p + 1 >= nb) v.y = 0.0;
+                    if (r >= nb) {   // identity padding
+                        v.x = (2 * p == r) ? 1.0 : 0.0;
+                        v.y = (2 * p + 1 == r) ? 1.0 : 0.0;
+                    }
+                    d[s][2 * p] = v.x;
+                    d[s][2 * p + 1] = v.y;
+                }
+            }
+        }
+        // |.|_1 of the nb x nb part (max column abs-sum, NaN propagating)
+        auto colnorm = [&]() -> double {
+#pragma unroll
+            for (int s = 0; s < ROWS; ++s) {
+                const int r = lane + 32 * s;
+                if (r < nb)
+#pragma unroll
+                    for (int c = 0; c < NBR; ++c) X[r * LDX + c] = fabs(d[s][c]);
+            }
+            __syncwarp();
+            double mx = -1.0;
+            int nan = 0;
+            for (int c = lane; c < nb; c += 32) {
+                double sum = 0.0;
+                for (int r = 0; r < nb; ++r) sum += X[r * LDX + c];
+                if (sum != sum) nan = 1;
+                mx = fmax(mx, sum);
+            }
+#pragma unroll
+            for (int o = 16; o; o >>= 1) {
+                mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+                nan |= __shfl_xor_sync(0xffffffffu, nan, o);
+            }
+            __syncwarp();
+            return nan ? __longlong_as_double(0x7ff8000000000000LL) : mx;
+        };
+        const double n1 = colnorm();
+        auto step = [&](int k, auto uc) {
+            constexpr int u = decltype(uc)::value;
+            bool has = false;
+            double best = 0.0;
+            int br = 0x7fffffff;
+#pragma unroll
+            for (int s = 0; s < ROWS; ++s) {
+                const double a = fabs(d[s][u]);
+                if (!used[s] && (!has || a > best)) { best = a; br = lane + 32 * s; has = true; }
+            }
+            const int pw = warp_pivot(has, best, br);
+            const int p = (pw == 0x7fffffff) ? k : pw;
+            double sv = d[0][u];
+#pragma unroll
+            for (int s = 1; s < ROWS; ++s) sv = ((p >> 5) == s) ? d[s][u] : sv;
+            const double pv = __shfl_sync(0xffffffffu, sv, p & 31);
+            const double inv = 1.0 / pv;
+            double* pr = prow + (k & 1) * NBR;
+            if (lane == (p & 31)) {
+#pragma unroll
+                for (int s = 0; s < ROWS; ++s)
+                    if (s == (p >> 5))
+#pragma unroll
+                        for (int c = 0; c < NBR; c += 2)
+                            *reinterpret_cast<double2*>(pr + c) = make_double2(d[s][c], d[s][c + 1]);
+            }
+            __syncwarp();
+            if (lane == 0) { pvb[k] = pv; piv[k] = p; }
+#pragma unroll
+            for (int s = 0; s < ROWS; ++s) {
+                const bool is_p = (lane + 32 * s) == p;
+                if (is_p) { used[s] = 1; pstep[s] = k; }
+                const double a = is_p ? 0.0 : -d[s][u] * inv;
+                const double ck = is_p ? 1.0 : a;
+#pragma unroll
+                for (int c = 0; c < NBR; c += 2) {
+                    const double2 pc = *reinterpret_cast<const double2*>(pr + c);
+                    d[s][c] = (c == u) ? ck : fma(a, pc.x, d[s][c]);
+                    d[s][c + 1] = (c + 1 == u) ? ck : fma(a, pc.y, d[s][c + 1]);
+                }
+            }
+        };
+#pragma unroll 1
+        for (int ch = 0; ch < NBR / 8; ++ch) {
+            static_for([&](auto uc) { step(ch * 8 + decltype(uc)::value, uc); },
+                       std::make_integer_sequence<int, 8>{});
+#pragma unroll
+            for (int s = 0; s < ROWS; ++s) {
+                double tmp[8];
+#pragma unroll
+                for (int u = 0; u < 8; ++u) tmp[u] = d[s][u];
+#pragma unroll
+                for (int c = 0; c < NBR - 8; ++c) d[s][c] = d[s][c + 8];
+#pragma unroll
+                for (int u = 0; u < 8; ++u) d[s][NBR - 8 + u] = tmp[u];
+            }
+        }
+        __syncwarp();
+        // det = exp(sum_k log|pivot_k|), k < nb, summed in step order
+        for (int m = lane; m < nb; m += 32) X[m] = log(fabs(pvb[m]));
+        __syncwarp();
+        double logdet = 0.0;
+        int zero = 0;
+        if (lane == 0)
+            for (int m = 0; m < nb; ++m) {
+                logdet += X[m];
+                if (pvb[m] == 0.0) zero = 1;
+            }
+        __syncwarp();
+        // stage real rows at their pivot step (scaled by 1/pivot), then un-permute columns
+#pragma unroll
+        for (int s = 0; s < ROWS; ++s)
+            if (pstep[s] >= 0 && pstep[s] < nb) {
+                const double rs = 1.0 / pvb[pstep[s]];
+#pragma unroll
+                for (int c = 0; c < NBR; ++c) X[pstep[s] * LDX + c] = d[s][c] * rs;
+            }
+        for (int m = lane; m < nb; m += 32) invp[piv[m]] = m;
+        __syncwarp();
+        double2* dst = reinterpret_cast<double2*>(A.Dinv + (j * A.s + k_st) * bsz);
+#pragma unroll
+        for (int s = 0; s < ROWS; ++s) {
+            const int r = lane + 32 * s;
+            if (r < nb)
+                for (int p = 0; p < P; ++p)
+                    dst[(int64_t)p * nb + r] = make_double2(X[r * LDX + invp[2 * p]],
+                                                            (2 * p + 1 < nb) ? X[r * LDX + invp[2 * p + 1]] : 0.0);
+        }
+        __syncwarp();
+        // |inv|_1 from the staged rows (a row permutation of inv(D))
+        double mx = -1.0;
+        int nan = 0;
+        for (int c = lane; c < nb; c += 32) {
+            double sum = 0.0;
+            for (int r = 0; r < nb; ++r) sum += fabs(X[r * LDX + c]);
+            if (sum != sum) nan = 1;
+            mx = fmax(mx, sum);
+        }
+#pragma unroll
+        for (int o = 16; o; o >>= 1) {
+            mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+            nan |= __shfl_xor_sync(0xffffffffu, nan, o);
+        }
+        const double n2 = nan ? __longlong_as_double(0x7ff8000000000000LL) : mx;
+        if (lane == 0) {
+            const double det = exp(logdet);
+            const double cond = n1 * n2;
+            const bool bad = zero || det == 0.0 || !isfinite(det) || !(cond <= 1e14);
+            if (bad) atomicMin(A.fail_key, (unsigned long long)code);
+        }
+        __syncwarp();
+    }
+}
+
+template <int NBR>
+static int launch3(const irk_ctx* ctx, const InvArgs& A, cudaStream_t st) {
+    using C = Inv3Cfg<NBR>;
+    static bool attr = false;
+    if (!attr) {
+        IRK_CK(cudaFuncSetAttribute(k_inverse3<NBR>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::smem));
+        IRK_CK(cudaFuncSetAttribute(k_inverse3<NBR>, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+        attr = true;
+    }
+    const int threads = 32 * C::WARPS;
+    int per_sm = 1;
+    IRK_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_inverse3<NBR>, threads, C::smem));
+    const int64_t need = (A.ntasks + C::WARPS - 1) / C::WARPS;
+    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(need, (int64_t)ctx->num_sms * std::max(per_sm, 1)));
+    k_inverse3<NBR><<<grid, threads, C::smem, st>>>(A);
+    IRK_LAUNCHED();
+    return IRK_OK;
+}
+
+// ---------------------------------------------------------------------------
+// 32 < nb <= 40: one warp per block with a split layout.  Lane l holds row l
+// (40 rotated positions, registers d[]) and a quarter of extra row 32 + l/4:
+// positions [10q, 10q + 10) with q = l % 4 (registers x[]).  In pivot step u
+// the extra-row entries of position u live in the lanes with q == u / 10 at
+// x[u % 10] (a static index), and the extra row's multiplier is broadcast
+// from that lane within its 4-lane group.  Rotating by 8 positions moves 8
+// of the 10 quarter values in from the next lane of the group (shuffles).
+// Rows nb..39 are identity padding, as in k_inverse3.
+// ---------------------------------------------------------------------------
+struct Inv4Cfg {
+    static constexpr int NBR = 40, LDX = 42, WARPS = 4;
+    static constexpr size_t warp_doubles = 2 * NBR + (size_t)NBR * LDX + NBR;
+    static constexpr size_t smem = WARPS * (warp_doubles * sizeof(double) + 2 * NBR * sizeof(int));
+};
+
+template <int MINB>
+__global__ void __launch_bounds__(32 * Inv4Cfg::WARPS, MINB) k_inverse4(InvArgs A) {
+    using C = Inv4Cfg;
+    constexpr int NBR = C::NBR, LDX = C::LDX;
+    extern __shared__ __align__(16) double sm4[];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    double* prow = sm4 + (size_t)warp * C::warp_doubles;
+    double* X = prow + 2 * NBR;
+    double* pvb = X + (size_t)NBR * LDX;
+    int* piv = reinterpret_cast<int*>(sm4 + (size_t)C::WARPS * C::warp_doubles) + warp * 2 * NBR;
+    int* invp = piv + NBR;
+    const int nb = A.nb;
+    const int P = (nb + 1) >> 1;
+    const int64_t bsz = (int64_t)nb * 2 * P;
+    const int q = lane & 3, e = lane >> 2, re = 32 + e;
+    const int gbase = lane & ~3, gnext = gbase | ((q + 1) & 3);
+    for (int64_t t = (int64_t)blockIdx.x * C::WARPS + warp; t < A.ntasks; t += (int64_t)gridDim.x * C::WARPS) {
+        const int64_t code = A.tasks[t];
+        const int k_st = (int)(code / A.T);
+        const int64_t j = code - (int64_t)k_st * A.T;
+        const double* srcd = A.D + (j * A.s + k_st) * bsz;
+        double d[NBR], x[10];
+        {
+            const double2* src = reinterpret_cast<const double2*>(srcd);
+#pragma unroll
+            for (int p = 0; p < NBR / 2; ++p) {
+                double2 v = make_double2(0.0, 0.0);
+                if (p < P) v = src[(int64_t)p * nb + lane];
+                if (2 * p + 1 >= nb) v.y = 0.0;
+                d[2 * p] = v.x;
+                d[2 * p + 1] = v.y;
+            }
+#pragma unroll
+            for (int i = 0; i < 10; ++i) {
+                const int c = 10 * q + i;
+                double v;
+                if (re < nb) v = (c < nb) ? srcd[((int64_t)(c >> 1) * nb + re) * 2 + (c & 1)] : 0.0;
+                else v = (c == re) ? 1.0 : 0.0;   // identity padding
+                x[i] = v;
+            }
+        }
+        int used_m = 0, used_e = 0, pstep_m = -1, pstep_e = -1;
+        // |.|_1 of the nb x nb part
+        auto stage_abs = [&]() {
+#pragma unroll
+            for (int c = 0; c < NBR; ++c) X[lane * LDX + c] = fabs(d[c]);
+#pragma unroll
+            for (int i = 0; i < 10; ++i) X[re * LDX + 10 * q + i] = fabs(x[i]);
+            __syncwarp();
+        };
+        auto norm_X = [&]() -> double {
+            double mx = -1.0;
+            int nan = 0;
+            for (int c = lane; c < nb; c += 32) {
+                double s4[4] = {0.0, 0.0, 0.0, 0.0};   // four independent chains
+                int r = 0;
+                for (; r + 4 <= nb; r += 4)
+#pragma unroll
+                    for (int h = 0; h < 4; ++h) s4[h] += fabs(X[(r + h) * LDX + c]);
+                for (; r < nb; ++r) s4[0] += fabs(X[r * LDX + c]);
+                const double sum = (s4[0] + s4[1]) + (s4[2] + s4[3]);
+                if (sum != sum) nan = 1;
+                mx = fmax(mx, sum);
+            }
+#pragma unroll
+            for (int o = 16; o; o >>= 1) {
+                mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+                nan |= __shfl_xor_sync(0xffffffffu, nan, o);
+            }
+            __syncwarp();
+            return nan ? __longlong_as_double(0x7ff8000000000000LL) : mx;
+        };
+        stage_abs();
+        const double n1 = norm_X();
+        auto step = [&](int k, auto uc) {
+            constexpr int u = decltype(uc)::value;
+            constexpr int uq = u / 10, ui = u % 10;
+            // candidates: own row first (smaller index wins ties), then the extra row
+            bool has = !used_m;
+            double best = fabs(d[u]);
+            int br = lane;
+            if (q == uq && !used_e) {
+                const double a = fabs(x[ui]);
+                if (!has || a > best) { best = a; br = re; has = true; }
+            }
+            const int pw = warp_pivot(has, best, br);
+            const int p = (pw == 0x7fffffff) ? k : pw;
+            // signed pivot straight from its owner lane: the reciprocal overlaps the row broadcast
+            const double pv = __shfl_sync(0xffffffffu, p < 32 ? d[u] : x[ui], p < 32 ? p : (((p - 32) << 2) | uq));
+            const double inv = 1.0 / pv;
+            double* pr = prow + (k & 1) * NBR;
+            if (p < 32) {
+                if (lane == p)
+#pragma unroll
+                    for (int c = 0; c < NBR; c += 2) *reinterpret_cast<double2*>(pr + c) = make_double2(d[c], d[c + 1]);
+            } else if (re == p) {
+#pragma unroll
+                for (int i = 0; i < 10; i += 2) *reinterpret_cast<double2*>(pr + 10 * q + i) = make_double2(x[i], x[i + 1]);
+            }
+            // extra row's column-u entry, from the group lane holding position u
+            const double fe = __shfl_sync(0xffffffffu, x[ui], gbase | uq);
+            __syncwarp();
+            if (lane == 0) { pvb[k] = pv; piv[k] = p; }
+            {
+                const bool is_p = lane == p;
+                if (is_p) { used_m = 1; pstep_m = k; }
+                const double a = is_p ? 0.0 : -d[u] * inv;
+                const double ck = is_p ? 1.0 : a;
+#pragma unroll
+                for (int c = 0; c < NBR; c += 2) {
+                    const double2 pc = *reinterpret_cast<const double2*>(pr + c);
+                    d[c] = (c == u) ? ck : fma(a, pc.x, d[c]);
+                    d[c + 1] = (c + 1 == u) ? ck : fma(a, pc.y, d[c + 1]);
+                }
+            }
+            {
+                const bool is_p = re == p;
+                if (is_p) { used_e = 1; pstep_e = k; }
+                const double a = is_p ? 0.0 : -fe * inv;
+                const double ck = is_p ? 1.0 : a;
+                const double* pq = pr + 10 * q;
+#pragma unroll
+                for (int i = 0; i < 10; i += 2) {
+                    const double2 pc = *reinterpret_cast<const double2*>(pq + i);
+                    x[i] = (q == uq && i == ui) ? ck : fma(a, pc.x, x[i]);
+                    x[i + 1] = (q == uq && i + 1 == ui) ? ck : fma(a, pc.y, x[i + 1]);
+                }
+            }
+        };
+#pragma unroll 1
+        for (int ch = 0; ch < NBR / 8; ++ch) {
+            static_for([&](auto uc) { step(ch * 8 + decltype(uc)::value, uc); },
+                       std::make_integer_sequence<int, 8>{});
+            double tmp[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) tmp[u] = d[u];
+#pragma unroll
+            for (int c = 0; c < NBR - 8; ++c) d[c] = d[c + 8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) d[NBR - 8 + u] = tmp[u];
+            // quarter rotation: new x[i] = position 10q + i + 8
+            double nx[10];
+            nx[0] = x[8];
+            nx[1] = x[9];
+#pragma unroll
+            for (int i = 2; i < 10; ++i) nx[i] = __shfl_sync(0xffffffffu, x[i - 2], gnext);
+#pragma unroll
+            for (int i = 0; i < 10; ++i) x[i] = nx[i];
+        }
+        __syncwarp();
+        // det = exp(sum log|pivot|) (slogdet); |pivot| == 0 -> singular
+        double lg = 0.0;
+        int zero = 0;
+        for (int m = lane; m < nb; m += 32) {
+            const double pv = pvb[m];
+            lg += log(fabs(pv));
+            zero |= pv == 0.0;
+        }
+#pragma unroll
+        for (int o = 16; o; o >>= 1) {
+            lg += __shfl_xor_sync(0xffffffffu, lg, o);
+            zero |= __shfl_xor_sync(0xffffffffu, zero, o);
+        }
+        const double logdet = lg;
+        // stage row k of inv(D) = (row pivoted at step k) / pivot_k with the column
+        // permutation folded in: inv(D)[k][piv[m]] = X[p_k][m]
+        int pc[NBR];
+#pragma unroll
+        for (int m = 0; m < NBR; m += 4) {
+            const int4 v = *reinterpret_cast<const int4*>(piv + m);
+            pc[m] = v.x; pc[m + 1] = v.y; pc[m + 2] = v.z; pc[m + 3] = v.w;
+        }
+        if (pstep_m >= 0 && pstep_m < nb) {
+            const double rs = 1.0 / pvb[pstep_m];
+#pragma unroll
+            for (int c = 0; c < NBR; ++c)
+                if (c < nb) X[pstep_m * LDX + pc[c]] = d[c] * rs;
+        }
+        if (pstep_e >= 0 && pstep_e < nb) {
+            const double rs = 1.0 / pvb[pstep_e];
+#pragma unroll
+            for (int i = 0; i < 10; ++i)
+                if (10 * q + i < nb) X[pstep_e * LDX + piv[10 * q + i]] = x[i] * rs;
+        }
+        __syncwarp();
+        double2* dst = reinterpret_cast<double2*>(A.Dinv + (j * A.s + k_st) * bsz);
+        for (int r = lane; r < nb; r += 32)
+            for (int p = 0; p < P; ++p) {
+                double2 v = *reinterpret_cast<const double2*>(X + r * LDX + 2 * p);
+                if (2 * p + 1 >= nb) v.y = 0.0;
+                dst[(int64_t)p * nb + r] = v;
+            }
+        __syncwarp();
+        const double n2 = norm_X();
+        if (lane == 0) {
+            const double det = exp(logdet);
+            const double cond = n1 * n2;
+            const bool bad = zero || det == 0.0 || !isfinite(det) || !(cond <= 1e14);
+            if (bad) atomicMin(A.fail_key, (unsigned long long)code);
+        }
+        __syncwarp();
+    }
+}
+
+template <int MINB>
+static int launch4_t(const irk_ctx* ctx, const InvArgs& A, cudaStream_t st) {
+    using C = Inv4Cfg;
+    static bool attr = false;
+    if (!attr) {
+        IRK_CK(cudaFuncSetAttribute(k_inverse4<MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::smem));
+        IRK_CK(cudaFuncSetAttribute(k_inverse4<MINB>, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+        attr = true;
+    }
+    const int threads = 32 * C::WARPS;
+    int per_sm = 1;
+    IRK_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_inverse4<MINB>, threads, C::smem));
+    const int64_t need = (A.ntasks + C::WARPS - 1) / C::WARPS;
+    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(need, (int64_t)ctx->num_sms * std::max(per_sm, 1)));
+    k_inverse4<MINB><<<grid, threads, C::smem, st>>>(A);
+    IRK_LAUNCHED();
+    return IRK_OK;
+}
+
+static int launch4(const irk_ctx* ctx, const InvArgs& A, cudaStream_t st) {
+    const char* e = getenv("IRK_INV4_MINB");   // tuning knob
+    switch (e ? atoi(e) : 1) {
+        case 2: return launch4_t<2>(ctx, A, st);
+        case 3: return launch4_t<3>(ctx, A, st);
+        case 4: return launch4_t<4>(ctx, A, st);
+        default: return launch4_t<1>(ctx, A, st);
     }
 }
 
@@ -515,11 +1006,12 @@ int launch_inverse(const irk_ctx* ctx, const int32_t* tasks, int64_t ntasks, int
                    const double* D, double* Dinv, unsigned long long* fail_key, cudaStream_t st) {
     if (ntasks <= 0) return IRK_OK;
     InvArgs A{tasks, ntasks, T, s, nb, D, Dinv, fail_key};
-    if (nb == 24) return launch_t<24, true>(ctx, A, st);
-    if (nb == 40) return launch2<40>(ctx, A, st);
+    if (nb <= 8) return launch3<8>(ctx, A, st);
+    if (nb <= 16) return launch3<16>(ctx, A, st);
+    if (nb <= 24) return launch3<24>(ctx, A, st);
+    if (nb <= 32) return launch3<32>(ctx, A, st);
+    if (nb <= 40) return launch4(ctx, A, st);
     if (nb == 50) return launch2<50>(ctx, A, st);
-    if (nb <= 16) return launch_t<16, false>(ctx, A, st);
-    if (nb <= 32) return launch_t<32, false>(ctx, A, st);
     if (nb <= 64) return launch_t<64, false>(ctx, A, st);
     return IRK_EINVAL;
 }

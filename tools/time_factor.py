@@ -1,0 +1,42 @@
+"""Factor a config once (warm), then once more for timing; run under
+`ncu --metrics gpu__time_duration.sum` to get per-kernel durations.
+
+usage: python tools/time_factor.py [config] [ordering]
+"""
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+
+import torch  # noqa: E402
+
+from paper_1701_07181_b200 import workloads as W  # noqa: E402
+from paper_1701_07181_b200.blocks import DevicePattern  # noqa: E402
+from paper_1701_07181_b200.krylov import GmresConfig  # noqa: E402
+from paper_1701_07181_b200.solver import StageSolver  # noqa: E402
+from paper_1701_07181_b200.tableau import builtin_tableau, derive  # noqa: E402
+
+
+def main():
+    ci = int(sys.argv[1]) if len(sys.argv) > 1 else 1
+    order = sys.argv[2] if len(sys.argv) > 2 else "color"
+    cfg = W.CONFIGS[ci].scaled(ordering=order)
+    wl = W.make_workload(cfg, jnorm=1.0)
+    der = derive(builtin_tableau(cfg.scheme))
+    dt = cfg.dt_norm / 2.4496432463318416
+    dpat = DevicePattern(wl.pattern.indptr, wl.pattern.indices, wl.pattern.diag_pos)
+    solver = StageSolver(dpat, wl.J, wl.M, der.a_inv, dt, kind=cfg.precond, shifts=der.shifts,
+                         gmres_cfg=GmresConfig(rel_tol=cfg.rtol, restart=cfg.restart))
+    solver.factorize()
+    torch.cuda.synchronize()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record()
+    for _ in range(3):
+        solver.factorize()
+    b.record()
+    torch.cuda.synchronize()
+    print(f"factorize {a.elapsed_time(b) / 3:.3f} ms", flush=True)
+
+
+if __name__ == "__main__":
+    main()
