@@ -25,6 +25,7 @@
 #include <vector>
 
 #include "irk_internal.cuh"
+#include "pipeline.cuh"
 
 namespace irk {
 
@@ -595,6 +596,261 @@ static size_t factor_smem(int nbp4, int ld, int KC) {
            sizeof(int) * (2 * nbp4 + 16);
 }
 
+// ---------------------------------------------------------------------------
+// Schur phase, stage-uncoupled simplified ILU(0) with stage-shared off-diagonal
+// blocks (B_ji = alpha J_ji for every stage; the benchmark's path).
+//
+// One CTA per element j and all S stages; warp w owns the 8-row strip
+// [8w, 8w+8) of every nb x nb block (NB = 8 * warps).  Per kept lower
+// neighbour i the CTA bulk-copies J_ji, J_ij and Dinv_{k,i} (k < S) into
+// shared memory -- one cp.async.bulk per column pair, at a pair stride of
+// 2 NB + 8 doubles so that both DMMA operand fragments read conflict-free --
+// then
+//   T_k = J_ji Dinv_{k,i}          (DMMA m8n8k4, J_ji fragments shared by the S stages)
+//   L_k = alpha T_k  -> global      (numba_backend.py:58-61, L_ji = B_ji D_i^-1)
+//   D_k += (-alpha L_k) J_ij        (D_j -= L_ji U_ij, U_ij = alpha J_ij)
+// with -alpha L_k staged back into the (consumed) Dinv slots as the A operand.
+// The pivot accumulators D_k = fl(alpha J_jj) + fl(coef_k M_j) stay in
+// registers across neighbours and are stored once for the batched inverse.
+// ---------------------------------------------------------------------------
+template <int NB>
+struct SchurGeo {
+    static constexpr int NT = NB / 8;          // 8x8 tiles per strip row = warps
+    static constexpr int NP = NB / 2;          // column pairs
+    static constexpr int LDP = 2 * NB + 8;     // pair stride (doubles), = 8 mod 16
+    static constexpr int SLOT = NP * LDP;      // doubles per staged block
+    // warp-private A' strip (8 x NB, row-major): row stride = 4 or 12 mod 16 makes
+    // both the C-fragment double2 stores and the A-fragment loads conflict-free
+    static constexpr int LDA = ((NB + 3) / 4 * 4) % 16 == 4 || ((NB + 3) / 4 * 4) % 16 == 12
+                                   ? (NB + 3) / 4 * 4 : (NB + 3) / 4 * 4 + 4;
+    static_assert(NT * 8 * LDA <= SLOT, "A' strips must fit in one staged block");
+};
+
+__device__ __forceinline__ void fence_proxy_async_smem() {
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+
+template <int S, int NB>
+__global__ void __launch_bounds__(4 * NB) k_schur(FactorArgs F, const int32_t* __restrict__ elems, int64_t nelem) {
+    using Gm = SchurGeo<NB>;
+    constexpr int NT = Gm::NT, NP = Gm::NP, LDP = Gm::LDP, SLOT = Gm::SLOT;
+    constexpr int64_t BSZ = (int64_t)NB * NB;
+    constexpr int SJ = 0, SU = 1;   // slots: J_ji, J_ij, then Dinv_k / A'_k at 2 + k
+    extern __shared__ __align__(128) double shs[];
+    __shared__ __align__(8) uint64_t bars[S + 2];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int fr = lane >> 2, fk = lane & 3;
+    const int r0 = warp * 8;
+    const double* J = F.J[0];
+    if (threadIdx.x == 0) {
+        for (int b = 0; b < S + 2; ++b) mbar_init(&bars[b], 1);
+        fence_mbar_init();
+    }
+    __syncthreads();
+    uint32_t phases = 0;   // bit b: parity of the next completion of slot b
+    auto wait_slot = [&](int b) {
+        mbar_wait(&bars[b], (phases >> b) & 1u);
+        phases ^= 1u << b;
+    };
+    // warp 0 refills slot b with a block (one bulk copy per column pair); the
+    // caller has made every earlier generic access to the slot CTA-visible
+    auto fill = [&](int b, const double* src) {
+        if (warp == 0) {
+            if (lane == 0) {
+                fence_proxy_async_smem();
+                mbar_expect_tx(&bars[b], (uint32_t)(NP * NB * 16));
+            }
+            __syncwarp();
+            for (int p = lane; p < NP; p += 32)
+                bulk_g2s(shs + (size_t)b * SLOT + p * LDP, src + (int64_t)p * NB * 2, NB * 16, &bars[b]);
+        }
+    };
+    // a "unit" is a (element, lower neighbour q) pair whose Schur update runs on
+    // the tensor cores (both blocks kept); units are visited in CTA order
+    struct Unit { int64_t it; int q; int i, tq; };
+    auto find_unit = [&](int64_t it, int q) -> Unit {
+        for (; it < nelem; it += gridDim.x) {
+            const int j = elems[it];
+            const int dpos = F.diag[j];
+            if (q < 0) q = F.indptr[j];
+            for (; q < dpos; ++q) {
+                const int tq = F.tpos[q];
+                if (F.keep[q] && tq >= 0 && F.keep[tq]) return Unit{it, q, F.indices[q], tq};
+            }
+            q = -1;
+        }
+        return Unit{-1, -1, -1, -1};
+    };
+    auto src_dinv = [&](const Unit& u, int k) { return F.Dinv + ((int64_t)u.i * S + k) * BSZ; };
+    Unit nxt = find_unit(blockIdx.x, -1);
+    if (nxt.it >= 0) {
+        fill(SJ, J + (int64_t)nxt.q * BSZ);
+        fill(SU, J + (int64_t)nxt.tq * BSZ);
+#pragma unroll
+        for (int k = 0; k < S; ++k) fill(2 + k, src_dinv(nxt, k));
+    }
+    auto frag_a = [&](const double* slotp, int kk) -> double {   // A(r0 + fr, 4kk + fk)
+        return slotp[((4 * kk + fk) >> 1) * LDP + 2 * (r0 + fr) + (fk & 1)];
+    };
+    auto frag_b = [&](const double* slotp, int kk, int t) -> double {   // B(4kk + fk, 8t + fr)
+        return slotp[((8 * t + fr) >> 1) * LDP + 2 * (4 * kk + fk) + (fr & 1)];
+    };
+    auto gl_off = [&](int t) -> int64_t { return (int64_t)(4 * t + fk) * NB + r0 + fr; };   // in double2
+
+    for (int64_t it = blockIdx.x; it < nelem; it += gridDim.x) {
+        const int j = elems[it];
+        const int dpos = F.diag[j];
+        double dacc[S][NT][2];
+        // ---- D_k = fl(alpha J_jj) + fl(coef_k M_j)  (build_stage_matrix, precond.py:48-54)
+        {
+            const bool keep_d = F.keep[dpos] != 0;
+            const double2* Jd = reinterpret_cast<const double2*>(J + (int64_t)dpos * BSZ);
+            const double2* Md = F.M ? reinterpret_cast<const double2*>(F.M + (int64_t)j * BSZ) : nullptr;
+#pragma unroll
+            for (int t = 0; t < NT; ++t) {
+                const double2 jv = Jd[gl_off(t)];
+                const double2 mv = Md ? Md[gl_off(t)] : make_double2(0.0, 0.0);
+#pragma unroll
+                for (int k = 0; k < S; ++k) {
+                    double x0 = __dmul_rn(F.alpha, jv.x), x1 = __dmul_rn(F.alpha, jv.y);
+                    if (Md) {
+                        x0 = __dadd_rn(x0, __dmul_rn(F.coef[k], mv.x));
+                        x1 = __dadd_rn(x1, __dmul_rn(F.coef[k], mv.y));
+                    }
+                    dacc[k][t][0] = keep_d ? x0 : 0.0;
+                    dacc[k][t][1] = keep_d ? x1 : 0.0;
+                }
+            }
+        }
+        const int q0 = F.indptr[j];
+        const int lq0 = F.lptr[j];
+        for (int q = q0; q < dpos; ++q) {
+            double* Lout = F.L + (int64_t)(lq0 + (q - q0)) * S * BSZ;
+            if (!(nxt.it == it && nxt.q == q)) {
+                // not a unit: the reference never forms L_ji D_i^-1 here, so L stays
+                // B_ji (upper block dropped) or 0 (lower block dropped); D unchanged
+                const int tq = F.tpos[q];
+                const bool keep_lo = F.keep[q] != 0;
+                const bool keep_up = tq >= 0 && F.keep[tq] != 0;
+                const double* Jq = J + (int64_t)q * BSZ;
+                for (int64_t e = threadIdx.x; e < S * BSZ; e += blockDim.x) {
+                    const int64_t o = e % BSZ;
+                    Lout[e] = (keep_lo && !keep_up) ? F.alpha * Jq[o] : 0.0;
+                }
+                continue;
+            }
+            const Unit cur = nxt;
+            nxt = find_unit(it, q + 1);
+            const bool more = nxt.it >= 0;
+#pragma unroll
+            for (int k = 0; k < S; ++k) {
+                // T_k = J_ji Dinv_k on this warp's strip
+                if (k == 0) wait_slot(SJ);
+                wait_slot(2 + k);
+                double acc[NT][2];
+#pragma unroll
+                for (int t = 0; t < NT; ++t) acc[t][0] = acc[t][1] = 0.0;
+                const double* Dk = shs + (size_t)(2 + k) * SLOT;
+#pragma unroll 2
+                for (int kk = 0; kk < NB / 4; ++kk) {
+                    const double a = frag_a(shs + SJ * SLOT, kk);
+#pragma unroll
+                    for (int t = 0; t < NT; ++t) dmma(acc[t][0], acc[t][1], a, frag_b(Dk, kk, t));
+                }
+                // L_k = alpha T_k -> global (numba_backend.py:58-61)
+                double2* Lk = reinterpret_cast<double2*>(Lout + (int64_t)k * BSZ);
+#pragma unroll
+                for (int t = 0; t < NT; ++t) {
+                    acc[t][0] *= F.alpha;
+                    acc[t][1] *= F.alpha;
+                    Lk[gl_off(t)] = make_double2(acc[t][0], acc[t][1]);
+                }
+                __syncthreads();   // all warps: GEMM1_k done (Dinv_k slot), GEMM2_{k-1} done (A'_{k-1})
+                if (more && k > 0) fill(2 + k - 1, src_dinv(nxt, k - 1));
+                if (more && k == S - 1) fill(SJ, J + (int64_t)nxt.q * BSZ);
+                // A'_k = -alpha L_k into the consumed Dinv_k slot (warp-private row-major strip)
+                double* Ak = shs + (size_t)(2 + k) * SLOT + warp * 8 * Gm::LDA;
+#pragma unroll
+                for (int t = 0; t < NT; ++t)
+                    *reinterpret_cast<double2*>(Ak + fr * Gm::LDA + 8 * t + 2 * fk) =
+                        make_double2(-F.alpha * acc[t][0], -F.alpha * acc[t][1]);
+                __syncwarp();
+                if (k == 0) wait_slot(SU);
+                // D_k += A'_k J_ij   (D_j -= L_ji U_ij, U_ij = alpha J_ij)
+#pragma unroll 2
+                for (int kk = 0; kk < NB / 4; ++kk) {
+                    const double a = Ak[fr * Gm::LDA + 4 * kk + fk];
+#pragma unroll
+                    for (int t = 0; t < NT; ++t) dmma(dacc[k][t][0], dacc[k][t][1], a, frag_b(shs + SU * SLOT, kk, t));
+                }
+            }
+            __syncthreads();       // all warps: GEMM2_{S-1} done (A'_{S-1}, J_ij)
+            if (more) {
+                fill(2 + S - 1, src_dinv(nxt, S - 1));
+                fill(SU, J + (int64_t)nxt.tq * BSZ);
+            }
+            (void)cur;
+        }
+        // ---- pivot blocks -> F.Dst for the batched inverse
+#pragma unroll
+        for (int k = 0; k < S; ++k) {
+            double2* Dk = reinterpret_cast<double2*>(F.Dst + ((int64_t)j * S + k) * BSZ);
+#pragma unroll
+            for (int t = 0; t < NT; ++t) Dk[gl_off(t)] = make_double2(dacc[k][t][0], dacc[k][t][1]);
+        }
+    }
+}
+
+template <int S, int NB>
+static int launch_schur_t(const irk_ctx* ctx, const FactorArgs& F, const int32_t* elems, int64_t nelem,
+                          cudaStream_t st) {
+    const size_t smem = sizeof(double) * (size_t)(S + 2) * SchurGeo<NB>::SLOT;
+    static bool attr = false;
+    if (!attr) {
+        IRK_CK(cudaFuncSetAttribute(k_schur<S, NB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        IRK_CK(cudaFuncSetAttribute(k_schur<S, NB>, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+        attr = true;
+    }
+    int per_sm = 1;
+    IRK_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_schur<S, NB>, 4 * NB, smem));
+    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(nelem, (int64_t)ctx->num_sms * std::max(per_sm, 1)));
+    k_schur<S, NB><<<grid, 4 * NB, smem, st>>>(F, elems, nelem);
+    IRK_LAUNCHED();
+    return IRK_OK;
+}
+
+template <int S>
+static int launch_schur_s(const irk_ctx* ctx, const FactorArgs& F, const int32_t* elems, int64_t nelem,
+                          cudaStream_t st) {
+    switch (F.nb) {
+        case 16: return launch_schur_t<S, 16>(ctx, F, elems, nelem, st);
+        case 24: return launch_schur_t<S, 24>(ctx, F, elems, nelem, st);
+        case 32: return launch_schur_t<S, 32>(ctx, F, elems, nelem, st);
+        case 40: return launch_schur_t<S, 40>(ctx, F, elems, nelem, st);
+        case 48: return launch_schur_t<S, 48>(ctx, F, elems, nelem, st);
+        case 56: return launch_schur_t<S, 56>(ctx, F, elems, nelem, st);
+        case 64: return launch_schur_t<S, 64>(ctx, F, elems, nelem, st);
+        default: return IRK_EINVAL;
+    }
+}
+
+static bool schur_eligible(const irk_factor* f, const FactorArgs& F) {
+    if (getenv("IRK_NO_SCHUR")) return false;   // A/B switch for the generic kernel
+    return f->kind == IRK_FACTOR_UNCOUPLED && f->simplified && f->u_shared && F.Dst != nullptr &&
+           F.nb % 8 == 0 && F.nb >= 16 && F.nb <= 64 && F.s <= 4;
+}
+
+static int launch_schur(const irk_ctx* ctx, const FactorArgs& F, const int32_t* elems, int64_t nelem,
+                        cudaStream_t st) {
+    switch (F.s) {
+        case 1: return launch_schur_s<1>(ctx, F, elems, nelem, st);
+        case 2: return launch_schur_s<2>(ctx, F, elems, nelem, st);
+        case 3: return launch_schur_s<3>(ctx, F, elems, nelem, st);
+        case 4: return launch_schur_s<4>(ctx, F, elems, nelem, st);
+        default: return IRK_EINVAL;
+    }
+}
+
 int launch_inverse(const irk_ctx* ctx, const int32_t* tasks, int64_t ntasks, int64_t T, int s, int nb,
                    const double* D, double* Dinv, unsigned long long* fail_key, cudaStream_t st);
 
@@ -617,7 +873,11 @@ static int launch_levels(const irk_factor* f, FactorArgs& F, const irk_sched& sc
         F.tasks = sched.d_order + lo;
         F.ntasks = hi - lo;
         const int grid = (int)std::min<int64_t>(hi - lo, (int64_t)f->ctx->num_sms * 8);
-        if (split) {
+        if (split && schur_eligible(f, F)) {
+            // level tasks are stage-major (k*T + e, skew 0): the first 1/s are the elements
+            IRK_TRY(launch_schur(f->ctx, F, F.tasks, F.ntasks / F.s, st));
+            IRK_TRY(launch_inverse(f->ctx, F.tasks, F.ntasks, F.T, F.s, F.nb, F.Dst, F.Dinv, F.fail_key, st));
+        } else if (split) {
             k_factor<MAXT, false><<<grid, 256, smem, st>>>(F);
             IRK_LAUNCHED();
             IRK_TRY(launch_inverse(f->ctx, F.tasks, F.ntasks, F.T, F.s, F.nb, F.Dst, F.Dinv, F.fail_key, st));
