@@ -53,6 +53,25 @@ __device__ __forceinline__ void block_store_partials(const double* vals, int nv,
     __syncthreads();
 }
 
+// block_store_partials with a compile-time bound: vals[] stays in registers
+template <int NVM>
+__device__ __forceinline__ void block_store_partials_t(const double* vals, int nv, double* red, double* out) {
+    const int w = threadIdx.x >> 5, l = threadIdx.x & 31, nw = blockDim.x >> 5;
+#pragma unroll
+    for (int v = 0; v < NVM; ++v)
+        if (v < nv) {
+            const double s = warp_sum(vals[v]);
+            if (l == 0) red[v * nw + w] = s;
+        }
+    __syncthreads();
+    for (int v = threadIdx.x; v < nv; v += blockDim.x) {
+        double s = 0.0;
+        for (int i = 0; i < nw; ++i) s += red[v * nw + i];
+        out[(int64_t)v * gridDim.x + blockIdx.x] = s;
+    }
+    __syncthreads();
+}
+
 __device__ __forceinline__ void chunk_range(int64_t n, int64_t& lo, int64_t& hi) {
     const int64_t per = ((n + gridDim.x - 1) / gridDim.x + 1) & ~int64_t(1);
     lo = std::min<int64_t>(n, per * blockIdx.x);
@@ -124,6 +143,128 @@ __global__ void __launch_bounds__(VB) k_update(const double* __restrict__ V, int
     block_store_partials(&nrm, 1, red, partials);
 }
 
+// ---- fused CGS2 passes with in-kernel (last-CTA) reductions ---------------
+//
+// The CTA that finishes last reduces the per-CTA partials in a fixed order
+// (one warp per value, lanes strided over CTAs, then a shuffle tree), so the
+// results stay bitwise reproducible; the counter is reset for the next use.
+__device__ __forceinline__ bool last_cta(unsigned* counter) {
+    __shared__ bool last;
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) last = atomicAdd(counter, 1u) == gridDim.x - 1;
+    __syncthreads();
+    return last;
+}
+
+__device__ __forceinline__ void reduce_partials_cta(const double* partials, int nblk, int nv, double* out,
+                                                    unsigned* counter) {
+    __threadfence();
+    const int w = threadIdx.x >> 5, l = threadIdx.x & 31, nw = blockDim.x >> 5;
+    for (int v = w; v < nv; v += nw) {
+        double s = 0.0;
+        for (int b = l; b < nblk; b += 32) s += __ldcg(partials + (int64_t)v * nblk + b);
+        s = warp_sum(s);
+        if (l == 0) out[v] = s;
+    }
+    if (threadIdx.x == 0) *counter = 0u;
+}
+
+// pass 1: out[i] = V_i . w (i < nv), out[nv] = w . w
+__global__ void __launch_bounds__(VB) k_multidot_r(const double* __restrict__ V, int64_t ldv, int nv,
+                                                   const double* __restrict__ w, int64_t n, double* partials,
+                                                   double* out, unsigned* counter) {
+    __shared__ double red[(VGROUP + 1) * (VB / 32)];
+    int64_t lo, hi;
+    chunk_range(n, lo, hi);
+    for (int v0 = 0;; v0 += VGROUP) {
+        const int cnt = min(VGROUP, nv - v0);
+        const bool with_ww = (v0 == 0);
+        double acc[VGROUP + 1];
+#pragma unroll
+        for (int i = 0; i <= VGROUP; ++i) acc[i] = 0.0;
+        for (int64_t e = lo + threadIdx.x; e < hi; e += VB) {
+            const double wv = w[e];
+#pragma unroll
+            for (int i = 0; i < VGROUP; ++i)
+                if (i < cnt) acc[i] = fma(V[(int64_t)(v0 + i) * ldv + e], wv, acc[i]);
+            if (with_ww) acc[VGROUP] = fma(wv, wv, acc[VGROUP]);
+        }
+        if (cnt > 0) block_store_partials_t<VGROUP>(acc, cnt, red, partials + (int64_t)v0 * gridDim.x);
+        if (with_ww) block_store_partials_t<1>(acc + VGROUP, 1, red, partials + (int64_t)nv * gridDim.x);
+        if (v0 + VGROUP >= nv) break;
+    }
+    if (last_cta(counter)) reduce_partials_cta(partials, gridDim.x, nv + 1, out, counter);
+}
+
+// pass 2: w' = w - V h (h = h1[0..nv)); out[i] = V_i . w', out[nv] = w' . w'.
+// V_i[e] is read once for both the update and the dots (kept in registers).
+template <int NVM>
+__global__ void __launch_bounds__(VB) k_update_dots_r(const double* __restrict__ V, int64_t ldv, int nv,
+                                                      const double* __restrict__ h, double* __restrict__ w,
+                                                      int64_t n, double* partials, double* out,
+                                                      unsigned* counter) {
+    __shared__ double hs[NVM];
+    __shared__ double red[(NVM + 1) * (VB / 32)];
+    for (int i = threadIdx.x; i < nv; i += blockDim.x) hs[i] = h[i];
+    __syncthreads();
+    int64_t lo, hi;
+    chunk_range(n, lo, hi);
+    double d[NVM + 1];
+#pragma unroll
+    for (int i = 0; i <= NVM; ++i) d[i] = 0.0;
+    for (int64_t e = lo + threadIdx.x; e < hi; e += VB) {
+        double vv[NVM];
+        double acc = w[e];
+#pragma unroll
+        for (int i = 0; i < NVM; ++i)
+            if (i < nv) {
+                vv[i] = V[(int64_t)i * ldv + e];
+                acc -= hs[i] * vv[i];
+            }
+        w[e] = acc;
+#pragma unroll
+        for (int i = 0; i < NVM; ++i)
+            if (i < nv) d[i] = fma(vv[i], acc, d[i]);
+        d[NVM] = fma(acc, acc, d[NVM]);
+    }
+    block_store_partials_t<NVM>(d, nv, red, partials);
+    block_store_partials_t<1>(d + NVM, 1, red, partials + (int64_t)nv * gridDim.x);   // w'.w' after the dots
+    if (last_cta(counter)) reduce_partials_cta(partials, gridDim.x, nv + 1, out, counter);
+}
+
+// pass 3 (DGKS, decided on the device): if ||w'|| < eta ||w||, w'' = w' - V h2
+// and out[0] = w''.w'', out[1] = 1; else w'' = w' (untouched), out[0] = w'.w',
+// out[1] = 0.  ww0 = w.w (pass 1), h2[0..nv) and h2[nv] = w'.w' (pass 2).
+__global__ void __launch_bounds__(VB) k_update_cond_r(const double* __restrict__ V, int64_t ldv, int nv,
+                                                      const double* __restrict__ ww0, const double* __restrict__ h2,
+                                                      double eta, double* __restrict__ w, int64_t n,
+                                                      double* partials, double* out, unsigned* counter) {
+    extern __shared__ double hs[];
+    __shared__ double red[VB / 32];
+    const bool reorth = sqrt(h2[nv]) < eta * sqrt(*ww0);
+    if (!reorth) {
+        if (blockIdx.x == 0 && threadIdx.x == 0) { out[0] = h2[nv]; out[1] = 0.0; }
+        return;
+    }
+    for (int i = threadIdx.x; i < nv; i += blockDim.x) hs[i] = h2[i];
+    __syncthreads();
+    int64_t lo, hi;
+    chunk_range(n, lo, hi);
+    double nrm = 0.0;
+    for (int64_t e = lo + threadIdx.x; e < hi; e += VB) {
+        double acc = w[e];
+        for (int i = 0; i < nv; ++i) acc -= hs[i] * V[(int64_t)i * ldv + e];
+        w[e] = acc;
+        nrm = fma(acc, acc, nrm);
+    }
+    block_store_partials(&nrm, 1, red, partials);
+    if (last_cta(counter)) {
+        reduce_partials_cta(partials, gridDim.x, 1, out, counter);
+        if (threadIdx.x == 0) out[1] = 1.0;
+    }
+}
+
 // y = x / d  (d on host)
 __global__ void k_scale_div(const double* __restrict__ x, double* __restrict__ y, int64_t n, double d) {
     for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x)
@@ -185,14 +326,38 @@ struct Workspace {
     double* tmp = nullptr;
     double* partials = nullptr;
     double* small = nullptr;   // device scratch for reduced values / coefficients
+    unsigned* counters = nullptr;   // last-CTA tickets of the fused passes
     cudaStream_t st = nullptr;
     ~Workspace() {
         if (V) cudaFreeAsync(V, st);
         if (tmp) cudaFreeAsync(tmp, st);
         if (partials) cudaFreeAsync(partials, st);
         if (small) cudaFreeAsync(small, st);
+        if (counters) cudaFreeAsync(counters, st);
     }
 };
+
+// Fused CGS2 step on device: pass 1 h1 = V^T w (+ w.w); pass 2 w' = w - V h1
+// with h2 = V^T w' (+ w'.w') in the same sweep; pass 3 the DGKS correction
+// w'' = w' - V h2, applied only if ||w'|| < eta ||w|| (decided on the device).
+// out layout: [h1 (nv+1) | h2 (nv+1) | w''.w'', reorth flag].  nv <= 32.
+static int cgs2_fused(const irk_ctx* ctx, int64_t n, int nv, const double* V, double* w, double eta,
+                      double* partials, unsigned* counters, double* out, cudaStream_t st) {
+    const int nb = vec_blocks(ctx);
+    double* h1 = out;
+    double* h2 = out + nv + 1;
+    double* n3 = out + 2 * (nv + 1);
+    k_multidot_r<<<nb, VB, 0, st>>>(V, n, nv, w, n, partials, h1, counters);
+    IRK_LAUNCHED();
+    if (nv <= 8) k_update_dots_r<8><<<nb, VB, 0, st>>>(V, n, nv, h1, w, n, partials, h2, counters + 1);
+    else if (nv <= 16) k_update_dots_r<16><<<nb, VB, 0, st>>>(V, n, nv, h1, w, n, partials, h2, counters + 1);
+    else k_update_dots_r<32><<<nb, VB, 0, st>>>(V, n, nv, h1, w, n, partials, h2, counters + 1);
+    IRK_LAUNCHED();
+    k_update_cond_r<<<nb, VB, sizeof(double) * nv, st>>>(V, n, nv, h1 + nv, h2, eta, w, n, partials, n3,
+                                                         counters + 2);
+    IRK_LAUNCHED();
+    return IRK_OK;
+}
 
 static int multidot(const irk_ctx* ctx, int64_t n, int nv, const double* V, int64_t ldv, const double* w,
                     double* partials, double* out, cudaStream_t st) {
@@ -305,11 +470,14 @@ int irk_gmres(irk_ctx* ctx, int64_t n, irk_linop op, irk_linop pre, irk_allreduc
     IRK_CK(cudaMallocAsync(&ws.V, sizeof(double) * n * (restart + 1), st));
     IRK_CK(cudaMallocAsync(&ws.tmp, sizeof(double) * n, st));
     IRK_CK(cudaMallocAsync(&ws.partials, sizeof(double) * nblk * (restart + 2) * 2, st));
-    IRK_CK(cudaMallocAsync(&ws.small, sizeof(double) * 4 * (restart + 4), st));
+    IRK_CK(cudaMallocAsync(&ws.small, sizeof(double) * 6 * (restart + 4), st));
+    IRK_CK(cudaMallocAsync(&ws.counters, sizeof(unsigned) * 4, st));
+    IRK_CK(cudaMemsetAsync(ws.counters, 0, sizeof(unsigned) * 4, st));
     double* hdev = ws.small;                       // restart+2
     double* ndev = ws.small + (restart + 2);       // 2
     double* cdev = ws.small + 2 * (restart + 4);   // restart+1 coefficients
-    std::vector<double> hbuf(restart + 4);
+    double* fdev = ws.small + 3 * (restart + 4);   // fused CGS2 outputs, 2 (restart+1) + 2
+    std::vector<double> hbuf(2 * (restart + 4));
     auto V = [&](int i) { return ws.V + (int64_t)i * n; };
     const int g1 = grid_1d(ctx, n);
 
@@ -402,6 +570,19 @@ int irk_gmres(irk_ctx* ctx, int64_t n, irk_linop op, irk_linop pre, irk_allreduc
                 IRK_TRY(call(op, V(j), w));
             }
             stats->operator_applies += 1;
+            double nw;
+            if (!allreduce && j + 1 <= 32) {
+                // fused CGS2 (3 passes, DGKS decided on the device), one host sync
+                const int nv = j + 1;
+                IRK_TRY(cgs2_fused(ctx, n, nv, ws.V, w, eta, ws.partials, ws.counters, fdev, st));
+                IRK_CK(cudaMemcpyAsync(hbuf.data(), fdev, sizeof(double) * (2 * (nv + 1) + 2),
+                                       cudaMemcpyDeviceToHost, st));
+                IRK_CK(cudaStreamSynchronize(st));
+                const bool reorth = hbuf[2 * (nv + 1) + 1] != 0.0;
+                for (int i = 0; i <= j; ++i) Hc(i, j) = hbuf[i] + (reorth ? hbuf[nv + 1 + i] : 0.0);
+                if (reorth) stats->reorth_passes += 1;
+                nw = std::sqrt(hbuf[2 * (nv + 1)]);
+            } else {
             // classical Gram-Schmidt: h = V^T w (+ w.w), then w -= V h (+ w.w)
             IRK_TRY(multidot(ctx, n, j + 1, ws.V, n, w, ws.partials, hdev, st));
             IRK_TRY(ar(hdev, j + 2));
@@ -413,7 +594,7 @@ int irk_gmres(irk_ctx* ctx, int64_t n, irk_linop op, irk_linop pre, irk_allreduc
             IRK_CK(cudaStreamSynchronize(st));
             const double norm_before = std::sqrt(hbuf[j + 1]);
             for (int i = 0; i <= j; ++i) Hc(i, j) = hbuf[i];
-            double nw = std::sqrt(nrm2);
+            nw = std::sqrt(nrm2);
             if (nw < eta * norm_before) {
                 // DGKS second pass
                 IRK_TRY(multidot(ctx, n, j + 1, ws.V, n, w, ws.partials, hdev, st));
@@ -426,6 +607,7 @@ int irk_gmres(irk_ctx* ctx, int64_t n, irk_linop op, irk_linop pre, irk_allreduc
                 for (int i = 0; i <= j; ++i) Hc(i, j) += hbuf[i];
                 nw = std::sqrt(nrm2);
                 stats->reorth_passes += 1;
+            }
             }
             Hc(j + 1, j) = nw;
             if (nw > 1e-14 * std::max(b_norm, 1.0)) {

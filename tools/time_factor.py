@@ -1,4 +1,4 @@
-"""Factor a config once (warm), then once more for timing; run under
+"""Factor (and with TIME_SOLVE=1 also solve) a config, warm then timed; run under
 `ncu --metrics gpu__time_duration.sum` to get per-kernel durations.
 
 usage: python tools/time_factor.py [config] [ordering]
@@ -36,6 +36,18 @@ def main():
     b.record()
     torch.cuda.synchronize()
     print(f"factorize {a.elapsed_time(b) / 3:.3f} ms", flush=True)
+    if os.environ.get("TIME_SOLVE"):
+        rhs = torch.from_numpy(wl.rhs).cuda()
+        x = torch.empty_like(rhs)
+        _, st = solver.solve(rhs, x=x)
+        torch.cuda.synchronize()
+        a.record()
+        for _ in range(3):
+            _, st = solver.solve(rhs, x=x)
+        b.record()
+        torch.cuda.synchronize()
+        print(f"solve {a.elapsed_time(b) / 3:.3f} ms iters {st.iterations} reorth {st.reorth_passes} "
+              f"applies {st.operator_applies}", flush=True)
 
 
 if __name__ == "__main__":
