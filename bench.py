@@ -139,11 +139,18 @@ def bytes_matvec(T, r, nb, s):
     return nnzb * Bk + T * Bk + 2 * s * v + 4 * (nnzb + T + 1)
 
 
-def bytes_apply_uncoupled_shared(T, r, nb, s):
-    """L and D^-1 per stage, U = -dt J upper read once for all stages."""
+def bytes_apply_uncoupled_shared(T, r, nb, s, implicit_l=False, t_up=None):
+    """Stored L: L and D^-1 per stage, U = -dt J upper read once for all stages.
+    Implicit L: the stage-shared J is read once for the lower and once for the
+    upper blocks; D^-1 of rows with upper blocks is read twice (w = D^-1 z in
+    the forward sweep, x in the backward one) and their w is written and
+    gathered back (t_up = number of such rows)."""
     Bk, v = 8 * nb * nb, 8 * T * nb
     up = T * r // 2
-    return up * Bk + s * (up + T) * Bk + 2 * s * v
+    if not implicit_l:
+        return up * Bk + s * (up + T) * Bk + 2 * s * v
+    t_up = T if t_up is None else t_up
+    return 2 * up * Bk + s * (T + t_up) * Bk + 2 * s * v + 2 * s * 8 * t_up * nb
 
 
 def make_config(args):
@@ -369,7 +376,10 @@ def run_b200(args):
     t_sol = timed(lambda: solver.solve(rhs, x=x), 3)
     peak, peak_src = hbm_peak()
     bm = bytes_matvec(T, r, nb, s)
-    ba = bytes_apply_uncoupled_shared(T, r, nb, s) if cfg.precond.startswith("uncoupled") else None
+    implicit_l = bool(getattr(solver.fac, "implicit_l", False))
+    t_up = int(np.count_nonzero(pat.indptr[1:] - 1 > pat.diag_pos))   # rows with an upper block
+    ba = (bytes_apply_uncoupled_shared(T, r, nb, s, implicit_l, t_up)
+          if cfg.precond.startswith("uncoupled") else None)
     ms_step = 1e3 * t / args.steps
     it_mean = float(np.mean(iters))
     # operator applications per stage-solve: 1 (P^-1 b) + iters (+ restarts) applies,

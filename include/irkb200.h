@@ -140,6 +140,10 @@ IRK_API int irk_factor_apply(const irk_factor *f, const double *y, double *x, vo
 IRK_API int irk_factor_export(const irk_factor *f, double *fstage, double *dinv, double *fcoupling,
                       void *stream);
 IRK_API int irk_factor_levels(const irk_factor *f, int64_t *fwd_levels, int64_t *bwd_levels);
+/* 1 if the factor keeps L implicit (L_ij = alpha J_ij Dinv_j is never stored;
+ * uncoupled simplified ILU with one stage-shared J and a symmetric keep mask),
+ * 0 if L is stored, <0 on error.  Results are the same either way. */
+IRK_API int irk_factor_implicit_l(const irk_factor *f);
 
 /* ---- GMRES ----------------------------------------------------------------- */
 typedef int (*irk_apply_fn)(void *user, const double *in, double *out, void *stream);

@@ -86,6 +86,7 @@ _SIGS = {
     "irk_factor_apply": (c_int, [c_vp, c_vp, c_vp, c_vp]),
     "irk_factor_export": (c_int, [c_vp, c_vp, c_vp, c_vp, c_vp]),
     "irk_factor_levels": (c_int, [c_vp, P(c_i64), P(c_i64)]),
+    "irk_factor_implicit_l": (c_int, [c_vp]),
     "irk_linop_stage_op": (c_int, [c_vp, P(Linop)]),
     "irk_linop_factor": (c_int, [c_vp, P(Linop)]),
     "irk_gmres": (c_int, [c_vp, c_i64, Linop, Linop, c_vp, c_vp, c_vp, c_vp, P(GmresCfg),

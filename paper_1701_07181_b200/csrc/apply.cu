@@ -38,6 +38,9 @@ struct ApplyArgs {
     double cup_scale[IRK_MAX_STAGES * IRK_MAX_STAGES];
     const double* y;
     double* x;
+    double* W;                 // implicit-L forward sweep: w_i = Dinv_i z_i (s x n) or NULL
+    const uint8_t* hasup;      // element has a kept upper block (implicit-L mode)
+    unsigned* flags2;          // bwd flags, released by the implicit forward sweep for fused rows
     // persistent sweep: tasks in topological (level) order, claimed by ticket;
     // a task publishes flags[task] = epoch when its output is in memory
     const int32_t* order;
@@ -618,7 +621,12 @@ __global__ void __launch_bounds__(288) k_unc_fwd_pipe(ApplyArgs A, PipeCfg PC) {
     }
 }
 
-template <int S, bool DEPS>
+// FWDI = false: backward sweep x_i = Dinv_i (z_i - uscale sum_{j>i} J_ij x_j).
+// FWDI = true (implicit-L forward sweep, stage-shared J): t_i = y_i - alpha
+// sum_{j<i} J_ij w_j with w_j = Dinv_j z_j; then z_i = t_i and w_i = Dinv_i z_i
+// for rows with a kept upper block (their backward task follows), else the
+// row is finished here: x_i = Dinv_i z_i (fused backward step).
+template <int S, bool DEPS, bool FWDI>
 __global__ void __launch_bounds__(288) k_unc_bwd_pipe(ApplyArgs A, PipeCfg PC) {
     extern __shared__ __align__(128) unsigned char smem_raw[];
     const int nb = A.nb;
@@ -637,27 +645,32 @@ __global__ void __launch_bounds__(288) k_unc_bwd_pipe(ApplyArgs A, PipeCfg PC) {
             const int tl = tb + lane;
             const bool valid = tl < tend;
             const int64_t il = valid ? A.order[tl] : 0;
-            const int dl = valid ? A.diag[il] : 0, q1l = valid ? A.indptr[il + 1] : 0, u0l = valid ? A.uptr[il] : 0;
-            const int nnl = valid ? q1l - dl - 1 : 0;
+            const int dl = valid ? A.diag[il] : 0, u0l = valid ? A.uptr[il] : 0;
+            // neighbour range: upper (d, q1) for the backward sweep, lower [q0, d) for FWDI
+            const int b0l = valid ? (FWDI ? A.indptr[il] : dl + 1) : 0;
+            const int nnl = valid ? (FWDI ? dl : A.indptr[il + 1]) - b0l : 0;
+            const int szl = (FWDI && valid && A.hasup[il]) ? 1 : 0;
             int coll[MAXD];
             unsigned kml = 0;
 #pragma unroll
             for (int m = 0; m < MAXD; ++m) {
                 coll[m] = 0;
-                if (m < nnl) { coll[m] = A.indices[dl + 1 + m]; kml |= (A.keep[dl + 1 + m] ? 1u : 0u) << m; }
+                if (m < nnl) { coll[m] = A.indices[b0l + m]; kml |= (A.keep[b0l + m] ? 1u : 0u) << m; }
             }
             for (int bt = 0; bt < 32 && tb + bt < tend; ++bt) {
                 const int t = tb + bt;
                 const int64_t i = __shfl_sync(0xffffffffu, il, bt);
-                const int d = __shfl_sync(0xffffffffu, dl, bt), nn = __shfl_sync(0xffffffffu, nnl, bt);
+                const int nn = __shfl_sync(0xffffffffu, nnl, bt);
+                const int b0 = __shfl_sync(0xffffffffu, b0l, bt);
                 const int u0 = __shfl_sync(0xffffffffu, u0l, bt);
+                const int store_z = __shfl_sync(0xffffffffu, szl, bt);
                 unsigned km = __shfl_sync(0xffffffffu, kml, bt);
                 int col[MAXD];
 #pragma unroll
                 for (int m = 0; m < MAXD; ++m) col[m] = __shfl_sync(0xffffffffu, coll[m], bt);
                 if (nn > MAXD) {
                     km = 0;
-                    for (int m = 0; m < nn && m < 32; ++m) km |= (A.keep[d + 1 + m] ? 1u : 0u) << m;
+                    for (int m = 0; m < nn && m < 32; ++m) km |= (A.keep[b0 + m] ? 1u : 0u) << m;
                 }
                 auto colm = [&](int m) -> int64_t {
                     if (m < MAXD) {
@@ -666,9 +679,9 @@ __global__ void __launch_bounds__(288) k_unc_bwd_pipe(ApplyArgs A, PipeCfg PC) {
                         for (int mm = 0; mm < MAXD; ++mm) v = (mm == m) ? col[mm] : v;
                         return v;
                     }
-                    return A.indices[d + 1 + m];
+                    return A.indices[b0 + m];
                 };
-                auto kept = [&](int m) -> bool { return m < 32 ? ((km >> m) & 1u) : A.keep[d + 1 + m] != 0; };
+                auto kept = [&](int m) -> bool { return m < 32 ? ((km >> m) & 1u) : A.keep[b0 + m] != 0; };
                 int nu = 0;
                 for (int m = 0; m < nn; ++m) nu += kept(m) ? (A.u_shared ? 1 : S) : 0;
                 const int ntot = nu + S;
@@ -676,23 +689,23 @@ __global__ void __launch_bounds__(288) k_unc_bwd_pipe(ApplyArgs A, PipeCfg PC) {
                     int n = 0;
                     for (int m = 0; m < nn; ++m) {
                         if (!kept(m)) continue;
-                        const int qq = d + 1 + m;
+                        const int qq = b0 + m;
                         if (A.u_shared) {
                             if (n >= from && n < to)
-                                pr.push(make_int4((int)i, m * S, PD_USH | (n == 0 ? PD_FIRST : 0), nn << 1), A.ubase[0] + qq * bsz);
+                                pr.push(make_int4((int)i, m * S, PD_USH | (n == 0 ? PD_FIRST : 0), nn << 2), A.ubase[0] + qq * bsz);
                             ++n;
                         } else {
                             for (int k = 0; k < S; ++k, ++n) {
                                 if (n < from || n >= to) continue;
                                 const double* ub = A.U ? A.U + ((int64_t)(u0 + m) * S + k) * bsz : A.ubase[k] + qq * bsz;
-                                pr.push(make_int4((int)i, m * S + k, PD_U | (n == 0 ? PD_FIRST : 0), nn << 1), ub);
+                                pr.push(make_int4((int)i, m * S + k, PD_U | (n == 0 ? PD_FIRST : 0), nn << 2), ub);
                             }
                         }
                     }
                     for (int k = 0; k < S; ++k, ++n) {
                         if (n < from || n >= to) continue;
                         const int fl = PD_DINV | (n == 0 ? PD_FIRST : 0) | (k == S - 1 ? PD_LAST : 0);
-                        pr.push(make_int4((int)i, k, fl, (nn << 1) | (nu == 0 ? 1 : 0)), A.Dinv + (i * S + k) * bsz);
+                        pr.push(make_int4((int)i, k, fl, (nn << 2) | (store_z << 1) | (nu == 0 ? 1 : 0)), A.Dinv + (i * S + k) * bsz);
                     }
                 };
                 const int npre = DEPS ? min(ntot, PC.nst - 1) : 0;
@@ -718,8 +731,9 @@ __global__ void __launch_bounds__(288) k_unc_bwd_pipe(ApplyArgs A, PipeCfg PC) {
                 __syncwarp();
                 for (int e = lane; e < (nn + 1) * S; e += 32) {
                     const int m = e / S, k = e - m * S;
-                    if (m == nn) bulk_g2s(xs + e * nb, A.x + k * A.n + i * nb, seg, P.xfull + xb);
-                    else if (kept(m)) bulk_g2s(xs + e * nb, A.x + k * A.n + colm(m) * nb, seg, P.xfull + xb);
+                    // own segment: z_i (backward) or y_i (FWDI); neighbours: x_j (backward) or w_j (FWDI)
+                    if (m == nn) bulk_g2s(xs + e * nb, (FWDI ? A.y : A.x) + k * A.n + i * nb, seg, P.xfull + xb);
+                    else if (kept(m)) bulk_g2s(xs + e * nb, (FWDI ? A.W : A.x) + k * A.n + colm(m) * nb, seg, P.xfull + xb);
                 }
                 if (lane == 0) push_items(npre, ntot);
                 if (lane == 0) pr.x_next();
@@ -740,7 +754,8 @@ __global__ void __launch_bounds__(288) k_unc_bwd_pipe(ApplyArgs A, PipeCfg PC) {
         if (dsc.z & PD_END) break;
         const int64_t i = dsc.x;     // element id and upper-neighbour count from the descriptor
         double* red = P.red + (size_t)par * q.G * S * nb;
-        const int nup = dsc.w >> 1;
+        const int nup = dsc.w >> 2;                     // neighbour count: own segment index
+        const bool store_z = FWDI && ((dsc.w >> 1) & 1);  // FWDI row with a backward task
         if (dsc.z & PD_FIRST) {
 #pragma unroll
             for (int k = 0; k < S; ++k) part[k] = 0.0;
@@ -764,9 +779,12 @@ __global__ void __launch_bounds__(288) k_unc_bwd_pipe(ApplyArgs A, PipeCfg PC) {
             const int kk = dsc.y;
             const bool no_upper = (dsc.z & PD_FIRST) || (dsc.w & 1);
             if (kk == 0 && no_upper) {
-                // no kept upper neighbour: t = z_i, read straight from the x slot
+                // no kept neighbour block: t = own segment, read straight from the x slot
 #pragma unroll
                 for (int k = 0; k < S; ++k) part[k] = 0.0;
+                if (store_z && q.active && q.g == 0)
+#pragma unroll
+                    for (int k = 0; k < S; ++k) A.x[k * A.n + i * nb + q.a] = xs[(nup * S + k) * nb + q.a];
             } else if (kk == 0) {
                 // t_k = z_{i,k} - uscale * sum_j U_ij x_{j,k}  (all stages)
                 if (q.active)
@@ -778,7 +796,9 @@ __global__ void __launch_bounds__(288) k_unc_bwd_pipe(ApplyArgs A, PipeCfg PC) {
                     for (int k = 0; k < S; ++k) {
                         double sum = 0.0;
                         for (int gg = 0; gg < q.G; ++gg) sum += red[(gg * S + k) * nb + q.a];
-                        P.tv[k * nb + q.a] = xs[(nup * S + k) * nb + q.a] - A.uscale * sum;
+                        const double tval = xs[(nup * S + k) * nb + q.a] - A.uscale * sum;
+                        P.tv[k * nb + q.a] = tval;
+                        if (store_z) A.x[k * A.n + i * nb + q.a] = tval;   // z_i for the backward sweep
                     }
                 }
                 consumer_sync(1, ncons);
@@ -805,13 +825,17 @@ __global__ void __launch_bounds__(288) k_unc_bwd_pipe(ApplyArgs A, PipeCfg PC) {
                 for (int k = 0; k < S; ++k) {
                     double sum = 0.0;
                     for (int gg = 0; gg < q.G; ++gg) sum += red[(gg * S + k) * nb + q.a];
-                    A.x[k * A.n + i * nb + q.a] = sum;
+                    (store_z ? A.W : A.x)[k * A.n + i * nb + q.a] = sum;
                 }
             }
             cs.x_release();
             if (DEPS) {
                 consumer_sync(1, ncons);
-                if (c == 0) { __threadfence(); st_release(A.flags + i, A.epoch); }
+                if (c == 0) {
+                    __threadfence();
+                    st_release(A.flags + i, A.epoch);
+                    if (FWDI && !store_z) st_release(A.flags2 + i, A.epoch);   // row finished here
+                }
             }
         }
     }
@@ -917,8 +941,18 @@ template <int S, bool EVEN>
 static int unc_apply(const irk_factor* f, ApplyArgs& A, cudaStream_t st) {
     if (EVEN && S <= 4 && A.G_ * A.nb <= 256) {
         const int64_t nf = (int64_t)f->pat->T;
+        if (f->l_implicit) {
+            // implicit L: forward sweep streams the stage-shared J_ij with w_j = Dinv_j z_j and
+            // finishes rows without upper blocks; the backward sweep covers the remaining rows
+            A.flags2 = f->d_flags + nf;
+            IRK_TRY(run_pipe(f, k_unc_bwd_pipe<S, true, true>, k_unc_bwd_pipe<S, false, true>, A, f->fwd,
+                             f->d_flags, f->d_ticket, S, st));
+            IRK_TRY(run_pipe(f, k_unc_bwd_pipe<S, true, false>, k_unc_bwd_pipe<S, false, false>, A, f->bwd,
+                             f->d_flags + nf, f->d_ticket + 1, S, st));
+            return IRK_OK;
+        }
         IRK_TRY(run_pipe(f, k_unc_fwd_pipe<S, true>, k_unc_fwd_pipe<S, false>, A, f->fwd, f->d_flags, f->d_ticket, S, st));
-        IRK_TRY(run_pipe(f, k_unc_bwd_pipe<S, true>, k_unc_bwd_pipe<S, false>, A, f->bwd, f->d_flags + nf,
+        IRK_TRY(run_pipe(f, k_unc_bwd_pipe<S, true, false>, k_unc_bwd_pipe<S, false, false>, A, f->bwd, f->d_flags + nf,
                          f->d_ticket + 1, S, st));
         return IRK_OK;
     }
@@ -951,6 +985,9 @@ static void fill_args(const irk_factor* f, ApplyArgs& A) {
     A.uptr = p->d_uptr;
     A.keep = f->d_keep;
     A.L = f->d_L;
+    A.W = f->d_W;
+    A.hasup = f->d_hasup;
+    A.flags2 = nullptr;
     A.Dinv = f->d_Dinv;
     A.U = f->u_stored ? f->d_U : nullptr;
     for (int k = 0; k < f->s; ++k) A.ubase[k] = f->ubase[k];
@@ -967,6 +1004,8 @@ static void fill_args(const irk_factor* f, ApplyArgs& A) {
     A.G_ = choose_groups(f->nb, 256);
     if (const char* g = getenv("IRK_APPLY_G")) A.G_ = std::max(1, std::min(atoi(g), (f->nb + 1) / 2));
 }
+
+int factor_materialize_L(const irk_factor* f, double** out, cudaStream_t st);   // factor.cu
 
 int factor_apply(const irk_factor* f, const double* y, double* x, cudaStream_t st) {
     ApplyArgs A{};
@@ -1082,7 +1121,10 @@ int irk_factor_export(const irk_factor* f, double* fstage, double* dinv, double*
                 }
             if (!f->u_stored) rc = copy_blocks(f->ubase[k], sJ, out, dJ, bsz, f->uscale, st);
         }
-        if (!rc) rc = copy_blocks(f->d_L, sL, out, dL, bsz, 1.0, st);
+        double* Lm = f->d_L;
+        if (!rc && f->l_implicit) rc = factor_materialize_L(f, &Lm, st);
+        if (!rc) rc = copy_blocks(Lm, sL, out, dL, bsz, 1.0, st);
+        if (f->l_implicit && Lm) cudaFreeAsync(Lm, st);
         if (!rc) rc = copy_blocks(f->d_D, sD, out, dD, bsz, 1.0, st);
         if (!rc && f->u_stored) rc = copy_blocks(f->d_U, sU, out, dU, bsz, 1.0, st);
         if (!rc) rc = copy_blocks(nullptr, zs, out, zd, bsz, 1.0, st);

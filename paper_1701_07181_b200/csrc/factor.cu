@@ -427,10 +427,10 @@ __global__ void __launch_bounds__(256) k_factor(FactorArgs F) {
             const int tq = F.tpos[q];   // (i, j) block in row i
             const bool keep_lo = F.keep[q] != 0;
             const bool keep_up = tq >= 0 && F.keep[tq] != 0;
-            double* Lout = F.L + ((int64_t)(lq0 + (q - q0)) * F.s + k) * bsz;
+            double* Lout = F.L ? F.L + ((int64_t)(lq0 + (q - q0)) * F.s + k) * bsz : nullptr;
             if (!keep_up) {
                 // reference never touches this block: it stays B_ji (or 0 if dropped)
-                for (int e = threadIdx.x; e < nb * nb; e += blockDim.x) {
+                for (int e = threadIdx.x; Lout && e < nb * nb; e += blockDim.x) {
                     const int a = e / nb, b = e - a * nb;
                     Lout[lay(a, b, nb)] = keep_lo ? F.alpha * Jk[(int64_t)q * bsz + lay(a, b, nb)] : 0.0;
                 }
@@ -532,7 +532,7 @@ static void levels_backward(const irk_pattern* p, const std::vector<uint8_t>& ke
 
 // group task codes by level: tasks (k, elem) with level = lev[elem] + skew(k)
 static int build_sched(irk_sched& S, const std::vector<int64_t>& lev, int64_t T, int s, bool per_stage,
-                       int skew_dir) {
+                       int skew_dir, const std::vector<uint8_t>* include = nullptr) {
     int64_t maxl = 0;
     for (auto v : lev) maxl = std::max(maxl, v);
     const int kstages = per_stage ? s : 1;
@@ -543,12 +543,14 @@ static int build_sched(irk_sched& S, const std::vector<int64_t>& lev, int64_t T,
         return lev[e] + (skew_dir > 0 ? k : (s - 1 - k));
     };
     for (int k = 0; k < kstages; ++k)
-        for (int64_t e = 0; e < T; ++e) cnt[level_of(k, e) + 1]++;
+        for (int64_t e = 0; e < T; ++e)
+            if (!include || (*include)[e]) cnt[level_of(k, e) + 1]++;
     for (int64_t l = 0; l < nlev; ++l) cnt[l + 1] += cnt[l];
     std::vector<int32_t> order(cnt[nlev]);
     std::vector<int64_t> pos(cnt.begin(), cnt.end() - 1);
     for (int k = 0; k < kstages; ++k)
-        for (int64_t e = 0; e < T; ++e) order[pos[level_of(k, e)]++] = (int32_t)((int64_t)k * T + e);
+        for (int64_t e = 0; e < T; ++e)
+            if (!include || (*include)[e]) order[pos[level_of(k, e)]++] = (int32_t)((int64_t)k * T + e);
     S.nlevels = nlev;
     S.h_lvl_ptr = cnt;
     IRK_CK(cudaMalloc(&S.d_order, sizeof(int32_t) * std::max<size_t>(order.size(), 1)));
@@ -573,8 +575,20 @@ int build_apply_schedules(irk_factor* f, const std::vector<uint8_t>& keep) {
     levels_backward(f->pat, keep, levb);
     const bool cpl = f->kind == IRK_FACTOR_COUPLED;
     IRK_TRY(build_sched(f->fwd, levf, f->pat->T, f->s, cpl, +1));
-    IRK_TRY(build_sched(f->bwd, levb, f->pat->T, f->s, cpl, -1));
-    if (!cpl) {
+    if (f->l_implicit) {
+        // rows without a kept upper block are finished by the forward sweep
+        const irk_pattern* p = f->pat;
+        std::vector<uint8_t> hasup(p->T, 0);
+        for (int64_t i = 0; i < p->T; ++i)
+            for (int64_t q = p->h_diag[i] + 1; q < p->h_indptr[i + 1]; ++q)
+                if (keep[q]) hasup[i] = 1;
+        IRK_TRY(build_sched(f->bwd, levb, p->T, f->s, false, -1, &hasup));
+        IRK_CK(cudaMalloc(&f->d_hasup, std::max<int64_t>(p->T, 1)));
+        IRK_CK(cudaMemcpy(f->d_hasup, hasup.data(), p->T, cudaMemcpyHostToDevice));
+    } else {
+        IRK_TRY(build_sched(f->bwd, levb, f->pat->T, f->s, cpl, -1));
+    }
+    if (!cpl && !f->l_implicit) {
         // forward levels whose elements have no kept lower block: z_i = y_i
         const irk_pattern* p = f->pat;
         std::vector<char> has(f->fwd.nlevels, 0);
@@ -725,7 +739,7 @@ __global__ void __launch_bounds__(4 * NB) k_schur(FactorArgs F, const int32_t* _
         const int q0 = F.indptr[j];
         const int lq0 = F.lptr[j];
         for (int q = q0; q < dpos; ++q) {
-            double* Lout = F.L + (int64_t)(lq0 + (q - q0)) * S * BSZ;
+            double* Lout = F.L ? F.L + (int64_t)(lq0 + (q - q0)) * S * BSZ : nullptr;   // NULL: implicit L
             if (!(nxt.it == it && nxt.q == q)) {
                 // not a unit: the reference never forms L_ji D_i^-1 here, so L stays
                 // B_ji (upper block dropped) or 0 (lower block dropped); D unchanged
@@ -733,10 +747,11 @@ __global__ void __launch_bounds__(4 * NB) k_schur(FactorArgs F, const int32_t* _
                 const bool keep_lo = F.keep[q] != 0;
                 const bool keep_up = tq >= 0 && F.keep[tq] != 0;
                 const double* Jq = J + (int64_t)q * BSZ;
-                for (int64_t e = threadIdx.x; e < S * BSZ; e += blockDim.x) {
-                    const int64_t o = e % BSZ;
-                    Lout[e] = (keep_lo && !keep_up) ? F.alpha * Jq[o] : 0.0;
-                }
+                if (F.L)
+                    for (int64_t e = threadIdx.x; e < S * BSZ; e += blockDim.x) {
+                        const int64_t o = e % BSZ;
+                        Lout[e] = (keep_lo && !keep_up) ? F.alpha * Jq[o] : 0.0;
+                    }
                 continue;
             }
             const Unit cur = nxt;
@@ -757,13 +772,13 @@ __global__ void __launch_bounds__(4 * NB) k_schur(FactorArgs F, const int32_t* _
 #pragma unroll
                     for (int t = 0; t < NT; ++t) dmma(acc[t][0], acc[t][1], a, frag_b(Dk, kk, t));
                 }
-                // L_k = alpha T_k -> global (numba_backend.py:58-61)
-                double2* Lk = reinterpret_cast<double2*>(Lout + (int64_t)k * BSZ);
+                // L_k = alpha T_k -> global (numba_backend.py:58-61), unless L is implicit
 #pragma unroll
                 for (int t = 0; t < NT; ++t) {
                     acc[t][0] *= F.alpha;
                     acc[t][1] *= F.alpha;
-                    Lk[gl_off(t)] = make_double2(acc[t][0], acc[t][1]);
+                    if (Lout)
+                        reinterpret_cast<double2*>(Lout + (int64_t)k * BSZ)[gl_off(t)] = make_double2(acc[t][0], acc[t][1]);
                 }
                 __syncthreads();   // all warps: GEMM1_k done (Dinv_k slot), GEMM2_{k-1} done (A'_{k-1})
                 if (more && k > 0) fill(2 + k - 1, src_dinv(nxt, k - 1));
@@ -988,6 +1003,33 @@ static int factor_numeric(irk_factor* f, int64_t* fail_stage, int64_t* fail_elem
     return IRK_OK;
 }
 
+int choose_groups(int nb, int max_threads);   // matvec.cu
+
+// Implicit L (never store L_ij = alpha J_ij Dinv_j) needs: stage-uncoupled
+// simplified ILU, one J shared by all stages, a symmetric keep mask (so every
+// kept lower block is a Schur pair), and the pipelined sweep kernels (even nb,
+// s <= 4, G nb <= 256).  IRK_EXPLICIT_L=1 forces stored L (A/B comparisons).
+static bool implicit_l_ok(const irk_pattern* pat, const FactorSetup& P, const std::vector<uint8_t>& keep,
+                          int simplified) {
+    if (P.coupled || !simplified || P.literal || getenv("IRK_EXPLICIT_L")) return false;
+    const int nb = P.J[0]->nb;
+    if (nb % 2 || P.s > 4 || choose_groups(nb, 256) * nb > 256) return false;
+    const int64_t bsz = block_doubles(nb);
+    const double* b0 = P.J[0]->d + (P.jfirst ? P.jfirst[0] : 0) * bsz;
+    for (int k = 1; k < P.s; ++k)
+        if (P.J[k]->d + (P.jfirst ? P.jfirst[k] : 0) * bsz != b0) return false;
+    for (int64_t i = 0; i < pat->T; ++i)
+        for (int64_t q = pat->h_indptr[i]; q < pat->h_indptr[i + 1]; ++q) {
+            const int64_t j = pat->h_indices[q];
+            const int64_t* b = pat->h_indices.data() + pat->h_indptr[j];
+            const int64_t* e = pat->h_indices.data() + pat->h_indptr[j + 1];
+            const int64_t* t = std::lower_bound(b, e, i);
+            const bool kt = (t != e && *t == i) && keep[pat->h_indptr[j] + (t - b)];
+            if (q != pat->h_diag[i] && (keep[q] != 0) != kt) return false;
+        }
+    return true;
+}
+
 static int factor_common(irk_ctx* ctx, const irk_pattern* pat, const FactorSetup& P, irk_factor** out,
                          int64_t* fail_stage, int64_t* fail_elem, cudaStream_t st) {
     IRK_ARG(ctx && pat && P.J && P.J[0] && out, "NULL argument");
@@ -1011,9 +1053,11 @@ static int factor_common(irk_ctx* ctx, const irk_pattern* pat, const FactorSetup
 #define FCK(call) do { cudaError_t _e = (call); if (_e != cudaSuccess) return fail(fail_cuda(_e, #call, __FILE__, __LINE__)); } while (0)
     f->u_stored = !f->simplified;
     const int npairs = P.s * (P.s - 1) / 2;
+    f->l_implicit = implicit_l_ok(pat, P, keep, f->simplified);
     FCK(cudaMalloc(&f->d_keep, pat->nnzb));
     FCK(cudaMemcpy(f->d_keep, keep.data(), pat->nnzb, cudaMemcpyHostToDevice));
-    FCK(cudaMalloc(&f->d_L, sizeof(double) * bsz * std::max<int64_t>(pat->nlow * P.s, 1)));
+    if (f->l_implicit) FCK(cudaMalloc(&f->d_W, sizeof(double) * bsz / nb * pat->T * P.s));   // s x T x nb
+    else FCK(cudaMalloc(&f->d_L, sizeof(double) * bsz * std::max<int64_t>(pat->nlow * P.s, 1)));
     FCK(cudaMalloc(&f->d_Dinv, sizeof(double) * bsz * pat->T * P.s));
     // pivot blocks: needed for export/literal, and as the hand-off to the batched inverse
     if (P.store_diag || P.literal || nb <= 64) FCK(cudaMalloc(&f->d_D, sizeof(double) * bsz * pat->T * P.s));
@@ -1062,6 +1106,56 @@ static int factor_common(irk_ctx* ctx, const irk_pattern* pat, const FactorSetup
     if (rc < 0) return fail(rc);
     *out = f;
     return rc;
+}
+
+// Implicit L, for export: L[lq][k] = alpha J_q Dinv_{j,k} (j = column of q) for
+// kept lower blocks, 0 for dropped ones.  Cold path: one CTA per row, plain FMAs.
+__global__ void k_materialize_L(FactorArgs F, double* out) {
+    extern __shared__ double sm[];
+    const int nb = F.nb;
+    const int64_t bsz = (int64_t)nb * 2 * ((nb + 1) >> 1);
+    double* Ja = sm;                 // nb x nb row-major
+    double* Db = sm + nb * nb;
+    for (int64_t i = blockIdx.x; i < F.T; i += gridDim.x) {
+        const int q0 = F.indptr[i], d = F.diag[i], lq0 = F.lptr[i];
+        for (int q = q0; q < d; ++q) {
+            const int j = F.indices[q];
+            for (int k = 0; k < F.s; ++k) {
+                double* dst = out + ((int64_t)(lq0 + q - q0) * F.s + k) * bsz;
+                if (!F.keep[q]) {
+                    for (int e = threadIdx.x; e < bsz; e += blockDim.x) dst[e] = 0.0;
+                    continue;
+                }
+                const double* Jq = F.J[0] + (int64_t)q * bsz;
+                const double* Dk = F.Dinv + ((int64_t)j * F.s + k) * bsz;
+                for (int e = threadIdx.x; e < nb * nb; e += blockDim.x) {
+                    const int a = e / nb, b = e - a * nb;
+                    Ja[e] = Jq[lay(a, b, nb)];
+                    Db[e] = Dk[lay(a, b, nb)];
+                }
+                __syncthreads();
+                for (int e = threadIdx.x; e < bsz; e += blockDim.x) {
+                    const int p = (int)(e >> 1) / nb, a = (int)(e >> 1) % nb, b = 2 * p + (int)(e & 1);
+                    double acc = 0.0;
+                    if (b < nb)
+                        for (int c = 0; c < nb; ++c) acc = fma(Ja[a * nb + c], Db[c * nb + b], acc);
+                    dst[e] = F.alpha * acc;
+                }
+                __syncthreads();
+            }
+        }
+    }
+}
+
+int factor_materialize_L(const irk_factor* f, double** out, cudaStream_t st) {
+    const FactorArgs& F = *static_cast<const FactorArgs*>(f->fargs);
+    const int64_t bsz = block_doubles(f->nb);
+    IRK_CK(cudaMallocAsync(out, sizeof(double) * bsz * std::max<int64_t>(f->pat->nlow * f->s, 1), st));
+    const size_t smem = sizeof(double) * 2 * f->nb * f->nb;
+    IRK_CK(cudaFuncSetAttribute(k_materialize_L, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    k_materialize_L<<<(int)std::min<int64_t>(f->pat->T, f->ctx->num_sms * 4), 256, smem, st>>>(F, *out);
+    IRK_LAUNCHED();
+    return IRK_OK;
 }
 
 }  // namespace irk
@@ -1126,6 +1220,7 @@ int irk_factor_refactor(irk_factor* f, const irk_blocks* const* J, const int64_t
     P.alpha = alpha;
     P.coupling = coupling;
     IRK_TRY(set_sources(f, P));
+    IRK_ARG(!f->l_implicit || f->u_shared, "implicit-L factor: refactor needs one J shared by all stages");
     return factor_numeric(f, fail_stage, fail_elem, (cudaStream_t)stream);
 }
 
@@ -1133,6 +1228,8 @@ void irk_factor_destroy(irk_factor* f) {
     if (!f) return;
     cudaFree(f->d_keep);
     cudaFree(f->d_L);
+    cudaFree(f->d_W);
+    cudaFree(f->d_hasup);
     cudaFree(f->d_Dinv);
     cudaFree(f->d_D);
     cudaFree(f->d_U);
@@ -1154,6 +1251,11 @@ int irk_factor_levels(const irk_factor* f, int64_t* fwd_levels, int64_t* bwd_lev
     if (fwd_levels) *fwd_levels = f->fwd.nlevels;
     if (bwd_levels) *bwd_levels = f->bwd.nlevels;
     return IRK_OK;
+}
+
+int irk_factor_implicit_l(const irk_factor* f) {
+    IRK_ARG(f, "NULL factor");
+    return f->l_implicit ? 1 : 0;
 }
 
 }  // extern "C"

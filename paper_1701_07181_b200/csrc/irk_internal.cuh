@@ -121,6 +121,11 @@ struct irk_factor {
     double* d_L = nullptr;
     double* d_Dinv = nullptr;
     double* d_D = nullptr;
+    // implicit L (uncoupled, stage-shared J, symmetric keep): L_ij = alpha J_ij Dinv_j is
+    // never stored; the forward sweep uses w_j = Dinv_j z_j (d_W, s x T x nb) instead
+    bool l_implicit = false;
+    double* d_W = nullptr;
+    uint8_t* d_hasup = nullptr;       // T: row has a kept upper block
     // upper blocks: either implicit (ubase[k] block array at pattern position q,
     // scaled by uscale) or stored U[uq][k] (uscale = 1)
     bool u_stored = false;

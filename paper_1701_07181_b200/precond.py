@@ -173,6 +173,13 @@ class _Factor:
         L.check(L.lib().irk_linop_factor(self.handle, op), "irk_linop_factor")
         return op, self
 
+    @property
+    def implicit_l(self) -> bool:
+        """True when L is never stored (forward sweep uses w_j = Dinv_j z_j)."""
+        rc = L.lib().irk_factor_implicit_l(self.handle)
+        L.check(min(rc, 0), "irk_factor_implicit_l")
+        return rc == 1
+
     def levels(self) -> tuple[int, int]:
         f, b = ctypes.c_int64(), ctypes.c_int64()
         L.check(L.lib().irk_factor_levels(self.handle, ctypes.byref(f), ctypes.byref(b)))
