@@ -330,6 +330,8 @@ def run_b200(args):
     launches0 = L.lib().irk_launch_count()
     torch.cuda.synchronize()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    if args.profile:
+        torch.cuda.profiler.start()    # ncu --profile-from-start off: the timed steps only
     ev0.record(stream)
     iters = []
     for _ in range(args.steps):
@@ -337,6 +339,8 @@ def run_b200(args):
         iters.append(st.iterations)
     ev1.record(stream)
     torch.cuda.synchronize()
+    if args.profile:
+        torch.cuda.profiler.stop()
     launches = L.lib().irk_launch_count() - launches0
     log('timed region done')
     clocks = clk.stop()

@@ -55,28 +55,31 @@ def main():
     ap.add_argument("launches")
     ap.add_argument("raw", nargs="*")
     ap.add_argument("--out", required=True)
+    ap.add_argument("--steps", type=int, default=1, help="timed steps in the launch list")
+    ap.add_argument("--last", type=int, default=0, help="keep only the last N launches")
     a = ap.parse_args()
     L = read_launches(a.launches)
-    # the timed step: from the second k_factor launch pair on
-    fidx = [i for i, d in enumerate(L) if "k_factor" in d["name"]]
-    start = fidx[len(fidx) // 2] if len(fidx) >= 2 else 0
-    step = L[start:]
+    # bench.py --profile brackets the timed steps with cudaProfilerStart/Stop and ncu runs
+    # with --profile-from-start off, so every listed launch belongs to the timed steps
+    step = L[-a.last:] if a.last else L
     agg = collections.OrderedDict()
     for d in step:
         g = agg.setdefault(d["name"], {"n": 0, "us": 0.0, "dram": 0.0})
         g["n"] += 1
         g["us"] += d.get("gpu__time_duration.sum", 0.0)
         g["dram"] += d.get("dram__bytes_read.sum", 0.0) + d.get("dram__bytes_write.sum", 0.0)
-    tot = sum(g["us"] for g in agg.values())
+    for g in agg.values():
+        g["n_step"] = g["n"] / a.steps
+    tot = sum(g["us"] for g in agg.values()) / a.steps
     lines = ["# ncu summary (one timed stage-solve, config 1, colour ordering)", "",
              "Launch list: `ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum "
              "--clock-control none` over `bench.py --steps 1 --warmup 1 --profile` (serialised, cold "
              "caches: compare shares, not absolute times).", "",
-             f"Step total (serialised): {tot/1e3:.3f} ms", "",
-             "| kernel | launches | time (ms) | share | DRAM bytes / launch (GB) |",
+             f"Step total (serialised, per step over {a.steps} timed step(s)): {tot/1e3:.3f} ms", "",
+             "| kernel | launches / step | time / step (ms) | share | DRAM bytes / launch (GB) |",
              "|---|---|---|---|---|"]
     for name, g in sorted(agg.items(), key=lambda kv: -kv[1]["us"]):
-        lines.append(f"| `{name}` | {g['n']} | {g['us']/1e3:.3f} | {100*g['us']/tot:.1f}% | "
+        lines.append(f"| `{name}` | {g['n_step']:g} | {g['us']/1e3/a.steps:.3f} | {100*g['us']/a.steps/tot:.1f}% | "
                      f"{g['dram']/g['n']/1e9:.4f} |")
     # traffic per operation (apply = copy + fwd + bwd launches of one apply)
     traffic = {}
@@ -85,15 +88,16 @@ def main():
         per = [agg[n]["dram"] / agg[n]["n"] for n in agg if any(k in n for k in names)]
         cnt = [agg[n]["n"] for n in agg if any(k in n for k in names)]
         if key == "ilu0_apply":
-            # launches per apply: one copy + one fwd + two bwd levels; scale to one apply
-            napply = next((agg[n]["n"] for n in agg if "k_copy_rows" in n), 1)
+            # a stage-solve makes as many applies (P^-1 b + one per iteration) as matvecs
+            # (one per iteration + the true residual): scale the sweep launches to one apply
+            napply = next((agg[n]["n"] for n in agg if "k_stage_matvec" in n), 1)
             val = sum(agg[n]["dram"] for n in agg if any(k in n for k in names)) / max(napply, 1)
         else:
             val = per[0] if per else None
         traffic[key] = val
     lines += ["", "DRAM traffic per operation (bytes):", "",
               f"* stage matvec: {traffic['stage_matvec']:.4e} (algorithmic 2.161e9)",
-              f"* ILU apply (all launches of one apply): {traffic['ilu0_apply']:.4e} (algorithmic 3.838e9)"]
+              f"* ILU apply (all launches of one apply): {traffic['ilu0_apply']:.4e} (algorithmic 3.240e9 with the implicit-L factor)"]
     want = ["gpu__time_duration.sum", "dram__throughput.avg.pct_of_peak_sustained_elapsed",
             "sm__throughput.avg.pct_of_peak_sustained_elapsed", "sm__warps_active.avg.pct_of_peak_sustained_active",
             "launch__registers_per_thread", "dram__bytes_read.sum", "dram__bytes_write.sum",
