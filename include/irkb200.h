@@ -133,6 +133,12 @@ IRK_API void irk_factor_destroy(irk_factor *f);
  * StageUncoupledIlu0.apply / StageCoupledIlu0.apply, precond.py:79-87,
  * 222-241, 152-162).  x may alias nothing else; y is not modified. */
 IRK_API int irk_factor_apply(const irk_factor *f, const double *y, double *x, void *stream);
+/* One single-stage factor (s = 1, e.g. ilu0_factorize of J itself) applied to
+ * nrhs stage-major right-hand sides y (nrhs, T, m) -> x in one sweep that reads
+ * every factor block once (BASELINE config 3).  Same result as nrhs separate
+ * irk_factor_apply calls (ilu0_solve, numba_backend.py:75-91, per column).
+ * Needs even m, nrhs <= 4, m <= 256; IRK_EINVAL otherwise. */
+IRK_API int irk_factor_apply_rhs(const irk_factor *f, int nrhs, const double *y, double *x, void *stream);
 /* factor data in the reference's output layout (host, row-major):
  * fstage (s,nnzb,m,m): lower = L, diagonal = updated pivot, upper = U;
  * dinv (s,T,m,m); fcoupling (s,s,T,m,m) (coupled only, may be NULL).

@@ -84,6 +84,7 @@ _SIGS = {
                                     c_vp]),
     "irk_factor_destroy": (None, [c_vp]),
     "irk_factor_apply": (c_int, [c_vp, c_vp, c_vp, c_vp]),
+    "irk_factor_apply_rhs": (c_int, [c_vp, c_int, c_vp, c_vp, c_vp]),
     "irk_factor_export": (c_int, [c_vp, c_vp, c_vp, c_vp, c_vp]),
     "irk_factor_levels": (c_int, [c_vp, P(c_i64), P(c_i64)]),
     "irk_factor_implicit_l": (c_int, [c_vp]),

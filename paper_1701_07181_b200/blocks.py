@@ -287,6 +287,28 @@ class BlockSparseMatrix:
             counter.block_multiplies += self.nnz_blocks
         return from_device(y, was_np)
 
+    def rhs_op(self, nrhs: int) -> _Op:
+        """Native operator Y -> [J y_0, ..., J y_{nrhs-1}] (stage-major) that reads
+        each block once for all right-hand sides (BASELINE config 3)."""
+        ops = self.__dict__.setdefault("_rhs_ops", {})
+        if nrhs not in ops:
+            ops[nrhs] = make_stage_op(self.pattern, nrhs, [self.blocks] * nrhs, [self.first] * nrhs,
+                                      None, None, 1.0)
+        return ops[nrhs]
+
+    def matvec_rhs(self, Y, counter: OpCounter | None = None):
+        """J applied to the rows of Y (nrhs, n) in one sweep."""
+        nrhs = int(Y.shape[0])
+        if tuple(Y.shape) != (nrhs, self.n):
+            raise ValueError(f"expected shape (nrhs, {self.n}), got {tuple(Y.shape)}")
+        yd, was_np = to_device(Y.reshape(-1))
+        out = empty_like_dev(nrhs * self.n)
+        L.check(L.lib().irk_stage_op_apply(self.rhs_op(nrhs).handle, yd.data_ptr(), out.data_ptr(),
+                                           L.stream_ptr()), "irk_stage_op_apply")
+        if counter is not None:
+            counter.block_multiplies += nrhs * self.nnz_blocks
+        return from_device(out, was_np).reshape(nrhs, self.n)
+
 
 class BlockDiagonalMatrix:
     """T dense m x m blocks on the diagonal (mass matrices), on the GPU."""

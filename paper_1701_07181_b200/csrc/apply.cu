@@ -50,6 +50,7 @@ struct ApplyArgs {
     unsigned epoch;
     int64_t T, n;
     int s, nb, G_;
+    int fac_shared;            // one factor (s = 1) applied to s right-hand sides
 };
 
 __device__ __forceinline__ int pidx(int hi, int lo) { return hi * (hi - 1) / 2 + lo; }
@@ -304,7 +305,8 @@ __global__ void __launch_bounds__(256) k_cpl_bwd(ApplyArgs A) {
 // Deadlock-free: tasks enter every ring in ticket order, dependencies have
 // smaller tickets, and a task's x is loaded only after its dependencies.
 // ---------------------------------------------------------------------------
-enum { PD_FIRST = 1, PD_LAST = 2, PD_END = 4, PD_USH = 8, PD_U = 16, PD_DINV = 32, PD_L = 64 };
+enum { PD_FIRST = 1, PD_LAST = 2, PD_END = 4, PD_USH = 8, PD_U = 16, PD_DINV = 32, PD_L = 64, PD_SH = 128 };
+// PD_SH: a factor block shared by all right-hand sides (fac_shared), applied to every k
 
 struct PipeCfg {
     int nst;
@@ -503,8 +505,9 @@ __global__ void __launch_bounds__(288) k_unc_fwd_pipe(ApplyArgs A, PipeCfg PC) {
                 };
                 auto kept = [&](int m) -> bool { return m < 32 ? ((km >> m) & 1u) : A.keep[q0 + m] != 0; };
                 // item n of the task: (kept neighbour, stage) in order
+                const int SF = A.fac_shared ? 1 : S;   // factor blocks per neighbour
                 int nitems = 0;
-                for (int m = 0; m < nn; ++m) nitems += kept(m) ? S : 0;
+                for (int m = 0; m < nn; ++m) nitems += kept(m) ? SF : 0;
                 auto push_items = [&](int from, int to) {
                     if (nitems == 0) {
                         if (from == 0 && to > 0) pr.push(make_int4((int)i, -1, PD_FIRST | PD_LAST, nn), nullptr);
@@ -513,10 +516,11 @@ __global__ void __launch_bounds__(288) k_unc_fwd_pipe(ApplyArgs A, PipeCfg PC) {
                     int n = 0;
                     for (int m = 0; m < nn; ++m) {
                         if (!kept(m)) continue;
-                        for (int k = 0; k < S; ++k, ++n) {
+                        for (int k = 0; k < SF; ++k, ++n) {
                             if (n < from || n >= to) continue;
-                            const int fl = PD_L | (n == 0 ? PD_FIRST : 0) | (n == nitems - 1 ? PD_LAST : 0);
-                            pr.push(make_int4((int)i, m * S + k, fl, nn), A.L + ((int64_t)(l0 + m) * S + k) * bsz);
+                            const int fl = PD_L | (n == 0 ? PD_FIRST : 0) | (n == nitems - 1 ? PD_LAST : 0) |
+                                           (A.fac_shared ? PD_SH : 0);
+                            pr.push(make_int4((int)i, m * S + k, fl, nn), A.L + ((int64_t)(l0 + m) * SF + k) * bsz);
                         }
                     }
                 };
@@ -577,10 +581,10 @@ __global__ void __launch_bounds__(288) k_unc_fwd_pipe(ApplyArgs A, PipeCfg PC) {
         if (dsc.y >= 0 && q.active) {
             const int m = dsc.y / S, kk = dsc.y - m * S;
             const double2* B = cs.block();
-            const double* xv = xs + (m * S + kk) * nb;
+            const bool sh = (dsc.z & PD_SH) != 0;
 #pragma unroll
             for (int k = 0; k < S; ++k)
-                if (k == kk) part[k] = smem_gemv(B, xv, q, part[k]);
+                if (k == kk || sh) part[k] = smem_gemv(B, xs + (m * S + k) * nb, q, part[k]);
         }
         cs.release();
         if (dsc.z & PD_LAST) {
@@ -682,17 +686,20 @@ __global__ void __launch_bounds__(288) k_unc_bwd_pipe(ApplyArgs A, PipeCfg PC) {
                     return A.indices[b0 + m];
                 };
                 auto kept = [&](int m) -> bool { return m < 32 ? ((km >> m) & 1u) : A.keep[b0 + m] != 0; };
+                const bool ush = A.u_shared || A.fac_shared;
+                const int nd = A.fac_shared ? 1 : S;   // Dinv items
                 int nu = 0;
-                for (int m = 0; m < nn; ++m) nu += kept(m) ? (A.u_shared ? 1 : S) : 0;
-                const int ntot = nu + S;
+                for (int m = 0; m < nn; ++m) nu += kept(m) ? (ush ? 1 : S) : 0;
+                const int ntot = nu + nd;
                 auto push_items = [&](int from, int to) {
                     int n = 0;
                     for (int m = 0; m < nn; ++m) {
                         if (!kept(m)) continue;
                         const int qq = b0 + m;
-                        if (A.u_shared) {
+                        if (ush) {
                             if (n >= from && n < to)
-                                pr.push(make_int4((int)i, m * S, PD_USH | (n == 0 ? PD_FIRST : 0), nn << 2), A.ubase[0] + qq * bsz);
+                                pr.push(make_int4((int)i, m * S, PD_USH | (n == 0 ? PD_FIRST : 0), nn << 2),
+                                        A.U ? A.U + (int64_t)(u0 + m) * bsz : A.ubase[0] + qq * bsz);
                             ++n;
                         } else {
                             for (int k = 0; k < S; ++k, ++n) {
@@ -702,10 +709,11 @@ __global__ void __launch_bounds__(288) k_unc_bwd_pipe(ApplyArgs A, PipeCfg PC) {
                             }
                         }
                     }
-                    for (int k = 0; k < S; ++k, ++n) {
+                    for (int k = 0; k < nd; ++k, ++n) {
                         if (n < from || n >= to) continue;
-                        const int fl = PD_DINV | (n == 0 ? PD_FIRST : 0) | (k == S - 1 ? PD_LAST : 0);
-                        pr.push(make_int4((int)i, k, fl, (nn << 2) | (store_z << 1) | (nu == 0 ? 1 : 0)), A.Dinv + (i * S + k) * bsz);
+                        const int fl = PD_DINV | (n == 0 ? PD_FIRST : 0) | (k == nd - 1 ? PD_LAST : 0) |
+                                       (A.fac_shared ? PD_SH : 0);
+                        pr.push(make_int4((int)i, k, fl, (nn << 2) | (store_z << 1) | (nu == 0 ? 1 : 0)), A.Dinv + (i * nd + k) * bsz);
                     }
                 };
                 const int npre = DEPS ? min(ntot, PC.nst - 1) : 0;
@@ -807,9 +815,10 @@ __global__ void __launch_bounds__(288) k_unc_bwd_pipe(ApplyArgs A, PipeCfg PC) {
             }
             if (q.active) {
                 const bool direct = (dsc.w & 1) != 0;
+                const bool sh = (dsc.z & PD_SH) != 0;
 #pragma unroll
                 for (int k = 0; k < S; ++k)
-                    if (k == kk)
+                    if (k == kk || sh)
                         part[k] = smem_gemv(B, direct ? xs + (nup * S + k) * nb : P.tv + k * nb, q, part[k]);
             }
         }
@@ -1023,6 +1032,42 @@ int factor_apply(const irk_factor* f, const double* y, double* x, cudaStream_t s
     }
 }
 
+// One factor (s = 1) applied to nrhs stage-major right-hand sides in one sweep:
+// every factor block (Dinv_i, the implicit/stored upper blocks, stored L) is read
+// once for all right-hand sides (BASELINE config 3: plain ILU(0) of J, s RHS).
+int factor_apply_rhs(const irk_factor* f, int nrhs, const double* y, double* x, cudaStream_t st) {
+    if (nrhs == 1) return factor_apply(f, y, x, st);
+    if (f->kind != IRK_FACTOR_UNCOUPLED || f->s != 1) {
+        set_error("multi-RHS apply needs a single uncoupled factor (s = 1)");
+        return IRK_EINVAL;
+    }
+    ApplyArgs A{};
+    fill_args(f, A);
+    if (f->nb % 2 || nrhs > 4 || A.G_ * f->nb > 256) {
+        set_error("multi-RHS apply needs even nb, nrhs <= 4 and nb <= 256");
+        return IRK_EINVAL;
+    }
+    if (f->l_implicit && f->wrhs < nrhs) {
+        cudaFree(f->d_Wrhs);
+        f->d_Wrhs = nullptr;
+        f->wrhs = 0;
+        IRK_CK(cudaMalloc(&f->d_Wrhs, sizeof(double) * nrhs * f->pat->T * f->nb));
+        f->wrhs = nrhs;
+    }
+    A.y = y;
+    A.x = x;
+    A.s = nrhs;
+    A.fac_shared = 1;
+    if (f->l_implicit) A.W = f->d_Wrhs;
+    A.epoch = ++f->epoch;
+    switch (nrhs) {
+        case 2: return unc_apply<2, true>(f, A, st);
+        case 3: return unc_apply<3, true>(f, A, st);
+        case 4: return unc_apply<4, true>(f, A, st);
+        default: set_error("nrhs out of range"); return IRK_EINVAL;
+    }
+}
+
 // ---------------------------------------------------------------------------
 // block gather/scatter used by export/import: dst[didx[e]] = scale*src[sidx[e]]
 // (sidx < 0: zero block)
@@ -1091,6 +1136,13 @@ int irk_factor_apply(const irk_factor* f, const double* y, double* x, void* stre
     IRK_ARG(f && y && x, "NULL argument");
     IRK_ARG(y != x, "x must not alias y");
     return factor_apply(f, y, x, (cudaStream_t)stream);
+}
+
+int irk_factor_apply_rhs(const irk_factor* f, int nrhs, const double* y, double* x, void* stream) {
+    IRK_ARG(f && y && x, "NULL argument");
+    IRK_ARG(y != x, "x must not alias y");
+    IRK_ARG(nrhs >= 1, "nrhs must be positive");
+    return factor_apply_rhs(f, nrhs, y, x, (cudaStream_t)stream);
 }
 
 int irk_factor_export(const irk_factor* f, double* fstage, double* dinv, double* fcoupling, void* stream) {

@@ -1229,6 +1229,7 @@ void irk_factor_destroy(irk_factor* f) {
     cudaFree(f->d_keep);
     cudaFree(f->d_L);
     cudaFree(f->d_W);
+    cudaFree(f->d_Wrhs);
     cudaFree(f->d_hasup);
     cudaFree(f->d_Dinv);
     cudaFree(f->d_D);

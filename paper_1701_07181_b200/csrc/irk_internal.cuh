@@ -125,6 +125,8 @@ struct irk_factor {
     // never stored; the forward sweep uses w_j = Dinv_j z_j (d_W, s x T x nb) instead
     bool l_implicit = false;
     double* d_W = nullptr;
+    mutable double* d_Wrhs = nullptr; // multi-RHS apply of a single factor: nrhs x T x nb
+    mutable int wrhs = 0;
     uint8_t* d_hasup = nullptr;       // T: row has a kept upper block
     // upper blocks: either implicit (ubase[k] block array at pattern position q,
     // scaled by uscale) or stored U[uq][k] (uscale = 1)

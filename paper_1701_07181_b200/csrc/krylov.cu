@@ -30,7 +30,7 @@ int factor_apply(const irk_factor* f, const double* y, double* x, cudaStream_t s
 constexpr int VB = 256;      // threads per vector CTA
 constexpr int VGROUP = 8;    // vectors per multidot pass
 
-static int vec_blocks(const irk_ctx* ctx) { return ctx->num_sms * 2; }
+static int vec_blocks(const irk_ctx* ctx) { return ctx->num_sms * 4; }
 
 __device__ __forceinline__ double warp_sum(double v) {
     for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
@@ -265,6 +265,177 @@ __global__ void __launch_bounds__(VB) k_update_cond_r(const double* __restrict__
     }
 }
 
+// ---- 128-bit fused CGS2 passes (nv <= NVM), element pairs -----------------
+//
+// V columns are ldv-strided with ldv a multiple of 32 elements, so every column
+// and w (= a V column) is 256-byte aligned and an element pair is one LDG.128.
+// The CTA chunk starts at an even element; an odd n leaves one scalar tail
+// element, handled by the CTA that owns it.
+
+__device__ __forceinline__ void chunk_pairs(int64_t n, int64_t& lo2, int64_t& hi2, bool& tail) {
+    int64_t lo, hi;
+    chunk_range(n, lo, hi);
+    lo2 = lo >> 1;
+    hi2 = hi >> 1;
+    tail = (hi & 1) && hi > lo;   // hi == n odd: element n-1 is unpaired
+}
+
+// pass 1: out[i] = V_i . w (i < nv), out[nv] = w . w
+template <int NVM>
+__global__ void __launch_bounds__(VB) k_multidot_v(const double* __restrict__ V, int64_t ldv, int nv,
+                                                   const double* __restrict__ w, int64_t n, double* partials,
+                                                   double* out, unsigned* counter) {
+    __shared__ double red[(NVM + 1) * (VB / 32)];
+    int64_t lo2, hi2;
+    bool tail;
+    chunk_pairs(n, lo2, hi2, tail);
+    const double2* w2 = reinterpret_cast<const double2*>(w);
+    double acc[NVM + 1];
+#pragma unroll
+    for (int i = 0; i <= NVM; ++i) acc[i] = 0.0;
+    for (int64_t e = lo2 + threadIdx.x; e < hi2; e += VB) {
+        const double2 wv = __ldcs(w2 + e);
+        double2 vv[NVM];
+#pragma unroll
+        for (int i = 0; i < NVM; ++i)
+            if (i < nv) vv[i] = __ldcs(reinterpret_cast<const double2*>(V + (int64_t)i * ldv) + e);
+#pragma unroll
+        for (int i = 0; i < NVM; ++i)
+            if (i < nv) acc[i] = fma(vv[i].y, wv.y, fma(vv[i].x, wv.x, acc[i]));
+        acc[NVM] = fma(wv.y, wv.y, fma(wv.x, wv.x, acc[NVM]));
+    }
+    if (tail && threadIdx.x == 0) {
+        const double wv = w[n - 1];
+#pragma unroll
+        for (int i = 0; i < NVM; ++i)
+            if (i < nv) acc[i] = fma(V[(int64_t)i * ldv + n - 1], wv, acc[i]);
+        acc[NVM] = fma(wv, wv, acc[NVM]);
+    }
+    block_store_partials_t<NVM>(acc, nv, red, partials);
+    block_store_partials_t<1>(acc + NVM, 1, red, partials + (int64_t)nv * gridDim.x);
+    if (last_cta(counter)) reduce_partials_cta(partials, gridDim.x, nv + 1, out, counter);
+}
+
+// pass 2: w' = w - V h (h = h1[0..nv)); out[i] = V_i . w', out[nv] = w' . w'
+template <int NVM>
+__global__ void __launch_bounds__(VB) k_update_dots_v(const double* __restrict__ V, int64_t ldv, int nv,
+                                                      const double* __restrict__ h, double* __restrict__ w,
+                                                      int64_t n, double* partials, double* out,
+                                                      unsigned* counter) {
+    __shared__ double hs[NVM];
+    __shared__ double red[(NVM + 1) * (VB / 32)];
+    for (int i = threadIdx.x; i < nv; i += blockDim.x) hs[i] = h[i];
+    __syncthreads();
+    int64_t lo2, hi2;
+    bool tail;
+    chunk_pairs(n, lo2, hi2, tail);
+    double2* w2 = reinterpret_cast<double2*>(w);
+    double d[NVM + 1];
+#pragma unroll
+    for (int i = 0; i <= NVM; ++i) d[i] = 0.0;
+    for (int64_t e = lo2 + threadIdx.x; e < hi2; e += VB) {
+        double2 vv[NVM];
+        double2 acc = w2[e];
+#pragma unroll
+        for (int i = 0; i < NVM; ++i)
+            if (i < nv) vv[i] = __ldcs(reinterpret_cast<const double2*>(V + (int64_t)i * ldv) + e);
+#pragma unroll
+        for (int i = 0; i < NVM; ++i)
+            if (i < nv) {
+                acc.x -= hs[i] * vv[i].x;
+                acc.y -= hs[i] * vv[i].y;
+            }
+        w2[e] = acc;
+#pragma unroll
+        for (int i = 0; i < NVM; ++i)
+            if (i < nv) d[i] = fma(vv[i].y, acc.y, fma(vv[i].x, acc.x, d[i]));
+        d[NVM] = fma(acc.y, acc.y, fma(acc.x, acc.x, d[NVM]));
+    }
+    if (tail && threadIdx.x == 0) {
+        double vv[NVM];
+        double acc = w[n - 1];
+#pragma unroll
+        for (int i = 0; i < NVM; ++i)
+            if (i < nv) {
+                vv[i] = V[(int64_t)i * ldv + n - 1];
+                acc -= hs[i] * vv[i];
+            }
+        w[n - 1] = acc;
+#pragma unroll
+        for (int i = 0; i < NVM; ++i)
+            if (i < nv) d[i] = fma(vv[i], acc, d[i]);
+        d[NVM] = fma(acc, acc, d[NVM]);
+    }
+    block_store_partials_t<NVM>(d, nv, red, partials);
+    block_store_partials_t<1>(d + NVM, 1, red, partials + (int64_t)nv * gridDim.x);
+    if (last_cta(counter)) reduce_partials_cta(partials, gridDim.x, nv + 1, out, counter);
+}
+
+// pass 3: DGKS correction (decided on the device) fused with the normalisation.
+// reorth = ||w'|| < eta ||w|| (ww0 = w.w from pass 1, h2[nv] = w'.w' from pass 2).
+// ||w''||^2 = w'.w' - |h2|^2 (V orthonormal, V^T w' = h2; |h2|^2 << w'.w' whenever
+// the pass runs, so the difference is exact to rounding) when reorth, else w'.w'.
+// w <- (reorth ? w' - V h2 : w') / ||w''|| unless ||w''|| <= brk (breakdown:
+// the vector is left unscaled, krylov.py:98-102).  out = [||w''||^2, reorth].
+template <int NVM>
+__global__ void __launch_bounds__(VB) k_finish_v(const double* __restrict__ V, int64_t ldv, int nv,
+                                                 const double* __restrict__ ww0, const double* __restrict__ h2,
+                                                 double eta, double brk, double* __restrict__ w, int64_t n,
+                                                 double* out) {
+    __shared__ double hs[NVM];
+    const bool reorth = sqrt(h2[nv]) < eta * sqrt(*ww0);
+    double nw2 = h2[nv];
+    if (reorth) {
+        double q = 0.0;
+        for (int i = 0; i < nv; ++i) q = fma(h2[i], h2[i], q);
+        nw2 -= q;
+    }
+    // a large correction (near breakdown / lost orthogonality): the host measures
+    // ||w''|| with a reduction and scales (out[2] = 1)
+    const bool exact = !reorth || nw2 >= 0.75 * h2[nv];
+    const double nw = sqrt(nw2);
+    const bool scale = exact && nw > brk;
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        out[0] = nw2;
+        out[1] = reorth ? 1.0 : 0.0;
+        out[2] = exact ? 0.0 : 1.0;
+    }
+    if (!reorth && !scale) return;
+    for (int i = threadIdx.x; i < nv; i += blockDim.x) hs[i] = reorth ? h2[i] : 0.0;
+    __syncthreads();
+    int64_t lo2, hi2;
+    bool tail;
+    chunk_pairs(n, lo2, hi2, tail);
+    double2* w2 = reinterpret_cast<double2*>(w);
+    for (int64_t e = lo2 + threadIdx.x; e < hi2; e += VB) {
+        double2 acc = w2[e];
+        if (reorth) {
+            double2 vv[NVM];
+#pragma unroll
+            for (int i = 0; i < NVM; ++i)
+                if (i < nv) vv[i] = __ldcs(reinterpret_cast<const double2*>(V + (int64_t)i * ldv) + e);
+#pragma unroll
+            for (int i = 0; i < NVM; ++i)
+                if (i < nv) {
+                    acc.x -= hs[i] * vv[i].x;
+                    acc.y -= hs[i] * vv[i].y;
+                }
+        }
+        if (scale) {
+            acc.x /= nw;
+            acc.y /= nw;
+        }
+        w2[e] = acc;
+    }
+    if (tail && threadIdx.x == 0) {
+        double acc = w[n - 1];
+        if (reorth)
+            for (int i = 0; i < nv; ++i) acc -= hs[i] * V[(int64_t)i * ldv + n - 1];
+        if (scale) acc /= nw;
+        w[n - 1] = acc;
+    }
+}
+
 // y = x / d  (d on host)
 __global__ void k_scale_div(const double* __restrict__ x, double* __restrict__ y, int64_t n, double d) {
     for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x)
@@ -341,22 +512,47 @@ struct Workspace {
 // with h2 = V^T w' (+ w'.w') in the same sweep; pass 3 the DGKS correction
 // w'' = w' - V h2, applied only if ||w'|| < eta ||w|| (decided on the device).
 // out layout: [h1 (nv+1) | h2 (nv+1) | w''.w'', reorth flag].  nv <= 32.
-static int cgs2_fused(const irk_ctx* ctx, int64_t n, int nv, const double* V, double* w, double eta,
+static int cgs2_fused(const irk_ctx* ctx, int64_t n, int64_t ldv, int nv, const double* V, double* w, double eta,
                       double* partials, unsigned* counters, double* out, cudaStream_t st) {
     const int nb = vec_blocks(ctx);
     double* h1 = out;
     double* h2 = out + nv + 1;
     double* n3 = out + 2 * (nv + 1);
-    k_multidot_r<<<nb, VB, 0, st>>>(V, n, nv, w, n, partials, h1, counters);
+    k_multidot_r<<<nb, VB, 0, st>>>(V, ldv, nv, w, n, partials, h1, counters);
     IRK_LAUNCHED();
-    if (nv <= 8) k_update_dots_r<8><<<nb, VB, 0, st>>>(V, n, nv, h1, w, n, partials, h2, counters + 1);
-    else if (nv <= 16) k_update_dots_r<16><<<nb, VB, 0, st>>>(V, n, nv, h1, w, n, partials, h2, counters + 1);
-    else k_update_dots_r<32><<<nb, VB, 0, st>>>(V, n, nv, h1, w, n, partials, h2, counters + 1);
+    if (nv <= 8) k_update_dots_r<8><<<nb, VB, 0, st>>>(V, ldv, nv, h1, w, n, partials, h2, counters + 1);
+    else if (nv <= 16) k_update_dots_r<16><<<nb, VB, 0, st>>>(V, ldv, nv, h1, w, n, partials, h2, counters + 1);
+    else k_update_dots_r<32><<<nb, VB, 0, st>>>(V, ldv, nv, h1, w, n, partials, h2, counters + 1);
     IRK_LAUNCHED();
-    k_update_cond_r<<<nb, VB, sizeof(double) * nv, st>>>(V, n, nv, h1 + nv, h2, eta, w, n, partials, n3,
+    k_update_cond_r<<<nb, VB, sizeof(double) * nv, st>>>(V, ldv, nv, h1 + nv, h2, eta, w, n, partials, n3,
                                                          counters + 2);
     IRK_LAUNCHED();
     return IRK_OK;
+}
+
+// 128-bit fused CGS2 + normalisation, nv <= 16: pass 1 h1 = V^T w (+ w.w); pass 2
+// w' = w - V h1 with h2 = V^T w' (+ w'.w'); pass 3 DGKS correction and the
+// scaling by ||w''|| (k_finish_v).  out = [h1 (nv+1) | h2 (nv+1) | ||w''||^2,
+// reorth, needs-exact-norm].
+template <int NVM>
+static int cgs2_v_t(const irk_ctx* ctx, int64_t n, int64_t ldv, int nv, const double* V, double* w, double eta,
+                     double brk, double* partials, unsigned* counters, double* out, cudaStream_t st) {
+    const int nb = vec_blocks(ctx);
+    double* h1 = out;
+    double* h2 = out + nv + 1;
+    k_multidot_v<NVM><<<nb, VB, 0, st>>>(V, ldv, nv, w, n, partials, h1, counters);
+    IRK_LAUNCHED();
+    k_update_dots_v<NVM><<<nb, VB, 0, st>>>(V, ldv, nv, h1, w, n, partials, h2, counters + 1);
+    IRK_LAUNCHED();
+    k_finish_v<NVM><<<nb, VB, 0, st>>>(V, ldv, nv, h1 + nv, h2, eta, brk, w, n, out + 2 * (nv + 1));
+    IRK_LAUNCHED();
+    return IRK_OK;
+}
+
+static int cgs2_v(const irk_ctx* ctx, int64_t n, int64_t ldv, int nv, const double* V, double* w, double eta,
+                  double brk, double* partials, unsigned* counters, double* out, cudaStream_t st) {
+    if (nv <= 8) return cgs2_v_t<8>(ctx, n, ldv, nv, V, w, eta, brk, partials, counters, out, st);
+    return cgs2_v_t<16>(ctx, n, ldv, nv, V, w, eta, brk, partials, counters, out, st);
 }
 
 static int multidot(const irk_ctx* ctx, int64_t n, int nv, const double* V, int64_t ldv, const double* w,
@@ -457,6 +653,7 @@ int irk_gmres(irk_ctx* ctx, int64_t n, irk_linop op, irk_linop pre, irk_allreduc
     const int restart = std::min(cfg->restart > 0 ? cfg->restart : cfg->max_iters, cfg->max_iters);
     IRK_ARG(restart <= 4096, "restart length above 4096 is not supported");
     const double eta = cfg->reorth_eta > 0 ? cfg->reorth_eta : 0.70710678118654752;
+    static const bool cgs_r = getenv("IRK_CGS_R") != nullptr;   // A/B: the scalar fused passes
     *stats = irk_gmres_stats{};
     stats->final_true_residual = NAN;
     int hist_n = 0;
@@ -467,7 +664,9 @@ int irk_gmres(irk_ctx* ctx, int64_t n, irk_linop op, irk_linop pre, irk_allreduc
     Workspace ws;
     ws.st = st;
     const int nblk = vec_blocks(ctx);
-    IRK_CK(cudaMallocAsync(&ws.V, sizeof(double) * n * (restart + 1), st));
+    // V columns padded to 32 elements: 256-byte aligned, pairs are single 128-bit loads
+    const int64_t ldV = (n + 31) & ~int64_t(31);
+    IRK_CK(cudaMallocAsync(&ws.V, sizeof(double) * ldV * (restart + 1), st));
     IRK_CK(cudaMallocAsync(&ws.tmp, sizeof(double) * n, st));
     IRK_CK(cudaMallocAsync(&ws.partials, sizeof(double) * nblk * (restart + 2) * 2, st));
     IRK_CK(cudaMallocAsync(&ws.small, sizeof(double) * 6 * (restart + 4), st));
@@ -478,7 +677,7 @@ int irk_gmres(irk_ctx* ctx, int64_t n, irk_linop op, irk_linop pre, irk_allreduc
     double* cdev = ws.small + 2 * (restart + 4);   // restart+1 coefficients
     double* fdev = ws.small + 3 * (restart + 4);   // fused CGS2 outputs, 2 (restart+1) + 2
     std::vector<double> hbuf(2 * (restart + 4));
-    auto V = [&](int i) { return ws.V + (int64_t)i * n; };
+    auto V = [&](int i) { return ws.V + (int64_t)i * ldV; };
     const int g1 = grid_1d(ctx, n);
 
     auto ar = [&](double* buf, int64_t cnt) -> int {
@@ -571,10 +770,28 @@ int irk_gmres(irk_ctx* ctx, int64_t n, irk_linop op, irk_linop pre, irk_allreduc
             }
             stats->operator_applies += 1;
             double nw;
-            if (!allreduce && j + 1 <= 32) {
+            bool scaled = false;   // w already divided by nw on the device
+            const double brk = 1e-14 * std::max(b_norm, 1.0);
+            if (!allreduce && j + 1 <= 16 && !cgs_r) {
+                // 128-bit fused CGS2 + normalisation (3 passes), one host sync
+                const int nv = j + 1;
+                IRK_TRY(cgs2_v(ctx, n, ldV, nv, ws.V, w, eta, brk, ws.partials, ws.counters, fdev, st));
+                IRK_CK(cudaMemcpyAsync(hbuf.data(), fdev, sizeof(double) * (2 * (nv + 1) + 3),
+                                       cudaMemcpyDeviceToHost, st));
+                IRK_CK(cudaStreamSynchronize(st));
+                const bool reorth = hbuf[2 * (nv + 1) + 1] != 0.0;
+                for (int i = 0; i <= j; ++i) Hc(i, j) = hbuf[i] + (reorth ? hbuf[nv + 1 + i] : 0.0);
+                if (reorth) stats->reorth_passes += 1;
+                if (hbuf[2 * (nv + 1) + 2] != 0.0) {
+                    IRK_TRY(norm(w, nw, nullptr));   // large correction: measured norm, host scaling
+                } else {
+                    nw = std::sqrt(hbuf[2 * (nv + 1)]);
+                    scaled = true;
+                }
+            } else if (!allreduce && j + 1 <= 32) {
                 // fused CGS2 (3 passes, DGKS decided on the device), one host sync
                 const int nv = j + 1;
-                IRK_TRY(cgs2_fused(ctx, n, nv, ws.V, w, eta, ws.partials, ws.counters, fdev, st));
+                IRK_TRY(cgs2_fused(ctx, n, ldV, nv, ws.V, w, eta, ws.partials, ws.counters, fdev, st));
                 IRK_CK(cudaMemcpyAsync(hbuf.data(), fdev, sizeof(double) * (2 * (nv + 1) + 2),
                                        cudaMemcpyDeviceToHost, st));
                 IRK_CK(cudaStreamSynchronize(st));
@@ -584,9 +801,9 @@ int irk_gmres(irk_ctx* ctx, int64_t n, irk_linop op, irk_linop pre, irk_allreduc
                 nw = std::sqrt(hbuf[2 * (nv + 1)]);
             } else {
             // classical Gram-Schmidt: h = V^T w (+ w.w), then w -= V h (+ w.w)
-            IRK_TRY(multidot(ctx, n, j + 1, ws.V, n, w, ws.partials, hdev, st));
+            IRK_TRY(multidot(ctx, n, j + 1, ws.V, ldV, w, ws.partials, hdev, st));
             IRK_TRY(ar(hdev, j + 2));
-            IRK_TRY(update(ctx, n, j + 1, ws.V, n, hdev, w, ws.partials, ndev, st));
+            IRK_TRY(update(ctx, n, j + 1, ws.V, ldV, hdev, w, ws.partials, ndev, st));
             IRK_TRY(ar(ndev, 1));
             IRK_CK(cudaMemcpyAsync(hbuf.data(), hdev, sizeof(double) * (j + 2), cudaMemcpyDeviceToHost, st));
             double nrm2;
@@ -597,9 +814,9 @@ int irk_gmres(irk_ctx* ctx, int64_t n, irk_linop op, irk_linop pre, irk_allreduc
             nw = std::sqrt(nrm2);
             if (nw < eta * norm_before) {
                 // DGKS second pass
-                IRK_TRY(multidot(ctx, n, j + 1, ws.V, n, w, ws.partials, hdev, st));
+                IRK_TRY(multidot(ctx, n, j + 1, ws.V, ldV, w, ws.partials, hdev, st));
                 IRK_TRY(ar(hdev, j + 2));
-                IRK_TRY(update(ctx, n, j + 1, ws.V, n, hdev, w, ws.partials, ndev, st));
+                IRK_TRY(update(ctx, n, j + 1, ws.V, ldV, hdev, w, ws.partials, ndev, st));
                 IRK_TRY(ar(ndev, 1));
                 IRK_CK(cudaMemcpyAsync(hbuf.data(), hdev, sizeof(double) * (j + 2), cudaMemcpyDeviceToHost, st));
                 IRK_CK(cudaMemcpyAsync(&nrm2, ndev, sizeof(double), cudaMemcpyDeviceToHost, st));
@@ -610,9 +827,11 @@ int irk_gmres(irk_ctx* ctx, int64_t n, irk_linop op, irk_linop pre, irk_allreduc
             }
             }
             Hc(j + 1, j) = nw;
-            if (nw > 1e-14 * std::max(b_norm, 1.0)) {
-                k_scale_div<<<g1, 256, 0, st>>>(w, w, n, nw);
-                IRK_LAUNCHED();
+            if (nw > brk) {
+                if (!scaled) {
+                    k_scale_div<<<g1, 256, 0, st>>>(w, w, n, nw);
+                    IRK_LAUNCHED();
+                }
             } else {
                 breakdown = true;
             }
@@ -642,7 +861,7 @@ int irk_gmres(irk_ctx* ctx, int64_t n, irk_linop op, irk_linop pre, irk_allreduc
             y[i] = acc / Hc(i, i);
         }
         IRK_CK(cudaMemcpyAsync(cdev, y.data(), sizeof(double) * j_done, cudaMemcpyHostToDevice, st));
-        k_axpy_multi<<<g1, 256, sizeof(double) * std::max(j_done, 1), st>>>(ws.V, n, j_done, cdev, x, n);
+        k_axpy_multi<<<g1, 256, sizeof(double) * std::max(j_done, 1), st>>>(ws.V, ldV, j_done, cdev, x, n);
         IRK_LAUNCHED();
         if (last_res <= tol_abs || breakdown) {
             converged = true;

@@ -120,19 +120,36 @@ class StageMatrix:
         out[self.diag_pos] += self.coef * self.mass.blocks
         return out
 
-    def matvec(self, x, counter: OpCounter | None = None):
-        if tuple(x.shape) != (self.n,):
-            raise ValueError(f"expected vector of length {self.n}, got {tuple(x.shape)}")
+    def _native_op(self):
         if self._op is None:
             self._op = make_stage_op(self.pattern, 1, [self.jac.blocks], [self.jac.first],
                                      self.mass.device, np.array([[self.coef]]), -self.dt)
+        return self._op
+
+    def native_linop(self):
+        op = L.Linop()
+        L.check(L.lib().irk_linop_stage_op(self._native_op().handle, op), "irk_linop_stage_op")
+        return op, self
+
+    def apply_device(self, x, y) -> None:
+        L.check(L.lib().irk_stage_op_apply(self._native_op().handle, x.data_ptr(), y.data_ptr(),
+                                           L.stream_ptr()), "irk_stage_op_apply")
+
+    def matvec(self, x, counter: OpCounter | None = None):
+        if tuple(x.shape) != (self.n,):
+            raise ValueError(f"expected vector of length {self.n}, got {tuple(x.shape)}")
+        self._native_op()
         xd, was_np = to_device(x)
         y = empty_like_dev(self.n)
         L.check(L.lib().irk_stage_op_apply(self._op.handle, xd.data_ptr(), y.data_ptr(),
                                            L.stream_ptr()), "irk_stage_op_apply")
         if counter is not None:
-            counter.block_multiplies += self.nnz_blocks
+            self._charge(counter)
         return from_device(y, was_np)
+
+    def _charge(self, counter: OpCounter) -> None:
+        """Counter increments of one matvec (precond.py:57 via BlockSparseMatrix.matvec)."""
+        counter.block_multiplies += self.nnz_blocks
 
 
 def build_stage_matrix(coef: float, mass, jac, dt: float) -> StageMatrix:
@@ -262,8 +279,30 @@ class BlockIlu0(_Factor):
     def apply(self, y, counter: OpCounter | None = None):
         x = self._apply(y, self.n)
         if counter is not None:
-            counter.block_multiplies += self.num_kept_offdiag + self.T_elems
+            self._charge(counter)
         return x
+
+    def _charge(self, counter: OpCounter) -> None:
+        """precond.py:84-86"""
+        counter.block_multiplies += self.num_kept_offdiag + self.T_elems
+
+    def apply_rhs_device(self, y, x, nrhs: int) -> None:
+        """x = P^-1 y for nrhs stage-major columns (nrhs, T, m) in one sweep that
+        reads the factor once (BASELINE config 3; same result as nrhs applies)."""
+        L.check(L.lib().irk_factor_apply_rhs(self.handle, int(nrhs), y.data_ptr(), x.data_ptr(),
+                                             L.stream_ptr()), "irk_factor_apply_rhs")
+
+    def apply_rhs(self, Y, counter: OpCounter | None = None):
+        """Apply to the rows of Y (nrhs, n) (numpy or CUDA tensor)."""
+        nrhs = int(Y.shape[0])
+        if tuple(Y.shape) != (nrhs, self.n):
+            raise ValueError(f"expected shape (nrhs, {self.n}), got {tuple(Y.shape)}")
+        yd, was_np = to_device(Y.reshape(-1))
+        x = empty_like_dev(nrhs * self.n)
+        self.apply_rhs_device(yd, x, nrhs)
+        if counter is not None:
+            counter.block_multiplies += nrhs * (self.num_kept_offdiag + self.T_elems)
+        return from_device(x, was_np).reshape(nrhs, self.n)
 
     @property
     def fdata(self) -> np.ndarray:
@@ -319,9 +358,13 @@ class StageUncoupledIlu0(_Factor):
     def apply(self, y, counter: OpCounter | None = None):
         x = self._apply(y, self.s * self.n)
         if counter is not None:
-            kept_off = int(self.keep.sum()) - self.T_elems
-            counter.block_multiplies += self.s * (kept_off + self.T_elems)
+            self._charge(counter)
         return x
+
+    def _charge(self, counter: OpCounter) -> None:
+        """precond.py:228-241 (s per-stage applies, precond.py:84-86 each)"""
+        kept_off = int(self.keep.sum()) - self.T_elems
+        counter.block_multiplies += self.s * (kept_off + self.T_elems)
 
 
 def stage_uncoupled_factorize(op: StageOperator, shifts=None, counter: OpCounter | None = None,
@@ -376,9 +419,13 @@ class StageCoupledIlu0(_Factor):
     def apply(self, y, counter: OpCounter | None = None):
         x = self._apply(y, self.n_total)
         if counter is not None:
-            counter.block_multiplies += (self.s * self.num_kept_offdiag_per_stage
-                                         + self.num_coupling_blocks + self.s * self.T_elems)
+            self._charge(counter)
         return x
+
+    def _charge(self, counter: OpCounter) -> None:
+        """precond.py:158-161"""
+        counter.block_multiplies += (self.s * self.num_kept_offdiag_per_stage
+                                     + self.num_coupling_blocks + self.s * self.T_elems)
 
 
 def stage_coupled_factorize(op: StageOperator, counter: OpCounter | None = None,

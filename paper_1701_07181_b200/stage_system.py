@@ -97,12 +97,16 @@ class StageOperator:
         y = empty_like_dev(self.total_dim)
         self.apply_device(wd, y)
         if counter is not None:
-            jac = sum(J.nnz_blocks for J in self.jacobians)
-            T = self.mass.T_elems
-            counter.jacobian_multiplies += jac
-            counter.mass_multiplies += self.s * self.s * T
-            counter.block_multiplies += jac + self.s * self.s * T
+            self._charge(counter)
         return from_device(y, was_np)
+
+    def _charge(self, counter: OpCounter) -> None:
+        """Counter increments of one matvec, exactly as stage_system.py:65-69."""
+        jac = sum(J.nnz_blocks for J in self.jacobians)
+        T = self.mass.T_elems
+        counter.jacobian_multiplies += jac
+        counter.mass_multiplies += self.s * self.s * T
+        counter.block_multiplies += jac + self.s * self.s * T
 
     def native_linop(self):
         op = L.Linop()

@@ -389,3 +389,35 @@ def test_partitioned_ranks_emulated_on_one_gpu():
         sol.factorize()
         a = sol.fac.apply(wl).view(s, -1, nb).cpu().numpy()
         assert rel(a, aref[:, plan.lo:plan.hi]) < TOL
+
+
+@pytest.mark.parametrize("nb", [24, 40, 50, 100])
+@pytest.mark.parametrize("ordering", ["color", "natural"])
+def test_config3_multi_rhs_vs_oracle(nb, ordering):
+    """BASELINE config 3 kernels: plain ILU(0) of J itself and the BSR matvec,
+    one factor / one matrix applied to s = 1..4 right-hand sides in one sweep
+    (factor blocks read once).  Each column must match the oracle's ilu0_solve /
+    bsr_matvec (numba_backend.py:21-30, 75-91) and the single-RHS device apply."""
+    import torch
+    from paper_1701_07181_b200.blocks import BlockSparseMatrix, DeviceBlocks, DevicePattern
+    from paper_1701_07181_b200.precond import ilu0_factorize
+    cfg = W.CONFIGS[1].scaled(N=6, nb=nb, ordering=ordering)
+    wl = W.make_workload(cfg, jnorm=1.0)
+    p = wl.pattern
+    keep = np.ones(p.nnzb, bool)
+    fo, do, fail = O.ilu0_factor(p.indptr, p.indices, p.diag_pos, wl.J, keep, True)
+    assert fail == -1
+    J = BlockSparseMatrix(DevicePattern(p.indptr, p.indices, p.diag_pos), DeviceBlocks.from_host(wl.J))
+    fac = ilu0_factorize(J)
+    n = p.T * nb
+    rng = np.random.default_rng(nb)
+    for nrhs in (1, 2, 3, 4):
+        Y = rng.standard_normal((nrhs, n))
+        X = fac.apply_rhs(Y)
+        Z = J.matvec_rhs(Y)
+        for k in range(nrhs):
+            xo = O.ilu0_solve(p.indptr, p.indices, p.diag_pos, fo, do, keep, Y[k])
+            assert rel(X[k], xo) < TOL
+            assert rel(Z[k], O.bsr_matvec(p.indptr, p.indices, wl.J, Y[k])) < TOL
+            x1 = fac.apply(torch.from_numpy(Y[k]).cuda()).cpu().numpy()
+            assert rel(X[k], x1) < 1e-14

@@ -15,7 +15,7 @@ timeout 600 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__byte
   > $O/ncu_launch_$TAG.log 2>&1; echo "ncu launches rc=$?"
 # full capture of the hot kernels of one timed step (launches after warmup)
 timeout 1200 ncu --set full --clock-control none --import-source on \
-  -k regex:"k_unc_fwd|k_unc_bwd|k_stage_matvec|k_factor|k_inverse|k_cgs|k_multidot|k_update" \
+  -k regex:"k_schur|k_inverse|k_unc|k_stage_matvec|k_multidot|k_update|k_finish" \
   --profile-from-start off -c ${NCU_COUNT:-12} -f -o $O/full_$TAG \
   python bench.py --steps 1 --warmup 1 --profile --no-alt --jnorm 2.4496432463318416 > $O/ncu_full_$TAG.log 2>&1
 echo "ncu full rc=$?"
