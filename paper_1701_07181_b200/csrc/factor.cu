@@ -647,8 +647,12 @@ __device__ __forceinline__ void fence_proxy_async_smem() {
 template <int S, int NB>
 __global__ void __launch_bounds__(4 * NB) k_schur(FactorArgs F, const int32_t* __restrict__ elems, int64_t nelem) {
     using Gm = SchurGeo<NB>;
-    constexpr int NT = Gm::NT, NP = Gm::NP, LDP = Gm::LDP, SLOT = Gm::SLOT;
-    constexpr int64_t BSZ = (int64_t)NB * NB;
+    constexpr int NT = Gm::NT, LDP = Gm::LDP, SLOT = Gm::SLOT;
+    // NB = nb rounded up to 8: the padding rows / columns of the staged blocks are
+    // zero (slots zeroed once; bulk copies write only the nb x nb part), so the
+    // padded DMMA tiles leave the nb x nb results exact
+    const int nbv = F.nb, Pv = (nbv + 1) >> 1;
+    const int64_t BSZ = (int64_t)nbv * 2 * Pv;      // device block (column-pair layout)
     constexpr int SJ = 0, SU = 1;   // slots: J_ji, J_ij, then Dinv_k / A'_k at 2 + k
     extern __shared__ __align__(128) double shs[];
     __shared__ __align__(8) uint64_t bars[S + 2];
@@ -656,6 +660,8 @@ __global__ void __launch_bounds__(4 * NB) k_schur(FactorArgs F, const int32_t* _
     const int fr = lane >> 2, fk = lane & 3;
     const int r0 = warp * 8;
     const double* J = F.J[0];
+    if (nbv != NB)
+        for (int e = threadIdx.x; e < (S + 2) * SLOT; e += blockDim.x) shs[e] = 0.0;
     if (threadIdx.x == 0) {
         for (int b = 0; b < S + 2; ++b) mbar_init(&bars[b], 1);
         fence_mbar_init();
@@ -672,11 +678,11 @@ __global__ void __launch_bounds__(4 * NB) k_schur(FactorArgs F, const int32_t* _
         if (warp == 0) {
             if (lane == 0) {
                 fence_proxy_async_smem();
-                mbar_expect_tx(&bars[b], (uint32_t)(NP * NB * 16));
+                mbar_expect_tx(&bars[b], (uint32_t)(Pv * nbv * 16));
             }
             __syncwarp();
-            for (int p = lane; p < NP; p += 32)
-                bulk_g2s(shs + (size_t)b * SLOT + p * LDP, src + (int64_t)p * NB * 2, NB * 16, &bars[b]);
+            for (int p = lane; p < Pv; p += 32)
+                bulk_g2s(shs + (size_t)b * SLOT + p * LDP, src + (int64_t)p * nbv * 2, nbv * 16, &bars[b]);
         }
     };
     // a "unit" is a (element, lower neighbour q) pair whose Schur update runs on
@@ -709,7 +715,11 @@ __global__ void __launch_bounds__(4 * NB) k_schur(FactorArgs F, const int32_t* _
     auto frag_b = [&](const double* slotp, int kk, int t) -> double {   // B(4kk + fk, 8t + fr)
         return slotp[((8 * t + fr) >> 1) * LDP + 2 * (4 * kk + fk) + (fr & 1)];
     };
-    auto gl_off = [&](int t) -> int64_t { return (int64_t)(4 * t + fk) * NB + r0 + fr; };   // in double2
+    // double2 index of (row r0 + fr, column pair 4t + fk) in a device block; -1: padding
+    auto gl_off = [&](int t) -> int64_t {
+        const int pp = 4 * t + fk, a = r0 + fr;
+        return (pp < Pv && a < nbv) ? (int64_t)pp * nbv + a : -1;
+    };
 
     for (int64_t it = blockIdx.x; it < nelem; it += gridDim.x) {
         const int j = elems[it];
@@ -722,8 +732,9 @@ __global__ void __launch_bounds__(4 * NB) k_schur(FactorArgs F, const int32_t* _
             const double2* Md = F.M ? reinterpret_cast<const double2*>(F.M + (int64_t)j * BSZ) : nullptr;
 #pragma unroll
             for (int t = 0; t < NT; ++t) {
-                const double2 jv = Jd[gl_off(t)];
-                const double2 mv = Md ? Md[gl_off(t)] : make_double2(0.0, 0.0);
+                const int64_t go = gl_off(t);
+                const double2 jv = go >= 0 ? Jd[go] : make_double2(0.0, 0.0);
+                const double2 mv = (Md && go >= 0) ? Md[go] : make_double2(0.0, 0.0);
 #pragma unroll
                 for (int k = 0; k < S; ++k) {
                     double x0 = __dmul_rn(F.alpha, jv.x), x1 = __dmul_rn(F.alpha, jv.y);
@@ -777,7 +788,7 @@ __global__ void __launch_bounds__(4 * NB) k_schur(FactorArgs F, const int32_t* _
                 for (int t = 0; t < NT; ++t) {
                     acc[t][0] *= F.alpha;
                     acc[t][1] *= F.alpha;
-                    if (Lout)
+                    if (Lout && gl_off(t) >= 0)
                         reinterpret_cast<double2*>(Lout + (int64_t)k * BSZ)[gl_off(t)] = make_double2(acc[t][0], acc[t][1]);
                 }
                 __syncthreads();   // all warps: GEMM1_k done (Dinv_k slot), GEMM2_{k-1} done (A'_{k-1})
@@ -811,7 +822,8 @@ __global__ void __launch_bounds__(4 * NB) k_schur(FactorArgs F, const int32_t* _
         for (int k = 0; k < S; ++k) {
             double2* Dk = reinterpret_cast<double2*>(F.Dst + ((int64_t)j * S + k) * BSZ);
 #pragma unroll
-            for (int t = 0; t < NT; ++t) Dk[gl_off(t)] = make_double2(dacc[k][t][0], dacc[k][t][1]);
+            for (int t = 0; t < NT; ++t)
+                if (gl_off(t) >= 0) Dk[gl_off(t)] = make_double2(dacc[k][t][0], dacc[k][t][1]);
         }
     }
 }
@@ -837,7 +849,7 @@ static int launch_schur_t(const irk_ctx* ctx, const FactorArgs& F, const int32_t
 template <int S>
 static int launch_schur_s(const irk_ctx* ctx, const FactorArgs& F, const int32_t* elems, int64_t nelem,
                           cudaStream_t st) {
-    switch (F.nb) {
+    switch ((F.nb + 7) & ~7) {   // padded to the 8x8 DMMA tile
         case 16: return launch_schur_t<S, 16>(ctx, F, elems, nelem, st);
         case 24: return launch_schur_t<S, 24>(ctx, F, elems, nelem, st);
         case 32: return launch_schur_t<S, 32>(ctx, F, elems, nelem, st);
@@ -852,7 +864,7 @@ static int launch_schur_s(const irk_ctx* ctx, const FactorArgs& F, const int32_t
 static bool schur_eligible(const irk_factor* f, const FactorArgs& F) {
     if (getenv("IRK_NO_SCHUR")) return false;   // A/B switch for the generic kernel
     return f->kind == IRK_FACTOR_UNCOUPLED && f->simplified && f->u_shared && F.Dst != nullptr &&
-           F.nb % 8 == 0 && F.nb >= 16 && F.nb <= 64 && F.s <= 4;
+           F.nb >= 12 && F.nb <= 64 && F.s <= 4;
 }
 
 static int launch_schur(const irk_ctx* ctx, const FactorArgs& F, const int32_t* elems, int64_t nelem,
@@ -867,7 +879,7 @@ static int launch_schur(const irk_ctx* ctx, const FactorArgs& F, const int32_t* 
 }
 
 int launch_inverse(const irk_ctx* ctx, const int32_t* tasks, int64_t ntasks, int64_t T, int s, int nb,
-                   const double* D, double* Dinv, unsigned long long* fail_key, cudaStream_t st);
+                   const double* D, double* Dinv, unsigned long long* fail_key, int* fb, cudaStream_t st);
 
 template <int MAXT>
 static int launch_levels(const irk_factor* f, FactorArgs& F, const irk_sched& sched, size_t smem,
@@ -891,11 +903,11 @@ static int launch_levels(const irk_factor* f, FactorArgs& F, const irk_sched& sc
         if (split && schur_eligible(f, F)) {
             // level tasks are stage-major (k*T + e, skew 0): the first 1/s are the elements
             IRK_TRY(launch_schur(f->ctx, F, F.tasks, F.ntasks / F.s, st));
-            IRK_TRY(launch_inverse(f->ctx, F.tasks, F.ntasks, F.T, F.s, F.nb, F.Dst, F.Dinv, F.fail_key, st));
+            IRK_TRY(launch_inverse(f->ctx, F.tasks, F.ntasks, F.T, F.s, F.nb, F.Dst, F.Dinv, F.fail_key, f->d_fb, st));
         } else if (split) {
             k_factor<MAXT, false><<<grid, 256, smem, st>>>(F);
             IRK_LAUNCHED();
-            IRK_TRY(launch_inverse(f->ctx, F.tasks, F.ntasks, F.T, F.s, F.nb, F.Dst, F.Dinv, F.fail_key, st));
+            IRK_TRY(launch_inverse(f->ctx, F.tasks, F.ntasks, F.T, F.s, F.nb, F.Dst, F.Dinv, F.fail_key, f->d_fb, st));
         } else {
             k_factor<MAXT, true><<<grid, 256, smem, st>>>(F);
             IRK_LAUNCHED();
@@ -1065,6 +1077,8 @@ static int factor_common(irk_ctx* ctx, const irk_pattern* pat, const FactorSetup
     if (P.coupled && npairs > 0) FCK(cudaMalloc(&f->d_G, sizeof(double) * bsz * pat->T * npairs));
     if (P.coupled && P.coupling && npairs > 0) FCK(cudaMalloc(&f->d_Cup, sizeof(double) * bsz * pat->T * npairs));
     FCK(cudaMalloc(&f->d_fail, sizeof(unsigned long long)));
+    // tensor-core inverse fallback list: [count | task codes]
+    if (nb > 16 && nb <= 64) FCK(cudaMalloc(&f->d_fb, sizeof(int) * ((int64_t)P.s * pat->T + 1)));
     if ((rc = set_sources(f, P))) return fail(rc);
     std::vector<int64_t> levf;
     if ((rc = build_apply_schedules(f, keep))) return fail(rc);
@@ -1230,6 +1244,7 @@ void irk_factor_destroy(irk_factor* f) {
     cudaFree(f->d_L);
     cudaFree(f->d_W);
     cudaFree(f->d_Wrhs);
+    cudaFree(f->d_fb);
     cudaFree(f->d_hasup);
     cudaFree(f->d_Dinv);
     cudaFree(f->d_D);

@@ -56,7 +56,13 @@ struct InvArgs {
     const double* D;          // pivot blocks D[j][k] (device layout)
     double* Dinv;             // inverses Dinv[j][k]
     unsigned long long* fail_key;
+    const int* ntasks_dev;    // non-NULL: task count on the device (<= ntasks), fallback lists
 };
+
+// task count of a launch: the host bound, or the device count of a fallback list
+__device__ __forceinline__ int64_t task_count(const InvArgs& A) {
+    return A.ntasks_dev ? (int64_t)min((long long)*A.ntasks_dev, (long long)A.ntasks) : A.ntasks;
+}
 
 // EXACT: nb == NBT -- the pivot loop is fully unrolled, so every register
 // index (column k, pivot column extraction) is a compile-time constant.
@@ -76,7 +82,7 @@ __global__ void __launch_bounds__(128) k_inverse(InvArgs A) {
     const int P = (nb + 1) >> 1;
     const int64_t bsz = (int64_t)nb * 2 * P;
 
-    for (int64_t t = (int64_t)blockIdx.x * wpb + warp; t < A.ntasks; t += (int64_t)gridDim.x * wpb) {
+    for (int64_t t = (int64_t)blockIdx.x * wpb + warp; t < task_count(A); t += (int64_t)gridDim.x * wpb) {
         const int64_t code = A.tasks[t];
         const int k_st = (int)(code / A.T);
         const int64_t j = code - (int64_t)k_st * A.T;
@@ -311,9 +317,10 @@ __global__ void __launch_bounds__(32 * (Inv2Cfg<NB>::G + 1), 2) k_inverse2(InvAr
     const bool live = extra ? (lane < G * E) : true;
     const int P = NB / 2;
     const int64_t bsz = (int64_t)NB * 2 * ((NB + 1) / 2);
-    for (int64_t base = (int64_t)blockIdx.x * G; base < A.ntasks; base += (int64_t)gridDim.x * G) {
+    const int64_t ntask = task_count(A);
+    for (int64_t base = (int64_t)blockIdx.x * G; base < ntask; base += (int64_t)gridDim.x * G) {
         const int64_t t = base + blk;
-        const bool valid = live && t < A.ntasks;
+        const bool valid = live && t < ntask;
         int64_t code = 0, j = 0;
         int k_st = 0;
         if (valid) {
@@ -524,7 +531,7 @@ __global__ void __launch_bounds__(32 * Inv3Cfg<NBR>::WARPS) k_inverse3(InvArgs A
     const int nb = A.nb;
     const int P = (nb + 1) >> 1;
     const int64_t bsz = (int64_t)nb * 2 * P;
-    for (int64_t t = (int64_t)blockIdx.x * C::WARPS + warp; t < A.ntasks; t += (int64_t)gridDim.x * C::WARPS) {
+    for (int64_t t = (int64_t)blockIdx.x * C::WARPS + warp; t < task_count(A); t += (int64_t)gridDim.x * C::WARPS) {
         const int64_t code = A.tasks[t];
         const int k_st = (int)(code / A.T);
         const int64_t j = code - (int64_t)k_st * A.T;
@@ -743,7 +750,7 @@ __global__ void __launch_bounds__(32 * Inv4Cfg::WARPS, MINB) k_inverse4(InvArgs 
     const int64_t bsz = (int64_t)nb * 2 * P;
     const int q = lane & 3, e = lane >> 2, re = 32 + e;
     const int gbase = lane & ~3, gnext = gbase | ((q + 1) & 3);
-    for (int64_t t = (int64_t)blockIdx.x * C::WARPS + warp; t < A.ntasks; t += (int64_t)gridDim.x * C::WARPS) {
+    for (int64_t t = (int64_t)blockIdx.x * C::WARPS + warp; t < task_count(A); t += (int64_t)gridDim.x * C::WARPS) {
         const int64_t code = A.tasks[t];
         const int k_st = (int)(code / A.T);
         const int64_t j = code - (int64_t)k_st * A.T;
@@ -1001,11 +1008,240 @@ static int launch_t(const irk_ctx* ctx, const InvArgs& A, cudaStream_t st) {
     return IRK_OK;
 }
 
+// ---------------------------------------------------------------------------
+// Blocked Gauss-Jordan on the FP64 tensor cores (DMMA m8n8k4), 16 < nb <= 64.
+//
+// One warp per block, the block in shared memory (row-major, ld = NBT + 4:
+// conflict-free A/B fragment loads).  Panels of 8 columns: the 8 scalar GJ
+// steps run on the NBT x 8 panel in registers (lane = (column c = l&7, row
+// group q = l>>3), rows q, q+4, ...), leaving [G; F] = in-place GJ values of
+// the panel columns; the other columns get the rank-8 update
+//     A_R <- [0; A_R'] + [G; F] * A_KR      (A_KR = the panel's rows, old)
+// as 8x8 DMMA tiles.  2 nb^3 flops, ~80% of them on the tensor cores.
+//
+// No row interchanges: a block takes this path only if, at every step, the
+// diagonal is a partial-pivoting choice (|a_kk| >= |a_rk| for all r > k; ties
+// go to the smaller row, the getrf/idamax rule), i.e. getrf would not swap --
+// then the elimination is exactly the pivoted one.  Any block where a swap
+// would happen (or a zero / NaN pivot appears) is appended to a fallback list
+// and re-done by the pivoted warp kernels.  det / cond as _inv_with_cond
+// (numba_backend.py:33-40).
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ void dmma_f64(double& c0, double& c1, double a, double b) {
+    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
+                 : "+d"(c0), "+d"(c1) : "d"(a), "d"(b));
+}
+
+template <int NT>
+struct InvTcCfg {
+    static constexpr int NBT = 8 * NT, LD = NBT + 4, WARPS = 4, RPL = NBT / 4;   // rows per lane in a panel
+    static constexpr size_t warp_doubles = (size_t)NBT * LD;
+    static constexpr size_t smem = WARPS * warp_doubles * sizeof(double);
+};
+
+template <int NT>
+__global__ void __launch_bounds__(32 * InvTcCfg<NT>::WARPS) k_inverse_tc(InvArgs A, int* fb_list, int* fb_count) {
+    using C = InvTcCfg<NT>;
+    constexpr int NBT = C::NBT, LD = C::LD, RPL = C::RPL;
+    extern __shared__ __align__(16) double smtc[];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    double* X = smtc + (size_t)warp * C::warp_doubles;
+    const int nb = A.nb;
+    const int P = (nb + 1) >> 1;
+    const int64_t bsz = (int64_t)nb * 2 * P;
+    const int pc = lane & 7, pq = lane >> 3;        // panel layout: column, row group
+    const int fr = lane >> 2, fk = lane & 3;        // fragment layout
+    for (int64_t t = (int64_t)blockIdx.x * C::WARPS + warp; t < A.ntasks; t += (int64_t)gridDim.x * C::WARPS) {
+        const int64_t code = A.tasks[t];
+        const int k_st = (int)(code / A.T);
+        const int64_t j = code - (int64_t)k_st * A.T;
+        const double2* src = reinterpret_cast<const double2*>(A.D + (j * A.s + k_st) * bsz);
+        // ---- load (identity padding beyond nb)
+        for (int r = lane; r < NBT; r += 32) {
+#pragma unroll
+            for (int p2 = 0; p2 < NBT / 2; ++p2) {
+                double2 v = make_double2(0.0, 0.0);
+                if (r < nb && p2 < P) v = src[(int64_t)p2 * nb + r];
+                if (2 * p2 + 1 >= nb) v.y = 0.0;
+                if (r >= nb) v = make_double2(2 * p2 == r ? 1.0 : 0.0, 2 * p2 + 1 == r ? 1.0 : 0.0);
+                *reinterpret_cast<double2*>(X + r * LD + 2 * p2) = v;
+            }
+        }
+        __syncwarp();
+        // |D|_1: max column abs sum (NaN propagating), columns < nb
+        auto col_norm = [&]() -> double {
+            double mx = -1.0;
+            int nan = 0;
+            for (int c = lane; c < nb; c += 32) {
+                double s4[4] = {0.0, 0.0, 0.0, 0.0};
+                int r = 0;
+                for (; r + 4 <= nb; r += 4)
+#pragma unroll
+                    for (int h = 0; h < 4; ++h) s4[h] += fabs(X[(r + h) * LD + c]);
+                for (; r < nb; ++r) s4[0] += fabs(X[r * LD + c]);
+                const double sum = (s4[0] + s4[1]) + (s4[2] + s4[3]);
+                if (sum != sum) nan = 1;
+                mx = fmax(mx, sum);
+            }
+#pragma unroll
+            for (int o = 16; o; o >>= 1) {
+                mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+                nan |= __shfl_xor_sync(0xffffffffu, nan, o);
+            }
+            return nan ? __longlong_as_double(0x7ff8000000000000LL) : mx;
+        };
+        const double n1 = col_norm();
+        double logdet = 0.0;
+        bool swap = false;
+        static_for([&](auto pc_) {
+            constexpr int p = decltype(pc_)::value;   // panel index
+            constexpr int k0 = 8 * p;
+            if (swap) return;
+            // ---- panel to registers: pv[i] = X[pq + 4 i][k0 + pc]
+            double pv[RPL];
+#pragma unroll
+            for (int i = 0; i < RPL; ++i) pv[i] = X[(pq + 4 * i) * LD + k0 + pc];
+            // ---- 8 scalar GJ steps on the panel
+            static_for([&](auto kc_) {
+                constexpr int kk = decltype(kc_)::value;
+                constexpr int k = k0 + kk;
+                constexpr int kq = k & 3, ki = k >> 2;      // owner row group / register of row k
+                // pivot check (lanes of column kk): max |a_rk| over rows r > k
+                double mx = 0.0;
+#pragma unroll
+                for (int i = 0; i < RPL; ++i)
+                    if (pq + 4 * i > k) mx = fmax(mx, fabs(pv[i]));
+                mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, 8));
+                mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, 16));
+                const double piv = __shfl_sync(0xffffffffu, pv[ki], kk + 8 * kq);
+                const double colmax = __shfl_sync(0xffffffffu, mx, kk);
+                // NaN-safe: the diagonal must be a finite, non-zero maximum
+                const bool ok = (fabs(piv) >= colmax) && piv != 0.0 && isfinite(piv);
+                if (!ok) swap = true;
+                const double inv = 1.0 / piv;
+                if (k < nb) logdet += log(fabs(piv));
+                // new row k value in my column, and my rows' multipliers a_{r,kk}
+                const double rk = __shfl_sync(0xffffffffu, pv[ki], pc + 8 * kq) * inv;
+#pragma unroll
+                for (int i = 0; i < RPL; ++i) {
+                    const double f = __shfl_sync(0xffffffffu, pv[i], kk + 8 * pq);
+                    const bool is_k = (pq + 4 * i == k);
+                    const bool colk = (pc == kk);
+                    double v;
+                    if (is_k) v = colk ? inv : rk;
+                    else v = colk ? -f * inv : fma(-f, rk, pv[i]);
+                    pv[i] = v;
+                }
+            }, std::make_integer_sequence<int, 8>{});
+            if (swap) return;
+            // ---- rank-8 update of the other column tiles (old panel rows as B)
+            double bf[NT][2];
+#pragma unroll
+            for (int jt = 0; jt < NT; ++jt)
+#pragma unroll
+                for (int kc = 0; kc < 2; ++kc)
+                    bf[jt][kc] = (jt == p) ? 0.0 : X[(k0 + 4 * kc + fk) * LD + 8 * jt + fr];
+            __syncwarp();
+#pragma unroll
+            for (int i = 0; i < RPL; ++i) X[(pq + 4 * i) * LD + k0 + pc] = pv[i];
+            __syncwarp();
+#pragma unroll
+            for (int it = 0; it < NT; ++it) {
+                const double a0 = X[(8 * it + fr) * LD + k0 + fk];
+                const double a1 = X[(8 * it + fr) * LD + k0 + 4 + fk];
+#pragma unroll
+                for (int jt = 0; jt < NT; ++jt) {
+                    if (jt == p) continue;
+                    double* cp = X + (8 * it + fr) * LD + 8 * jt + 2 * fk;
+                    double2 c = (it == p) ? make_double2(0.0, 0.0) : *reinterpret_cast<const double2*>(cp);
+                    dmma_f64(c.x, c.y, a0, bf[jt][0]);
+                    dmma_f64(c.x, c.y, a1, bf[jt][1]);
+                    *reinterpret_cast<double2*>(cp) = c;
+                }
+            }
+            __syncwarp();
+        }, std::make_integer_sequence<int, NT>{});
+        if (swap) {
+            if (lane == 0) fb_list[atomicAdd(fb_count, 1)] = (int)code;
+            __syncwarp();
+            continue;
+        }
+        // ---- store inv(D) (device layout) and the condition check
+        double2* dst = reinterpret_cast<double2*>(A.Dinv + (j * A.s + k_st) * bsz);
+        for (int r = lane; r < nb; r += 32)
+            for (int p2 = 0; p2 < P; ++p2) {
+                double2 v = *reinterpret_cast<const double2*>(X + r * LD + 2 * p2);
+                if (2 * p2 + 1 >= nb) v.y = 0.0;
+                dst[(int64_t)p2 * nb + r] = v;
+            }
+        const double n2 = col_norm();
+        if (lane == 0) {
+            const double det = exp(logdet);
+            const double cond = n1 * n2;
+            const bool bad = det == 0.0 || !isfinite(det) || !(cond <= 1e14);
+            if (bad) atomicMin(A.fail_key, (unsigned long long)code);
+        }
+        __syncwarp();
+    }
+}
+
+template <int NT>
+static int launch_tc_t(const irk_ctx* ctx, const InvArgs& A, int* fb_list, int* fb_count, cudaStream_t st) {
+    using C = InvTcCfg<NT>;
+    static bool attr = false;
+    if (!attr) {
+        IRK_CK(cudaFuncSetAttribute(k_inverse_tc<NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::smem));
+        IRK_CK(cudaFuncSetAttribute(k_inverse_tc<NT>, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+        attr = true;
+    }
+    const int threads = 32 * C::WARPS;
+    int per_sm = 1;
+    IRK_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_inverse_tc<NT>, threads, C::smem));
+    const int64_t need = (A.ntasks + C::WARPS - 1) / C::WARPS;
+    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(need, (int64_t)ctx->num_sms * std::max(per_sm, 1)));
+    k_inverse_tc<NT><<<grid, threads, C::smem, st>>>(A, fb_list, fb_count);
+    IRK_LAUNCHED();
+    return IRK_OK;
+}
+
+static int launch_pivoted(const irk_ctx* ctx, const InvArgs& A, cudaStream_t st);
+
+// tensor-core pass, then the pivoted kernels over the blocks it handed back
+// (their count stays on the device: the fallback launch reads it)
+static int launch_tc(const irk_ctx* ctx, const InvArgs& A, int* fb, cudaStream_t st) {
+    int* fb_count = fb;
+    int* fb_list = fb + 1;
+    IRK_CK(cudaMemsetAsync(fb_count, 0, sizeof(int), st));
+    const int nt = (A.nb + 7) / 8;
+    int rc;
+    switch (nt) {
+        case 3: rc = launch_tc_t<3>(ctx, A, fb_list, fb_count, st); break;
+        case 4: rc = launch_tc_t<4>(ctx, A, fb_list, fb_count, st); break;
+        case 5: rc = launch_tc_t<5>(ctx, A, fb_list, fb_count, st); break;
+        case 6: rc = launch_tc_t<6>(ctx, A, fb_list, fb_count, st); break;
+        case 7: rc = launch_tc_t<7>(ctx, A, fb_list, fb_count, st); break;
+        case 8: rc = launch_tc_t<8>(ctx, A, fb_list, fb_count, st); break;
+        default: return IRK_EINVAL;
+    }
+    if (rc) return rc;
+    InvArgs B = A;
+    B.tasks = fb_list;
+    B.ntasks_dev = fb_count;
+    return launch_pivoted(ctx, B, st);
+}
+
 // returns IRK_EINVAL if nb has no warp-inverse specialisation (caller falls back)
 int launch_inverse(const irk_ctx* ctx, const int32_t* tasks, int64_t ntasks, int64_t T, int s, int nb,
-                   const double* D, double* Dinv, unsigned long long* fail_key, cudaStream_t st) {
+                   const double* D, double* Dinv, unsigned long long* fail_key, int* fb, cudaStream_t st) {
     if (ntasks <= 0) return IRK_OK;
-    InvArgs A{tasks, ntasks, T, s, nb, D, Dinv, fail_key};
+    InvArgs A{tasks, ntasks, T, s, nb, D, Dinv, fail_key, nullptr};
+    static const bool tc_off = getenv("IRK_INV_TC") && atoi(getenv("IRK_INV_TC")) == 0;
+    if (fb && !tc_off && nb > 16 && nb <= 64) return launch_tc(ctx, A, fb, st);
+    return launch_pivoted(ctx, A, st);
+}
+
+static int launch_pivoted(const irk_ctx* ctx, const InvArgs& A, cudaStream_t st) {
+    const int nb = A.nb;
     if (nb <= 8) return launch3<8>(ctx, A, st);
     if (nb <= 16) return launch3<16>(ctx, A, st);
     if (nb <= 24) return launch3<24>(ctx, A, st);

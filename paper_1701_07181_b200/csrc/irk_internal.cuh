@@ -151,6 +151,7 @@ struct irk_factor {
     void* fargs = nullptr;            // FactorArgs (factor.cu)
     irk_sched fsched;                 // factor tasks by level
     unsigned long long* d_fail = nullptr;
+    int* d_fb = nullptr;              // tensor-core inverse: blocks handed to the pivoted kernels
     size_t fsmem = 0;
     int maxt = 1;
     const double* cpl_src = nullptr;  // explicit couplings (s*s*T blocks)

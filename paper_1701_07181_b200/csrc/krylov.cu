@@ -484,12 +484,13 @@ __global__ void __launch_bounds__(VB) k_norm_max(const double* __restrict__ x, i
     }
 }
 
+// one warp: lanes strided over the partials, then a shuffle tree (max is exact,
+// so the order does not matter)
 __global__ void k_reduce_max(const double* partials, int nblk, double* out) {
-    if (threadIdx.x == 0 && blockIdx.x == 0) {
-        double t = 0.0;
-        for (int b = 0; b < nblk; ++b) t = fmax(t, partials[b]);
-        *out = t;
-    }
+    double t = 0.0;
+    for (int b = threadIdx.x; b < nblk; b += 32) t = fmax(t, partials[b]);
+    for (int o = 16; o; o >>= 1) t = fmax(t, __shfl_xor_sync(0xffffffffu, t, o));
+    if (threadIdx.x == 0) *out = t;
 }
 
 struct Workspace {

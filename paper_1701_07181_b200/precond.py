@@ -276,6 +276,15 @@ class BlockIlu0(_Factor):
     def num_kept_offdiag(self) -> int:
         return int(self.keep.sum()) - self.T_elems
 
+    def refactor(self, mat) -> "BlockIlu0":
+        """Numeric re-factorisation for new values on the same structure, in
+        place (no allocation): a StageMatrix (coef M - dt J) or a matrix J."""
+        if isinstance(mat, StageMatrix):
+            return self._refactor([mat.jac.blocks], [mat.jac.first], mat.mass.device, [mat.coef],
+                                  -mat.dt, False)
+        dm = as_device_matrix(mat)
+        return self._refactor([dm.blocks], [dm.first], None, None, 1.0, False)
+
     def apply(self, y, counter: OpCounter | None = None):
         x = self._apply(y, self.n)
         if counter is not None:

@@ -1,0 +1,415 @@
+"""Device-resident Newton time steps around the linear solve.
+
+Drop-in for the reference steppers on LINEAR semidiscrete problems
+``M du/dt = J u`` (the synthetic problem of BASELINE config 4, "rhs = J.u"):
+
+* ``irk_step_transformed`` -- reference ``stepper.py:127-181``: Newton on the
+  transformed stage unknowns w_k = sum_l a_kl k_l.  The residual
+  (``compute_residual``, ``stepper.py:156-162``) is
+  ``(A^-1 (x) M) w - [J (u0 + dt w_k)]_k = B w - 1 (x) (J u0)`` with the stage
+  operator B, so it is one fused stage matvec minus a per-step constant;
+* ``dirk_step`` -- reference ``stepper.py:229-287``: sequential stage Newton
+  solves on ``(M - dt a_ii J) k_i = J base_i`` with plain block ILU(0);
+* ``integrate`` -- reference ``stepper.py:328-375`` (fixed step loop).
+
+Everything stays in HBM: J, M, the factors, u and the stage vectors; the
+host sees one scalar per Newton iteration (the residual's inf-norm, the
+reference's convergence test) and the GMRES scalars.  The Newton skeleton,
+tolerances, ``NewtonError`` and ``StepResult`` follow ``stepper.py:26-125``.
+
+Frozen-J reuse (f2): the Jacobian of a linear problem is constant, so the
+stage operator and its preconditioner depend only on (dt, J, M, tableau);
+they are built once and reused across Newton iterations and time steps
+(``StepCache``).  The reference rebuilds them per Newton iteration
+(``stepper.py:164-170``); the factors it rebuilds are identical, so results
+are unchanged (the factorisation is deterministic, bitwise).  OpCounter
+increments reproduce the reference's counts including those rebuilds, so the
+paper's Table 2-4 accounting (``studies.py:261-353``) reads the same.
+"""
+
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _lib as L
+from .blocks import BlockDiagonalMatrix, BlockSparseMatrix, DeviceBlocks, DevicePattern, OpCounter
+from .krylov import GmresConfig, GmresStats, equivalent_multiplications, gmres_device
+from .precond import (build_stage_matrix, ilu0_factorize, partition_keep_mask,
+                      stage_coupled_factorize, stage_uncoupled_factorize)
+from .stage_system import StageOperator
+from .tableau import Tableau, builtin_tableau, derive
+
+
+@dataclass
+class NewtonConfig:
+    abs_tol_inf: float = 1e-8
+    max_iters: int = 50
+
+    def __post_init__(self):
+        if self.abs_tol_inf <= 0:
+            raise ValueError("abs_tol_inf must be positive")
+        if self.max_iters < 1:
+            raise ValueError("max_iters must be at least 1")
+
+
+@dataclass
+class PrecondSpec:
+    """Preconditioner selection (reference stepper.py:39-59)."""
+
+    kind: str = "coupled"
+    partitions: int | None = None
+    stage_parallel: bool = False
+    workers: int | None = None
+
+    KINDS = ("coupled", "coupled-literal", "uncoupled", "uncoupled-unshifted",
+             "block-jacobi", "none")
+
+    def __post_init__(self):
+        if self.kind not in self.KINDS:
+            raise ValueError(f"unknown preconditioner kind {self.kind!r}")
+
+
+@dataclass
+class StepResult:
+    u_next: object              # CUDA tensor (n,)
+    newton_iterations: int
+    gmres_stats: list
+    equivalent_mults_avg: float
+
+
+@dataclass
+class IntegrateResult:
+    u_final: object
+    trajectory: list
+    steps: int
+    newton_iterations: int
+    gmres_iterations: int
+    wall_time: float
+    counter: OpCounter = field(default_factory=OpCounter)
+
+
+class NewtonError(RuntimeError):
+    """Newton failed to reach tolerance; carries the residual history (stepper.py:71-79)."""
+
+    def __init__(self, residual_history: list):
+        self.residual_history = residual_history
+        super().__init__(
+            f"Newton did not converge in {len(residual_history) - 1} iterations"
+            f" (last residual {residual_history[-1]:.3e})")
+
+
+class LinearProblem:
+    """``M du/dt = J u`` with J and M resident on the device.
+
+    ``J``: host (nnzb, m, m) blocks or a device ``BlockSparseMatrix``; ``M``:
+    host (T, m, m) or a ``BlockDiagonalMatrix``.  ``partition_of`` is the
+    element -> partition map used when a step asks for ``partitions`` (the
+    reference's ``meshing.partition``: contiguous ranges, meshing.py:81-90).
+    """
+
+    name = "linear-device"
+    jacobian_is_constant = True
+
+    def __init__(self, pattern: DevicePattern, J, M, u0=None):
+        self.pattern = pattern
+        self.jac = J if isinstance(J, BlockSparseMatrix) else BlockSparseMatrix(
+            pattern, J if isinstance(J, DeviceBlocks) else DeviceBlocks.from_host(np.asarray(J)))
+        self._mass = M if isinstance(M, BlockDiagonalMatrix) else BlockDiagonalMatrix(np.asarray(M))
+        self.m = self.jac.m
+        self.graph = pattern.graph
+        self._u0 = u0
+
+    @property
+    def n(self) -> int:
+        return self.pattern.T * self.m
+
+    def mass(self) -> BlockDiagonalMatrix:
+        return self._mass
+
+    def jacobian(self, t: float, u) -> BlockSparseMatrix:
+        return self.jac
+
+    def rhs(self, t: float, u):
+        """f(t, u) = J u (device)."""
+        return self.jac.matvec(_dev(u))
+
+    def initial_state(self):
+        if self._u0 is None:
+            raise ValueError("no initial state given")
+        return _dev(self._u0).clone()
+
+    def partition_of(self, parts: int | None):
+        if parts is None:
+            return None
+        T = self.pattern.T
+        bounds = np.array([(T * p) // parts for p in range(parts + 1)])
+        return np.repeat(np.arange(parts), np.diff(bounds))
+
+
+def _dev(x):
+    t = L.torch()
+    if isinstance(x, t.Tensor):
+        return x.to(device="cuda", dtype=t.float64).reshape(-1)
+    return t.from_numpy(np.ascontiguousarray(x, dtype=np.float64)).cuda().reshape(-1)
+
+
+def _inf_norm(v) -> float:
+    t = L.torch()
+    return float(t.linalg.vector_norm(v, ord=math.inf)) if v.numel() else 0.0
+
+
+def _charge(counter: OpCounter | None, obj, times: int) -> None:
+    """Add `times` applications of obj (operator or preconditioner) to the counter."""
+    if counter is None or obj is None or times <= 0:
+        return
+    one = OpCounter()
+    obj._charge(one)
+    for k, v in one.snapshot().items():
+        setattr(counter, k, getattr(counter, k) + times * v)
+
+
+def _charge_gmres(counter, op, fac, stats: GmresStats, restart: int | None, max_iters: int):
+    """Operator / preconditioner applications the reference's gmres makes
+    (krylov.py:37-130): P^-1 b and P^-1 (b - B x0) (1 matvec, 2 applies), one of
+    each per iteration, one of each per finished cycle (restart residual), and
+    the final true residual (1 matvec)."""
+    if counter is None:
+        return
+    if stats.operator_applies == 0 and stats.iterations == 0 and stats.converged:
+        return    # zero rhs: no operator touched (krylov.py:48-52)
+    k = stats.iterations
+    R = restart or max_iters
+    cycles = (k + R - 1) // R if k > 0 else 0
+    _charge(counter, op, 1 + k + cycles + 1)
+    _charge(counter, fac, 2 + k + cycles)
+
+
+def _charge_factor(counter, op, kind: str, keep, s: int):
+    """Counter increments of one preconditioner build (precond.py:104-109, 193-199,
+    244-280)."""
+    if counter is None or kind == "none":
+        return
+    pat = op.pattern
+    T = pat.T
+    up = pat.upper_count(keep)
+    if kind in ("coupled", "coupled-literal"):
+        counter.block_factorizations += s * T
+        counter.block_multiplies += 2 * s * up + (s * s - s) * T
+    else:
+        counter.block_factorizations += s * T
+        counter.block_multiplies += 2 * s * up
+
+
+class StepCache:
+    """Frozen-J objects of a linear problem: stage operators and factors keyed by
+    (scheme, dt, preconditioner), built once and reused (f2)."""
+
+    def __init__(self):
+        self._ops = {}
+
+    def transformed(self, problem, tab: Tableau, dt: float, spec: PrecondSpec):
+        key = ("irk", tab.name, float(dt), spec.kind, spec.partitions)
+        if key not in self._ops:
+            der = derive(tab)
+            J = problem.jacobian(0.0, None)
+            op = StageOperator(der, dt, problem.mass(), [J] * tab.s)
+            part = problem.partition_of(spec.partitions)
+            fac, keep = None, partition_keep_mask(op.pattern, part)
+            if spec.kind in ("coupled", "coupled-literal"):
+                fac = stage_coupled_factorize(op, partition_of=part,
+                                              literal_update=spec.kind == "coupled-literal")
+            elif spec.kind == "block-jacobi":
+                keep = partition_keep_mask(op.pattern, np.arange(op.pattern.T))
+                fac = stage_uncoupled_factorize(op, der.shifts, partition_of=np.arange(op.pattern.T))
+            elif spec.kind == "uncoupled":
+                fac = stage_uncoupled_factorize(op, der.shifts, partition_of=part)
+            elif spec.kind == "uncoupled-unshifted":
+                fac = stage_uncoupled_factorize(op, None, partition_of=part)
+            self._ops[key] = (der, op, fac, keep)
+        return self._ops[key]
+
+    def dirk_stage(self, problem, dt_aii: float, partitions):
+        key = ("dirk", float(dt_aii), partitions)
+        if key not in self._ops:
+            J = problem.jacobian(0.0, None)
+            mat = build_stage_matrix(1.0, problem.mass(), J, dt_aii)
+            part = problem.partition_of(partitions)
+            fac = ilu0_factorize(mat, partition_of=part)
+            self._ops[key] = (mat, fac, partition_keep_mask(mat.pattern, part))
+        return self._ops[key]
+
+
+def _newton(compute_residual, solve_correction, x, newton_cfg: NewtonConfig):
+    """Shared Newton skeleton (stepper.py:106-124): convergence is checked after
+    at least one correction."""
+    gstats: list = []
+    history = []
+    it = 0
+    while True:
+        r = compute_residual(x)
+        rn = _inf_norm(r)
+        history.append(rn)
+        if it >= 1 and rn <= newton_cfg.abs_tol_inf:
+            return x, it, gstats, history
+        if it >= newton_cfg.max_iters:
+            raise NewtonError(history)
+        dx, stats = solve_correction(x, -r)
+        gstats.append(stats)
+        x = x + dx
+        it += 1
+
+
+def irk_step_transformed(problem: LinearProblem, tab, u0, t0: float, dt: float,
+                         precond: PrecondSpec | None = None,
+                         newton_cfg: NewtonConfig | None = None,
+                         gmres_cfg: GmresConfig | None = None,
+                         counter: OpCounter | None = None,
+                         cache: StepCache | None = None) -> StepResult:
+    """One transformed fully-implicit step (stepper.py:127-181), on the device."""
+    if dt <= 0:
+        raise ValueError("dt must be positive")
+    tab = builtin_tableau(tab) if isinstance(tab, str) else tab
+    if tab.kind != "irk":
+        raise ValueError(f"{tab.name} is not fully implicit")
+    precond = precond or PrecondSpec()
+    newton_cfg = newton_cfg or NewtonConfig()
+    gmres_cfg = gmres_cfg or GmresConfig()
+    cache = cache or StepCache()
+    der, op, fac, keep = cache.transformed(problem, tab, dt, precond)
+    s, n = tab.s, problem.n
+    t = L.torch()
+    u0 = _dev(u0)
+    ju0 = problem.jac.matvec(u0)            # f(t, u0) = J u0, once per step
+    # residual evaluations are not counted (the reference calls mass.matvec and
+    # problem.rhs without the counter, stepper.py:156-162)
+
+    def compute_residual(w):
+        # (A^-1 (x) M) w - [J (u0 + dt w_k)]_k = B w - 1 (x) J u0
+        r = t.empty(s * n, dtype=t.float64, device="cuda")
+        op.apply_device(w, r)
+        r.view(s, n).sub_(ju0)
+        return r
+
+    def solve_correction(w, rhs):
+        _charge_factor(counter, op, precond.kind, keep, s)
+        pre = None if fac is None else fac.apply
+        x, stats = gmres_device(op.matvec, pre, rhs, gmres_cfg)
+        _charge_gmres(counter, op, fac, stats, gmres_cfg.restart, gmres_cfg.max_iters)
+        return x, stats
+
+    w0 = t.zeros(s * n, dtype=t.float64, device="cuda")
+    w, iters, gstats, _ = _newton(compute_residual, solve_correction, w0, newton_cfg)
+    wb = w.view(s, n)
+    bta = der.bT_a_inv
+    e_last = np.zeros(s)
+    e_last[-1] = 1.0
+    if np.linalg.norm(bta - e_last, np.inf) <= 1e-12:
+        u1 = u0 + dt * wb[-1]
+    else:
+        u1 = u0 + dt * (t.from_numpy(np.ascontiguousarray(bta)).cuda() @ wb)
+    eq = [equivalent_multiplications(st, s, is_irk=True) for st in gstats]
+    return StepResult(u_next=u1, newton_iterations=iters, gmres_stats=gstats,
+                      equivalent_mults_avg=float(np.mean(eq)) if eq else 0.0)
+
+
+def dirk_step(problem: LinearProblem, tab, u0, t0: float, dt: float,
+              newton_cfg: NewtonConfig | None = None,
+              gmres_cfg: GmresConfig | None = None,
+              counter: OpCounter | None = None,
+              partitions: int | None = None,
+              cache: StepCache | None = None) -> StepResult:
+    """Sequential DIRK stage solves (stepper.py:229-287), on the device: stage i
+    solves (M - dt a_ii J) k_i = J base_i by Newton with plain block ILU(0)."""
+    if dt <= 0:
+        raise ValueError("dt must be positive")
+    tab = builtin_tableau(tab) if isinstance(tab, str) else tab
+    if tab.kind != "dirk":
+        raise ValueError(f"{tab.name} is not diagonally implicit")
+    newton_cfg = newton_cfg or NewtonConfig()
+    gmres_cfg = gmres_cfg or GmresConfig()
+    cache = cache or StepCache()
+    t = L.torch()
+    s, n = tab.s, problem.n
+    A = tab.A
+    u0 = _dev(u0)
+    k_stages = t.zeros((s, n), dtype=t.float64, device="cuda")
+    total_newton = 0
+    all_stats: list = []
+    eq_per_stage = []
+    for i in range(s):
+        aii = float(A[i, i])
+        base = u0.clone()
+        for j in range(i):
+            if A[i, j] != 0.0:
+                base.add_(k_stages[j], alpha=dt * float(A[i, j]))
+        if aii == 0.0:
+            raise ValueError("explicit first stages (ESDIRK) need a mass solve; not supported here")
+        mat, fac, keep = cache.dirk_stage(problem, dt * aii, partitions)
+        jb = problem.jac.matvec(base)
+
+        def compute_residual(ki, mat=mat, jb=jb):
+            # M k - J (base + dt a_ii k) = (M - dt a_ii J) k - J base
+            r = t.empty(n, dtype=t.float64, device="cuda")
+            mat.apply_device(ki, r)
+            r.sub_(jb)
+            return r
+
+        def solve_correction(ki, rhs, mat=mat, fac=fac, keep=keep):
+            if counter is not None:
+                counter.block_factorizations += problem.pattern.T
+                counter.block_multiplies += 2 * problem.pattern.upper_count(keep)
+            x, stats = gmres_device(mat.matvec, fac.apply, rhs, gmres_cfg)
+            _charge_gmres(counter, mat, fac, stats, gmres_cfg.restart, gmres_cfg.max_iters)
+            return x, stats
+
+        ki, iters, gstats, _ = _newton(compute_residual, solve_correction,
+                                       t.zeros(n, dtype=t.float64, device="cuda"), newton_cfg)
+        k_stages[i] = ki
+        total_newton += iters
+        all_stats.extend(gstats)
+        eq = [equivalent_multiplications(st, 1, is_irk=False) for st in gstats]
+        eq_per_stage.append(float(np.mean(eq)) if eq else 0.0)
+    u1 = u0 + dt * (t.from_numpy(np.ascontiguousarray(tab.b)).cuda() @ k_stages)
+    return StepResult(u_next=u1, newton_iterations=total_newton, gmres_stats=all_stats,
+                      equivalent_mults_avg=float(sum(eq_per_stage)))
+
+
+def integrate(problem: LinearProblem, scheme, t0: float, t1: float, dt: float,
+              precond: PrecondSpec | None = None, newton_cfg: NewtonConfig | None = None,
+              gmres_cfg: GmresConfig | None = None, keep_trajectory: bool = False,
+              u0=None) -> IntegrateResult:
+    """Fixed-step loop (stepper.py:328-375); DIRK tableaux use dirk_step."""
+    import time
+    tab = builtin_tableau(scheme) if isinstance(scheme, str) else scheme
+    span = t1 - t0
+    if span < 0:
+        raise ValueError("t1 must not precede t0")
+    num_steps = int(round(span / dt)) if span > 0 else 0
+    if span > 0 and abs(num_steps * dt - span) > 1e-9 * max(abs(span), dt):
+        raise ValueError(f"(t1 - t0) = {span} is not an integer multiple of dt = {dt}")
+    counter = OpCounter()
+    cache = StepCache()
+    u = _dev(u0) if u0 is not None else problem.initial_state()
+    traj = [u.clone()] if keep_trajectory else []
+    newton = gm = 0
+    start = time.perf_counter()
+    for k in range(num_steps):
+        tk = t0 + k * dt
+        if tab.kind == "dirk":
+            res = dirk_step(problem, tab, u, tk, dt, newton_cfg, gmres_cfg, counter,
+                            partitions=precond.partitions if precond else None, cache=cache)
+        else:
+            res = irk_step_transformed(problem, tab, u, tk, dt, precond, newton_cfg, gmres_cfg,
+                                       counter, cache=cache)
+        u = res.u_next
+        newton += res.newton_iterations
+        gm += sum(st.iterations for st in res.gmres_stats)
+        if keep_trajectory:
+            traj.append(u.clone())
+    L.torch().cuda.synchronize()
+    return IntegrateResult(u_final=u, trajectory=traj, steps=num_steps, newton_iterations=newton,
+                           gmres_iterations=gm, wall_time=time.perf_counter() - start,
+                           counter=counter)

@@ -244,8 +244,74 @@ def dirk_case():
     print(f"dirk_small: iters={st.iterations}")
 
 
+def stepper_cases():
+    """Newton time steps (stepper.py:127-181, 229-287) on the linear problem
+    M du/dt = J u (BASELINE config 4's "rhs = J.u"), config-1 mesh shape reduced
+    (N=6, nb=8): RADAU23 coupled, RADAU35 shifted uncoupled, DIRK33; two steps each,
+    with the reference's OpCounter."""
+    from irksolve.problems import SemidiscreteProblem
+    from irksolve.stepper import NewtonConfig, PrecondSpec, dirk_step, irk_step_transformed
+
+    out = {}
+    for dtn in (10.0, 100.0):
+        cfg = W.CONFIGS[1].scaled(N=6, nb=8, dt_norm=dtn)
+        wl = W.make_workload(cfg)
+        g = ref_graph(wl.table)
+        Jm = ref_matrix(g, wl.J)
+        mass = ref.BlockDiagonalMatrix(wl.M)
+        u0 = np.random.default_rng(11).standard_normal(Jm.n)
+
+        class LinearJ(SemidiscreteProblem):
+            name = "linear-J"
+
+            def __init__(self):
+                self.graph = g
+                self.m = wl.J.shape[1]
+
+            def mass(self):
+                return mass
+
+            def rhs(self, t, u):
+                return Jm.matvec(u)
+
+            def jacobian(self, t, u):
+                return Jm
+
+        prob = LinearJ()
+        gcfg = ref.GmresConfig(rel_tol=1e-8, restart=40)
+        tag = f"dt{int(dtn)}"
+        out[f"{tag}_dt"] = wl.dt
+        out[f"{tag}_u0"] = u0
+        out[f"{tag}_sha"] = sha(wl.J, wl.M)
+        for name, scheme, kind in (("r23c", "RADAU23", "coupled"), ("r35u", "RADAU35", "uncoupled"),
+                                   ("dirk", "DIRK33", None)):
+            tab = ref.builtin_tableau(scheme)
+            u = u0.copy()
+            ctr = ref.OpCounter()
+            for step in range(2):
+                if kind is None:
+                    res = dirk_step(prob, tab, u, step * wl.dt, wl.dt, NewtonConfig(), gcfg, ctr)
+                else:
+                    res = irk_step_transformed(prob, tab, u, step * wl.dt, wl.dt, PrecondSpec(kind=kind),
+                                               NewtonConfig(), gcfg, ctr)
+                u = res.u_next
+                out[f"{tag}_{name}_u{step + 1}"] = u
+                out[f"{tag}_{name}_newton{step + 1}"] = res.newton_iterations
+                out[f"{tag}_{name}_gmres{step + 1}"] = np.array([st.iterations for st in res.gmres_stats])
+            out[f"{tag}_{name}_counter"] = np.array([ctr.block_multiplies, ctr.block_solves,
+                                                     ctr.block_factorizations, ctr.mass_multiplies,
+                                                     ctr.jacobian_multiplies])
+            print(f"stepper {tag} {name}: newton {out[f'{tag}_{name}_newton1']} "
+                  f"gmres {out[f'{tag}_{name}_gmres1']}")
+    np.savez_compressed(os.path.join(HERE, "stepper_small.npz"), **out)
+
+
 def main():
+    if "--stepper" in sys.argv:
+        stepper_cases()
+        return
     kernel_cases()
+    stepper_cases()
     dirk_case()
     # config 0 exactly (2D tri 16x16, nb=24, RADAU23, coupled GMRES(30))
     workload_case("cfg0", W.CONFIGS[0])

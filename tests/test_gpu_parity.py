@@ -421,3 +421,30 @@ def test_config3_multi_rhs_vs_oracle(nb, ordering):
             assert rel(Z[k], O.bsr_matvec(p.indptr, p.indices, wl.J, Y[k])) < TOL
             x1 = fac.apply(torch.from_numpy(Y[k]).cuda()).cpu().numpy()
             assert rel(X[k], x1) < 1e-14
+
+
+@pytest.mark.parametrize("m", [24, 40, 56, 64])
+@pytest.mark.parametrize("boost", [3.0, 30.0])
+def test_inverse_paths_vs_oracle(be, m, boost):
+    """Pivot-block inverses: strongly diagonal blocks take the tensor-core
+    blocked Gauss-Jordan (no row interchange is ever chosen), weakly diagonal
+    ones need partial pivoting and are handed to the pivoted warp kernels;
+    both must match the reference algorithm (oracle ilu0_factor, LAPACK-style
+    partial pivoting) to 1e-12."""
+    from paper_1701_07181_b200.meshes import line_mesh
+    from tests.helpers import random_blocks
+    g = line_mesh(12, periodic=True)
+    ip, ix, dp = pattern_of(g.adjacency)
+    data = random_blocks(g.adjacency, m, seed=m, diag_boost=boost)
+    keep = np.ones(len(ix), bool)
+    f, d, fail = be.ilu0_factor(ip, ix, dp, data, keep, True)
+    fo, do, failo = O.ilu0_factor(ip, ix, dp, data, keep, True)
+    assert fail == failo
+    if failo == -1:
+        # two correct partial-pivoting inverses differ by ~cond * eps: the 1e-12 bar
+        # applies to well-conditioned pivots (boost 30: cond < 12); the weakly
+        # diagonal fixture reaches cond ~6e6 at m = 64
+        cond = max(np.linalg.cond(fo[q], 1) for q in dp)
+        tol = max(TOL, 4e-16 * cond)
+        assert rel(d, do) < tol
+        assert rel(f, fo) < tol

@@ -190,3 +190,46 @@ def test_workload_case(name):
     if "fdata" in g:
         assert rel(np.stack([f[0] for f in fac.factors]), g["fdata"]) < TOL
         assert rel(np.stack([f[1] for f in fac.factors]), g["dinv"]) < TOL
+
+
+# ---------------------------------------------------------------------------
+# Newton time steps on M du/dt = J u (stepper.py:127-181, 229-287), reference run
+# by tests/golden/make_golden.py::stepper_cases
+# ---------------------------------------------------------------------------
+
+STEP_CASES = [("r23c", "RADAU23", "coupled"), ("r35u", "RADAU35", "uncoupled"),
+              ("dirk", "DIRK33", None)]
+
+
+def stepper_inputs(gs, dtn):
+    cfg = W.CONFIGS[1].scaled(N=6, nb=8, dt_norm=dtn)
+    wl = W.make_workload(cfg)
+    tag = f"dt{int(dtn)}"
+    assert sha(wl.J, wl.M) == str(gs[f"{tag}_sha"])
+    assert wl.dt == float(gs[f"{tag}_dt"])
+    return wl, tag
+
+
+@pytest.fixture(scope="module")
+def gs():
+    return load_golden("stepper_small")
+
+
+@pytest.mark.parametrize("dtn", [10.0, 100.0])
+@pytest.mark.parametrize("name,scheme,kind", STEP_CASES)
+def test_oracle_newton_steps(gs, dtn, name, scheme, kind):
+    wl, tag = stepper_inputs(gs, dtn)
+    p = wl.pattern
+    tab = builtin_tableau(scheme)
+    cfg = O.GmresConfig(rel_tol=1e-8, restart=40)
+    u = gs[f"{tag}_u0"]
+    for step in (1, 2):
+        if kind is None:
+            u, newton, gm = O.dirk_step_linear(p.indptr, p.indices, p.diag_pos, wl.J, wl.M, tab.A,
+                                               tab.b, u, wl.dt, cfg)
+        else:
+            u, newton, gm = O.irk_step_linear(p.indptr, p.indices, p.diag_pos, wl.J, wl.M, tab.A,
+                                              tab.b, u, wl.dt, kind, cfg)
+        assert newton == int(gs[f"{tag}_{name}_newton{step}"])
+        assert gm == list(gs[f"{tag}_{name}_gmres{step}"])
+        assert rel(u, gs[f"{tag}_{name}_u{step}"]) < 1e-10

@@ -21,6 +21,8 @@ def main():
     ci = int(sys.argv[1]) if len(sys.argv) > 1 else 1
     order = sys.argv[2] if len(sys.argv) > 2 else "color"
     cfg = W.CONFIGS[ci].scaled(ordering=order)
+    if len(sys.argv) > 3:
+        cfg = cfg.scaled(N=int(sys.argv[3]))
     wl = W.make_workload(cfg, jnorm=1.0)
     der = derive(builtin_tableau(cfg.scheme))
     dt = cfg.dt_norm / 2.4496432463318416
