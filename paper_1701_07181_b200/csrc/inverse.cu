@@ -1034,19 +1034,22 @@ __device__ __forceinline__ void dmma_f64(double& c0, double& c1, double a, doubl
 
 template <int NT>
 struct InvTcCfg {
-    static constexpr int NBT = 8 * NT, LD = NBT + 4, WARPS = 4, RPL = NBT / 4;   // rows per lane in a panel
+    // ld = 8 (mod 16) doubles: conflict-free panel column loads and C-tile double2 accesses
+    static constexpr int NBT = 8 * NT, LD = NBT + 8, WARPS = 4, RPL = NBT / 4;   // RPL: panel rows per lane
     static constexpr size_t warp_doubles = (size_t)NBT * LD;
     static constexpr size_t smem = WARPS * warp_doubles * sizeof(double);
 };
 
-template <int NT>
+// EXACT: nb == 8 NT (block index math and loops fold to constants)
+template <int NT, bool EXACT>
 __global__ void __launch_bounds__(32 * InvTcCfg<NT>::WARPS) k_inverse_tc(InvArgs A, int* fb_list, int* fb_count) {
     using C = InvTcCfg<NT>;
     constexpr int NBT = C::NBT, LD = C::LD, RPL = C::RPL;
+    constexpr int NPAIR = NBT * NBT / 2;            // double2 per padded block
     extern __shared__ __align__(16) double smtc[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     double* X = smtc + (size_t)warp * C::warp_doubles;
-    const int nb = A.nb;
+    const int nb = EXACT ? NBT : A.nb;
     const int P = (nb + 1) >> 1;
     const int64_t bsz = (int64_t)nb * 2 * P;
     const int pc = lane & 7, pq = lane >> 3;        // panel layout: column, row group
@@ -1056,32 +1059,53 @@ __global__ void __launch_bounds__(32 * InvTcCfg<NT>::WARPS) k_inverse_tc(InvArgs
         const int k_st = (int)(code / A.T);
         const int64_t j = code - (int64_t)k_st * A.T;
         const double2* src = reinterpret_cast<const double2*>(A.D + (j * A.s + k_st) * bsz);
-        // ---- load (identity padding beyond nb)
-        for (int r = lane; r < NBT; r += 32) {
+        // ---- load: device pair p2 of row r is double2 index p2 * nb + r
+        if constexpr (EXACT) {
 #pragma unroll
-            for (int p2 = 0; p2 < NBT / 2; ++p2) {
-                double2 v = make_double2(0.0, 0.0);
-                if (r < nb && p2 < P) v = src[(int64_t)p2 * nb + r];
-                if (2 * p2 + 1 >= nb) v.y = 0.0;
-                if (r >= nb) v = make_double2(2 * p2 == r ? 1.0 : 0.0, 2 * p2 + 1 == r ? 1.0 : 0.0);
+            for (int e = 0; e < (NPAIR + 31) / 32; ++e) {
+                const int idx = lane + 32 * e;
+                if (NPAIR % 32 == 0 || idx < NPAIR) {
+                    const int p2 = idx / NBT, r = idx - p2 * NBT;
+                    *reinterpret_cast<double2*>(X + r * LD + 2 * p2) = src[idx];
+                }
+            }
+        } else {
+            for (int idx = lane; idx < NPAIR; idx += 32) {
+                const int p2 = idx / NBT, r = idx - p2 * NBT;
+                double2 v;
+                if (r < nb && p2 < P) {
+                    v = src[p2 * nb + r];
+                    if (2 * p2 + 1 >= nb) v.y = 0.0;
+                } else {   // identity padding
+                    v = make_double2(2 * p2 == r ? 1.0 : 0.0, 2 * p2 + 1 == r ? 1.0 : 0.0);
+                }
                 *reinterpret_cast<double2*>(X + r * LD + 2 * p2) = v;
             }
         }
         __syncwarp();
-        // |D|_1: max column abs sum (NaN propagating), columns < nb
+        // |.|_1: max column abs sum over the nb x nb part (NaN propagating)
         auto col_norm = [&]() -> double {
             double mx = -1.0;
             int nan = 0;
-            for (int c = lane; c < nb; c += 32) {
-                double s4[4] = {0.0, 0.0, 0.0, 0.0};
-                int r = 0;
-                for (; r + 4 <= nb; r += 4)
 #pragma unroll
-                    for (int h = 0; h < 4; ++h) s4[h] += fabs(X[(r + h) * LD + c]);
-                for (; r < nb; ++r) s4[0] += fabs(X[r * LD + c]);
-                const double sum = (s4[0] + s4[1]) + (s4[2] + s4[3]);
-                if (sum != sum) nan = 1;
-                mx = fmax(mx, sum);
+            for (int h = 0; h < (NBT + 31) / 32; ++h) {
+                const int c = lane + 32 * h;
+                if (c < nb) {
+                    double s4[4] = {0.0, 0.0, 0.0, 0.0};
+                    if constexpr (EXACT) {
+#pragma unroll
+                        for (int r = 0; r < NBT; ++r) s4[r & 3] += fabs(X[r * LD + c]);
+                    } else {
+                        int r = 0;
+                        for (; r + 4 <= nb; r += 4)
+#pragma unroll
+                            for (int q4 = 0; q4 < 4; ++q4) s4[q4] += fabs(X[(r + q4) * LD + c]);
+                        for (; r < nb; ++r) s4[0] += fabs(X[r * LD + c]);
+                    }
+                    const double sum = (s4[0] + s4[1]) + (s4[2] + s4[3]);
+                    if (sum != sum) nan = 1;
+                    mx = fmax(mx, sum);
+                }
             }
 #pragma unroll
             for (int o = 16; o; o >>= 1) {
@@ -1091,7 +1115,10 @@ __global__ void __launch_bounds__(32 * InvTcCfg<NT>::WARPS) k_inverse_tc(InvArgs
             return nan ? __longlong_as_double(0x7ff8000000000000LL) : mx;
         };
         const double n1 = col_norm();
-        double logdet = 0.0;
+        // |pivot_k| kept by lane k mod 32 (log-determinant after the sweep)
+        double apiv[(NBT + 31) / 32];
+#pragma unroll
+        for (int h = 0; h < (NBT + 31) / 32; ++h) apiv[h] = 1.0;
         bool swap = false;
         static_for([&](auto pc_) {
             constexpr int p = decltype(pc_)::value;   // panel index
@@ -1101,36 +1128,35 @@ __global__ void __launch_bounds__(32 * InvTcCfg<NT>::WARPS) k_inverse_tc(InvArgs
             double pv[RPL];
 #pragma unroll
             for (int i = 0; i < RPL; ++i) pv[i] = X[(pq + 4 * i) * LD + k0 + pc];
-            // ---- 8 scalar GJ steps on the panel
+            // ---- 8 scalar GJ steps on the panel columns
             static_for([&](auto kc_) {
                 constexpr int kk = decltype(kc_)::value;
                 constexpr int k = k0 + kk;
-                constexpr int kq = k & 3, ki = k >> 2;      // owner row group / register of row k
-                // pivot check (lanes of column kk): max |a_rk| over rows r > k
-                double mx = 0.0;
-#pragma unroll
-                for (int i = 0; i < RPL; ++i)
-                    if (pq + 4 * i > k) mx = fmax(mx, fabs(pv[i]));
-                mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, 8));
-                mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, 16));
+                constexpr int kq = k & 3, ki = k >> 2;      // row k: group kq, register ki
+                const bool colk = pc == kk;
+                const bool rowk = pq == kq;
                 const double piv = __shfl_sync(0xffffffffu, pv[ki], kk + 8 * kq);
-                const double colmax = __shfl_sync(0xffffffffu, mx, kk);
-                // NaN-safe: the diagonal must be a finite, non-zero maximum
-                const bool ok = (fabs(piv) >= colmax) && piv != 0.0 && isfinite(piv);
+                // partial-pivoting equivalence: no row r > k of column k beats the diagonal
+                // (rows r = pq + 4 i > k: all i > ki, and i == ki for groups pq > kq)
+                const double ap = fabs(piv);
+                bool beat = false;
+#pragma unroll
+                for (int i = ki; i < RPL; ++i)
+                    if (i > ki || pq > kq) beat |= fabs(pv[i]) > ap;
+                const bool ok = !__any_sync(0xffffffffu, colk && beat) && piv != 0.0 && isfinite(piv);
                 if (!ok) swap = true;
                 const double inv = 1.0 / piv;
-                if (k < nb) logdet += log(fabs(piv));
-                // new row k value in my column, and my rows' multipliers a_{r,kk}
+                if (k < nb && lane == (k & 31)) apiv[k >> 5] = ap;
+                // new row k in my column: rk = a_kc / piv; every other row r: a_rc - a_rk rk,
+                // column k itself -a_rk / piv: new = fma(h, f, g * old)
                 const double rk = __shfl_sync(0xffffffffu, pv[ki], pc + 8 * kq) * inv;
+                const double g = colk ? 0.0 : 1.0;
+                const double h = colk ? -inv : -rk;
 #pragma unroll
                 for (int i = 0; i < RPL; ++i) {
                     const double f = __shfl_sync(0xffffffffu, pv[i], kk + 8 * pq);
-                    const bool is_k = (pq + 4 * i == k);
-                    const bool colk = (pc == kk);
-                    double v;
-                    if (is_k) v = colk ? inv : rk;
-                    else v = colk ? -f * inv : fma(-f, rk, pv[i]);
-                    pv[i] = v;
+                    const double nv = fma(h, f, g * pv[i]);
+                    pv[i] = (i == ki && rowk) ? (colk ? inv : rk) : nv;
                 }
             }, std::make_integer_sequence<int, 8>{});
             if (swap) return;
@@ -1166,15 +1192,31 @@ __global__ void __launch_bounds__(32 * InvTcCfg<NT>::WARPS) k_inverse_tc(InvArgs
             __syncwarp();
             continue;
         }
-        // ---- store inv(D) (device layout) and the condition check
+        // ---- store inv(D) in the device layout and the condition check
         double2* dst = reinterpret_cast<double2*>(A.Dinv + (j * A.s + k_st) * bsz);
-        for (int r = lane; r < nb; r += 32)
-            for (int p2 = 0; p2 < P; ++p2) {
+        if constexpr (EXACT) {
+#pragma unroll
+            for (int e = 0; e < (NPAIR + 31) / 32; ++e) {
+                const int idx = lane + 32 * e;
+                if (NPAIR % 32 == 0 || idx < NPAIR) {
+                    const int p2 = idx / NBT, r = idx - p2 * NBT;
+                    dst[idx] = *reinterpret_cast<const double2*>(X + r * LD + 2 * p2);
+                }
+            }
+        } else {
+            for (int idx = lane; idx < P * nb; idx += 32) {
+                const int p2 = idx / nb, r = idx - p2 * nb;
                 double2 v = *reinterpret_cast<const double2*>(X + r * LD + 2 * p2);
                 if (2 * p2 + 1 >= nb) v.y = 0.0;
-                dst[(int64_t)p2 * nb + r] = v;
+                dst[idx] = v;
             }
+        }
         const double n2 = col_norm();
+        double logdet = 0.0;
+#pragma unroll
+        for (int h = 0; h < (NBT + 31) / 32; ++h) logdet += log(apiv[h]);
+#pragma unroll
+        for (int o = 16; o; o >>= 1) logdet += __shfl_xor_sync(0xffffffffu, logdet, o);
         if (lane == 0) {
             const double det = exp(logdet);
             const double cond = n1 * n2;
@@ -1185,23 +1227,29 @@ __global__ void __launch_bounds__(32 * InvTcCfg<NT>::WARPS) k_inverse_tc(InvArgs
     }
 }
 
-template <int NT>
+template <int NT, bool EXACT>
 static int launch_tc_t(const irk_ctx* ctx, const InvArgs& A, int* fb_list, int* fb_count, cudaStream_t st) {
     using C = InvTcCfg<NT>;
     static bool attr = false;
     if (!attr) {
-        IRK_CK(cudaFuncSetAttribute(k_inverse_tc<NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::smem));
-        IRK_CK(cudaFuncSetAttribute(k_inverse_tc<NT>, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+        IRK_CK(cudaFuncSetAttribute(k_inverse_tc<NT, EXACT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::smem));
+        IRK_CK(cudaFuncSetAttribute(k_inverse_tc<NT, EXACT>, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
         attr = true;
     }
     const int threads = 32 * C::WARPS;
     int per_sm = 1;
-    IRK_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_inverse_tc<NT>, threads, C::smem));
+    IRK_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_inverse_tc<NT, EXACT>, threads, C::smem));
     const int64_t need = (A.ntasks + C::WARPS - 1) / C::WARPS;
     const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(need, (int64_t)ctx->num_sms * std::max(per_sm, 1)));
-    k_inverse_tc<NT><<<grid, threads, C::smem, st>>>(A, fb_list, fb_count);
+    k_inverse_tc<NT, EXACT><<<grid, threads, C::smem, st>>>(A, fb_list, fb_count);
     IRK_LAUNCHED();
     return IRK_OK;
+}
+
+template <int NT>
+static int launch_tc_n(const irk_ctx* ctx, const InvArgs& A, int* fb_list, int* fb_count, cudaStream_t st) {
+    return A.nb == 8 * NT ? launch_tc_t<NT, true>(ctx, A, fb_list, fb_count, st)
+                          : launch_tc_t<NT, false>(ctx, A, fb_list, fb_count, st);
 }
 
 static int launch_pivoted(const irk_ctx* ctx, const InvArgs& A, cudaStream_t st);
@@ -1215,12 +1263,12 @@ static int launch_tc(const irk_ctx* ctx, const InvArgs& A, int* fb, cudaStream_t
     const int nt = (A.nb + 7) / 8;
     int rc;
     switch (nt) {
-        case 3: rc = launch_tc_t<3>(ctx, A, fb_list, fb_count, st); break;
-        case 4: rc = launch_tc_t<4>(ctx, A, fb_list, fb_count, st); break;
-        case 5: rc = launch_tc_t<5>(ctx, A, fb_list, fb_count, st); break;
-        case 6: rc = launch_tc_t<6>(ctx, A, fb_list, fb_count, st); break;
-        case 7: rc = launch_tc_t<7>(ctx, A, fb_list, fb_count, st); break;
-        case 8: rc = launch_tc_t<8>(ctx, A, fb_list, fb_count, st); break;
+        case 3: rc = launch_tc_n<3>(ctx, A, fb_list, fb_count, st); break;
+        case 4: rc = launch_tc_n<4>(ctx, A, fb_list, fb_count, st); break;
+        case 5: rc = launch_tc_n<5>(ctx, A, fb_list, fb_count, st); break;
+        case 6: rc = launch_tc_n<6>(ctx, A, fb_list, fb_count, st); break;
+        case 7: rc = launch_tc_n<7>(ctx, A, fb_list, fb_count, st); break;
+        case 8: rc = launch_tc_n<8>(ctx, A, fb_list, fb_count, st); break;
         default: return IRK_EINVAL;
     }
     if (rc) return rc;
