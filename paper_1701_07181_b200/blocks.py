@@ -345,3 +345,62 @@ class BlockDiagonalMatrix:
     @property
     def n(self) -> int:
         return self.T_elems * self.m
+
+
+# ---------------------------------------------------------------------------
+# Line-oriented text exchange format (reference blocks.py:193-216)
+# ---------------------------------------------------------------------------
+
+def dump_matrix(mat, path: str) -> None:
+    """Reference ``dump_matrix`` (blocks.py:193-201), byte-identical output:
+    header ``T m nnz_blocks``, then per stored block (row-major pattern order) a
+    line ``i j`` and a line of the m*m row-major values as ``repr(float)``.
+    ``mat`` is a device ``BlockSparseMatrix`` (downloaded once) or any object
+    with ``indptr / indices / data``."""
+    indptr = np.asarray(mat.indptr)
+    indices = np.asarray(mat.indices)
+    data = np.asarray(mat.data)
+    T = len(indptr) - 1
+    m = data.shape[1]
+    rows = np.repeat(np.arange(T), np.diff(indptr))
+    with open(path, "w") as fh:
+        fh.write(f"{T} {m} {len(indices)}\n")
+        flat = data.reshape(len(indices), m * m).tolist()   # Python floats: repr is the shortest round trip
+        for k in range(len(indices)):
+            fh.write(f"{rows[k]} {indices[k]}\n")
+            fh.write(" ".join(map(repr, flat[k])) + "\n")
+
+
+def read_matrix_blocks(path: str, indptr, indices) -> np.ndarray:
+    """Parse a ``dump_matrix`` file onto a pattern (host): the checks and the
+    ``set_block`` placement of reference ``load_matrix`` (blocks.py:204-216)."""
+    indptr, indices = np.asarray(indptr), np.asarray(indices)
+    T_pat, nnzb = len(indptr) - 1, len(indices)
+    with open(path) as fh:
+        T, m, nnz = (int(tok) for tok in fh.readline().split())
+        if T != T_pat:
+            raise ValueError(f"file has T={T}, graph has {T_pat}")
+        if nnz != nnzb:
+            raise ValueError(f"file has {nnz} blocks, pattern expects {nnzb}")
+        lines = fh.read().split("\n")
+    ij = np.array([ln.split() for ln in lines[0:2 * nnz:2]], dtype=np.int64).reshape(nnz, 2)
+    vals = np.array(" ".join(lines[1:2 * nnz:2]).split(), dtype=np.float64)
+    if vals.size != nnz * m * m:
+        raise ValueError("truncated block data")
+    vals = vals.reshape(nnz, m, m)
+    data = np.zeros((nnzb, m, m))
+    for k in range(nnz):
+        i, j = int(ij[k, 0]), int(ij[k, 1])
+        lo, hi = indptr[i], indptr[i + 1]
+        pos = int(np.searchsorted(indices[lo:hi], j)) + lo
+        if pos >= hi or indices[pos] != j:
+            raise KeyError(f"block ({i}, {j}) not in pattern")
+        data[pos] = vals[k]   # later duplicates overwrite, as set_block does
+    return data
+
+
+def load_matrix(path: str, graph_or_pattern) -> "BlockSparseMatrix":
+    """Reference ``load_matrix`` (blocks.py:204-216) into a device matrix."""
+    pat = graph_or_pattern if isinstance(graph_or_pattern, DevicePattern) else pattern_for(graph_or_pattern)
+    data = read_matrix_blocks(path, pat.indptr, pat.indices)
+    return BlockSparseMatrix(pat, DeviceBlocks.from_host(data), host=data)

@@ -850,6 +850,389 @@ __global__ void __launch_bounds__(288) k_unc_bwd_pipe(ApplyArgs A, PipeCfg PC) {
     }
 }
 
+// ---------------------------------------------------------------------------
+// Stage-coupled sweeps on the bulk-copy pipeline (coupled_solve,
+// numba_backend.py:128-151).  One task = one element i with ALL s stages: the
+// element DAG is the uncoupled one (2 levels on the colour-ordered meshes instead
+// of the s + 1 stage-skewed levels of (stage, element) tasks), a stage-shared
+// upper block -dt J_ij is read once for s vectors, and the stage coupling of
+// the element is solved inside the task:
+//   forward  (k ascending):  z_k = (y_k - sum_j L_kij z_kj) - sum_{l<k} G_kl,i z_l
+//   backward (k descending): x_k = Dinv_k ((z_k - sum_j U_ij x_kj) - sum_{l>k} C_kl,i x_l)
+// with C_kl,i = A^-1_kl M_i (implicit: one M_i gemv per stage on sum_l a_kl x_l)
+// or stored couplings.  Within-task stage dependencies go through shared
+// memory (tv: z or t, xv: finished x_l, cv: the combined coupling vector).
+// ---------------------------------------------------------------------------
+enum { PD_G = 256, PD_C = 512 };
+
+// reduce one value per (group, row) over the G groups into dst[a] (op: dst = base - sum)
+__device__ __forceinline__ void group_sum_into(double* red, double v, const Geo& q, int ncons, const double* base,
+                                               double* dst) {
+    if (q.active) red[q.g * q.nb + q.a] = v;
+    consumer_sync(1, ncons);
+    if (q.active && q.g == 0) {
+        double sum = 0.0;
+        for (int gg = 0; gg < q.G; ++gg) sum += red[gg * q.nb + q.a];
+        dst[q.a] = base[q.a] - sum;
+    }
+    consumer_sync(1, ncons);
+}
+
+template <int S, bool DEPS>
+__global__ void __launch_bounds__(288) k_cpl_fwd_pipe(ApplyArgs A, PipeCfg PC) {
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    const int nb = A.nb;
+    PipeSmem P = pipe_carve<S>(smem_raw, PC, A.G_, nb);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int ncons_warps = (blockDim.x >> 5) - 1, ncons = ncons_warps * 32;
+    pipe_init(P, PC.nst, ncons_warps);
+    const int64_t bsz = (int64_t)PC.block_bytes / 8;
+    const uint32_t seg = (uint32_t)nb * 8;
+    constexpr int NPAIRS = S * (S - 1) / 2;
+    if (warp == 0) {
+        Producer pr{&P, &PC};
+        int cur = (int)(A.ntasks * blockIdx.x / gridDim.x);
+        const int hi = (int)(A.ntasks * (blockIdx.x + 1) / gridDim.x);
+        int tb, tend;
+        while (next_batch<DEPS>(A, tb, tend, cur, hi)) {
+            const int tl = tb + lane;
+            const bool valid = tl < tend;
+            const int64_t il = valid ? A.order[tl] : 0;
+            const int q0l = valid ? A.indptr[il] : 0, dl = valid ? A.diag[il] : 0, l0l = valid ? A.lptr[il] : 0;
+            const int nnl = dl - q0l;
+            for (int bt = 0; bt < 32 && tb + bt < tend; ++bt) {
+                const int64_t i = __shfl_sync(0xffffffffu, il, bt);
+                const int q0 = __shfl_sync(0xffffffffu, q0l, bt), nn = __shfl_sync(0xffffffffu, nnl, bt);
+                const int l0 = __shfl_sync(0xffffffffu, l0l, bt);
+                int nitems = NPAIRS;
+                for (int m = 0; m < nn; ++m) nitems += A.keep[q0 + m] ? S : 0;
+                const int ntot = nitems > 0 ? nitems : 1;
+                auto push_items = [&](int from, int to) {
+                    if (nitems == 0) {
+                        if (from == 0 && to > 0) pr.push(make_int4((int)i, -1, PD_FIRST | PD_LAST, nn), nullptr);
+                        return;
+                    }
+                    int n = 0;
+                    for (int m = 0; m < nn; ++m) {
+                        if (!A.keep[q0 + m]) continue;
+                        for (int k = 0; k < S; ++k, ++n) {
+                            if (n < from || n >= to) continue;
+                            const int fl = PD_L | (n == 0 ? PD_FIRST : 0) | (n == nitems - 1 ? PD_LAST : 0);
+                            pr.push(make_int4((int)i, m * S + k, fl, nn), A.L + ((int64_t)(l0 + m) * S + k) * bsz);
+                        }
+                    }
+                    for (int k = 1; k < S; ++k)
+                        for (int l = 0; l < k; ++l, ++n) {
+                            if (n < from || n >= to) continue;
+                            const int fl = PD_G | (n == 0 ? PD_FIRST : 0) | (n == nitems - 1 ? PD_LAST : 0);
+                            pr.push(make_int4((int)i, k * S + l, fl, nn), A.G + (i * NPAIRS + pidx(k, l)) * bsz);
+                        }
+                };
+                const int npre = DEPS ? min(ntot, PC.nst - 1) : 0;
+                double* xs = nullptr;
+                int xb = 0;
+                if (lane == 0) {
+                    xs = pr.x_acquire();
+                    xb = pr.xb;
+                    push_items(0, npre);
+                }
+                if (DEPS)
+                    for (int m = lane; m < nn; m += 32)
+                        if (A.keep[q0 + m]) wait_flag(A.flags + A.indices[q0 + m], A.epoch);
+                __syncwarp();
+                uint32_t bytes = S * seg;
+                for (int m = 0; m < nn; ++m) bytes += A.keep[q0 + m] ? S * seg : 0;
+                if (lane == 0) {
+                    if (DEPS) fence_proxy_async_global();
+                    pr.x_commit(bytes);
+                }
+                xs = reinterpret_cast<double*>(__shfl_sync(0xffffffffu, reinterpret_cast<uintptr_t>(xs), 0));
+                xb = __shfl_sync(0xffffffffu, xb, 0);
+                __syncwarp();
+                for (int e = lane; e < (nn + 1) * S; e += 32) {
+                    const int m = e / S, k = e - m * S;
+                    if (m == nn) bulk_g2s(xs + e * nb, A.y + k * A.n + i * nb, seg, P.xfull + xb);
+                    else if (A.keep[q0 + m]) bulk_g2s(xs + e * nb, A.x + k * A.n + (int64_t)A.indices[q0 + m] * nb, seg, P.xfull + xb);
+                }
+                if (lane == 0) push_items(npre, ntot);
+                if (lane == 0) pr.x_next();
+            }
+        }
+        if (lane == 0) pr.push(make_int4(-1, 0, PD_END, 0), nullptr);
+        return;
+    }
+    const int c = threadIdx.x - 32;
+    Geo q;
+    q.nb = nb; q.P = (nb + 1) >> 1; q.G = A.G_; q.g = c / nb; q.a = c - q.g * nb; q.active = q.g < q.G;
+    Consumer cs{&P, &PC};
+    double part[S];
+    double gacc = 0.0;
+    const double* xs = nullptr;
+    bool t_done = false;
+    double* tv = P.tv;   // [S][nb]: t_k, then z_k
+    auto finalize_t = [&](int nn) {
+        // t_k = y_k - sum_groups part_k for all stages
+        if (q.active)
+#pragma unroll
+            for (int k = 0; k < S; ++k) P.red[(q.g * S + k) * nb + q.a] = part[k];
+        consumer_sync(1, ncons);
+        if (q.active && q.g == 0)
+#pragma unroll
+            for (int k = 0; k < S; ++k) {
+                double sum = 0.0;
+                for (int gg = 0; gg < q.G; ++gg) sum += P.red[(gg * S + k) * nb + q.a];
+                tv[k * nb + q.a] = xs[(nn * S + k) * nb + q.a] - sum;
+            }
+        consumer_sync(1, ncons);
+        t_done = true;
+    };
+    for (;;) {
+        const int4 dsc = cs.take();
+        if (dsc.z & PD_END) break;
+        const int64_t i = dsc.x;
+        const int nn = dsc.w;
+        if (dsc.z & PD_FIRST) {
+#pragma unroll
+            for (int k = 0; k < S; ++k) part[k] = 0.0;
+            gacc = 0.0;
+            t_done = false;
+            xs = cs.x_wait();
+        }
+        if (dsc.z & PD_L) {
+            if (q.active) {
+                const int m = dsc.y / S, kk = dsc.y - m * S;
+                const double2* B = cs.block();
+#pragma unroll
+                for (int k = 0; k < S; ++k)
+                    if (k == kk) part[k] = smem_gemv(B, xs + (m * S + k) * nb, q, part[k]);
+            }
+            cs.release();
+        } else if (dsc.z & PD_G) {
+            const int k = dsc.y / S, l = dsc.y - k * S;
+            if (!t_done) finalize_t(nn);
+            if (q.active) gacc = smem_gemv(cs.block(), tv + l * nb, q, gacc);
+            cs.release();
+            if (l == k - 1) {   // last coupling of stage k: z_k = t_k - sum_l G_kl z_l
+                group_sum_into(P.red, gacc, q, ncons, tv + k * nb, tv + k * nb);
+                gacc = 0.0;
+            }
+        } else {
+            cs.release();
+        }
+        if (dsc.z & PD_LAST) {
+            if (!t_done) finalize_t(nn);
+            if (q.active && q.g == 0)
+#pragma unroll
+                for (int k = 0; k < S; ++k) A.x[k * A.n + i * nb + q.a] = tv[k * nb + q.a];
+            cs.x_release();
+            consumer_sync(1, ncons);   // tv / red reuse by the next task
+            if (DEPS && c == 0) { __threadfence(); st_release(A.flags + i, A.epoch); }
+        }
+    }
+}
+
+template <int S, bool DEPS>
+__global__ void __launch_bounds__(288) k_cpl_bwd_pipe(ApplyArgs A, PipeCfg PC) {
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    const int nb = A.nb;
+    PipeSmem P = pipe_carve<S>(smem_raw, PC, A.G_, nb);
+    double* xv = P.tv + S * nb;   // [S][nb] finished x_l of the task
+    double* cv = xv + S * nb;     // [nb] combined coupling vector
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int ncons_warps = (blockDim.x >> 5) - 1, ncons = ncons_warps * 32;
+    pipe_init(P, PC.nst, ncons_warps);
+    const int64_t bsz = (int64_t)PC.block_bytes / 8;
+    const uint32_t seg = (uint32_t)nb * 8;
+    constexpr int NPAIRS = S * (S - 1) / 2;
+    const bool explicit_c = A.Cup != nullptr;
+    if (warp == 0) {
+        Producer pr{&P, &PC};
+        int cur = (int)(A.ntasks * blockIdx.x / gridDim.x);
+        const int hi = (int)(A.ntasks * (blockIdx.x + 1) / gridDim.x);
+        int tb, tend;
+        while (next_batch<DEPS>(A, tb, tend, cur, hi)) {
+            const int tl = tb + lane;
+            const bool valid = tl < tend;
+            const int64_t il = valid ? A.order[tl] : 0;
+            const int dl = valid ? A.diag[il] : 0, u0l = valid ? A.uptr[il] : 0;
+            const int nnl = valid ? A.indptr[il + 1] - dl - 1 : 0;
+            for (int bt = 0; bt < 32 && tb + bt < tend; ++bt) {
+                const int64_t i = __shfl_sync(0xffffffffu, il, bt);
+                const int nn = __shfl_sync(0xffffffffu, nnl, bt);
+                const int b0 = __shfl_sync(0xffffffffu, dl, bt) + 1;
+                const int u0 = __shfl_sync(0xffffffffu, u0l, bt);
+                const bool ush = A.u_shared != 0;
+                int nu = 0;
+                for (int m = 0; m < nn; ++m) nu += A.keep[b0 + m] ? (ush ? 1 : S) : 0;
+                // stage chain: (couplings, Dinv) for k = S-1 .. 0
+                const int nchain = S + (explicit_c ? NPAIRS : S - 1);
+                const int ntot = nu + nchain;
+                auto push_items = [&](int from, int to) {
+                    int n = 0;
+                    for (int m = 0; m < nn; ++m) {
+                        if (!A.keep[b0 + m]) continue;
+                        const int qq = b0 + m;
+                        if (ush) {
+                            if (n >= from && n < to)
+                                pr.push(make_int4((int)i, m * S, PD_USH | (n == 0 ? PD_FIRST : 0), nn), A.ubase[0] + qq * bsz);
+                            ++n;
+                        } else {
+                            for (int k = 0; k < S; ++k, ++n) {
+                                if (n < from || n >= to) continue;
+                                const double* ub = A.U ? A.U + ((int64_t)(u0 + m) * S + k) * bsz : A.ubase[k] + qq * bsz;
+                                pr.push(make_int4((int)i, m * S + k, PD_U | (n == 0 ? PD_FIRST : 0), nn), ub);
+                            }
+                        }
+                    }
+                    for (int k = S - 1; k >= 0; --k) {
+                        if (k < S - 1) {
+                            if (explicit_c) {
+                                for (int l = k + 1; l < S; ++l, ++n)
+                                    if (n >= from && n < to)
+                                        pr.push(make_int4((int)i, k * S + l, PD_C | (n == 0 ? PD_FIRST : 0), nn),
+                                                A.Cup + (i * NPAIRS + pidx(l, k)) * bsz);
+                            } else {
+                                if (n >= from && n < to)
+                                    pr.push(make_int4((int)i, k * S + S - 1, PD_C | (n == 0 ? PD_FIRST : 0), nn),
+                                            A.mass + i * bsz);
+                                ++n;
+                            }
+                        }
+                        if (n >= from && n < to)
+                            pr.push(make_int4((int)i, k, PD_DINV | (n == 0 ? PD_FIRST : 0) | (k == 0 ? PD_LAST : 0), nn),
+                                    A.Dinv + (i * S + k) * bsz);
+                        ++n;
+                    }
+                };
+                const int npre = DEPS ? min(ntot, PC.nst - 1) : 0;
+                double* xs = nullptr;
+                int xb = 0;
+                if (lane == 0) {
+                    xs = pr.x_acquire();
+                    xb = pr.xb;
+                    push_items(0, npre);
+                }
+                if (DEPS)
+                    for (int m = lane; m < nn; m += 32)
+                        if (A.keep[b0 + m]) wait_flag(A.flags + A.indices[b0 + m], A.epoch);
+                __syncwarp();
+                uint32_t bytes = S * seg;
+                for (int m = 0; m < nn; ++m) bytes += A.keep[b0 + m] ? S * seg : 0;
+                if (lane == 0) {
+                    if (DEPS) fence_proxy_async_global();
+                    pr.x_commit(bytes);
+                }
+                xs = reinterpret_cast<double*>(__shfl_sync(0xffffffffu, reinterpret_cast<uintptr_t>(xs), 0));
+                xb = __shfl_sync(0xffffffffu, xb, 0);
+                __syncwarp();
+                for (int e = lane; e < (nn + 1) * S; e += 32) {
+                    const int m = e / S, k = e - m * S;
+                    if (m == nn) bulk_g2s(xs + e * nb, A.x + k * A.n + i * nb, seg, P.xfull + xb);   // z_i
+                    else if (A.keep[b0 + m]) bulk_g2s(xs + e * nb, A.x + k * A.n + (int64_t)A.indices[b0 + m] * nb, seg, P.xfull + xb);
+                }
+                if (lane == 0) push_items(npre, ntot);
+                if (lane == 0) pr.x_next();
+            }
+        }
+        if (lane == 0) pr.push(make_int4(-1, 0, PD_END, 0), nullptr);
+        return;
+    }
+    const int c = threadIdx.x - 32;
+    Geo q;
+    q.nb = nb; q.P = (nb + 1) >> 1; q.G = A.G_; q.g = c / nb; q.a = c - q.g * nb; q.active = q.g < q.G;
+    Consumer cs{&P, &PC};
+    double part[S];
+    double acc = 0.0;
+    const double* xs = nullptr;
+    bool t_done = false;
+    double* tv = P.tv;
+    for (;;) {
+        const int4 dsc = cs.take();
+        if (dsc.z & PD_END) break;
+        const int64_t i = dsc.x;
+        const int nn = dsc.w;
+        if (dsc.z & PD_FIRST) {
+#pragma unroll
+            for (int k = 0; k < S; ++k) part[k] = 0.0;
+            acc = 0.0;
+            t_done = false;
+            xs = cs.x_wait();
+        }
+        const double2* B = cs.block();
+        if (dsc.z & (PD_USH | PD_U)) {
+            if (q.active) {
+                const int m = dsc.y / S, kk = dsc.y - m * S;
+                const bool sh = (dsc.z & PD_USH) != 0;
+#pragma unroll
+                for (int k = 0; k < S; ++k)
+                    if (sh || k == kk) part[k] = smem_gemv(B, xs + (m * S + k) * nb, q, part[k]);
+            }
+            cs.release();
+            continue;
+        }
+        if (!t_done) {
+            // t_k = z_k - uscale * sum_j U_ij x_kj, all stages
+            if (q.active)
+#pragma unroll
+                for (int k = 0; k < S; ++k) P.red[(q.g * S + k) * nb + q.a] = part[k];
+            consumer_sync(1, ncons);
+            if (q.active && q.g == 0)
+#pragma unroll
+                for (int k = 0; k < S; ++k) {
+                    double sum = 0.0;
+                    for (int gg = 0; gg < q.G; ++gg) sum += P.red[(gg * S + k) * nb + q.a];
+                    tv[k * nb + q.a] = xs[(nn * S + k) * nb + q.a] - A.uscale * sum;
+                }
+            consumer_sync(1, ncons);
+            t_done = true;
+        }
+        if (dsc.z & PD_C) {
+            const int k = dsc.y / S, l = dsc.y - k * S;
+            if (explicit_c) {
+                if (q.active) acc = smem_gemv(B, xv + l * nb, q, acc);
+                cs.release();
+                if (l == S - 1) {   // all l > k done: t_k -= sum_l C_kl x_l
+                    group_sum_into(P.red, acc, q, ncons, tv + k * nb, tv + k * nb);
+                    acc = 0.0;
+                }
+            } else {
+                // implicit C_kl = a_kl M_i: cv = sum_{l>k} a_kl x_l, then t_k -= M_i cv
+                for (int e = c; e < nb; e += ncons) {
+                    double v = 0.0;
+                    for (int ll = k + 1; ll < S; ++ll) v = fma(A.cup_scale[k * A.s + ll], xv[ll * nb + e], v);
+                    cv[e] = v;
+                }
+                consumer_sync(1, ncons);
+                double pm = 0.0;
+                if (q.active) pm = smem_gemv(B, cv, q, 0.0);
+                cs.release();
+                group_sum_into(P.red, pm, q, ncons, tv + k * nb, tv + k * nb);
+            }
+            continue;
+        }
+        // Dinv item k: x_k = Dinv_k t_k
+        {
+            const int k = dsc.y;
+            double pd = 0.0;
+            if (q.active) pd = smem_gemv(B, tv + k * nb, q, 0.0);
+            cs.release();
+            if (q.active) P.red[q.g * nb + q.a] = pd;
+            consumer_sync(1, ncons);
+            if (q.active && q.g == 0) {
+                double sum = 0.0;
+                for (int gg = 0; gg < q.G; ++gg) sum += P.red[gg * nb + q.a];
+                xv[k * nb + q.a] = sum;
+                A.x[k * A.n + i * nb + q.a] = sum;
+            }
+            consumer_sync(1, ncons);
+        }
+        if (dsc.z & PD_LAST) {
+            cs.x_release();
+            if (DEPS && c == 0) { __threadfence(); st_release(A.flags + i, A.epoch); }
+        }
+    }
+}
+
 // x[k][i] = y[k][i] for the elements of a level with no kept lower neighbour
 // (forward sweep: z_i = y_i) -- a plain vectorised row copy.
 __global__ void k_copy_rows(const int32_t* __restrict__ rows, int64_t nrows, const double* __restrict__ y,
@@ -872,7 +1255,7 @@ constexpr int64_t LEVEL_LAUNCH_MAX = 16;
 
 template <typename K1, typename K2>
 static int run_pipe(const irk_factor* f, K1 kernel_deps, K2 kernel_level, ApplyArgs& A, const irk_sched& S,
-                    unsigned* flags, int* ticket, int s, cudaStream_t st) {
+                    unsigned* flags, int* ticket, int s, cudaStream_t st, int extra_doubles = 0) {
     A.flags = flags;
     A.ticket = ticket;
     const int nb = A.nb;
@@ -882,8 +1265,8 @@ static int run_pipe(const irk_factor* f, K1 kernel_deps, K2 kernel_level, ApplyA
     PC.maxdeg = f->maxdeg;
     PC.xslot_doubles = (((PC.maxdeg + 1) * s * nb) + 15) & ~15;
     const int threads = 32 + ((A.G_ * nb + 31) / 32) * 32;
-    const size_t fixed = sizeof(double) * (2 * (size_t)PC.xslot_doubles + 2 * (size_t)A.G_ * s * nb + (size_t)s * nb) +
-                         4 * sizeof(uint64_t);
+    const size_t fixed = sizeof(double) * (2 * (size_t)PC.xslot_doubles + 2 * (size_t)A.G_ * s * nb + (size_t)s * nb +
+                                           (size_t)extra_doubles) + 4 * sizeof(uint64_t);
     // Each task is a short serial chain (x gather -> 3..12 blocks -> reduction),
     // so throughput comes from tasks in flight per SM, not ring depth: size the
     // ring so that >= 4 CTAs fit on an SM (tools/tune_apply.py: 2-3 stages of a
@@ -974,8 +1357,25 @@ static int unc_apply(const irk_factor* f, ApplyArgs& A, cudaStream_t st) {
     return IRK_OK;
 }
 
+template <int S>
+static int cpl_apply_pipe(const irk_factor* f, ApplyArgs& A, cudaStream_t st) {
+    const int64_t nf = (int64_t)f->pat->T;
+    IRK_TRY(run_pipe(f, k_cpl_fwd_pipe<S, true>, k_cpl_fwd_pipe<S, false>, A, f->fwd, f->d_flags, f->d_ticket, S, st));
+    IRK_TRY(run_pipe(f, k_cpl_bwd_pipe<S, true>, k_cpl_bwd_pipe<S, false>, A, f->bwd, f->d_flags + nf, f->d_ticket + 1,
+                     S, st, (S + 1) * A.nb));
+    return IRK_OK;
+}
+
 template <bool EVEN>
 static int cpl_apply(const irk_factor* f, ApplyArgs& A, cudaStream_t st) {
+    if (f->cpl_pipe) {
+        switch (f->s) {
+            case 2: return cpl_apply_pipe<2>(f, A, st);
+            case 3: return cpl_apply_pipe<3>(f, A, st);
+            case 4: return cpl_apply_pipe<4>(f, A, st);
+            default: break;
+        }
+    }
     const int threads = ((A.G_ * A.nb + 31) / 32) * 32;
     const size_t smem_f = sizeof(double) * A.G_ * A.nb;
     const size_t smem_b = sizeof(double) * (A.G_ * 2 * A.nb + A.nb);

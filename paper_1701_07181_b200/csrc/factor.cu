@@ -560,6 +560,8 @@ static int build_sched(irk_sched& S, const std::vector<int64_t>& lev, int64_t T,
 
 // apply schedules: uncoupled -> element tasks; coupled -> (stage, element)
 // tasks on stage-skewed levels
+int choose_groups(int nb, int max_threads);   // matvec.cu
+
 int build_apply_schedules(irk_factor* f, const std::vector<uint8_t>& keep) {
     std::vector<int64_t> levf, levb;
     {
@@ -573,7 +575,15 @@ int build_apply_schedules(irk_factor* f, const std::vector<uint8_t>& keep) {
     }
     levels_forward(f->pat, keep, levf);
     levels_backward(f->pat, keep, levb);
-    const bool cpl = f->kind == IRK_FACTOR_COUPLED;
+    // coupled: (stage, element) tasks on stage-skewed levels for the generic kernels, or
+    // element tasks (all stages, coupling solved in the task) for the pipelined sweeps
+    // (a deep element DAG -- natural numbering -- keeps the stage-skewed tasks: s times more
+    // tasks per level and a shorter critical path than element tasks with in-task coupling)
+    const int64_t depth = std::max(levf.empty() ? 0 : *std::max_element(levf.begin(), levf.end()),
+                                   levb.empty() ? 0 : *std::max_element(levb.begin(), levb.end())) + 1;
+    f->cpl_pipe = f->kind == IRK_FACTOR_COUPLED && f->nb % 2 == 0 && f->s >= 2 && f->s <= 4 &&
+                  choose_groups(f->nb, 256) * f->nb <= 256 && depth <= 16 && !getenv("IRK_CPL_GENERIC");
+    const bool cpl = f->kind == IRK_FACTOR_COUPLED && !f->cpl_pipe;
     IRK_TRY(build_sched(f->fwd, levf, f->pat->T, f->s, cpl, +1));
     if (f->l_implicit) {
         // rows without a kept upper block are finished by the forward sweep
@@ -588,8 +598,9 @@ int build_apply_schedules(irk_factor* f, const std::vector<uint8_t>& keep) {
     } else {
         IRK_TRY(build_sched(f->bwd, levb, f->pat->T, f->s, cpl, -1));
     }
-    if (!cpl && !f->l_implicit) {
-        // forward levels whose elements have no kept lower block: z_i = y_i
+    if (f->kind != IRK_FACTOR_COUPLED && !f->l_implicit) {
+        // forward levels whose elements have no kept lower block: z_i = y_i (uncoupled only:
+        // a coupled element still needs its stage coupling)
         const irk_pattern* p = f->pat;
         std::vector<char> has(f->fwd.nlevels, 0);
         for (int64_t i = 0; i < p->T; ++i)
@@ -1015,7 +1026,6 @@ static int factor_numeric(irk_factor* f, int64_t* fail_stage, int64_t* fail_elem
     return IRK_OK;
 }
 
-int choose_groups(int nb, int max_threads);   // matvec.cu
 
 // Implicit L (never store L_ij = alpha J_ij Dinv_j) needs: stage-uncoupled
 // simplified ILU, one J shared by all stages, a symmetric keep mask (so every

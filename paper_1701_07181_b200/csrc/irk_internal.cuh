@@ -124,6 +124,7 @@ struct irk_factor {
     // implicit L (uncoupled, stage-shared J, symmetric keep): L_ij = alpha J_ij Dinv_j is
     // never stored; the forward sweep uses w_j = Dinv_j z_j (d_W, s x T x nb) instead
     bool l_implicit = false;
+    bool cpl_pipe = false;            // coupled: element-task pipelined sweeps (element schedules)
     double* d_W = nullptr;
     mutable double* d_Wrhs = nullptr; // multi-RHS apply of a single factor: nrhs x T x nb
     mutable int wrhs = 0;

@@ -306,12 +306,28 @@ def stepper_cases():
     np.savez_compressed(os.path.join(HERE, "stepper_small.npz"), **out)
 
 
+def text_format_case():
+    """Reference dump_matrix (blocks.py:193-201) on a small matrix: the exact text."""
+    from irksolve.blocks import dump_matrix
+    g = ref.build_line_mesh(6, periodic=True)
+    mat = ref_matrix(g, random_blocks(g.adjacency, 3, seed=21))
+    mat.data[0, 0, 0] = 1e-300
+    mat.data[1, 1, 1] = -0.1
+    mat.data[2, 2, 2] = 12345678901234.5
+    dump_matrix(mat, os.path.join(HERE, "matrix_line6.txt"))
+    print("matrix_line6.txt written")
+
+
 def main():
+    if "--text" in sys.argv:
+        text_format_case()
+        return
     if "--stepper" in sys.argv:
         stepper_cases()
         return
     kernel_cases()
     stepper_cases()
+    text_format_case()
     dirk_case()
     # config 0 exactly (2D tri 16x16, nb=24, RADAU23, coupled GMRES(30))
     workload_case("cfg0", W.CONFIGS[0])

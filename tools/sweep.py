@@ -225,9 +225,48 @@ def config2kernels(args):
           "device_mem_used_GB": (lambda f: (f[1] - f[0]) / 1e9)(torch.cuda.mem_get_info()), "gen_s": gen})
 
 
+def config0(args):
+    """BASELINE config 0 (16x16 quads -> 512 triangles, nb=24, RADAU23, coupled block
+    ILU(0), GMRES(30), dt*||J||=20): stage-solves/s (L2-resident plumbing case)."""
+    import torch
+    from paper_1701_07181_b200 import workloads as W
+    from paper_1701_07181_b200.blocks import DevicePattern
+    from paper_1701_07181_b200.krylov import GmresConfig
+    from paper_1701_07181_b200.solver import StageSolver
+    cfg = W.CONFIGS[0]
+    wl = W.make_workload(cfg)
+    p = wl.pattern
+    solver = StageSolver(DevicePattern(p.indptr, p.indices, p.diag_pos), wl.J, wl.M, wl.a_inv, wl.dt,
+                         kind="coupled", gmres_cfg=GmresConfig(rel_tol=cfg.rtol, restart=cfg.restart))
+    rhs = torch.from_numpy(wl.rhs).cuda()
+    x = torch.empty_like(rhs)
+
+    def step():
+        solver.factorize()
+        return solver.solve(rhs, x=x)[1]
+
+    for _ in range(3):
+        st = step()
+    torch.cuda.synchronize()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    reps = 20
+    a.record()
+    for _ in range(reps):
+        st = step()
+    b.record()
+    torch.cuda.synchronize()
+    ms = a.elapsed_time(b) / reps
+    t_ap = timed(lambda: solver.fac.apply_device(rhs, x), 50)
+    t_mv = timed(lambda: solver.op.apply_device(rhs, x), 50)
+    t_fac = timed(lambda: solver.factorize(), 10)
+    emit({"config": 0, "T": p.T, "nb": cfg.nb, "s": cfg.s, "precond": "coupled", "ms_per_stage_solve": ms,
+          "stage_solves_per_s": 1e3 / ms, "gmres_iterations": st.iterations, "apply_us": 1e6 * t_ap,
+          "matvec_us": 1e6 * t_mv, "factor_us": 1e6 * t_fac})
+
+
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("what", choices=["config3", "config4", "config2kernels"])
+    ap.add_argument("what", choices=["config0", "config3", "config4", "config2kernels"])
     ap.add_argument("--nb", type=int, nargs="+", default=[24, 40, 50, 100])
     ap.add_argument("--s", type=int, nargs="+", default=[1, 2, 3, 4])
     ap.add_argument("--dtn", type=float, nargs="+", default=[10.0, 100.0, 1000.0])
@@ -236,7 +275,7 @@ def main():
     a = ap.parse_args()
     import torch
     torch.cuda.set_device(0)
-    {"config3": config3, "config4": config4, "config2kernels": config2kernels}[a.what](a)
+    {"config0": config0, "config3": config3, "config4": config4, "config2kernels": config2kernels}[a.what](a)
 
 
 if __name__ == "__main__":
