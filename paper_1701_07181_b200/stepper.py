@@ -30,6 +30,7 @@ paper's Table 2-4 accounting (``studies.py:261-353``) reads the same.
 from __future__ import annotations
 
 import math
+import time
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -82,13 +83,36 @@ class StepResult:
 
 @dataclass
 class IntegrateResult:
-    u_final: object
+    """Reference stepper.py:290-319 (times, trajectory, step_results, counter,
+    wall_time and the averaged statistics); trajectory entries are CUDA tensors."""
+    times: np.ndarray
     trajectory: list
-    steps: int
-    newton_iterations: int
-    gmres_iterations: int
+    step_results: list
+    counter: OpCounter
     wall_time: float
-    counter: OpCounter = field(default_factory=OpCounter)
+
+    @property
+    def u_final(self):
+        return self.trajectory[-1]
+
+    @property
+    def newton_iters_avg(self) -> float:
+        if not self.step_results:
+            return 0.0
+        return float(np.mean([r.newton_iterations for r in self.step_results]))
+
+    @property
+    def gmres_iters_avg(self) -> float:
+        solves = [st for r in self.step_results for st in r.gmres_stats]
+        if not solves:
+            return 0.0
+        return float(np.mean([st.iterations for st in solves]))
+
+    @property
+    def equivalent_mults_avg(self) -> float:
+        if not self.step_results:
+            return 0.0
+        return float(np.mean([r.equivalent_mults_avg for r in self.step_results]))
 
 
 class NewtonError(RuntimeError):
@@ -379,10 +403,9 @@ def dirk_step(problem: LinearProblem, tab, u0, t0: float, dt: float,
 
 def integrate(problem: LinearProblem, scheme, t0: float, t1: float, dt: float,
               precond: PrecondSpec | None = None, newton_cfg: NewtonConfig | None = None,
-              gmres_cfg: GmresConfig | None = None, keep_trajectory: bool = False,
+              gmres_cfg: GmresConfig | None = None, keep_trajectory: bool = True,
               u0=None) -> IntegrateResult:
     """Fixed-step loop (stepper.py:328-375); DIRK tableaux use dirk_step."""
-    import time
     tab = builtin_tableau(scheme) if isinstance(scheme, str) else scheme
     span = t1 - t0
     if span < 0:
@@ -393,8 +416,8 @@ def integrate(problem: LinearProblem, scheme, t0: float, t1: float, dt: float,
     counter = OpCounter()
     cache = StepCache()
     u = _dev(u0) if u0 is not None else problem.initial_state()
-    traj = [u.clone()] if keep_trajectory else []
-    newton = gm = 0
+    trajectory = [u.clone()]
+    step_results = []
     start = time.perf_counter()
     for k in range(num_steps):
         tk = t0 + k * dt
@@ -405,11 +428,13 @@ def integrate(problem: LinearProblem, scheme, t0: float, t1: float, dt: float,
             res = irk_step_transformed(problem, tab, u, tk, dt, precond, newton_cfg, gmres_cfg,
                                        counter, cache=cache)
         u = res.u_next
-        newton += res.newton_iterations
-        gm += sum(st.iterations for st in res.gmres_stats)
+        step_results.append(res)
         if keep_trajectory:
-            traj.append(u.clone())
+            trajectory.append(u.clone())
+    if not keep_trajectory:
+        trajectory.append(u.clone())
     L.torch().cuda.synchronize()
-    return IntegrateResult(u_final=u, trajectory=traj, steps=num_steps, newton_iterations=newton,
-                           gmres_iterations=gm, wall_time=time.perf_counter() - start,
-                           counter=counter)
+    wall = time.perf_counter() - start
+    times = t0 + dt * np.arange(len(trajectory)) if keep_trajectory else np.array([t0, t1])
+    return IntegrateResult(times=times, trajectory=trajectory, step_results=step_results,
+                           counter=counter, wall_time=wall)
