@@ -460,10 +460,12 @@ __global__ void __launch_bounds__(288) k_unc_fwd_pipe(ApplyArgs A, PipeCfg PC) {
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int ncons_warps = (blockDim.x >> 5) - 1, ncons = ncons_warps * 32;
     pipe_init(P, PC.nst, ncons_warps);
+    griddep_launch();
     const int64_t bsz = (int64_t)PC.block_bytes / 8;
     const uint32_t seg = (uint32_t)nb * 8;
     if (warp == 0) {
         Producer pr{&P, &PC};
+        griddep_wait();   // PDL: CTA set up during the predecessor's drain
         int cur = (int)(A.ntasks * blockIdx.x / gridDim.x);
         const int hi = (int)(A.ntasks * (blockIdx.x + 1) / gridDim.x);
         int tb, tend;
@@ -565,6 +567,7 @@ __global__ void __launch_bounds__(288) k_unc_fwd_pipe(ApplyArgs A, PipeCfg PC) {
     Geo q;
     q.nb = nb; q.P = (nb + 1) >> 1; q.G = A.G_; q.g = c / nb; q.a = c - q.g * nb; q.active = q.g < q.G;
     Consumer cs{&P, &PC};
+    griddep_wait();
     double part[S];
     const double* xs = nullptr;
     int par = 0;   // reduction buffer of the current task
@@ -638,10 +641,12 @@ __global__ void __launch_bounds__(288) k_unc_bwd_pipe(ApplyArgs A, PipeCfg PC) {
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int ncons_warps = (blockDim.x >> 5) - 1, ncons = ncons_warps * 32;
     pipe_init(P, PC.nst, ncons_warps);
+    griddep_launch();
     const int64_t bsz = (int64_t)PC.block_bytes / 8;
     const uint32_t seg = (uint32_t)nb * 8;
     if (warp == 0) {
         Producer pr{&P, &PC};
+        griddep_wait();   // PDL: CTA set up during the predecessor's drain
         int cur = (int)(A.ntasks * blockIdx.x / gridDim.x);
         const int hi = (int)(A.ntasks * (blockIdx.x + 1) / gridDim.x);
         int tb, tend;
@@ -754,6 +759,7 @@ __global__ void __launch_bounds__(288) k_unc_bwd_pipe(ApplyArgs A, PipeCfg PC) {
     Geo q;
     q.nb = nb; q.P = (nb + 1) >> 1; q.G = A.G_; q.g = c / nb; q.a = c - q.g * nb; q.active = q.g < q.G;
     Consumer cs{&P, &PC};
+    griddep_wait();
     double part[S];
     const double* xs = nullptr;
     int par = 0;
@@ -886,11 +892,13 @@ __global__ void __launch_bounds__(288) k_cpl_fwd_pipe(ApplyArgs A, PipeCfg PC) {
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int ncons_warps = (blockDim.x >> 5) - 1, ncons = ncons_warps * 32;
     pipe_init(P, PC.nst, ncons_warps);
+    griddep_launch();
     const int64_t bsz = (int64_t)PC.block_bytes / 8;
     const uint32_t seg = (uint32_t)nb * 8;
     constexpr int NPAIRS = S * (S - 1) / 2;
     if (warp == 0) {
         Producer pr{&P, &PC};
+        griddep_wait();   // PDL: CTA set up during the predecessor's drain
         int cur = (int)(A.ntasks * blockIdx.x / gridDim.x);
         const int hi = (int)(A.ntasks * (blockIdx.x + 1) / gridDim.x);
         int tb, tend;
@@ -965,6 +973,7 @@ __global__ void __launch_bounds__(288) k_cpl_fwd_pipe(ApplyArgs A, PipeCfg PC) {
     Geo q;
     q.nb = nb; q.P = (nb + 1) >> 1; q.G = A.G_; q.g = c / nb; q.a = c - q.g * nb; q.active = q.g < q.G;
     Consumer cs{&P, &PC};
+    griddep_wait();
     double part[S];
     double gacc = 0.0;
     const double* xs = nullptr;
@@ -1041,12 +1050,14 @@ __global__ void __launch_bounds__(288) k_cpl_bwd_pipe(ApplyArgs A, PipeCfg PC) {
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int ncons_warps = (blockDim.x >> 5) - 1, ncons = ncons_warps * 32;
     pipe_init(P, PC.nst, ncons_warps);
+    griddep_launch();
     const int64_t bsz = (int64_t)PC.block_bytes / 8;
     const uint32_t seg = (uint32_t)nb * 8;
     constexpr int NPAIRS = S * (S - 1) / 2;
     const bool explicit_c = A.Cup != nullptr;
     if (warp == 0) {
         Producer pr{&P, &PC};
+        griddep_wait();   // PDL: CTA set up during the predecessor's drain
         int cur = (int)(A.ntasks * blockIdx.x / gridDim.x);
         const int hi = (int)(A.ntasks * (blockIdx.x + 1) / gridDim.x);
         int tb, tend;
@@ -1141,6 +1152,7 @@ __global__ void __launch_bounds__(288) k_cpl_bwd_pipe(ApplyArgs A, PipeCfg PC) {
     Geo q;
     q.nb = nb; q.P = (nb + 1) >> 1; q.G = A.G_; q.g = c / nb; q.a = c - q.g * nb; q.active = q.g < q.G;
     Consumer cs{&P, &PC};
+    griddep_wait();
     double part[S];
     double acc = 0.0;
     const double* xs = nullptr;
@@ -1296,7 +1308,7 @@ static int run_pipe(const irk_factor* f, K1 kernel_deps, K2 kernel_level, ApplyA
             }
             const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((A.ntasks + 1) / 2,
                                                                         (int64_t)f->ctx->num_sms * std::max(per_sm, 1)));
-            kernel_level<<<grid, threads, smem, st>>>(A, PC);
+            IRK_CK(launch_pdl(kernel_level, dim3(grid), dim3(threads), smem, st, A, PC));
             IRK_LAUNCHED();
         }
         return IRK_OK;
@@ -1307,7 +1319,7 @@ static int run_pipe(const irk_factor* f, K1 kernel_deps, K2 kernel_level, ApplyA
     IRK_CK(cudaMemsetAsync(ticket, 0, sizeof(int), st));
     IRK_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel_deps, threads, smem));
     const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(A.ntasks, (int64_t)f->ctx->num_sms * std::max(per_sm, 1)));
-    kernel_deps<<<grid, threads, smem, st>>>(A, PC);
+    IRK_CK(launch_pdl(kernel_deps, dim3(grid), dim3(threads), smem, st, A, PC));
     IRK_LAUNCHED();
     return IRK_OK;
 }

@@ -4,6 +4,7 @@
 
 #include <algorithm>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <atomic>
 #include <mutex>
@@ -12,6 +13,15 @@
 #include "irk_internal.cuh"
 
 namespace irk {
+
+bool pdl_enabled() {
+    static const bool on = [] {
+        const char* e = getenv("IRK_PDL");
+        return !(e && atoi(e) == 0);
+    }();
+    return on;
+}
+
 
 static thread_local std::string g_err;
 static std::atomic<long long> g_launches{0};

@@ -14,6 +14,7 @@
 #include <stdint.h>
 
 #include <string>
+#include <utility>
 #include <vector>
 
 #include "../../include/irkb200.h"
@@ -44,6 +45,35 @@ void count_launch();
 
 #define IRK_TRY(expr)                                                         \
     do { int _rc = (expr); if (_rc != IRK_OK) return _rc; } while (0)
+
+// ---- programmatic dependent launch (PDL) -----------------------------------
+// Hot kernels are launched with programmatic stream serialisation: each one
+// triggers its dependents at entry (every CTA of a single-wave grid is then
+// resident, so a waiting dependent can never block it), and waits for its
+// predecessor (griddepcontrol.wait) after its prologue, before its first
+// global read or write.  The next kernel's CTAs launch and initialise their
+// shared-memory pipelines (mbarriers, rings) during the previous kernel's
+// drain.  IRK_PDL=0 disables it (plain stream order).
+__device__ __forceinline__ void griddep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void griddep_launch() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
+bool pdl_enabled();
+
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                              Args&&... args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
+}
 
 inline int npairs(int nb) { return (nb + 1) / 2; }
 inline int64_t block_doubles(int nb) { return (int64_t)nb * 2 * npairs(nb); }

@@ -285,6 +285,8 @@ template <int NVM>
 __global__ void __launch_bounds__(VB) k_multidot_v(const double* __restrict__ V, int64_t ldv, int nv,
                                                    const double* __restrict__ w, int64_t n, double* partials,
                                                    double* out, unsigned* counter) {
+    griddep_launch();
+    griddep_wait();
     __shared__ double red[(NVM + 1) * (VB / 32)];
     int64_t lo2, hi2;
     bool tail;
@@ -322,6 +324,8 @@ __global__ void __launch_bounds__(VB) k_update_dots_v(const double* __restrict__
                                                       const double* __restrict__ h, double* __restrict__ w,
                                                       int64_t n, double* partials, double* out,
                                                       unsigned* counter) {
+    griddep_launch();
+    griddep_wait();
     __shared__ double hs[NVM];
     __shared__ double red[(NVM + 1) * (VB / 32)];
     for (int i = threadIdx.x; i < nv; i += blockDim.x) hs[i] = h[i];
@@ -382,6 +386,8 @@ __global__ void __launch_bounds__(VB) k_finish_v(const double* __restrict__ V, i
                                                  const double* __restrict__ ww0, const double* __restrict__ h2,
                                                  double eta, double brk, double* __restrict__ w, int64_t n,
                                                  double* out) {
+    griddep_launch();
+    griddep_wait();
     __shared__ double hs[NVM];
     const bool reorth = sqrt(h2[nv]) < eta * sqrt(*ww0);
     double nw2 = h2[nv];
@@ -541,11 +547,14 @@ static int cgs2_v_t(const irk_ctx* ctx, int64_t n, int64_t ldv, int nv, const do
     const int nb = vec_blocks(ctx);
     double* h1 = out;
     double* h2 = out + nv + 1;
-    k_multidot_v<NVM><<<nb, VB, 0, st>>>(V, ldv, nv, w, n, partials, h1, counters);
+    IRK_CK(launch_pdl(k_multidot_v<NVM>, dim3(nb), dim3(VB), 0, st, V, ldv, nv, (const double*)w, n, partials, h1,
+                      counters));
     IRK_LAUNCHED();
-    k_update_dots_v<NVM><<<nb, VB, 0, st>>>(V, ldv, nv, h1, w, n, partials, h2, counters + 1);
+    IRK_CK(launch_pdl(k_update_dots_v<NVM>, dim3(nb), dim3(VB), 0, st, V, ldv, nv, (const double*)h1, w, n, partials,
+                      h2, counters + 1));
     IRK_LAUNCHED();
-    k_finish_v<NVM><<<nb, VB, 0, st>>>(V, ldv, nv, h1 + nv, h2, eta, brk, w, n, out + 2 * (nv + 1));
+    IRK_CK(launch_pdl(k_finish_v<NVM>, dim3(nb), dim3(VB), 0, st, V, ldv, nv, (const double*)(h1 + nv),
+                      (const double*)h2, eta, brk, w, n, out + 2 * (nv + 1)));
     IRK_LAUNCHED();
     return IRK_OK;
 }

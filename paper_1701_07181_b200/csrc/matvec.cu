@@ -126,6 +126,8 @@ __global__ void __launch_bounds__(288) k_stage_matvec_pipe(MatvecArgs A, MixPara
         fence_mbar_init();
     }
     __syncthreads();
+    griddep_launch();
+    griddep_wait();   // PDL: pipeline set up during the predecessor's drain
     const int nb = A.nb;
     const int64_t bsz = (int64_t)PG.block_bytes / 8;
     if (warp == 0) {
@@ -281,7 +283,7 @@ static int launch_pipe(const irk_stage_op* op, MatvecArgs& A, const MixParams& C
     int per_sm = 1;
     IRK_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_stage_matvec_pipe<S, SHARED>, threads, smem));
     const int64_t grid = std::max<int64_t>(1, std::min<int64_t>(A.T_local, (int64_t)op->ctx->num_sms * std::max(per_sm, 1)));
-    k_stage_matvec_pipe<S, SHARED><<<(int)grid, threads, smem, st>>>(A, C, PG);
+    IRK_CK(launch_pdl(k_stage_matvec_pipe<S, SHARED>, dim3((unsigned)grid), dim3(threads), smem, st, A, C, PG));
     IRK_LAUNCHED();
     return IRK_OK;
 }
