@@ -841,7 +841,7 @@ __global__ void __launch_bounds__(4 * NB) k_schur(FactorArgs F, const int32_t* _
 
 template <int S, int NB>
 static int launch_schur_t(const irk_ctx* ctx, const FactorArgs& F, const int32_t* elems, int64_t nelem,
-                          cudaStream_t st) {
+                          cudaStream_t st, int cap_per_sm) {
     const size_t smem = sizeof(double) * (size_t)(S + 2) * SchurGeo<NB>::SLOT;
     static bool attr = false;
     if (!attr) {
@@ -851,6 +851,7 @@ static int launch_schur_t(const irk_ctx* ctx, const FactorArgs& F, const int32_t
     }
     int per_sm = 1;
     IRK_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_schur<S, NB>, 4 * NB, smem));
+    if (cap_per_sm > 0) per_sm = std::min(per_sm, cap_per_sm);
     const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(nelem, (int64_t)ctx->num_sms * std::max(per_sm, 1)));
     k_schur<S, NB><<<grid, 4 * NB, smem, st>>>(F, elems, nelem);
     IRK_LAUNCHED();
@@ -859,15 +860,15 @@ static int launch_schur_t(const irk_ctx* ctx, const FactorArgs& F, const int32_t
 
 template <int S>
 static int launch_schur_s(const irk_ctx* ctx, const FactorArgs& F, const int32_t* elems, int64_t nelem,
-                          cudaStream_t st) {
+                          cudaStream_t st, int cap) {
     switch ((F.nb + 7) & ~7) {   // padded to the 8x8 DMMA tile
-        case 16: return launch_schur_t<S, 16>(ctx, F, elems, nelem, st);
-        case 24: return launch_schur_t<S, 24>(ctx, F, elems, nelem, st);
-        case 32: return launch_schur_t<S, 32>(ctx, F, elems, nelem, st);
-        case 40: return launch_schur_t<S, 40>(ctx, F, elems, nelem, st);
-        case 48: return launch_schur_t<S, 48>(ctx, F, elems, nelem, st);
-        case 56: return launch_schur_t<S, 56>(ctx, F, elems, nelem, st);
-        case 64: return launch_schur_t<S, 64>(ctx, F, elems, nelem, st);
+        case 16: return launch_schur_t<S, 16>(ctx, F, elems, nelem, st, cap);
+        case 24: return launch_schur_t<S, 24>(ctx, F, elems, nelem, st, cap);
+        case 32: return launch_schur_t<S, 32>(ctx, F, elems, nelem, st, cap);
+        case 40: return launch_schur_t<S, 40>(ctx, F, elems, nelem, st, cap);
+        case 48: return launch_schur_t<S, 48>(ctx, F, elems, nelem, st, cap);
+        case 56: return launch_schur_t<S, 56>(ctx, F, elems, nelem, st, cap);
+        case 64: return launch_schur_t<S, 64>(ctx, F, elems, nelem, st, cap);
         default: return IRK_EINVAL;
     }
 }
@@ -879,18 +880,24 @@ static bool schur_eligible(const irk_factor* f, const FactorArgs& F) {
 }
 
 static int launch_schur(const irk_ctx* ctx, const FactorArgs& F, const int32_t* elems, int64_t nelem,
-                        cudaStream_t st) {
+                        cudaStream_t st, int cap = 0) {
     switch (F.s) {
-        case 1: return launch_schur_s<1>(ctx, F, elems, nelem, st);
-        case 2: return launch_schur_s<2>(ctx, F, elems, nelem, st);
-        case 3: return launch_schur_s<3>(ctx, F, elems, nelem, st);
-        case 4: return launch_schur_s<4>(ctx, F, elems, nelem, st);
+        case 1: return launch_schur_s<1>(ctx, F, elems, nelem, st, cap);
+        case 2: return launch_schur_s<2>(ctx, F, elems, nelem, st, cap);
+        case 3: return launch_schur_s<3>(ctx, F, elems, nelem, st, cap);
+        case 4: return launch_schur_s<4>(ctx, F, elems, nelem, st, cap);
         default: return IRK_EINVAL;
     }
 }
 
 int launch_inverse(const irk_ctx* ctx, const int32_t* tasks, int64_t ntasks, int64_t T, int s, int nb,
-                   const double* D, double* Dinv, unsigned long long* fail_key, int* fb, cudaStream_t st);
+                   const double* D, double* Dinv, unsigned long long* fail_key, int* fb, cudaStream_t st,
+                   int cap_per_sm = 0);
+
+static int env_int(const char* name, int dflt) {
+    const char* e = getenv(name);
+    return e ? atoi(e) : dflt;
+}
 
 template <int MAXT>
 static int launch_levels(const irk_factor* f, FactorArgs& F, const irk_sched& sched, size_t smem,
@@ -911,10 +918,37 @@ static int launch_levels(const irk_factor* f, FactorArgs& F, const irk_sched& sc
         F.tasks = sched.d_order + lo;
         F.ntasks = hi - lo;
         const int grid = (int)std::min<int64_t>(hi - lo, (int64_t)f->ctx->num_sms * 8);
-        if (split && schur_eligible(f, F)) {
-            // level tasks are stage-major (k*T + e, skew 0): the first 1/s are the elements
-            IRK_TRY(launch_schur(f->ctx, F, F.tasks, F.ntasks / F.s, st));
-            IRK_TRY(launch_inverse(f->ctx, F.tasks, F.ntasks, F.T, F.s, F.nb, F.Dst, F.Dinv, F.fail_key, f->d_fb, st));
+        if (split && schur_eligible(f, F) && f->d_fs_elems) {
+            // the level's elements and their (element-major) stage tasks
+            const int64_t e0 = f->h_fs_eptr[l], ne = f->h_fs_eptr[l + 1] - e0;
+            const int32_t* el = f->d_fs_elems + e0;
+            const int32_t* tk = f->d_fs_tasks + e0 * F.s;
+            static const int nchunk = env_int("IRK_FACTOR_CHUNKS", 1);   // measured: no gain at config 1
+            static const int schur_cap = env_int("IRK_SCHUR_CAP", 2);
+            static const int inv_cap = env_int("IRK_INV_CAP", 1);
+            if (l == 0 || nchunk <= 1 || ne < 4 * (int64_t)f->ctx->num_sms) {
+                IRK_TRY(launch_schur(f->ctx, F, el, ne, st));
+                IRK_TRY(launch_inverse(f->ctx, tk, ne * F.s, F.T, F.s, F.nb, F.Dst, F.Dinv, F.fail_key, f->d_fb, st));
+            } else {
+                // chunked: the latency-bound inverse of chunk c (side stream, capped grid) runs beside
+                // the DMMA-bound Schur phase of chunk c+1 (main stream, capped at schur_cap CTAs/SM)
+                if (!f->st2) {
+                    IRK_CK(cudaStreamCreateWithFlags(&f->st2, cudaStreamNonBlocking));
+                    f->ev.resize(nchunk + 1);
+                    for (auto& e : f->ev) IRK_CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+                }
+                for (int c = 0; c < nchunk; ++c) {
+                    const int64_t a = ne * c / nchunk, b = ne * (c + 1) / nchunk;
+                    if (b == a) continue;
+                    IRK_TRY(launch_schur(f->ctx, F, el + a, b - a, st, schur_cap));
+                    IRK_CK(cudaEventRecord(f->ev[c], st));
+                    IRK_CK(cudaStreamWaitEvent(f->st2, f->ev[c], 0));
+                    IRK_TRY(launch_inverse(f->ctx, tk + a * F.s, (b - a) * F.s, F.T, F.s, F.nb, F.Dst, F.Dinv,
+                                           F.fail_key, f->d_fb, f->st2, inv_cap));
+                }
+                IRK_CK(cudaEventRecord(f->ev[nchunk], f->st2));
+                IRK_CK(cudaStreamWaitEvent(st, f->ev[nchunk], 0));
+            }
         } else if (split) {
             k_factor<MAXT, false><<<grid, 256, smem, st>>>(F);
             IRK_LAUNCHED();
@@ -1095,6 +1129,23 @@ static int factor_common(irk_ctx* ctx, const irk_pattern* pat, const FactorSetup
     levels_forward(pat, keep, levf);
     // factor tasks: (stage, element) per level
     if ((rc = build_sched(f->fsched, levf, pat->T, P.s, true, P.coupled ? +1 : 0))) return fail(rc);
+    if (!P.coupled) {
+        // per-level element lists and element-major task codes for the Schur path
+        const int64_t nl = f->fsched.nlevels;
+        std::vector<int64_t> cnt(nl + 1, 0);
+        for (int64_t e = 0; e < pat->T; ++e) cnt[levf[e] + 1]++;
+        for (int64_t l = 0; l < nl; ++l) cnt[l + 1] += cnt[l];
+        std::vector<int32_t> elems(pat->T), tasks((size_t)pat->T * P.s);
+        std::vector<int64_t> pos(cnt.begin(), cnt.end() - 1);
+        for (int64_t e = 0; e < pat->T; ++e) elems[pos[levf[e]]++] = (int32_t)e;
+        for (int64_t q = 0; q < pat->T; ++q)
+            for (int k = 0; k < P.s; ++k) tasks[q * P.s + k] = (int32_t)((int64_t)k * pat->T + elems[q]);
+        f->h_fs_eptr = cnt;
+        FCK(cudaMalloc(&f->d_fs_elems, sizeof(int32_t) * std::max<int64_t>(pat->T, 1)));
+        FCK(cudaMalloc(&f->d_fs_tasks, sizeof(int32_t) * std::max<int64_t>(pat->T * P.s, 1)));
+        FCK(cudaMemcpy(f->d_fs_elems, elems.data(), sizeof(int32_t) * pat->T, cudaMemcpyHostToDevice));
+        FCK(cudaMemcpy(f->d_fs_tasks, tasks.data(), sizeof(int32_t) * pat->T * P.s, cudaMemcpyHostToDevice));
+    }
 
     FactorArgs& F = *static_cast<FactorArgs*>(f->fargs);
     F.indptr = pat->d_indptr;
@@ -1255,6 +1306,10 @@ void irk_factor_destroy(irk_factor* f) {
     cudaFree(f->d_W);
     cudaFree(f->d_Wrhs);
     cudaFree(f->d_fb);
+    cudaFree(f->d_fs_elems);
+    cudaFree(f->d_fs_tasks);
+    for (auto e : f->ev) cudaEventDestroy(e);
+    if (f->st2) cudaStreamDestroy(f->st2);
     cudaFree(f->d_hasup);
     cudaFree(f->d_Dinv);
     cudaFree(f->d_D);

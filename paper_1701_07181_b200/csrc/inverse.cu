@@ -57,6 +57,7 @@ struct InvArgs {
     double* Dinv;             // inverses Dinv[j][k]
     unsigned long long* fail_key;
     const int* ntasks_dev;    // non-NULL: task count on the device (<= ntasks), fallback lists
+    int cap_per_sm;           // > 0: at most this many CTAs per SM (runs beside another kernel)
 };
 
 // task count of a launch: the host bound, or the device count of a fallback list
@@ -1239,6 +1240,7 @@ static int launch_tc_t(const irk_ctx* ctx, const InvArgs& A, int* fb_list, int* 
     const int threads = 32 * C::WARPS;
     int per_sm = 1;
     IRK_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_inverse_tc<NT, EXACT>, threads, C::smem));
+    if (A.cap_per_sm > 0) per_sm = std::min(per_sm, A.cap_per_sm);
     const int64_t need = (A.ntasks + C::WARPS - 1) / C::WARPS;
     const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(need, (int64_t)ctx->num_sms * std::max(per_sm, 1)));
     k_inverse_tc<NT, EXACT><<<grid, threads, C::smem, st>>>(A, fb_list, fb_count);
@@ -1280,9 +1282,10 @@ static int launch_tc(const irk_ctx* ctx, const InvArgs& A, int* fb, cudaStream_t
 
 // returns IRK_EINVAL if nb has no warp-inverse specialisation (caller falls back)
 int launch_inverse(const irk_ctx* ctx, const int32_t* tasks, int64_t ntasks, int64_t T, int s, int nb,
-                   const double* D, double* Dinv, unsigned long long* fail_key, int* fb, cudaStream_t st) {
+                   const double* D, double* Dinv, unsigned long long* fail_key, int* fb, cudaStream_t st,
+                   int cap_per_sm) {
     if (ntasks <= 0) return IRK_OK;
-    InvArgs A{tasks, ntasks, T, s, nb, D, Dinv, fail_key, nullptr};
+    InvArgs A{tasks, ntasks, T, s, nb, D, Dinv, fail_key, nullptr, cap_per_sm};
     static const bool tc_off = getenv("IRK_INV_TC") && atoi(getenv("IRK_INV_TC")) == 0;
     if (fb && !tc_off && nb > 16 && nb <= 64) return launch_tc(ctx, A, fb, st);
     return launch_pivoted(ctx, A, st);

@@ -183,6 +183,13 @@ struct irk_factor {
     irk_sched fsched;                 // factor tasks by level
     unsigned long long* d_fail = nullptr;
     int* d_fb = nullptr;              // tensor-core inverse: blocks handed to the pivoted kernels
+    // Schur path: per factor level, its elements and element-major (stage fastest) task codes
+    int32_t* d_fs_elems = nullptr;
+    int32_t* d_fs_tasks = nullptr;
+    std::vector<int64_t> h_fs_eptr;   // nlevels+1 element offsets
+    // side stream + events: the inverse of Schur chunk c overlaps the Schur phase of chunk c+1
+    mutable cudaStream_t st2 = nullptr;
+    mutable std::vector<cudaEvent_t> ev;
     size_t fsmem = 0;
     int maxt = 1;
     const double* cpl_src = nullptr;  // explicit couplings (s*s*T blocks)
