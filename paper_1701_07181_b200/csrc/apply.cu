@@ -1289,7 +1289,8 @@ static int run_pipe(const irk_factor* f, K1 kernel_deps, K2 kernel_level, ApplyA
     PC.nst = (int)std::max<size_t>(2, std::min<size_t>(24, per_cta > fixed ? (per_cta - fixed) / per_stage : 0));
     if (const char* ns = getenv("IRK_APPLY_NST")) PC.nst = std::max(2, atoi(ns));
     const size_t smem = (size_t)PC.nst * per_stage + fixed;
-    const bool level_mode = S.nlevels <= LEVEL_LAUNCH_MAX;
+    static const bool force_deps = getenv("IRK_APPLY_DEPS") && atoi(getenv("IRK_APPLY_DEPS")) != 0;
+    const bool level_mode = S.nlevels <= LEVEL_LAUNCH_MAX && !force_deps;
     int per_sm = 1;
     if (level_mode) {
         IRK_CK(cudaFuncSetAttribute(kernel_level, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)f->ctx->smem_optin));
