@@ -16,8 +16,8 @@ timeout 600 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__byte
 # full capture of the hot kernels of one timed step (launches after warmup)
 timeout 1200 ncu --set full --clock-control none --import-source on \
   -k regex:"k_schur|k_inverse|k_unc|k_stage_matvec|k_multidot|k_update|k_finish" \
-  --profile-from-start off -c ${NCU_COUNT:-12} -f -o $O/full_$TAG \
+  --profile-from-start off -c ${NCU_COUNT:-12} -f -o /tmp/full_$TAG \
   python bench.py --steps 1 --warmup 1 --profile --no-alt --jnorm 2.4496432463318416 > $O/ncu_full_$TAG.log 2>&1
 echo "ncu full rc=$?"
-ncu -i $O/full_$TAG.ncu-rep --page raw --csv > $O/raw_$TAG.csv 2>/dev/null
+ncu -i /tmp/full_$TAG.ncu-rep --page raw --csv > $O/raw_$TAG.csv 2>/dev/null
 ls -la $O
