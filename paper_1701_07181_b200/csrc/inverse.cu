@@ -1035,9 +1035,10 @@ __device__ __forceinline__ void dmma_f64(double& c0, double& c1, double a, doubl
 
 template <int NT>
 struct InvTcCfg {
-    // ld = 8 (mod 16) doubles: conflict-free panel column loads and C-tile double2 accesses
-    static constexpr int NBT = 8 * NT, LD = NBT + 8, WARPS = 4, RPL = NBT / 4;   // RPL: panel rows per lane
-    static constexpr size_t warp_doubles = (size_t)NBT * LD;
+    // ld = 8 (mod 16) doubles: conflict-free C-tile double2 accesses (the DMMA update's traffic)
+    static constexpr int NBT = 8 * NT, LD = NBT + ((24 - NBT % 16) % 16), WARPS = 4;
+    static constexpr int RL = (NBT + 31) / 32;    // panel rows per lane (row-per-lane layout)
+    static constexpr size_t warp_doubles = (size_t)NBT * LD + 16;   // + 2 x 8 pivot-row buffer
     static constexpr size_t smem = WARPS * warp_doubles * sizeof(double);
 };
 
@@ -1045,15 +1046,15 @@ struct InvTcCfg {
 template <int NT, bool EXACT>
 __global__ void __launch_bounds__(32 * InvTcCfg<NT>::WARPS) k_inverse_tc(InvArgs A, int* fb_list, int* fb_count) {
     using C = InvTcCfg<NT>;
-    constexpr int NBT = C::NBT, LD = C::LD, RPL = C::RPL;
+    constexpr int NBT = C::NBT, LD = C::LD, RL = C::RL;
     constexpr int NPAIR = NBT * NBT / 2;            // double2 per padded block
     extern __shared__ __align__(16) double smtc[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     double* X = smtc + (size_t)warp * C::warp_doubles;
+    double* rowbuf = X + (size_t)NBT * LD;          // [2][8]: pivot row broadcast (alternating)
     const int nb = EXACT ? NBT : A.nb;
     const int P = (nb + 1) >> 1;
     const int64_t bsz = (int64_t)nb * 2 * P;
-    const int pc = lane & 7, pq = lane >> 3;        // panel layout: column, row group
     const int fr = lane >> 2, fk = lane & 3;        // fragment layout
     for (int64_t t = (int64_t)blockIdx.x * C::WARPS + warp; t < A.ntasks; t += (int64_t)gridDim.x * C::WARPS) {
         const int64_t code = A.tasks[t];
@@ -1125,39 +1126,63 @@ __global__ void __launch_bounds__(32 * InvTcCfg<NT>::WARPS) k_inverse_tc(InvArgs
             constexpr int p = decltype(pc_)::value;   // panel index
             constexpr int k0 = 8 * p;
             if (swap) return;
-            // ---- panel to registers: pv[i] = X[pq + 4 i][k0 + pc]
-            double pv[RPL];
+            // ---- panel to registers, one row per lane: pa[j][c] = X[lane + 32 j][k0 + c]
+            double pa[RL][8];
 #pragma unroll
-            for (int i = 0; i < RPL; ++i) pv[i] = X[(pq + 4 * i) * LD + k0 + pc];
+            for (int j = 0; j < RL; ++j) {
+                const int r = lane + 32 * j;
+#pragma unroll
+                for (int c = 0; c < 8; c += 2) {
+                    double2 v = make_double2(0.0, 0.0);
+                    if (r < NBT) v = *reinterpret_cast<const double2*>(X + r * LD + k0 + c);
+                    pa[j][c] = v.x;
+                    pa[j][c + 1] = v.y;
+                }
+            }
             // ---- 8 scalar GJ steps on the panel columns
             static_for([&](auto kc_) {
                 constexpr int kk = decltype(kc_)::value;
                 constexpr int k = k0 + kk;
-                constexpr int kq = k & 3, ki = k >> 2;      // row k: group kq, register ki
-                const bool colk = pc == kk;
-                const bool rowk = pq == kq;
-                const double piv = __shfl_sync(0xffffffffu, pv[ki], kk + 8 * kq);
+                constexpr int ko = k & 31, ks = k >> 5;      // owner lane / slot of row k
+                const bool own = lane == ko;
+                const double piv = __shfl_sync(0xffffffffu, pa[ks][kk], ko);
                 // partial-pivoting equivalence: no row r > k of column k beats the diagonal
-                // (rows r = pq + 4 i > k: all i > ki, and i == ki for groups pq > kq)
                 const double ap = fabs(piv);
                 bool beat = false;
 #pragma unroll
-                for (int i = ki; i < RPL; ++i)
-                    if (i > ki || pq > kq) beat |= fabs(pv[i]) > ap;
-                const bool ok = !__any_sync(0xffffffffu, colk && beat) && piv != 0.0 && isfinite(piv);
+                for (int j = 0; j < RL; ++j)
+                    if (lane + 32 * j > k && lane + 32 * j < NBT) beat |= fabs(pa[j][kk]) > ap;
+                const bool ok = !__any_sync(0xffffffffu, beat) && piv != 0.0 && isfinite(piv);
                 if (!ok) swap = true;
                 const double inv = 1.0 / piv;
-                if (k < nb && lane == (k & 31)) apiv[k >> 5] = ap;
-                // new row k in my column: rk = a_kc / piv; every other row r: a_rc - a_rk rk,
-                // column k itself -a_rk / piv: new = fma(h, f, g * old)
-                const double rk = __shfl_sync(0xffffffffu, pv[ki], pc + 8 * kq) * inv;
-                const double g = colk ? 0.0 : 1.0;
-                const double h = colk ? -inv : -rk;
+                if (k < nb && own) apiv[ks] = ap;
+                // new row k = a_k / piv (column k: 1 / piv), broadcast through shared memory
+                double* rb = rowbuf + 8 * (kk & 1);
+                if (own) {
 #pragma unroll
-                for (int i = 0; i < RPL; ++i) {
-                    const double f = __shfl_sync(0xffffffffu, pv[i], kk + 8 * pq);
-                    const double nv = fma(h, f, g * pv[i]);
-                    pv[i] = (i == ki && rowk) ? (colk ? inv : rk) : nv;
+                    for (int c = 0; c < 8; c += 2) {
+                        double2 v = make_double2(c == kk ? inv : pa[ks][c] * inv, c + 1 == kk ? inv : pa[ks][c + 1] * inv);
+                        *reinterpret_cast<double2*>(rb + c) = v;
+                    }
+                }
+                __syncwarp();
+                double rk[8];
+#pragma unroll
+                for (int c = 0; c < 8; c += 2) {
+                    const double2 v = *reinterpret_cast<const double2*>(rb + c);
+                    rk[c] = v.x;
+                    rk[c + 1] = v.y;
+                }
+                // other rows: a_rc - a_rk rk_c, column k: -a_rk / piv
+#pragma unroll
+                for (int j = 0; j < RL; ++j) {
+                    const bool isk = own && j == ks;
+                    const double f = pa[j][kk];
+#pragma unroll
+                    for (int c = 0; c < 8; ++c) {
+                        const double nv = (c == kk) ? -f * inv : fma(-f, rk[c], pa[j][c]);
+                        pa[j][c] = isk ? rk[c] : nv;
+                    }
                 }
             }, std::make_integer_sequence<int, 8>{});
             if (swap) return;
@@ -1170,7 +1195,13 @@ __global__ void __launch_bounds__(32 * InvTcCfg<NT>::WARPS) k_inverse_tc(InvArgs
                     bf[jt][kc] = (jt == p) ? 0.0 : X[(k0 + 4 * kc + fk) * LD + 8 * jt + fr];
             __syncwarp();
 #pragma unroll
-            for (int i = 0; i < RPL; ++i) X[(pq + 4 * i) * LD + k0 + pc] = pv[i];
+            for (int j = 0; j < RL; ++j) {
+                const int r = lane + 32 * j;
+                if (r < NBT)
+#pragma unroll
+                    for (int c = 0; c < 8; c += 2)
+                        *reinterpret_cast<double2*>(X + r * LD + k0 + c) = make_double2(pa[j][c], pa[j][c + 1]);
+            }
             __syncwarp();
 #pragma unroll
             for (int it = 0; it < NT; ++it) {
