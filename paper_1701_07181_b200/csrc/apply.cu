@@ -430,6 +430,20 @@ __device__ __forceinline__ double smem_gemv(const double2* B, const double* x, c
     return acc;
 }
 
+// acc[k] += rows of a staged block times S x segments x + k * nb: every block
+// pair is read from shared memory once for all S vectors
+template <int S>
+__device__ __forceinline__ void smem_gemv_all(const double2* B, const double* x, const Geo& q, double* acc) {
+    for (int p = q.g; p < q.P; p += q.G) {
+        const double2 b = B[p * q.nb + q.a];
+#pragma unroll
+        for (int k = 0; k < S; ++k) {
+            const double2 v = *reinterpret_cast<const double2*>(x + k * q.nb + 2 * p);
+            acc[k] = fma(b.y, v.y, fma(b.x, v.x, acc[k]));
+        }
+    }
+}
+
 constexpr int MAXD = 8;   // neighbour metadata held in registers per task
 
 // Task ranges: DEPS (persistent, many levels) -> batches of 32 tickets;
@@ -584,10 +598,13 @@ __global__ void __launch_bounds__(288) k_unc_fwd_pipe(ApplyArgs A, PipeCfg PC) {
         if (dsc.y >= 0 && q.active) {
             const int m = dsc.y / S, kk = dsc.y - m * S;
             const double2* B = cs.block();
-            const bool sh = (dsc.z & PD_SH) != 0;
+            if (dsc.z & PD_SH) {
+                smem_gemv_all<S>(B, xs + m * S * nb, q, part);
+            } else {
 #pragma unroll
-            for (int k = 0; k < S; ++k)
-                if (k == kk || sh) part[k] = smem_gemv(B, xs + (m * S + k) * nb, q, part[k]);
+                for (int k = 0; k < S; ++k)
+                    if (k == kk) part[k] = smem_gemv(B, xs + (m * S + k) * nb, q, part[k]);
+            }
         }
         cs.release();
         if (dsc.z & PD_LAST) {
@@ -777,11 +794,7 @@ __global__ void __launch_bounds__(288) k_unc_bwd_pipe(ApplyArgs A, PipeCfg PC) {
         }
         const double2* B = cs.block();
         if (dsc.z & PD_USH) {
-            if (q.active) {
-                const int m = dsc.y / S;
-#pragma unroll
-                for (int k = 0; k < S; ++k) part[k] = smem_gemv(B, xs + (m * S + k) * nb, q, part[k]);
-            }
+            if (q.active) smem_gemv_all<S>(B, xs + (dsc.y / S) * S * nb, q, part);
         } else if (dsc.z & PD_U) {
             if (q.active) {
                 const int m = dsc.y / S, kk = dsc.y - m * S;
@@ -821,11 +834,14 @@ __global__ void __launch_bounds__(288) k_unc_bwd_pipe(ApplyArgs A, PipeCfg PC) {
             }
             if (q.active) {
                 const bool direct = (dsc.w & 1) != 0;
-                const bool sh = (dsc.z & PD_SH) != 0;
+                const double* xv = direct ? xs + nup * S * nb : P.tv;
+                if (dsc.z & PD_SH) {
+                    smem_gemv_all<S>(B, xv, q, part);
+                } else {
 #pragma unroll
-                for (int k = 0; k < S; ++k)
-                    if (k == kk || sh)
-                        part[k] = smem_gemv(B, direct ? xs + (nup * S + k) * nb : P.tv + k * nb, q, part[k]);
+                    for (int k = 0; k < S; ++k)
+                        if (k == kk) part[k] = smem_gemv(B, xv + k * nb, q, part[k]);
+                }
             }
         }
         cs.release();
@@ -1174,10 +1190,13 @@ __global__ void __launch_bounds__(288) k_cpl_bwd_pipe(ApplyArgs A, PipeCfg PC) {
         if (dsc.z & (PD_USH | PD_U)) {
             if (q.active) {
                 const int m = dsc.y / S, kk = dsc.y - m * S;
-                const bool sh = (dsc.z & PD_USH) != 0;
+                if (dsc.z & PD_USH) {
+                    smem_gemv_all<S>(B, xs + m * S * nb, q, part);
+                } else {
 #pragma unroll
-                for (int k = 0; k < S; ++k)
-                    if (sh || k == kk) part[k] = smem_gemv(B, xs + (m * S + k) * nb, q, part[k]);
+                    for (int k = 0; k < S; ++k)
+                        if (k == kk) part[k] = smem_gemv(B, xs + (m * S + k) * nb, q, part[k]);
+                }
             }
             cs.release();
             continue;
@@ -1289,6 +1308,8 @@ static int run_pipe(const irk_factor* f, K1 kernel_deps, K2 kernel_level, ApplyA
     PC.nst = (int)std::max<size_t>(2, std::min<size_t>(24, per_cta > fixed ? (per_cta - fixed) / per_stage : 0));
     if (const char* ns = getenv("IRK_APPLY_NST")) PC.nst = std::max(2, atoi(ns));
     const size_t smem = (size_t)PC.nst * per_stage + fixed;
+    // PDL for the uncoupled sweeps only: measured 7.8 -> 9.1 ms per RADAU23 coupled step with it
+    const bool pdl = f->kind == IRK_FACTOR_UNCOUPLED;
     static const bool force_deps = getenv("IRK_APPLY_DEPS") && atoi(getenv("IRK_APPLY_DEPS")) != 0;
     const bool level_mode = S.nlevels <= LEVEL_LAUNCH_MAX && !force_deps;
     int per_sm = 1;
@@ -1309,7 +1330,7 @@ static int run_pipe(const irk_factor* f, K1 kernel_deps, K2 kernel_level, ApplyA
             }
             const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((A.ntasks + 1) / 2,
                                                                         (int64_t)f->ctx->num_sms * std::max(per_sm, 1)));
-            IRK_CK(launch_pdl(kernel_level, dim3(grid), dim3(threads), smem, st, A, PC));
+            IRK_CK(launch_pdl_if(pdl, kernel_level, dim3(grid), dim3(threads), smem, st, A, PC));
             IRK_LAUNCHED();
         }
         return IRK_OK;
@@ -1320,7 +1341,7 @@ static int run_pipe(const irk_factor* f, K1 kernel_deps, K2 kernel_level, ApplyA
     IRK_CK(cudaMemsetAsync(ticket, 0, sizeof(int), st));
     IRK_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel_deps, threads, smem));
     const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(A.ntasks, (int64_t)f->ctx->num_sms * std::max(per_sm, 1)));
-    IRK_CK(launch_pdl(kernel_deps, dim3(grid), dim3(threads), smem, st, A, PC));
+    IRK_CK(launch_pdl_if(pdl, kernel_deps, dim3(grid), dim3(threads), smem, st, A, PC));
     IRK_LAUNCHED();
     return IRK_OK;
 }
@@ -1423,7 +1444,10 @@ static void fill_args(const irk_factor* f, ApplyArgs& A) {
     A.n = p->T * f->nb;
     A.s = f->s;
     A.nb = f->nb;
-    A.G_ = choose_groups(f->nb, 256);
+    // consumer groups: the multi-stage uncoupled sweeps read each block once for all stages and
+    // run best with <= 4 consumer warps; the single-stage and coupled sweeps (more per-task
+    // reductions) keep up to 8 (tools/tune_apply.py, tools/sweep.py config4)
+    A.G_ = choose_groups(f->nb, (f->kind == IRK_FACTOR_UNCOUPLED && f->s > 1) ? 128 : 256);
     if (const char* g = getenv("IRK_APPLY_G")) A.G_ = std::max(1, std::min(atoi(g), (f->nb + 1) / 2));
 }
 
@@ -1471,6 +1495,7 @@ int factor_apply_rhs(const irk_factor* f, int nrhs, const double* y, double* x, 
     A.x = x;
     A.s = nrhs;
     A.fac_shared = 1;
+    A.G_ = choose_groups(f->nb, 128);   // several right-hand sides per block: <= 4 consumer warps
     if (f->l_implicit) A.W = f->d_Wrhs;
     A.epoch = ++f->epoch;
     switch (nrhs) {
