@@ -499,6 +499,39 @@ __global__ void k_reduce_max(const double* partials, int nblk, double* out) {
     if (threadIdx.x == 0) *out = t;
 }
 
+// Host-side waits of the GMRES loop (one per iteration: the reference's convergence
+// test needs |g_{j+1}| on the host).  Results land in a pinned per-thread buffer (a
+// truly asynchronous D2H) and completion is detected by spinning on an event, which
+// wakes the host within ~1 us instead of a blocking stream synchronisation.
+struct HostSync {
+    double* pin = nullptr;
+    size_t cap = 0;
+    cudaEvent_t ev = nullptr;
+};
+
+static int host_sync_get(HostSync*& hs, size_t doubles) {
+    static thread_local HostSync tls;   // per host thread: the C ABI stays reentrant
+    hs = &tls;
+    if (!tls.ev) IRK_CK(cudaEventCreateWithFlags(&tls.ev, cudaEventDisableTiming));
+    if (tls.cap < doubles) {
+        if (tls.pin) cudaFreeHost(tls.pin);
+        tls.pin = nullptr;
+        tls.cap = 0;
+        IRK_CK(cudaMallocHost(&tls.pin, sizeof(double) * doubles));
+        tls.cap = doubles;
+    }
+    return IRK_OK;
+}
+
+static int host_wait(HostSync* hs, cudaStream_t st) {
+    IRK_CK(cudaEventRecord(hs->ev, st));
+    cudaError_t e;
+    while ((e = cudaEventQuery(hs->ev)) == cudaErrorNotReady) {
+    }
+    if (e != cudaSuccess) return fail_cuda(e, "cudaEventQuery", __FILE__, __LINE__);
+    return IRK_OK;
+}
+
 struct Workspace {
     double* V = nullptr;
     double* tmp = nullptr;
@@ -686,7 +719,9 @@ int irk_gmres(irk_ctx* ctx, int64_t n, irk_linop op, irk_linop pre, irk_allreduc
     double* ndev = ws.small + (restart + 2);       // 2
     double* cdev = ws.small + 2 * (restart + 4);   // restart+1 coefficients
     double* fdev = ws.small + 3 * (restart + 4);   // fused CGS2 outputs, 2 (restart+1) + 2
-    std::vector<double> hbuf(2 * (restart + 4));
+    HostSync* hs = nullptr;
+    IRK_TRY(host_sync_get(hs, 2 * (restart + 4)));
+    double* hbuf = hs->pin;
     auto V = [&](int i) { return ws.V + (int64_t)i * ldV; };
     const int g1 = grid_1d(ctx, n);
 
@@ -710,11 +745,10 @@ int irk_gmres(irk_ctx* ctx, int64_t n, irk_linop op, irk_linop pre, irk_allreduc
     auto norm = [&](const double* v, double& nrm, double* mx) -> int {
         IRK_TRY(norm_max(ctx, n, v, ws.partials, ndev, st));
         IRK_TRY(ar(ndev, 1));
-        double h2[2];
-        IRK_CK(cudaMemcpyAsync(h2, ndev, sizeof h2, cudaMemcpyDeviceToHost, st));
-        IRK_CK(cudaStreamSynchronize(st));
-        nrm = std::sqrt(h2[0]);
-        if (mx) *mx = h2[1];
+        IRK_CK(cudaMemcpyAsync(hbuf, ndev, 2 * sizeof(double), cudaMemcpyDeviceToHost, st));
+        IRK_TRY(host_wait(hs, st));
+        nrm = std::sqrt(hbuf[0]);
+        if (mx) *mx = hbuf[1];
         return IRK_OK;
     };
     auto true_residual = [&](double& res) -> int {
@@ -786,9 +820,9 @@ int irk_gmres(irk_ctx* ctx, int64_t n, irk_linop op, irk_linop pre, irk_allreduc
                 // 128-bit fused CGS2 + normalisation (3 passes), one host sync
                 const int nv = j + 1;
                 IRK_TRY(cgs2_v(ctx, n, ldV, nv, ws.V, w, eta, brk, ws.partials, ws.counters, fdev, st));
-                IRK_CK(cudaMemcpyAsync(hbuf.data(), fdev, sizeof(double) * (2 * (nv + 1) + 3),
+                IRK_CK(cudaMemcpyAsync(hbuf, fdev, sizeof(double) * (2 * (nv + 1) + 3),
                                        cudaMemcpyDeviceToHost, st));
-                IRK_CK(cudaStreamSynchronize(st));
+                IRK_TRY(host_wait(hs, st));
                 const bool reorth = hbuf[2 * (nv + 1) + 1] != 0.0;
                 for (int i = 0; i <= j; ++i) Hc(i, j) = hbuf[i] + (reorth ? hbuf[nv + 1 + i] : 0.0);
                 if (reorth) stats->reorth_passes += 1;
@@ -802,9 +836,9 @@ int irk_gmres(irk_ctx* ctx, int64_t n, irk_linop op, irk_linop pre, irk_allreduc
                 // fused CGS2 (3 passes, DGKS decided on the device), one host sync
                 const int nv = j + 1;
                 IRK_TRY(cgs2_fused(ctx, n, ldV, nv, ws.V, w, eta, ws.partials, ws.counters, fdev, st));
-                IRK_CK(cudaMemcpyAsync(hbuf.data(), fdev, sizeof(double) * (2 * (nv + 1) + 2),
+                IRK_CK(cudaMemcpyAsync(hbuf, fdev, sizeof(double) * (2 * (nv + 1) + 2),
                                        cudaMemcpyDeviceToHost, st));
-                IRK_CK(cudaStreamSynchronize(st));
+                IRK_TRY(host_wait(hs, st));
                 const bool reorth = hbuf[2 * (nv + 1) + 1] != 0.0;
                 for (int i = 0; i <= j; ++i) Hc(i, j) = hbuf[i] + (reorth ? hbuf[nv + 1 + i] : 0.0);
                 if (reorth) stats->reorth_passes += 1;
@@ -815,10 +849,11 @@ int irk_gmres(irk_ctx* ctx, int64_t n, irk_linop op, irk_linop pre, irk_allreduc
             IRK_TRY(ar(hdev, j + 2));
             IRK_TRY(update(ctx, n, j + 1, ws.V, ldV, hdev, w, ws.partials, ndev, st));
             IRK_TRY(ar(ndev, 1));
-            IRK_CK(cudaMemcpyAsync(hbuf.data(), hdev, sizeof(double) * (j + 2), cudaMemcpyDeviceToHost, st));
+            IRK_CK(cudaMemcpyAsync(hbuf, hdev, sizeof(double) * (j + 2), cudaMemcpyDeviceToHost, st));
             double nrm2;
-            IRK_CK(cudaMemcpyAsync(&nrm2, ndev, sizeof(double), cudaMemcpyDeviceToHost, st));
-            IRK_CK(cudaStreamSynchronize(st));
+            IRK_CK(cudaMemcpyAsync(hbuf + (restart + 3), ndev, sizeof(double), cudaMemcpyDeviceToHost, st));
+            IRK_TRY(host_wait(hs, st));
+            nrm2 = hbuf[restart + 3];
             const double norm_before = std::sqrt(hbuf[j + 1]);
             for (int i = 0; i <= j; ++i) Hc(i, j) = hbuf[i];
             nw = std::sqrt(nrm2);
@@ -828,9 +863,10 @@ int irk_gmres(irk_ctx* ctx, int64_t n, irk_linop op, irk_linop pre, irk_allreduc
                 IRK_TRY(ar(hdev, j + 2));
                 IRK_TRY(update(ctx, n, j + 1, ws.V, ldV, hdev, w, ws.partials, ndev, st));
                 IRK_TRY(ar(ndev, 1));
-                IRK_CK(cudaMemcpyAsync(hbuf.data(), hdev, sizeof(double) * (j + 2), cudaMemcpyDeviceToHost, st));
-                IRK_CK(cudaMemcpyAsync(&nrm2, ndev, sizeof(double), cudaMemcpyDeviceToHost, st));
-                IRK_CK(cudaStreamSynchronize(st));
+                IRK_CK(cudaMemcpyAsync(hbuf, hdev, sizeof(double) * (j + 2), cudaMemcpyDeviceToHost, st));
+                IRK_CK(cudaMemcpyAsync(hbuf + (restart + 3), ndev, sizeof(double), cudaMemcpyDeviceToHost, st));
+                IRK_TRY(host_wait(hs, st));
+                nrm2 = hbuf[restart + 3];
                 for (int i = 0; i <= j; ++i) Hc(i, j) += hbuf[i];
                 nw = std::sqrt(nrm2);
                 stats->reorth_passes += 1;
