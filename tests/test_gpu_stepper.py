@@ -125,3 +125,28 @@ def test_partition_study_iterations_grow_with_p():
     its = [r.gmres_iters_avg for r in recs]
     assert all(r.converged for r in recs)
     assert its[-1] >= its[0], its
+
+
+def test_stepper_argument_errors_and_newton_failure():
+    """stepper.py:140-143, 241-244 (dt > 0, scheme kind) and the NewtonError of the
+    shared skeleton (stepper.py:119-120) with an unreachable tolerance."""
+    from paper_1701_07181_b200.blocks import DevicePattern
+    from paper_1701_07181_b200.stepper import (LinearProblem, NewtonConfig, NewtonError, PrecondSpec,
+                                               dirk_step, irk_step_transformed)
+    cfg = W.CONFIGS[1].scaled(N=4, nb=6)
+    wl = W.make_workload(cfg, norm_iters=10)
+    p = wl.pattern
+    prob = LinearProblem(DevicePattern(p.indptr, p.indices, p.diag_pos), wl.J, wl.M)
+    u0 = np.random.default_rng(1).standard_normal(prob.n)
+    with pytest.raises(ValueError):
+        irk_step_transformed(prob, "RADAU23", u0, 0.0, 0.0)
+    with pytest.raises(ValueError):
+        irk_step_transformed(prob, "DIRK33", u0, 0.0, wl.dt)
+    with pytest.raises(ValueError):
+        dirk_step(prob, "RADAU23", u0, 0.0, wl.dt)
+    with pytest.raises(ValueError):
+        PrecondSpec(kind="bogus")
+    with pytest.raises(NewtonError) as ei:
+        irk_step_transformed(prob, "RADAU23", u0, 0.0, wl.dt, PrecondSpec("coupled"),
+                             NewtonConfig(abs_tol_inf=1e-300, max_iters=1))
+    assert len(ei.value.residual_history) == 2
