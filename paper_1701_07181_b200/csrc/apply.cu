@@ -772,9 +772,21 @@ __global__ void __launch_bounds__(288) k_unc_bwd_pipe(ApplyArgs A, PipeCfg PC) {
         if (lane == 0) pr.push(make_int4(-1, 0, PD_END, 0), nullptr);
         return;
     }
+    // Consumers: warp-shuffle reduction layout.  G (1, 2 or 4) groups split the column
+    // pairs; warp w holds rows [R w, R w + R), R = 32 / G, lane = g R + (row - R w): every
+    // quarter-warp reads 8 distinct block rows (conflict-free 128-bit LDS) and the G partial
+    // sums of a row sit in lanes R apart (shfl_xor reduction, no shared-memory buffer).
     const int c = threadIdx.x - 32;
+    const int G = A.G_, R = 32 / G;
     Geo q;
-    q.nb = nb; q.P = (nb + 1) >> 1; q.G = A.G_; q.g = c / nb; q.a = c - q.g * nb; q.active = q.g < q.G;
+    q.nb = nb; q.P = (nb + 1) >> 1; q.G = G;
+    q.a = R * (c >> 5) + (c & (R - 1));
+    q.g = (c & 31) / R;
+    q.active = q.a < nb;
+    auto group_sum = [&](double v) -> double {
+        for (int o = R; o < 32; o <<= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+        return v;
+    };
     Consumer cs{&P, &PC};
     griddep_wait();
     double part[S];
@@ -784,7 +796,7 @@ __global__ void __launch_bounds__(288) k_unc_bwd_pipe(ApplyArgs A, PipeCfg PC) {
         const int4 dsc = cs.take();
         if (dsc.z & PD_END) break;
         const int64_t i = dsc.x;     // element id and upper-neighbour count from the descriptor
-        double* red = P.red + (size_t)par * q.G * S * nb;
+        double* tv = P.red + (size_t)par * S * nb;       // t of this task (task-parity double buffer)
         const int nup = dsc.w >> 2;                     // neighbour count: own segment index
         const bool store_z = FWDI && ((dsc.w >> 1) & 1);  // FWDI row with a backward task
         if (dsc.z & PD_FIRST) {
@@ -814,27 +826,21 @@ __global__ void __launch_bounds__(288) k_unc_bwd_pipe(ApplyArgs A, PipeCfg PC) {
                     for (int k = 0; k < S; ++k) A.x[k * A.n + i * nb + q.a] = xs[(nup * S + k) * nb + q.a];
             } else if (kk == 0) {
                 // t_k = z_{i,k} - uscale * sum_j U_ij x_{j,k}  (all stages)
-                if (q.active)
 #pragma unroll
-                    for (int k = 0; k < S; ++k) red[(q.g * S + k) * nb + q.a] = part[k];
-                consumer_sync(1, ncons);
-                if (q.active && q.g == 0) {
-#pragma unroll
-                    for (int k = 0; k < S; ++k) {
-                        double sum = 0.0;
-                        for (int gg = 0; gg < q.G; ++gg) sum += red[(gg * S + k) * nb + q.a];
+                for (int k = 0; k < S; ++k) {
+                    const double sum = group_sum(part[k]);
+                    if (q.active && q.g == 0) {
                         const double tval = xs[(nup * S + k) * nb + q.a] - A.uscale * sum;
-                        P.tv[k * nb + q.a] = tval;
+                        tv[k * nb + q.a] = tval;
                         if (store_z) A.x[k * A.n + i * nb + q.a] = tval;   // z_i for the backward sweep
                     }
+                    part[k] = 0.0;
                 }
                 consumer_sync(1, ncons);
-#pragma unroll
-                for (int k = 0; k < S; ++k) part[k] = 0.0;
             }
             if (q.active) {
                 const bool direct = (dsc.w & 1) != 0;
-                const double* xv = direct ? xs + nup * S * nb : P.tv;
+                const double* xv = direct ? xs + nup * S * nb : tv;
                 if (dsc.z & PD_SH) {
                     smem_gemv_all<S>(B, xv, q, part);
                 } else {
@@ -847,17 +853,10 @@ __global__ void __launch_bounds__(288) k_unc_bwd_pipe(ApplyArgs A, PipeCfg PC) {
         cs.release();
         if (dsc.z & PD_LAST) {
             par ^= 1;
-            if (q.active)
 #pragma unroll
-                for (int k = 0; k < S; ++k) red[(q.g * S + k) * nb + q.a] = part[k];
-            consumer_sync(1, ncons);
-            if (q.active && q.g == 0) {
-#pragma unroll
-                for (int k = 0; k < S; ++k) {
-                    double sum = 0.0;
-                    for (int gg = 0; gg < q.G; ++gg) sum += red[(gg * S + k) * nb + q.a];
-                    (store_z ? A.W : A.x)[k * A.n + i * nb + q.a] = sum;
-                }
+            for (int k = 0; k < S; ++k) {
+                const double sum = group_sum(part[k]);
+                if (q.active && q.g == 0) (store_z ? A.W : A.x)[k * A.n + i * nb + q.a] = sum;
             }
             cs.x_release();
             if (DEPS) {
@@ -1286,7 +1285,7 @@ constexpr int64_t LEVEL_LAUNCH_MAX = 16;
 
 template <typename K1, typename K2>
 static int run_pipe(const irk_factor* f, K1 kernel_deps, K2 kernel_level, ApplyArgs& A, const irk_sched& S,
-                    unsigned* flags, int* ticket, int s, cudaStream_t st, int extra_doubles = 0) {
+                    unsigned* flags, int* ticket, int s, cudaStream_t st, int extra_doubles = 0, int ctas_target = 4) {
     A.flags = flags;
     A.ticket = ticket;
     const int nb = A.nb;
@@ -1304,7 +1303,9 @@ static int run_pipe(const irk_factor* f, K1 kernel_deps, K2 kernel_level, ApplyA
     // 40x40 block at 4-5 CTAs/SM run at 84% of HBM peak, 7 stages at 2 CTAs/SM
     // at 59%).  IRK_APPLY_NST overrides.
     const size_t per_stage = PC.stage_bytes + 2 * sizeof(uint64_t) + sizeof(int4);
-    const size_t per_cta = (size_t)f->ctx->smem_per_sm / 4 - 1024;
+    static const int ctas_env = getenv("IRK_APPLY_CTAS") ? atoi(getenv("IRK_APPLY_CTAS")) : 0;   // tuning knob
+    const int ctas = ctas_env > 0 ? ctas_env : ctas_target;
+    const size_t per_cta = (size_t)f->ctx->smem_per_sm / ctas - 1024;
     PC.nst = (int)std::max<size_t>(2, std::min<size_t>(24, per_cta > fixed ? (per_cta - fixed) / per_stage : 0));
     if (const char* ns = getenv("IRK_APPLY_NST")) PC.nst = std::max(2, atoi(ns));
     const size_t smem = (size_t)PC.nst * per_stage + fixed;
@@ -1363,8 +1364,22 @@ static int run_sweep(const irk_factor* f, K kernel, ApplyArgs& A, const irk_sche
     return IRK_OK;
 }
 
+// groups of the shuffle-reduction sweep layout (k_unc_bwd_pipe): a power of two
+static int ws_groups(int nb) {
+    static const int force = getenv("IRK_APPLY_WSG") ? atoi(getenv("IRK_APPLY_WSG")) : 0;   // tuning knob
+    if (force == 1 || force == 2 || force == 4) return force;
+    // one thread per block row: small CTAs, many tasks in flight per SM (measured best for
+    // nb <= 64); two groups for the 100-row blocks of config 3
+    return (nb > 64 && nb <= 128) ? 2 : 1;
+}
+// CTAs per SM the shared-memory ring is sized for (2-3 stages each): the sweeps are bound by
+// tasks in flight, not by consumer width (tools/tune_apply.py: 0.57 ms at 6 vs 0.60 ms at 4)
+static int ws_ctas(int G) { return G == 1 ? 6 : 4; }
+
 template <int S, bool EVEN>
-static int unc_apply(const irk_factor* f, ApplyArgs& A, cudaStream_t st) {
+static int unc_apply(const irk_factor* f, ApplyArgs& A0, cudaStream_t st) {
+    ApplyArgs A = A0;
+    A.G_ = ws_groups(A.nb);
     if (EVEN && S <= 4 && A.G_ * A.nb <= 256) {
         const int64_t nf = (int64_t)f->pat->T;
         if (f->l_implicit) {
@@ -1372,16 +1387,20 @@ static int unc_apply(const irk_factor* f, ApplyArgs& A, cudaStream_t st) {
             // finishes rows without upper blocks; the backward sweep covers the remaining rows
             A.flags2 = f->d_flags + nf;
             IRK_TRY(run_pipe(f, k_unc_bwd_pipe<S, true, true>, k_unc_bwd_pipe<S, false, true>, A, f->fwd,
-                             f->d_flags, f->d_ticket, S, st));
+                             f->d_flags, f->d_ticket, S, st, 0, ws_ctas(A.G_)));
             IRK_TRY(run_pipe(f, k_unc_bwd_pipe<S, true, false>, k_unc_bwd_pipe<S, false, false>, A, f->bwd,
-                             f->d_flags + nf, f->d_ticket + 1, S, st));
+                             f->d_flags + nf, f->d_ticket + 1, S, st, 0, ws_ctas(A.G_)));
             return IRK_OK;
         }
-        IRK_TRY(run_pipe(f, k_unc_fwd_pipe<S, true>, k_unc_fwd_pipe<S, false>, A, f->fwd, f->d_flags, f->d_ticket, S, st));
+        if (A0.G_ * A0.nb <= 256)
+            IRK_TRY(run_pipe(f, k_unc_fwd_pipe<S, true>, k_unc_fwd_pipe<S, false>, A0, f->fwd, f->d_flags, f->d_ticket, S, st));
+        else
+            IRK_TRY(run_pipe(f, k_unc_fwd_pipe<S, true>, k_unc_fwd_pipe<S, false>, A, f->fwd, f->d_flags, f->d_ticket, S, st));
         IRK_TRY(run_pipe(f, k_unc_bwd_pipe<S, true, false>, k_unc_bwd_pipe<S, false, false>, A, f->bwd, f->d_flags + nf,
-                         f->d_ticket + 1, S, st));
+                         f->d_ticket + 1, S, st, 0, ws_ctas(A.G_)));
         return IRK_OK;
     }
+    A = A0;
     const int threads = ((A.G_ * A.nb + 31) / 32) * 32;
     const size_t smem_f = sizeof(double) * A.G_ * S * A.nb;
     const size_t smem_b = smem_f + sizeof(double) * S * A.nb;
