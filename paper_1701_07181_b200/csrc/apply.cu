@@ -1379,7 +1379,9 @@ static int ws_ctas(int G) { return G == 1 ? 6 : 4; }
 template <int S, bool EVEN>
 static int unc_apply(const irk_factor* f, ApplyArgs& A0, cudaStream_t st) {
     ApplyArgs A = A0;
-    A.G_ = ws_groups(A.nb);
+    // deep DAGs (persistent, flag-synchronised sweeps) prefer fewer, wider CTAs
+    const bool deep = f->fwd.nlevels > LEVEL_LAUNCH_MAX || f->bwd.nlevels > LEVEL_LAUNCH_MAX;
+    A.G_ = deep ? (A.nb <= 64 ? 4 : (A.nb <= 128 ? 2 : 1)) : ws_groups(A.nb);
     if (EVEN && S <= 4 && A.G_ * A.nb <= 256) {
         const int64_t nf = (int64_t)f->pat->T;
         if (f->l_implicit) {
