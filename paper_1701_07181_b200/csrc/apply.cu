@@ -1304,9 +1304,10 @@ static int run_pipe(const irk_factor* f, K1 kernel_deps, K2 kernel_level, ApplyA
     // at 59%).  IRK_APPLY_NST overrides.
     const size_t per_stage = PC.stage_bytes + 2 * sizeof(uint64_t) + sizeof(int4);
     static const int ctas_env = getenv("IRK_APPLY_CTAS") ? atoi(getenv("IRK_APPLY_CTAS")) : 0;   // tuning knob
-    const int ctas = ctas_env > 0 ? ctas_env : ctas_target;
+    const int ctas = ctas_env > 0 ? ctas_env : std::max(ctas_target, 1);
     const size_t per_cta = (size_t)f->ctx->smem_per_sm / ctas - 1024;
     PC.nst = (int)std::max<size_t>(2, std::min<size_t>(24, per_cta > fixed ? (per_cta - fixed) / per_stage : 0));
+    if (ctas_target <= 0 && ctas_env <= 0) PC.nst = 2;   // as many 2-stage CTAs as fit (occupancy-limited grid)
     if (const char* ns = getenv("IRK_APPLY_NST")) PC.nst = std::max(2, atoi(ns));
     const size_t smem = (size_t)PC.nst * per_stage + fixed;
     // PDL for the uncoupled sweeps only: measured 7.8 -> 9.1 ms per RADAU23 coupled step with it
@@ -1374,7 +1375,7 @@ static int ws_groups(int nb) {
 }
 // CTAs per SM the shared-memory ring is sized for (2-3 stages each): the sweeps are bound by
 // tasks in flight, not by consumer width (tools/tune_apply.py: 0.57 ms at 6 vs 0.60 ms at 4)
-static int ws_ctas(int G) { return G == 1 ? 6 : 4; }
+static int ws_ctas(int G) { return G == 1 ? 0 : 4; }   // 0: 2-stage rings, occupancy-limited
 
 template <int S, bool EVEN>
 static int unc_apply(const irk_factor* f, ApplyArgs& A0, cudaStream_t st) {
