@@ -271,7 +271,12 @@ static int launch_pipe(const irk_stage_op* op, MatvecArgs& A, const MixParams& C
     const int cons_threads = ((A.G * nb + 31) / 32) * 32;
     const int threads = 32 + cons_threads;
     const size_t red_bytes = sizeof(double) * A.G * 2 * S * nb;
-    const size_t budget = 100 * 1024;
+    // ring budget per CTA: about two stages' worth of consumer work per S vectors -- small
+    // blocks / few vectors run best as many small CTAs (config 3: nb=24 67% -> 96% of peak),
+    // the s=3 nb=40 benchmark operator with ~7 stages per CTA (tools/sweep.py config3)
+    static const int budget_kb = getenv("IRK_MATVEC_BUDGET_KB") ? atoi(getenv("IRK_MATVEC_BUDGET_KB")) : 0;   // tuning knob
+    const size_t budget = budget_kb > 0 ? (size_t)budget_kb * 1024
+                                        : std::min<size_t>(100 * 1024, std::max<size_t>(20 * 1024, (size_t)2 * S * PG.stage_bytes));
     PG.nst = (int)std::max<size_t>(2, std::min<size_t>(16, (budget - red_bytes) / PG.stage_bytes));
     const size_t smem = (size_t)PG.nst * PG.stage_bytes + 2 * sizeof(uint64_t) * PG.nst + red_bytes;
     static bool attr = false;
