@@ -95,6 +95,13 @@ IRK_API int irk_stage_op_create(irk_ctx *ctx, const irk_pattern *pat, int s, con
                         double alpha, irk_stage_op **out);
 IRK_API void irk_stage_op_destroy(irk_stage_op *op);
 IRK_API int irk_stage_op_apply(const irk_stage_op *op, const double *w, double *y, void *stream);
+/* Rows [row_lo, row_hi) of y = B w (the rest of y untouched): the interior rows of a
+ * slab, computed while its halo is in flight (multi-GPU). */
+IRK_API int irk_stage_op_apply_range(const irk_stage_op *op, const double *w, double *y, int64_t row_lo,
+                                     int64_t row_hi, void *stream);
+/* Rows rows[0..nrows) (device int32 list) of y = B w: the slab's boundary rows. */
+IRK_API int irk_stage_op_apply_rows(const irk_stage_op *op, const double *w, double *y, const int32_t *rows,
+                                    int64_t nrows, void *stream);
 /* element-partitioned operator: rows [0,T_local) of the pattern are local,
  * column indices >= T_local address `ghost` ((s, n_ghost, nb) device array) */
 IRK_API int irk_stage_op_set_halo(irk_stage_op *op, int64_t T_local, const double *ghost, int64_t n_ghost);

@@ -7,6 +7,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <vector>
 
 #include "blockops.cuh"
 #include "irk_internal.cuh"
@@ -30,6 +31,7 @@ struct MatvecArgs {
     const double* ghost;               // halo values (s, n_ghost, nb) or NULL
     const int32_t* rows;               // row subset or NULL (all rows)
     int64_t nrows;
+    int64_t row_lo, row_hi;            // pipelined kernel: contiguous row range
     int64_t n;                         // T_local * nb (stage stride of w, y)
     int64_t T_local;
     int64_t n_ghost;
@@ -116,8 +118,8 @@ __global__ void __launch_bounds__(288) k_stage_matvec_pipe(MatvecArgs A, MixPara
     double* red = reinterpret_cast<double*>(empty + PG.nst);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int ncons_warps = (blockDim.x >> 5) - 1;
-    const int64_t T = A.T_local;
-    const int64_t r0 = T * blockIdx.x / gridDim.x, r1 = T * (blockIdx.x + 1) / gridDim.x;
+    const int64_t T = A.row_hi - A.row_lo;
+    const int64_t r0 = A.row_lo + T * blockIdx.x / gridDim.x, r1 = A.row_lo + T * (blockIdx.x + 1) / gridDim.x;
     if (threadIdx.x == 0) {
         for (int i = 0; i < PG.nst; ++i) {
             mbar_init(full + i, 1);
@@ -287,7 +289,8 @@ static int launch_pipe(const irk_stage_op* op, MatvecArgs& A, const MixParams& C
     }
     int per_sm = 1;
     IRK_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_stage_matvec_pipe<S, SHARED>, threads, smem));
-    const int64_t grid = std::max<int64_t>(1, std::min<int64_t>(A.T_local, (int64_t)op->ctx->num_sms * std::max(per_sm, 1)));
+    if (A.row_hi <= A.row_lo) return IRK_OK;
+    const int64_t grid = std::max<int64_t>(1, std::min<int64_t>(A.row_hi - A.row_lo, (int64_t)op->ctx->num_sms * std::max(per_sm, 1)));
     IRK_CK(launch_pdl(k_stage_matvec_pipe<S, SHARED>, dim3((unsigned)grid), dim3(threads), smem, st, A, C, PG));
     IRK_LAUNCHED();
     return IRK_OK;
@@ -331,8 +334,10 @@ static int launch_s(const irk_stage_op* op, MatvecArgs& A, const MixParams& C, c
 }
 
 int stage_op_apply_rows(const irk_stage_op* op, const double* w, double* y, const int32_t* rows,
-                        int64_t nrows, cudaStream_t st) {
+                        int64_t nrows, cudaStream_t st, int64_t row_lo = 0, int64_t row_hi = -1) {
     MatvecArgs A{};
+    A.row_lo = row_lo;
+    A.row_hi = row_hi < 0 ? op->T_local : row_hi;
     A.indptr = op->pat->d_indptr;
     A.indices = op->pat->d_indices;
     for (int k = 0; k < op->s; ++k) A.J[k] = op->J[k]->d + op->jfirst[k] * block_doubles(op->nb);
@@ -414,6 +419,33 @@ int irk_stage_op_set_halo(irk_stage_op* op, int64_t T_local, const double* ghost
 int irk_stage_op_apply(const irk_stage_op* op, const double* w, double* y, void* stream) {
     IRK_ARG(op && w && y, "NULL argument");
     return stage_op_apply_rows(op, w, y, nullptr, op->T_local, (cudaStream_t)stream);
+}
+
+int irk_stage_op_apply_range(const irk_stage_op* op, const double* w, double* y, int64_t row_lo, int64_t row_hi,
+                             void* stream) {
+    IRK_ARG(op && w && y, "NULL argument");
+    IRK_ARG(0 <= row_lo && row_lo <= row_hi && row_hi <= op->T_local, "row range out of bounds");
+    if (row_hi == row_lo) return IRK_OK;
+    const bool pipe_ok = op->nb % 2 == 0 && op->s <= 4 && choose_groups(op->nb, 256) * op->nb <= 256;
+    if (pipe_ok) return stage_op_apply_rows(op, w, y, nullptr, row_hi - row_lo, (cudaStream_t)stream, row_lo, row_hi);
+    // generic kernel: an explicit row list
+    int32_t* d = nullptr;
+    std::vector<int32_t> rows(row_hi - row_lo);
+    for (int64_t r = row_lo; r < row_hi; ++r) rows[r - row_lo] = (int32_t)r;
+    cudaStream_t st = (cudaStream_t)stream;
+    IRK_CK(cudaMallocAsync(&d, sizeof(int32_t) * rows.size(), st));
+    IRK_CK(cudaMemcpyAsync(d, rows.data(), sizeof(int32_t) * rows.size(), cudaMemcpyHostToDevice, st));
+    const int rc = stage_op_apply_rows(op, w, y, d, (int64_t)rows.size(), st);
+    IRK_CK(cudaStreamSynchronize(st));   // host row list goes out of scope
+    cudaFreeAsync(d, st);
+    return rc;
+}
+
+int irk_stage_op_apply_rows(const irk_stage_op* op, const double* w, double* y, const int32_t* rows, int64_t nrows,
+                            void* stream) {
+    IRK_ARG(op && w && y && (rows || nrows == 0), "NULL argument");
+    if (nrows == 0) return IRK_OK;
+    return stage_op_apply_rows(op, w, y, rows, nrows, (cudaStream_t)stream);
 }
 
 }  // extern "C"

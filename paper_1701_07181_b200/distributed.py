@@ -157,9 +157,10 @@ class HaloExchange:
         self.recv_buf = {p: torch.empty((s, len(v), nb), dtype=torch.float64, device=device)
                          for p, v in plan.recv.items()}
 
-    def exchange(self, x, ghost) -> None:
+    def start(self, x):
+        """Pack and post the sends / receives; returns the pending work handles."""
         if self.plan.n_ghost == 0 and not self.send_idx:
-            return
+            return []
         dist = self.torch.distributed
         xv = x.view(self.s, self.plan.T_local, self.nb)
         ops = []
@@ -168,12 +169,20 @@ class HaloExchange:
             ops.append(dist.P2POp(dist.isend, self.send_buf[p], p, self.group))
         for p in self.recv_idx:
             ops.append(dist.P2POp(dist.irecv, self.recv_buf[p], p, self.group))
-        if ops:
-            for r in dist.batch_isend_irecv(ops):
-                r.wait()
+        return dist.batch_isend_irecv(ops) if ops else []
+
+    def finish(self, works, ghost) -> None:
+        """Wait for the posted exchange and scatter the received values into ``ghost``."""
+        for r in works:
+            r.wait()
+        if self.plan.n_ghost == 0:
+            return
         gv = ghost.view(self.s, self.plan.n_ghost, self.nb)
         for p, idx in self.recv_idx.items():
             gv.index_copy_(1, idx, self.recv_buf[p])
+
+    def exchange(self, x, ghost) -> None:
+        self.finish(self.start(x), ghost)
 
 
 def allreduce_sum(buf, group=None) -> None:
@@ -230,8 +239,14 @@ class DistributedStageSolver:
         self.ghost = torch.zeros(max(s * ng * nb, 1), dtype=torch.float64, device="cuda")
         L.check(L.lib().irk_stage_op_set_halo(self.op._op.handle, Tl, self.ghost.data_ptr(), ng),
                 "irk_stage_op_set_halo")
-        # exchange(w_local, ghost) fills the ghost buffer; default: NCCL send/recv
-        self.exchange = exchange or HaloExchange(plan, s, nb, "cuda", group).exchange
+        # exchange(w_local, ghost) fills the ghost buffer; default: NCCL send/recv, overlapped
+        # with the interior rows (plan.interior: rows without a ghost column)
+        self.halo = None if exchange is not None else HaloExchange(plan, s, nb, "cuda", group)
+        self.exchange = exchange or self.halo.exchange
+        r0, r1 = plan.interior
+        boundary = np.concatenate([np.arange(0, r0), np.arange(r1, Tl)]).astype(np.int32)
+        self.interior = (int(r0), int(r1))
+        self.boundary = torch.as_tensor(boundary, device="cuda")
         # factor operator: local blocks only (cross-partition blocks are dropped)
         self.fac_pat = DevicePattern(plan.loc_indptr, plan.loc_indices, plan.loc_diag)
         fj = DeviceBlocks.from_host(np.ascontiguousarray(J_rows[plan.loc_block_src - plan.q0]))
@@ -254,10 +269,19 @@ class DistributedStageSolver:
         return self.fac
 
     def matvec(self, w):
-        """Halo exchange, then this rank's rows of B w."""
-        self.exchange(w, self.ghost)
+        """This rank's rows of B w.  With the NCCL halo the exchange is posted first,
+        the interior rows (no ghost column) are computed while it is in flight, then
+        the boundary rows once the ghosts have arrived."""
         y = self.torch_empty()
-        self.op.apply_device(w, y)
+        if self.halo is None or self.plan.n_ghost == 0:
+            self.exchange(w, self.ghost)
+            self.op.apply_device(w, y)
+            return y
+        works = self.halo.start(w)
+        r0, r1 = self.interior
+        self.op.apply_device_range(w, y, r0, r1)
+        self.halo.finish(works, self.ghost)
+        self.op.apply_device_rows(w, y, self.boundary)
         return y
 
     def torch_empty(self):

@@ -90,6 +90,16 @@ class StageOperator:
         L.check(L.lib().irk_stage_op_apply(self._op.handle, w.data_ptr(), y.data_ptr(),
                                            L.stream_ptr()), "irk_stage_op_apply")
 
+    def apply_device_range(self, w, y, row_lo: int, row_hi: int) -> None:
+        """Rows [row_lo, row_hi) of y = B w (multi-GPU interior rows)."""
+        L.check(L.lib().irk_stage_op_apply_range(self._op.handle, w.data_ptr(), y.data_ptr(), int(row_lo),
+                                                 int(row_hi), L.stream_ptr()), "irk_stage_op_apply_range")
+
+    def apply_device_rows(self, w, y, rows) -> None:
+        """Rows ``rows`` (CUDA int32 tensor) of y = B w (multi-GPU boundary rows)."""
+        L.check(L.lib().irk_stage_op_apply_rows(self._op.handle, w.data_ptr(), y.data_ptr(), rows.data_ptr(),
+                                                rows.numel(), L.stream_ptr()), "irk_stage_op_apply_rows")
+
     def matvec(self, w, counter: OpCounter | None = None):
         if tuple(w.shape) != (self.total_dim,):
             raise ValueError(f"expected vector of length {self.total_dim}, got {tuple(w.shape)}")

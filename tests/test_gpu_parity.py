@@ -479,3 +479,29 @@ def test_coupled_pipe_vs_oracle(scheme, m, ordering):
     keep = np.ones(p.nnzb, bool)
     xp = be.coupled_solve(p.indptr, p.indices, p.diag_pos, cf.fstage, cf.fcoupling, cf.dinv, keep, y)
     assert rel(xp, xo) < TOL
+
+
+@pytest.mark.parametrize("nb", [8, 5])
+def test_stage_matvec_row_range_and_list(nb):
+    """irk_stage_op_apply_range (pipelined kernel on a contiguous row range, the
+    slab interior of the multi-GPU matvec) + irk_stage_op_apply_rows (row list, the
+    boundary) reproduce the full fused matvec bitwise."""
+    import torch
+    from paper_1701_07181_b200.blocks import BlockDiagonalMatrix, BlockSparseMatrix, DeviceBlocks, DevicePattern
+    from paper_1701_07181_b200.stage_system import StageOperator
+    cfg = W.CONFIGS[1].scaled(N=6, nb=nb)
+    wl = W.make_workload(cfg, norm_iters=10)
+    p = wl.pattern
+    J = BlockSparseMatrix(DevicePattern(p.indptr, p.indices, p.diag_pos), DeviceBlocks.from_host(wl.J))
+    op = StageOperator(_Der(wl.a_inv), wl.dt, BlockDiagonalMatrix(wl.M), [J] * cfg.s)
+    w = torch.from_numpy(np.random.default_rng(nb).standard_normal(op.total_dim)).cuda()
+    y_full = torch.empty_like(w)
+    op.apply_device(w, y_full)
+    r0, r1 = 7, p.T - 11
+    y = torch.full_like(w, float("nan"))
+    op.apply_device_range(w, y, r0, r1)
+    rest = torch.tensor(list(range(0, r0)) + list(range(r1, p.T)), dtype=torch.int32, device="cuda")
+    op.apply_device_rows(w, y, rest)
+    yf, yy = y_full.view(cfg.s, p.T, nb), y.view(cfg.s, p.T, nb)
+    assert torch.equal(yy[:, r0:r1], yf[:, r0:r1])
+    assert rel(yy.cpu().numpy(), yf.cpu().numpy()) < 1e-15
