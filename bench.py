@@ -405,13 +405,16 @@ def run_b200(args):
     roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                 "frac": achieved / peak, "traffic": traffic, "kernel": dom["name"],
                 "algorithmic_bytes_per_launch": dom["bytes"], "avg_launch_ms": 1e3 * dom["t"],
-                "share_of_step": dom["share"], "peak_source": peak_src}
+                "share_of_step": dom["share"], "peak_source": peak_src,
+                # DRAM bytes (ncu, profiles/) over the event-timed launch: wasted re-reads show here
+                "traffic_GBps": (traffic / dom["t"] / 1e9) if traffic else None}
     components = {
         "matvec_ms": 1e3 * t_mv, "matvec_GBps": bm / t_mv / 1e9, "matvec_frac": bm / t_mv / 1e9 / peak,
         "apply_ms": 1e3 * t_ap,
         "apply_GBps": (ba / t_ap / 1e9) if ba else None,
         "apply_frac": (ba / t_ap / 1e9 / peak) if ba else None,
         "factor_ms": 1e3 * t_fac, "gmres_ms": 1e3 * t_sol, "gmres_iterations": iters[-1],
+        "gmres_ms_per_iteration": 1e3 * t_sol / max(iters[-1], 1),
         "levels_fwd_bwd": list(solver.fac.levels()) if solver.fac is not None else None,
         "jnorm2": jnorm, "dt": dt,
     }
