@@ -1478,6 +1478,7 @@ static void fill_args(const irk_factor* f, ApplyArgs& A) {
 }
 
 int factor_materialize_L(const irk_factor* f, double** out, cudaStream_t st);   // factor.cu
+int factor_form_level0_d(const irk_factor* f, cudaStream_t st);                // factor.cu
 
 int factor_apply(const irk_factor* f, const double* y, double* x, cudaStream_t st) {
     ApplyArgs A{};
@@ -1613,6 +1614,7 @@ int irk_factor_export(const irk_factor* f, double* fstage, double* dinv, double*
     IRK_ARG(f, "NULL factor");
     IRK_ARG(f->d_D || !fstage, "factor was created without store_diag");
     cudaStream_t st = (cudaStream_t)stream;
+    if (fstage) IRK_TRY(factor_form_level0_d(f, st));
     const irk_pattern* p = f->pat;
     const int s = f->s, nb = f->nb;
     const int64_t bsz = block_doubles(nb), T = p->T, nnzb = p->nnzb;

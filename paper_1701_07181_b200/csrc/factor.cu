@@ -892,7 +892,7 @@ static int launch_schur(const irk_ctx* ctx, const FactorArgs& F, const int32_t* 
 
 int launch_inverse(const irk_ctx* ctx, const int32_t* tasks, int64_t ntasks, int64_t T, int s, int nb,
                    const double* D, double* Dinv, unsigned long long* fail_key, int* fb, cudaStream_t st,
-                   int cap_per_sm = 0);
+                   int cap_per_sm = 0, const InvForm* form = nullptr);
 
 static int env_int(const char* name, int dflt) {
     const char* e = getenv(name);
@@ -926,7 +926,23 @@ static int launch_levels(const irk_factor* f, FactorArgs& F, const irk_sched& sc
             static const int nchunk = env_int("IRK_FACTOR_CHUNKS", 1);   // measured: no gain at config 1
             static const int schur_cap = env_int("IRK_SCHUR_CAP", 2);
             static const int inv_cap = env_int("IRK_INV_CAP", 1);
-            if (l == 0 || nchunk <= 1 || ne < 4 * (int64_t)f->ctx->num_sms) {
+            static const bool form_off = env_int("IRK_FORM_D", 1) == 0;
+            if (l == 0 && F.L == nullptr && !F.literal && F.nb > 16 && F.nb <= 64 && f->d_fb && !form_off) {
+                // level 0 has no Schur update: the inverse kernel forms D = alpha J_jj + coef_k M_j itself
+                InvForm fm;
+                fm.J = F.J[0];
+                fm.diag = F.diag;
+                fm.keep = F.keep;
+                fm.M = F.M;
+                fm.Dst = F.Dst;
+                fm.alpha = F.alpha;
+                for (int k = 0; k < F.s; ++k) fm.coef[k] = F.coef[k];
+                fm.store = f->store_d ? 1 : 0;
+                IRK_TRY(launch_inverse(f->ctx, tk, ne * F.s, F.T, F.s, F.nb, F.Dst, F.Dinv, F.fail_key, f->d_fb, st,
+                                       0, &fm));
+                f->d0_unstored = !f->store_d;
+            } else if (l == 0 || nchunk <= 1 || ne < 4 * (int64_t)f->ctx->num_sms) {
+                if (l == 0) f->d0_unstored = false;
                 IRK_TRY(launch_schur(f->ctx, F, el, ne, st));
                 IRK_TRY(launch_inverse(f->ctx, tk, ne * F.s, F.T, F.s, F.nb, F.Dst, F.Dinv, F.fail_key, f->d_fb, st));
             } else {
@@ -1108,6 +1124,7 @@ static int factor_common(irk_ctx* ctx, const irk_pattern* pat, const FactorSetup
     auto fail = [&](int code) { irk_factor_destroy(f); return code; };
 #define FCK(call) do { cudaError_t _e = (call); if (_e != cudaSuccess) return fail(fail_cuda(_e, #call, __FILE__, __LINE__)); } while (0)
     f->u_stored = !f->simplified;
+    f->store_d = P.store_diag || P.literal;
     const int npairs = P.s * (P.s - 1) / 2;
     f->l_implicit = implicit_l_ok(pat, P, keep, f->simplified);
     FCK(cudaMalloc(&f->d_keep, pat->nnzb));
@@ -1181,6 +1198,37 @@ static int factor_common(irk_ctx* ctx, const irk_pattern* pat, const FactorSetup
     if (rc < 0) return fail(rc);
     *out = f;
     return rc;
+}
+
+// Export of a factor whose level-0 pivot blocks were formed inside the inverse and
+// not stored: re-form them (cold path), with the rounding of the Schur phase.
+__global__ void k_form_d(FactorArgs F, const int32_t* tasks, int64_t ntasks) {
+    const int nb = F.nb;
+    const int64_t bsz = (int64_t)nb * 2 * ((nb + 1) >> 1);
+    for (int64_t t = blockIdx.x; t < ntasks; t += gridDim.x) {
+        const int64_t code = tasks[t];
+        const int k = (int)(code / F.T);
+        const int64_t j = code - (int64_t)k * F.T;
+        const int dpos = F.diag[j];
+        const bool keep_d = F.keep[dpos] != 0;
+        double* dst = F.Dst + (j * F.s + k) * bsz;
+        for (int64_t e = threadIdx.x; e < bsz; e += blockDim.x) {
+            double x = __dmul_rn(F.alpha, F.J[0][(int64_t)dpos * bsz + e]);
+            if (F.M) x = __dadd_rn(x, __dmul_rn(F.coef[k], F.M[j * bsz + e]));
+            dst[e] = keep_d ? x : 0.0;
+        }
+    }
+}
+
+int factor_form_level0_d(const irk_factor* f, cudaStream_t st) {
+    if (!f->d0_unstored || !f->d_fs_tasks || f->h_fs_eptr.size() < 2) return IRK_OK;
+    const FactorArgs& F = *static_cast<const FactorArgs*>(f->fargs);
+    const int64_t n = (f->h_fs_eptr[1] - f->h_fs_eptr[0]) * f->s;
+    if (n <= 0) return IRK_OK;
+    k_form_d<<<(int)std::min<int64_t>(n, (int64_t)f->ctx->num_sms * 8), 256, 0, st>>>(F, f->d_fs_tasks, n);
+    IRK_LAUNCHED();
+    f->d0_unstored = false;
+    return IRK_OK;
 }
 
 // Implicit L, for export: L[lq][k] = alpha J_q Dinv_{j,k} (j = column of q) for

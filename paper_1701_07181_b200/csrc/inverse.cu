@@ -58,7 +58,22 @@ struct InvArgs {
     unsigned long long* fail_key;
     const int* ntasks_dev;    // non-NULL: task count on the device (<= ntasks), fallback lists
     int cap_per_sm;           // > 0: at most this many CTAs per SM (runs beside another kernel)
+    InvForm form;             // form.J != NULL: build D from J and M (level 0) instead of reading it
 };
+
+// D_{j,k} element pair idx (double2 index p2 * nb + r of the device layout), formed from J, M
+__device__ __forceinline__ double2 form_pair(const InvArgs& A, int64_t j, int k, int64_t bsz, int idx) {
+    const InvForm& F = A.form;
+    if (!F.keep[F.diag[j]]) return make_double2(0.0, 0.0);
+    const double2 jv = reinterpret_cast<const double2*>(F.J + (int64_t)F.diag[j] * bsz)[idx];
+    double x0 = __dmul_rn(A.form.alpha, jv.x), x1 = __dmul_rn(A.form.alpha, jv.y);
+    if (F.M) {
+        const double2 mv = reinterpret_cast<const double2*>(F.M + j * bsz)[idx];
+        x0 = __dadd_rn(x0, __dmul_rn(F.coef[k], mv.x));
+        x1 = __dadd_rn(x1, __dmul_rn(F.coef[k], mv.y));
+    }
+    return make_double2(x0, x1);
+}
 
 // task count of a launch: the host bound, or the device count of a fallback list
 __device__ __forceinline__ int64_t task_count(const InvArgs& A) {
@@ -1042,8 +1057,9 @@ struct InvTcCfg {
     static constexpr size_t smem = WARPS * warp_doubles * sizeof(double);
 };
 
-// EXACT: nb == 8 NT (block index math and loops fold to constants)
-template <int NT, bool EXACT>
+// EXACT: nb == 8 NT (block index math and loops fold to constants); FORM: build D from
+// J and M (factor level 0) instead of reading it
+template <int NT, bool EXACT, bool FORM>
 __global__ void __launch_bounds__(32 * InvTcCfg<NT>::WARPS) k_inverse_tc(InvArgs A, int* fb_list, int* fb_count) {
     using C = InvTcCfg<NT>;
     constexpr int NBT = C::NBT, LD = C::LD, RL = C::RL;
@@ -1061,6 +1077,8 @@ __global__ void __launch_bounds__(32 * InvTcCfg<NT>::WARPS) k_inverse_tc(InvArgs
         const int k_st = (int)(code / A.T);
         const int64_t j = code - (int64_t)k_st * A.T;
         const double2* src = reinterpret_cast<const double2*>(A.D + (j * A.s + k_st) * bsz);
+        constexpr bool form = FORM;
+        double2* dst_d = FORM ? reinterpret_cast<double2*>(A.form.Dst + (j * A.s + k_st) * bsz) : nullptr;
         // ---- load: device pair p2 of row r is double2 index p2 * nb + r
         if constexpr (EXACT) {
 #pragma unroll
@@ -1068,7 +1086,14 @@ __global__ void __launch_bounds__(32 * InvTcCfg<NT>::WARPS) k_inverse_tc(InvArgs
                 const int idx = lane + 32 * e;
                 if (NPAIR % 32 == 0 || idx < NPAIR) {
                     const int p2 = idx / NBT, r = idx - p2 * NBT;
-                    *reinterpret_cast<double2*>(X + r * LD + 2 * p2) = src[idx];
+                    double2 v;
+                    if constexpr (FORM) {
+                        v = form_pair(A, j, k_st, bsz, idx);
+                        if (A.form.store) dst_d[idx] = v;
+                    } else {
+                        v = src[idx];
+                    }
+                    *reinterpret_cast<double2*>(X + r * LD + 2 * p2) = v;
                 }
             }
         } else {
@@ -1076,7 +1101,12 @@ __global__ void __launch_bounds__(32 * InvTcCfg<NT>::WARPS) k_inverse_tc(InvArgs
                 const int p2 = idx / NBT, r = idx - p2 * NBT;
                 double2 v;
                 if (r < nb && p2 < P) {
-                    v = src[p2 * nb + r];
+                    if constexpr (FORM) {
+                        v = form_pair(A, j, k_st, bsz, p2 * nb + r);
+                        if (A.form.store) dst_d[p2 * nb + r] = v;
+                    } else {
+                        v = src[p2 * nb + r];
+                    }
                     if (2 * p2 + 1 >= nb) v.y = 0.0;
                 } else {   // identity padding
                     v = make_double2(2 * p2 == r ? 1.0 : 0.0, 2 * p2 + 1 == r ? 1.0 : 0.0);
@@ -1220,6 +1250,11 @@ __global__ void __launch_bounds__(32 * InvTcCfg<NT>::WARPS) k_inverse_tc(InvArgs
             __syncwarp();
         }, std::make_integer_sequence<int, NT>{});
         if (swap) {
+            // the pivoted kernels read D from memory: write it unless already stored
+            if (FORM && !A.form.store)
+                for (int idx = lane; idx < P * nb; idx += 32) dst_d[idx] = form_pair(A, j, k_st, bsz, idx);
+            __threadfence();
+            __syncwarp();
             if (lane == 0) fb_list[atomicAdd(fb_count, 1)] = (int)code;
             __syncwarp();
             continue;
@@ -1259,30 +1294,34 @@ __global__ void __launch_bounds__(32 * InvTcCfg<NT>::WARPS) k_inverse_tc(InvArgs
     }
 }
 
-template <int NT, bool EXACT>
+template <int NT, bool EXACT, bool FORM>
 static int launch_tc_t(const irk_ctx* ctx, const InvArgs& A, int* fb_list, int* fb_count, cudaStream_t st) {
     using C = InvTcCfg<NT>;
     static bool attr = false;
     if (!attr) {
-        IRK_CK(cudaFuncSetAttribute(k_inverse_tc<NT, EXACT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::smem));
-        IRK_CK(cudaFuncSetAttribute(k_inverse_tc<NT, EXACT>, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+        IRK_CK(cudaFuncSetAttribute(k_inverse_tc<NT, EXACT, FORM>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::smem));
+        IRK_CK(cudaFuncSetAttribute(k_inverse_tc<NT, EXACT, FORM>, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
         attr = true;
     }
     const int threads = 32 * C::WARPS;
     int per_sm = 1;
-    IRK_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_inverse_tc<NT, EXACT>, threads, C::smem));
+    IRK_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_inverse_tc<NT, EXACT, FORM>, threads, C::smem));
     if (A.cap_per_sm > 0) per_sm = std::min(per_sm, A.cap_per_sm);
     const int64_t need = (A.ntasks + C::WARPS - 1) / C::WARPS;
     const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(need, (int64_t)ctx->num_sms * std::max(per_sm, 1)));
-    k_inverse_tc<NT, EXACT><<<grid, threads, C::smem, st>>>(A, fb_list, fb_count);
+    k_inverse_tc<NT, EXACT, FORM><<<grid, threads, C::smem, st>>>(A, fb_list, fb_count);
     IRK_LAUNCHED();
     return IRK_OK;
 }
 
 template <int NT>
 static int launch_tc_n(const irk_ctx* ctx, const InvArgs& A, int* fb_list, int* fb_count, cudaStream_t st) {
-    return A.nb == 8 * NT ? launch_tc_t<NT, true>(ctx, A, fb_list, fb_count, st)
-                          : launch_tc_t<NT, false>(ctx, A, fb_list, fb_count, st);
+    const bool form = A.form.J != nullptr;
+    if (A.nb == 8 * NT)
+        return form ? launch_tc_t<NT, true, true>(ctx, A, fb_list, fb_count, st)
+                    : launch_tc_t<NT, true, false>(ctx, A, fb_list, fb_count, st);
+    return form ? launch_tc_t<NT, false, true>(ctx, A, fb_list, fb_count, st)
+                : launch_tc_t<NT, false, false>(ctx, A, fb_list, fb_count, st);
 }
 
 static int launch_pivoted(const irk_ctx* ctx, const InvArgs& A, cudaStream_t st);
@@ -1308,17 +1347,22 @@ static int launch_tc(const irk_ctx* ctx, const InvArgs& A, int* fb, cudaStream_t
     InvArgs B = A;
     B.tasks = fb_list;
     B.ntasks_dev = fb_count;
+    B.form = InvForm{};
     return launch_pivoted(ctx, B, st);
 }
 
 // returns IRK_EINVAL if nb has no warp-inverse specialisation (caller falls back)
 int launch_inverse(const irk_ctx* ctx, const int32_t* tasks, int64_t ntasks, int64_t T, int s, int nb,
                    const double* D, double* Dinv, unsigned long long* fail_key, int* fb, cudaStream_t st,
-                   int cap_per_sm) {
+                   int cap_per_sm, const InvForm* form) {
     if (ntasks <= 0) return IRK_OK;
-    InvArgs A{tasks, ntasks, T, s, nb, D, Dinv, fail_key, nullptr, cap_per_sm};
+    InvArgs A{tasks, ntasks, T, s, nb, D, Dinv, fail_key, nullptr, cap_per_sm, InvForm{}};
     static const bool tc_off = getenv("IRK_INV_TC") && atoi(getenv("IRK_INV_TC")) == 0;
-    if (fb && !tc_off && nb > 16 && nb <= 64) return launch_tc(ctx, A, fb, st);
+    if (fb && !tc_off && nb > 16 && nb <= 64) {
+        if (form) A.form = *form;
+        return launch_tc(ctx, A, fb, st);
+    }
+    if (form) return IRK_EINVAL;   // forming D needs the tensor-core path (caller runs the Schur phase)
     return launch_pivoted(ctx, A, st);
 }
 

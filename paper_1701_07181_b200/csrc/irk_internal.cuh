@@ -91,6 +91,20 @@ inline cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, s
     return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
 }
 
+// Pivot blocks formed inside the inverse kernel (factor level 0, no Schur update):
+// D_{j,k} = keep[diag_j] ? fl(alpha J_jj) + fl(coef_k M_j) : 0 (build_stage_matrix,
+// precond.py:48-54, the rounding of the Schur phase's initialisation).
+struct InvForm {
+    const double* J = nullptr;      // stage-shared Jacobian blocks (pattern order)
+    const int32_t* diag = nullptr;  // diagonal block position per element
+    const uint8_t* keep = nullptr;
+    const double* M = nullptr;      // mass blocks or NULL
+    double* Dst = nullptr;          // pivot blocks (written when store or for pivoted fallback)
+    double alpha = 0.0;
+    double coef[IRK_MAX_STAGES] = {};
+    int store = 0;                  // also write D (export / literal need it)
+};
+
 inline int npairs(int nb) { return (nb + 1) / 2; }
 inline int64_t block_doubles(int nb) { return (int64_t)nb * 2 * npairs(nb); }
 
@@ -199,6 +213,8 @@ struct irk_factor {
     irk_sched fsched;                 // factor tasks by level
     unsigned long long* d_fail = nullptr;
     int* d_fb = nullptr;              // tensor-core inverse: blocks handed to the pivoted kernels
+    bool store_d = false;             // pivot blocks must be kept (store_diag / literal)
+    mutable bool d0_unstored = false; // level-0 pivot blocks were formed in the inverse, not stored
     // Schur path: per factor level, its elements and element-major (stage fastest) task codes
     int32_t* d_fs_elems = nullptr;
     int32_t* d_fs_tasks = nullptr;
