@@ -655,7 +655,10 @@ __device__ __forceinline__ void fence_proxy_async_smem() {
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
 
-template <int S, int NB>
+// TWO: two-phase unit -- GEMM1 of all stages (J_ji fragments loaded once for S stages), one
+// barrier, A'_k into the consumed Dinv slots, GEMM2 of all stages (J_ij fragments loaded once),
+// one barrier, refills: 2 barriers per unit instead of S + 1, fewer fragment loads
+template <int S, int NB, bool TWO = false>
 __global__ void __launch_bounds__(4 * NB) k_schur(FactorArgs F, const int32_t* __restrict__ elems, int64_t nelem) {
     using Gm = SchurGeo<NB>;
     constexpr int NT = Gm::NT, LDP = Gm::LDP, SLOT = Gm::SLOT;
@@ -779,6 +782,68 @@ __global__ void __launch_bounds__(4 * NB) k_schur(FactorArgs F, const int32_t* _
             const Unit cur = nxt;
             nxt = find_unit(it, q + 1);
             const bool more = nxt.it >= 0;
+            if constexpr (TWO) {
+                wait_slot(SJ);
+#pragma unroll
+                for (int k = 0; k < S; ++k) wait_slot(2 + k);
+                double acc[S][NT][2];
+#pragma unroll
+                for (int k = 0; k < S; ++k)
+#pragma unroll
+                    for (int t = 0; t < NT; ++t) acc[k][t][0] = acc[k][t][1] = 0.0;
+#pragma unroll 2
+                for (int kk = 0; kk < NB / 4; ++kk) {
+                    const double a = frag_a(shs + SJ * SLOT, kk);
+#pragma unroll
+                    for (int k = 0; k < S; ++k)
+#pragma unroll
+                        for (int t = 0; t < NT; ++t)
+                            dmma(acc[k][t][0], acc[k][t][1], a, frag_b(shs + (size_t)(2 + k) * SLOT, kk, t));
+                }
+#pragma unroll
+                for (int k = 0; k < S; ++k)
+#pragma unroll
+                    for (int t = 0; t < NT; ++t) {
+                        acc[k][t][0] *= F.alpha;
+                        acc[k][t][1] *= F.alpha;
+                        if (Lout && gl_off(t) >= 0)
+                            reinterpret_cast<double2*>(Lout + (int64_t)k * BSZ)[gl_off(t)] =
+                                make_double2(acc[k][t][0], acc[k][t][1]);
+                    }
+                __syncthreads();   // all warps: GEMM1 done (J_ji and the Dinv slots)
+                if (more) fill(SJ, J + (int64_t)nxt.q * BSZ);
+#pragma unroll
+                for (int k = 0; k < S; ++k) {
+                    double* Ak = shs + (size_t)(2 + k) * SLOT + warp * 8 * Gm::LDA;
+#pragma unroll
+                    for (int t = 0; t < NT; ++t)
+                        *reinterpret_cast<double2*>(Ak + fr * Gm::LDA + 8 * t + 2 * fk) =
+                            make_double2(-F.alpha * acc[k][t][0], -F.alpha * acc[k][t][1]);
+                }
+                __syncwarp();
+                wait_slot(SU);
+#pragma unroll 2
+                for (int kk = 0; kk < NB / 4; ++kk) {
+                    double a[S];
+#pragma unroll
+                    for (int k = 0; k < S; ++k)
+                        a[k] = shs[(size_t)(2 + k) * SLOT + warp * 8 * Gm::LDA + fr * Gm::LDA + 4 * kk + fk];
+#pragma unroll
+                    for (int t = 0; t < NT; ++t) {
+                        const double b = frag_b(shs + SU * SLOT, kk, t);
+#pragma unroll
+                        for (int k = 0; k < S; ++k) dmma(dacc[k][t][0], dacc[k][t][1], a[k], b);
+                    }
+                }
+                __syncthreads();   // all warps: GEMM2 done (A' slots, J_ij)
+                if (more) {
+#pragma unroll
+                    for (int k = 0; k < S; ++k) fill(2 + k, src_dinv(nxt, k));
+                    fill(SU, J + (int64_t)nxt.tq * BSZ);
+                }
+                (void)cur;
+                continue;
+            }
 #pragma unroll
             for (int k = 0; k < S; ++k) {
                 // T_k = J_ji Dinv_k on this warp's strip
@@ -839,23 +904,34 @@ __global__ void __launch_bounds__(4 * NB) k_schur(FactorArgs F, const int32_t* _
     }
 }
 
-template <int S, int NB>
-static int launch_schur_t(const irk_ctx* ctx, const FactorArgs& F, const int32_t* elems, int64_t nelem,
-                          cudaStream_t st, int cap_per_sm) {
+template <int S, int NB, bool TWO>
+static int launch_schur_tt(const irk_ctx* ctx, const FactorArgs& F, const int32_t* elems, int64_t nelem,
+                           cudaStream_t st, int cap_per_sm) {
     const size_t smem = sizeof(double) * (size_t)(S + 2) * SchurGeo<NB>::SLOT;
     static bool attr = false;
     if (!attr) {
-        IRK_CK(cudaFuncSetAttribute(k_schur<S, NB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        IRK_CK(cudaFuncSetAttribute(k_schur<S, NB>, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+        IRK_CK(cudaFuncSetAttribute(k_schur<S, NB, TWO>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        IRK_CK(cudaFuncSetAttribute(k_schur<S, NB, TWO>, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
         attr = true;
     }
     int per_sm = 1;
-    IRK_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_schur<S, NB>, 4 * NB, smem));
+    IRK_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_schur<S, NB, TWO>, 4 * NB, smem));
     if (cap_per_sm > 0) per_sm = std::min(per_sm, cap_per_sm);
     const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(nelem, (int64_t)ctx->num_sms * std::max(per_sm, 1)));
-    k_schur<S, NB><<<grid, 4 * NB, smem, st>>>(F, elems, nelem);
+    k_schur<S, NB, TWO><<<grid, 4 * NB, smem, st>>>(F, elems, nelem);
     IRK_LAUNCHED();
     return IRK_OK;
+}
+
+template <int S, int NB>
+static int launch_schur_t(const irk_ctx* ctx, const FactorArgs& F, const int32_t* elems, int64_t nelem,
+                          cudaStream_t st, int cap_per_sm) {
+    // two-phase units where shared memory already limits the kernel to one CTA per SM (NB >= 56:
+    // config 2, 8.92 -> 8.75 ms at N=16); the per-stage form keeps 3 CTAs/SM at NB = 40
+    static const int env = getenv("IRK_SCHUR_TWO") ? atoi(getenv("IRK_SCHUR_TWO")) : -1;   // A/B knob
+    const bool two = env >= 0 ? env != 0 : NB >= 56;
+    return two ? launch_schur_tt<S, NB, true>(ctx, F, elems, nelem, st, cap_per_sm)
+               : launch_schur_tt<S, NB, false>(ctx, F, elems, nelem, st, cap_per_sm);
 }
 
 template <int S>
