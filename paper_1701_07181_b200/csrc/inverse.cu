@@ -61,18 +61,36 @@ struct InvArgs {
     InvForm form;             // form.J != NULL: build D from J and M (level 0) instead of reading it
 };
 
-// D_{j,k} element pair idx (double2 index p2 * nb + r of the device layout), formed from J, M
-__device__ __forceinline__ double2 form_pair(const InvArgs& A, int64_t j, int k, int64_t bsz, int idx) {
+// D_{j,k} formed from J and M, one element pair (double2 index p2 * nb + r of the device
+// layout) at a time; the per-block pointers and scalars are resolved once per task
+struct FormSrc {
+    const double2* J;   // J_jj
+    const double2* M;   // M_j or NULL
+    double alpha, coef;
+    bool keep;
+};
+
+__device__ __forceinline__ FormSrc form_src(const InvArgs& A, int64_t j, int k, int64_t bsz) {
     const InvForm& F = A.form;
-    if (!F.keep[F.diag[j]]) return make_double2(0.0, 0.0);
-    const double2 jv = reinterpret_cast<const double2*>(F.J + (int64_t)F.diag[j] * bsz)[idx];
-    double x0 = __dmul_rn(A.form.alpha, jv.x), x1 = __dmul_rn(A.form.alpha, jv.y);
-    if (F.M) {
-        const double2 mv = reinterpret_cast<const double2*>(F.M + j * bsz)[idx];
-        x0 = __dadd_rn(x0, __dmul_rn(F.coef[k], mv.x));
-        x1 = __dadd_rn(x1, __dmul_rn(F.coef[k], mv.y));
+    const int d = F.diag[j];
+    FormSrc f;
+    f.J = reinterpret_cast<const double2*>(F.J + (int64_t)d * bsz);
+    f.M = F.M ? reinterpret_cast<const double2*>(F.M + j * bsz) : nullptr;
+    f.alpha = F.alpha;
+    f.coef = F.coef[k];
+    f.keep = F.keep[d] != 0;
+    return f;
+}
+
+__device__ __forceinline__ double2 form_pair(const FormSrc& f, int idx) {
+    const double2 jv = f.J[idx];
+    double x0 = __dmul_rn(f.alpha, jv.x), x1 = __dmul_rn(f.alpha, jv.y);
+    if (f.M) {
+        const double2 mv = f.M[idx];
+        x0 = __dadd_rn(x0, __dmul_rn(f.coef, mv.x));
+        x1 = __dadd_rn(x1, __dmul_rn(f.coef, mv.y));
     }
-    return make_double2(x0, x1);
+    return f.keep ? make_double2(x0, x1) : make_double2(0.0, 0.0);
 }
 
 // task count of a launch: the host bound, or the device count of a fallback list
@@ -1077,8 +1095,9 @@ __global__ void __launch_bounds__(32 * InvTcCfg<NT>::WARPS) k_inverse_tc(InvArgs
         const int k_st = (int)(code / A.T);
         const int64_t j = code - (int64_t)k_st * A.T;
         const double2* src = reinterpret_cast<const double2*>(A.D + (j * A.s + k_st) * bsz);
-        constexpr bool form = FORM;
         double2* dst_d = FORM ? reinterpret_cast<double2*>(A.form.Dst + (j * A.s + k_st) * bsz) : nullptr;
+        FormSrc fsrc{};
+        if constexpr (FORM) fsrc = form_src(A, j, k_st, bsz);
         // ---- load: device pair p2 of row r is double2 index p2 * nb + r
         if constexpr (EXACT) {
 #pragma unroll
@@ -1088,7 +1107,7 @@ __global__ void __launch_bounds__(32 * InvTcCfg<NT>::WARPS) k_inverse_tc(InvArgs
                     const int p2 = idx / NBT, r = idx - p2 * NBT;
                     double2 v;
                     if constexpr (FORM) {
-                        v = form_pair(A, j, k_st, bsz, idx);
+                        v = form_pair(fsrc, idx);
                         if (A.form.store) dst_d[idx] = v;
                     } else {
                         v = src[idx];
@@ -1102,7 +1121,7 @@ __global__ void __launch_bounds__(32 * InvTcCfg<NT>::WARPS) k_inverse_tc(InvArgs
                 double2 v;
                 if (r < nb && p2 < P) {
                     if constexpr (FORM) {
-                        v = form_pair(A, j, k_st, bsz, p2 * nb + r);
+                        v = form_pair(fsrc, p2 * nb + r);
                         if (A.form.store) dst_d[p2 * nb + r] = v;
                     } else {
                         v = src[p2 * nb + r];
@@ -1252,7 +1271,7 @@ __global__ void __launch_bounds__(32 * InvTcCfg<NT>::WARPS) k_inverse_tc(InvArgs
         if (swap) {
             // the pivoted kernels read D from memory: write it unless already stored
             if (FORM && !A.form.store)
-                for (int idx = lane; idx < P * nb; idx += 32) dst_d[idx] = form_pair(A, j, k_st, bsz, idx);
+                for (int idx = lane; idx < P * nb; idx += 32) dst_d[idx] = form_pair(fsrc, idx);
             __threadfence();
             __syncwarp();
             if (lane == 0) fb_list[atomicAdd(fb_count, 1)] = (int)code;
