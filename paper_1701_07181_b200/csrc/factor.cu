@@ -844,52 +844,57 @@ __global__ void __launch_bounds__(4 * NB) k_schur(FactorArgs F, const int32_t* _
                 (void)cur;
                 continue;
             }
+            // software-pipelined stages: phase k runs GEMM1_k (T_k = J_ji Dinv_k) interleaved with
+            // GEMM2_{k-1} (D_{k-1} += A'_{k-1} J_ij), two independent accumulator sets per warp
+            // between the same S + 1 barriers
+            double acc[NT][2];
 #pragma unroll
-            for (int k = 0; k < S; ++k) {
-                // T_k = J_ji Dinv_k on this warp's strip
+            for (int k = 0; k <= S; ++k) {
+                const bool g1 = k < S, g2 = k > 0;
                 if (k == 0) wait_slot(SJ);
-                wait_slot(2 + k);
-                double acc[NT][2];
+                if (g1) wait_slot(2 + k);
+                if (k == 1) wait_slot(SU);
 #pragma unroll
                 for (int t = 0; t < NT; ++t) acc[t][0] = acc[t][1] = 0.0;
-                const double* Dk = shs + (size_t)(2 + k) * SLOT;
+                const double* Dk = shs + (size_t)(2 + (g1 ? k : 0)) * SLOT;
+                const double* Ap = shs + (size_t)(2 + (g2 ? k - 1 : 0)) * SLOT + warp * 8 * Gm::LDA;
 #pragma unroll 2
                 for (int kk = 0; kk < NB / 4; ++kk) {
-                    const double a = frag_a(shs + SJ * SLOT, kk);
+                    if (g1) {
+                        const double a = frag_a(shs + SJ * SLOT, kk);
 #pragma unroll
-                    for (int t = 0; t < NT; ++t) dmma(acc[t][0], acc[t][1], a, frag_b(Dk, kk, t));
+                        for (int t = 0; t < NT; ++t) dmma(acc[t][0], acc[t][1], a, frag_b(Dk, kk, t));
+                    }
+                    if (g2) {
+                        const double a = Ap[fr * Gm::LDA + 4 * kk + fk];
+#pragma unroll
+                        for (int t = 0; t < NT; ++t)
+                            dmma(dacc[g2 ? k - 1 : 0][t][0], dacc[g2 ? k - 1 : 0][t][1], a, frag_b(shs + SU * SLOT, kk, t));
+                    }
                 }
-                // L_k = alpha T_k -> global (numba_backend.py:58-61), unless L is implicit
+                if (g1) {
+                    // L_k = alpha T_k -> global (numba_backend.py:58-61), unless L is implicit
 #pragma unroll
-                for (int t = 0; t < NT; ++t) {
-                    acc[t][0] *= F.alpha;
-                    acc[t][1] *= F.alpha;
-                    if (Lout && gl_off(t) >= 0)
-                        reinterpret_cast<double2*>(Lout + (int64_t)k * BSZ)[gl_off(t)] = make_double2(acc[t][0], acc[t][1]);
+                    for (int t = 0; t < NT; ++t) {
+                        acc[t][0] *= F.alpha;
+                        acc[t][1] *= F.alpha;
+                        if (Lout && gl_off(t) >= 0)
+                            reinterpret_cast<double2*>(Lout + (int64_t)k * BSZ)[gl_off(t)] = make_double2(acc[t][0], acc[t][1]);
+                    }
                 }
                 __syncthreads();   // all warps: GEMM1_k done (Dinv_k slot), GEMM2_{k-1} done (A'_{k-1})
-                if (more && k > 0) fill(2 + k - 1, src_dinv(nxt, k - 1));
+                if (more && g2) fill(2 + k - 1, src_dinv(nxt, k - 1));
                 if (more && k == S - 1) fill(SJ, J + (int64_t)nxt.q * BSZ);
-                // A'_k = -alpha L_k into the consumed Dinv_k slot (warp-private row-major strip)
-                double* Ak = shs + (size_t)(2 + k) * SLOT + warp * 8 * Gm::LDA;
+                if (more && k == S) fill(SU, J + (int64_t)nxt.tq * BSZ);
+                if (g1) {
+                    // A'_k = -alpha L_k into the consumed Dinv_k slot (warp-private row-major strip)
+                    double* Ak = shs + (size_t)(2 + k) * SLOT + warp * 8 * Gm::LDA;
 #pragma unroll
-                for (int t = 0; t < NT; ++t)
-                    *reinterpret_cast<double2*>(Ak + fr * Gm::LDA + 8 * t + 2 * fk) =
-                        make_double2(-F.alpha * acc[t][0], -F.alpha * acc[t][1]);
-                __syncwarp();
-                if (k == 0) wait_slot(SU);
-                // D_k += A'_k J_ij   (D_j -= L_ji U_ij, U_ij = alpha J_ij)
-#pragma unroll 2
-                for (int kk = 0; kk < NB / 4; ++kk) {
-                    const double a = Ak[fr * Gm::LDA + 4 * kk + fk];
-#pragma unroll
-                    for (int t = 0; t < NT; ++t) dmma(dacc[k][t][0], dacc[k][t][1], a, frag_b(shs + SU * SLOT, kk, t));
+                    for (int t = 0; t < NT; ++t)
+                        *reinterpret_cast<double2*>(Ak + fr * Gm::LDA + 8 * t + 2 * fk) =
+                            make_double2(-F.alpha * acc[t][0], -F.alpha * acc[t][1]);
+                    __syncwarp();
                 }
-            }
-            __syncthreads();       // all warps: GEMM2_{S-1} done (A'_{S-1}, J_ij)
-            if (more) {
-                fill(2 + S - 1, src_dinv(nxt, S - 1));
-                fill(SU, J + (int64_t)nxt.tq * BSZ);
             }
             (void)cur;
         }
