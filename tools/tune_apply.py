@@ -9,6 +9,7 @@ import sys
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 
+import numpy as np  # noqa: E402
 import torch  # noqa: E402
 
 import bench  # noqa: E402
@@ -29,7 +30,8 @@ def main():
                          gmres_cfg=GmresConfig(rel_tol=cfg.rtol, restart=cfg.restart))
     solver.factorize()
     T, nb, s = wl.pattern.T, cfg.nb, cfg.s
-    ba = bench.bytes_apply_uncoupled_shared(T, 3, nb, s)
+    t_up = int(np.count_nonzero(wl.pattern.indptr[1:] - 1 > wl.pattern.diag_pos))
+    ba = bench.bytes_apply_uncoupled_shared(T, 3, nb, s, solver.fac.implicit_l, t_up)
     peak = bench.hbm_peak()[0]
     w = torch.randn(s * T * nb, dtype=torch.float64, device="cuda")
     y = torch.empty_like(w)
