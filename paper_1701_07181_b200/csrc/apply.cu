@@ -872,6 +872,188 @@ __global__ void __launch_bounds__(288) k_unc_bwd_pipe(ApplyArgs A, PipeCfg PC) {
 }
 
 // ---------------------------------------------------------------------------
+// Level-scheduled uncoupled sweep with the vector segments riding in the ring
+// stages (matvec-style): every stage holds one factor / Jacobian block plus the
+// x segments it multiplies (a neighbour's S stage segments, or the task's own S
+// segments on its first Dinv item), so there is no separate x-slot double buffer
+// and the shared memory of an SM goes to blocks in flight.  FWDI as in
+// k_unc_bwd_pipe; stage-shared upper blocks (u_shared) or one factor for several
+// right-hand sides (fac_shared).  One thread per block row (or 2 groups, shuffle
+// reduction), task-parity double-buffered t vector.
+// ---------------------------------------------------------------------------
+struct SegCfg {
+    int nst;
+    int stage_bytes;   // block + S segments, 128-B aligned
+    int block_bytes;
+};
+
+template <int S, bool FWDI>
+__global__ void __launch_bounds__(288) k_unc_sweep_seg(ApplyArgs A, SegCfg SC) {
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    const int nb = A.nb;
+    unsigned char* stages = smem_raw;
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem_raw + (size_t)SC.nst * SC.stage_bytes);
+    uint64_t* empty = full + SC.nst;
+    int4* desc = reinterpret_cast<int4*>(empty + SC.nst);
+    double* tvb = reinterpret_cast<double*>(desc + SC.nst);      // [2][S][nb]
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int ncons_warps = (blockDim.x >> 5) - 1, ncons = ncons_warps * 32;
+    if (threadIdx.x == 0) {
+        for (int i = 0; i < SC.nst; ++i) {
+            mbar_init(full + i, 1);
+            mbar_init(empty + i, ncons_warps);
+        }
+        fence_mbar_init();
+    }
+    __syncthreads();
+    griddep_launch();
+    const int64_t bsz = (int64_t)SC.block_bytes / 8;
+    const uint32_t seg = (uint32_t)nb * 8;
+    const bool ush = A.u_shared || A.fac_shared;
+    const int nd = A.fac_shared ? 1 : S;
+    if (warp == 0) {
+        griddep_wait();
+        if (lane != 0) return;
+        int st = 0;
+        uint32_t ph = 0;
+        auto push = [&](int4 d, const double* blk, const double* segbase, int64_t segstride) {
+            mbar_wait(empty + st, ph ^ 1);
+            desc[st] = d;
+            unsigned char* dst = stages + (size_t)st * SC.stage_bytes;
+            const int nsg = segbase ? S : 0;
+            mbar_expect_tx(full + st, SC.block_bytes + nsg * seg);
+            bulk_g2s(dst, blk, SC.block_bytes, full + st);
+            for (int k = 0; k < nsg; ++k)
+                bulk_g2s(dst + SC.block_bytes + k * seg, segbase + k * segstride, seg, full + st);
+            if (++st == SC.nst) { st = 0; ph ^= 1; }
+        };
+        const int64_t lo = A.ntasks * blockIdx.x / gridDim.x, hi = A.ntasks * (blockIdx.x + 1) / gridDim.x;
+        for (int64_t t = lo; t < hi; ++t) {
+            const int64_t i = A.order[t];
+            const int d = A.diag[i];
+            const int b0 = FWDI ? A.indptr[i] : d + 1;
+            const int nn = (FWDI ? d : A.indptr[i + 1]) - b0;
+            const int store_z = (FWDI && A.hasup[i]) ? 1 : 0;
+            int n = 0;
+            for (int m = 0; m < nn; ++m) {
+                const int qq = b0 + m;
+                if (!A.keep[qq]) continue;
+                const int64_t col = A.indices[qq];
+                const double* vsrc = (FWDI ? A.W : A.x) + col * nb;
+                push(make_int4((int)i, 0, PD_USH | (n == 0 ? PD_FIRST : 0), 0),
+                     A.U ? A.U + (int64_t)(A.uptr[i] + m) * bsz : A.ubase[0] + (int64_t)qq * bsz, vsrc, A.n);
+                ++n;
+            }
+            const double* own = (FWDI ? A.y : A.x) + i * nb;
+            for (int k = 0; k < nd; ++k) {
+                const int fl = PD_DINV | (n == 0 ? PD_FIRST : 0) | (k == nd - 1 ? PD_LAST : 0) |
+                               (A.fac_shared ? PD_SH : 0);
+                push(make_int4((int)i, k, fl, store_z), A.Dinv + (i * nd + k) * bsz, k == 0 ? own : nullptr, A.n);
+                ++n;
+            }
+        }
+        push(make_int4(-1, 0, PD_END, 0), A.Dinv, nullptr, 0);   // block copy unused (harmless)
+        return;
+    }
+    const int c = threadIdx.x - 32;
+    const int G = A.G_, R = 32 / G;
+    Geo q;
+    q.nb = nb; q.P = (nb + 1) >> 1; q.G = G;
+    q.a = R * (c >> 5) + (c & (R - 1));
+    q.g = (c & 31) / R;
+    q.active = q.a < nb;
+    auto group_sum = [&](double v) -> double {
+        for (int o = R; o < 32; o <<= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+        return v;
+    };
+    griddep_wait();
+    int st = 0;
+    uint32_t ph = 0;
+    double part[S];
+    int par = 0;
+    for (;;) {
+        mbar_wait(full + st, ph);
+        const int4 dsc = desc[st];
+        if (dsc.z & PD_END) break;
+        const int64_t i = dsc.x;
+        const unsigned char* base = stages + (size_t)st * SC.stage_bytes;
+        const double2* B = reinterpret_cast<const double2*>(base);
+        const double* segs = reinterpret_cast<const double*>(base + SC.block_bytes);
+        double* tv = tvb + (size_t)par * S * nb;
+        const bool store_z = FWDI && dsc.w;
+        if (dsc.z & PD_FIRST) {
+#pragma unroll
+            for (int k = 0; k < S; ++k) part[k] = 0.0;
+        }
+        if (dsc.z & PD_USH) {
+            if (q.active) smem_gemv_all<S>(B, segs, q, part);
+        } else {
+            const int kk = dsc.y;
+            if (kk == 0) {
+                // t_k = own_k - uscale * sum_j U_ij x_{j,k}: own segments ride on this item
+#pragma unroll
+                for (int k = 0; k < S; ++k) {
+                    const double sum = group_sum(part[k]);
+                    if (q.active && q.g == 0) {
+                        const double tval = segs[k * nb + q.a] - A.uscale * sum;
+                        tv[k * nb + q.a] = tval;
+                        if (store_z) A.x[k * A.n + i * nb + q.a] = tval;   // z_i for the backward sweep
+                    }
+                    part[k] = 0.0;
+                }
+                consumer_sync(1, ncons);
+            }
+            if (q.active) {
+                if (dsc.z & PD_SH) {
+                    smem_gemv_all<S>(B, tv, q, part);
+                } else {
+#pragma unroll
+                    for (int k = 0; k < S; ++k)
+                        if (k == kk) part[k] = smem_gemv(B, tv + k * nb, q, part[k]);
+                }
+            }
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(empty + st);
+        if (++st == SC.nst) { st = 0; ph ^= 1; }
+        if (dsc.z & PD_LAST) {
+            par ^= 1;
+#pragma unroll
+            for (int k = 0; k < S; ++k) {
+                const double sum = group_sum(part[k]);
+                if (q.active && q.g == 0) (store_z ? A.W : A.x)[k * A.n + i * nb + q.a] = sum;
+            }
+        }
+    }
+}
+
+template <typename K>
+static int run_seg(const irk_factor* f, K kernel, ApplyArgs& A, const irk_sched& S, int s, cudaStream_t st) {
+    const int nb = A.nb;
+    SegCfg SC;
+    SC.block_bytes = (int)(block_doubles(nb) * 8);
+    SC.stage_bytes = (SC.block_bytes + s * nb * 8 + 127) & ~127;
+    static const int nst_env = getenv("IRK_SEG_NST") ? atoi(getenv("IRK_SEG_NST")) : 0;   // tuning knob
+    SC.nst = nst_env > 1 ? nst_env : 2;
+    const int threads = 32 + ((A.G_ * nb + 31) / 32) * 32;
+    const size_t smem = (size_t)SC.nst * (SC.stage_bytes + 2 * sizeof(uint64_t) + sizeof(int4)) +
+                        sizeof(double) * 2 * (size_t)s * nb + 64;
+    IRK_CK(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)f->ctx->smem_optin));
+    int per_sm = 1;
+    IRK_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, threads, smem));
+    for (int64_t l = 0; l < S.nlevels; ++l) {
+        const int64_t lo = S.h_lvl_ptr[l], hi = S.h_lvl_ptr[l + 1];
+        if (hi == lo) continue;
+        A.order = S.d_order + lo;
+        A.ntasks = hi - lo;
+        const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(A.ntasks, (int64_t)f->ctx->num_sms * std::max(per_sm, 1)));
+        IRK_CK(launch_pdl_if(true, kernel, dim3(grid), dim3(threads), smem, st, A, SC));
+        IRK_LAUNCHED();
+    }
+    return IRK_OK;
+}
+
+// ---------------------------------------------------------------------------
 // Stage-coupled sweeps on the bulk-copy pipeline (coupled_solve,
 // numba_backend.py:128-151).  One task = one element i with ALL s stages: the
 // element DAG is the uncoupled one (2 levels on the colour-ordered meshes instead
@@ -1385,6 +1567,13 @@ static int unc_apply(const irk_factor* f, ApplyArgs& A0, cudaStream_t st) {
     A.G_ = deep ? (A.nb <= 64 ? 4 : (A.nb <= 128 ? 2 : 1)) : ws_groups(A.nb);
     if (EVEN && S <= 4 && A.G_ * A.nb <= 256) {
         const int64_t nf = (int64_t)f->pat->T;
+        static const bool seg_off = getenv("IRK_APPLY_SEG") && atoi(getenv("IRK_APPLY_SEG")) == 0;
+        if (f->l_implicit && !deep && !seg_off && (A.u_shared || A.fac_shared) && A.G_ <= 2) {
+            // level launches with the vector segments carried in the ring stages
+            IRK_TRY(run_seg(f, k_unc_sweep_seg<S, true>, A, f->fwd, S, st));
+            IRK_TRY(run_seg(f, k_unc_sweep_seg<S, false>, A, f->bwd, S, st));
+            return IRK_OK;
+        }
         if (f->l_implicit) {
             // implicit L: forward sweep streams the stage-shared J_ij with w_j = Dinv_j z_j and
             // finishes rows without upper blocks; the backward sweep covers the remaining rows
