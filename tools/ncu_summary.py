@@ -84,7 +84,7 @@ def main():
     # traffic per operation (apply = copy + fwd + bwd launches of one apply)
     traffic = {}
     for key, names in (("stage_matvec", ("k_stage_matvec_pipe",)),
-                       ("ilu0_apply", ("k_copy_rows", "k_unc_fwd_pipe", "k_unc_bwd_pipe"))):
+                       ("ilu0_apply", ("k_copy_rows", "k_unc_fwd_pipe", "k_unc_bwd_pipe", "k_unc_sweep_seg"))):
         per = [agg[n]["dram"] / agg[n]["n"] for n in agg if any(k in n for k in names)]
         cnt = [agg[n]["n"] for n in agg if any(k in n for k in names)]
         if key == "ilu0_apply":
