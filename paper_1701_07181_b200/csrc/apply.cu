@@ -1028,7 +1028,8 @@ __global__ void __launch_bounds__(288) k_unc_sweep_seg(ApplyArgs A, SegCfg SC) {
 }
 
 template <typename K>
-static int run_seg(const irk_factor* f, K kernel, ApplyArgs& A, const irk_sched& S, int s, cudaStream_t st) {
+static int run_seg(const irk_factor* f, K kernel, ApplyArgs& A, const irk_sched& S, int s, cudaStream_t st,
+                   int extra_doubles = 0, bool pdl = true) {
     const int nb = A.nb;
     SegCfg SC;
     SC.block_bytes = (int)(block_doubles(nb) * 8);
@@ -1037,7 +1038,7 @@ static int run_seg(const irk_factor* f, K kernel, ApplyArgs& A, const irk_sched&
     SC.nst = nst_env > 1 ? nst_env : 2;
     const int threads = 32 + ((A.G_ * nb + 31) / 32) * 32;
     const size_t smem = (size_t)SC.nst * (SC.stage_bytes + 2 * sizeof(uint64_t) + sizeof(int4)) +
-                        sizeof(double) * 2 * (size_t)s * nb + 64;
+                        sizeof(double) * (2 * (size_t)s * nb + (size_t)extra_doubles) + 64;
     IRK_CK(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)f->ctx->smem_optin));
     int per_sm = 1;
     IRK_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, threads, smem));
@@ -1047,7 +1048,7 @@ static int run_seg(const irk_factor* f, K kernel, ApplyArgs& A, const irk_sched&
         A.order = S.d_order + lo;
         A.ntasks = hi - lo;
         const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(A.ntasks, (int64_t)f->ctx->num_sms * std::max(per_sm, 1)));
-        IRK_CK(launch_pdl_if(true, kernel, dim3(grid), dim3(threads), smem, st, A, SC));
+        IRK_CK(launch_pdl_if(pdl, kernel, dim3(grid), dim3(threads), smem, st, A, SC));
         IRK_LAUNCHED();
     }
     return IRK_OK;
@@ -1445,6 +1446,232 @@ __global__ void __launch_bounds__(288) k_cpl_bwd_pipe(ApplyArgs A, PipeCfg PC) {
     }
 }
 
+// ---------------------------------------------------------------------------
+// Stage-coupled level sweeps with the vector segments in the ring stages (the
+// k_unc_sweep_seg layout applied to coupled_solve, numba_backend.py:128-151).
+// Element tasks, all stages; one thread per block row (G = 1) or 2 groups.
+//   forward:  items L_{k,ij} (+ segment z_{k,j}), then G_{kl,i} (the first one carries the
+//             own y_i segments); z_k = (y_k - sum L z) - sum_{l<k} G_kl z_l (in-task chain)
+//   backward: items U_ij (+ the S segments x_{.,j}), then for k = S-1..0 the coupling item
+//             (M_i with cv = sum_{l>k} a_kl x_l, or the stored C_kl blocks) and Dinv_k; the
+//             first chain item carries the own z_i segments
+// ---------------------------------------------------------------------------
+template <int S, bool FWD>
+__global__ void __launch_bounds__(288) k_cpl_sweep_seg(ApplyArgs A, SegCfg SC) {
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    const int nb = A.nb;
+    unsigned char* stages = smem_raw;
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem_raw + (size_t)SC.nst * SC.stage_bytes);
+    uint64_t* empty = full + SC.nst;
+    int4* desc = reinterpret_cast<int4*>(empty + SC.nst);
+    double* tv = reinterpret_cast<double*>(desc + SC.nst);   // [S][nb]: t / z of the task
+    double* xv = tv + S * nb;                                 // [S][nb]: finished x_l (backward)
+    double* cv = xv + S * nb;                                 // [nb]: combined coupling vector
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int ncons_warps = (blockDim.x >> 5) - 1, ncons = ncons_warps * 32;
+    constexpr int NPAIRS = S * (S - 1) / 2;
+    if (threadIdx.x == 0) {
+        for (int i = 0; i < SC.nst; ++i) {
+            mbar_init(full + i, 1);
+            mbar_init(empty + i, ncons_warps);
+        }
+        fence_mbar_init();
+    }
+    __syncthreads();
+    griddep_launch();
+    const int64_t bsz = (int64_t)SC.block_bytes / 8;
+    const uint32_t seg = (uint32_t)nb * 8;
+    const bool explicit_c = A.Cup != nullptr;
+    if (warp == 0) {
+        griddep_wait();   // PDL: the predecessor's output (y, x) is read from here on
+        if (lane != 0) return;
+        int st = 0;
+        uint32_t ph = 0;
+        auto push = [&](int4 d, const double* blk, const double* segbase, int64_t segstride, int nsg) {
+            mbar_wait(empty + st, ph ^ 1);
+            desc[st] = d;
+            unsigned char* dst = stages + (size_t)st * SC.stage_bytes;
+            mbar_expect_tx(full + st, SC.block_bytes + nsg * seg);
+            bulk_g2s(dst, blk, SC.block_bytes, full + st);
+            for (int k = 0; k < nsg; ++k)
+                bulk_g2s(dst + SC.block_bytes + k * seg, segbase + k * segstride, seg, full + st);
+            if (++st == SC.nst) { st = 0; ph ^= 1; }
+        };
+        const int64_t lo = A.ntasks * blockIdx.x / gridDim.x, hi = A.ntasks * (blockIdx.x + 1) / gridDim.x;
+        for (int64_t t = lo; t < hi; ++t) {
+            const int64_t i = A.order[t];
+            const int d = A.diag[i];
+            int n = 0;
+            if (FWD) {
+                const int q0 = A.indptr[i], l0 = A.lptr[i];
+                for (int m = 0; m < d - q0; ++m) {
+                    if (!A.keep[q0 + m]) continue;
+                    const int64_t col = A.indices[q0 + m];
+                    for (int k = 0; k < S; ++k, ++n)
+                        push(make_int4((int)i, k, PD_L | (n == 0 ? PD_FIRST : 0), 0),
+                             A.L + ((int64_t)(l0 + m) * S + k) * bsz, A.x + k * A.n + col * nb, 0, 1);
+                }
+                for (int k = 1; k < S; ++k)
+                    for (int l = 0; l < k; ++l, ++n) {
+                        const bool first_g = (k == 1 && l == 0);
+                        const int fl = PD_G | (n == 0 ? PD_FIRST : 0) | (k == S - 1 && l == k - 1 ? PD_LAST : 0);
+                        push(make_int4((int)i, k * S + l, fl, 0), A.G + (i * NPAIRS + pidx(k, l)) * bsz,
+                             A.y + i * nb, A.n, first_g ? S : 0);
+                    }
+            } else {
+                const int b0 = d + 1, nn = A.indptr[i + 1] - b0;
+                for (int m = 0; m < nn; ++m) {
+                    if (!A.keep[b0 + m]) continue;
+                    const int qq = b0 + m;
+                    const int64_t col = A.indices[qq];
+                    push(make_int4((int)i, 0, PD_USH | (n == 0 ? PD_FIRST : 0), 0), A.ubase[0] + (int64_t)qq * bsz,
+                         A.x + col * nb, A.n, S);
+                    ++n;
+                }
+                bool first_chain = true;
+                for (int k = S - 1; k >= 0; --k) {
+                    if (k < S - 1) {
+                        if (explicit_c) {
+                            for (int l = k + 1; l < S; ++l, ++n)
+                                push(make_int4((int)i, k * S + l, PD_C | (n == 0 ? PD_FIRST : 0), 0),
+                                     A.Cup + (i * NPAIRS + pidx(l, k)) * bsz, nullptr, 0, 0);
+                        } else {
+                            push(make_int4((int)i, k * S + S - 1, PD_C | (n == 0 ? PD_FIRST : 0), 0),
+                                 A.mass + i * bsz, nullptr, 0, 0);
+                            ++n;
+                        }
+                    }
+                    push(make_int4((int)i, k, PD_DINV | (n == 0 ? PD_FIRST : 0) | (k == 0 ? PD_LAST : 0), 0),
+                         A.Dinv + (i * S + k) * bsz, A.x + i * nb, A.n, first_chain ? S : 0);
+                    first_chain = false;
+                    ++n;
+                }
+            }
+        }
+        push(make_int4(-1, 0, PD_END, 0), A.Dinv, nullptr, 0, 0);
+        return;
+    }
+    const int c = threadIdx.x - 32;
+    const int G = A.G_, R = 32 / G;
+    Geo q;
+    q.nb = nb; q.P = (nb + 1) >> 1; q.G = G;
+    q.a = R * (c >> 5) + (c & (R - 1));
+    q.g = (c & 31) / R;
+    q.active = q.a < nb;
+    auto group_sum = [&](double v) -> double {
+        for (int o = R; o < 32; o <<= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+        return v;
+    };
+    griddep_wait();
+    int st = 0;
+    uint32_t ph = 0;
+    double part[S];
+    double acc = 0.0;
+    bool t_done = false;
+    for (;;) {
+        mbar_wait(full + st, ph);
+        const int4 dsc = desc[st];
+        if (dsc.z & PD_END) break;
+        const int64_t i = dsc.x;
+        const unsigned char* base = stages + (size_t)st * SC.stage_bytes;
+        const double2* B = reinterpret_cast<const double2*>(base);
+        const double* segs = reinterpret_cast<const double*>(base + SC.block_bytes);
+        if (dsc.z & PD_FIRST) {
+#pragma unroll
+            for (int k = 0; k < S; ++k) part[k] = 0.0;
+            acc = 0.0;
+            t_done = false;
+        }
+        auto release = [&]() {
+            __syncwarp();
+            if (lane == 0) mbar_arrive(empty + st);
+            if (++st == SC.nst) { st = 0; ph ^= 1; }
+        };
+        // t_k = own_k - uscale * sum part_k (own segments carried by this item)
+        auto finalize_t = [&](double scale) {
+#pragma unroll
+            for (int k = 0; k < S; ++k) {
+                const double sum = group_sum(part[k]);
+                if (q.active && q.g == 0) tv[k * nb + q.a] = segs[k * nb + q.a] - scale * sum;
+            }
+            consumer_sync(1, ncons);
+            t_done = true;
+        };
+        if (FWD) {
+            if (dsc.z & PD_L) {
+                const int kk = dsc.y;
+                if (q.active)
+#pragma unroll
+                    for (int k = 0; k < S; ++k)
+                        if (k == kk) part[k] = smem_gemv(B, segs, q, part[k]);
+                release();
+            } else {   // G item (k, l): z_k -= G_kl z_l
+                const int k = dsc.y / S, l = dsc.y - k * S;
+                if (!t_done) finalize_t(1.0);
+                if (q.active) acc = smem_gemv(B, tv + l * nb, q, acc);
+                release();
+                if (l == k - 1) {
+                    const double sum = group_sum(acc);
+                    if (q.active && q.g == 0) tv[k * nb + q.a] -= sum;
+                    consumer_sync(1, ncons);
+                    acc = 0.0;
+                }
+            }
+            if (dsc.z & PD_LAST) {
+                if (q.active && q.g == 0)
+#pragma unroll
+                    for (int k = 0; k < S; ++k) A.x[k * A.n + i * nb + q.a] = tv[k * nb + q.a];
+                consumer_sync(1, ncons);   // tv reuse by the next task
+            }
+        } else {
+            if (dsc.z & PD_USH) {
+                if (q.active) smem_gemv_all<S>(B, segs, q, part);
+                release();
+                continue;
+            }
+            if (!t_done) finalize_t(A.uscale);
+            if (dsc.z & PD_C) {
+                const int k = dsc.y / S, l = dsc.y - k * S;
+                if (explicit_c) {
+                    if (q.active) acc = smem_gemv(B, xv + l * nb, q, acc);
+                    release();
+                    if (l == S - 1) {
+                        const double sum = group_sum(acc);
+                        if (q.active && q.g == 0) tv[k * nb + q.a] -= sum;
+                        consumer_sync(1, ncons);
+                        acc = 0.0;
+                    }
+                } else {
+                    for (int e = c; e < nb; e += ncons) {
+                        double v = 0.0;
+                        for (int ll = k + 1; ll < S; ++ll) v = fma(A.cup_scale[k * A.s + ll], xv[ll * nb + e], v);
+                        cv[e] = v;
+                    }
+                    consumer_sync(1, ncons);
+                    double pm = 0.0;
+                    if (q.active) pm = smem_gemv(B, cv, q, 0.0);
+                    release();
+                    const double sum = group_sum(pm);
+                    if (q.active && q.g == 0) tv[k * nb + q.a] -= sum;
+                    consumer_sync(1, ncons);
+                }
+                continue;
+            }
+            // Dinv item k: x_k = Dinv_k t_k
+            const int k = dsc.y;
+            double pd = 0.0;
+            if (q.active) pd = smem_gemv(B, tv + k * nb, q, 0.0);
+            release();
+            const double sum = group_sum(pd);
+            if (q.active && q.g == 0) {
+                xv[k * nb + q.a] = sum;
+                A.x[k * A.n + i * nb + q.a] = sum;
+            }
+            consumer_sync(1, ncons);
+        }
+    }
+}
+
 // x[k][i] = y[k][i] for the elements of a level with no kept lower neighbour
 // (forward sweep: z_i = y_i) -- a plain vectorised row copy.
 __global__ void k_copy_rows(const int32_t* __restrict__ rows, int64_t nrows, const double* __restrict__ y,
@@ -1605,6 +1832,16 @@ static int unc_apply(const irk_factor* f, ApplyArgs& A0, cudaStream_t st) {
 template <int S>
 static int cpl_apply_pipe(const irk_factor* f, ApplyArgs& A0, cudaStream_t st) {
     const int64_t nf = (int64_t)f->pat->T;
+    static const bool seg_off = getenv("IRK_APPLY_SEG") && atoi(getenv("IRK_APPLY_SEG")) == 0;
+    const bool level = f->fwd.nlevels <= LEVEL_LAUNCH_MAX && f->bwd.nlevels <= LEVEL_LAUNCH_MAX;
+    if (level && !seg_off && f->u_shared && A0.nb <= 128) {
+        ApplyArgs A = A0;
+        A.G_ = ws_groups(A.nb);
+        static const bool cpl_pdl = getenv("IRK_CPL_PDL") && atoi(getenv("IRK_CPL_PDL")) != 0;   // A/B knob
+        IRK_TRY(run_seg(f, k_cpl_sweep_seg<S, true>, A, f->fwd, S, st, 0, cpl_pdl));
+        IRK_TRY(run_seg(f, k_cpl_sweep_seg<S, false>, A, f->bwd, S, st, A.nb, cpl_pdl));
+        return IRK_OK;
+    }
     // narrower CTAs, more tasks in flight (config 4: 7.85 -> 7.70 ms per RADAU23 step)
     ApplyArgs A = A0;
     if (!getenv("IRK_APPLY_G") && 2 * A.nb <= 256) A.G_ = std::min(2, (A.nb + 1) / 2);
