@@ -376,6 +376,17 @@ def run_b200(args):
     t_mv = timed(lambda: solver.op.apply_device(w, y), 20)
     log('components timed')
     t_ap = timed(lambda: solver.fac.apply_device(w, y), 10)
+    # the Arnoldi product P^-1 (B v) as irk_gmres runs it (stage matvec fused into the
+    # forward sweep when the factor qualifies, krylov.cu / apply.cu k_unc_fused_fwd)
+    import ctypes
+    from paper_1701_07181_b200 import _lib as L
+    fused_flag = ctypes.c_int(0)
+
+    def product():
+        L.check(L.lib().irk_op_factor_apply(solver.op._op.handle, solver.fac.handle, w.data_ptr(),
+                                            y.data_ptr(), ctypes.byref(fused_flag), L.stream_ptr()),
+                "irk_op_factor_apply")
+    t_fu = timed(product, 10) if solver.fac is not None else None
     t_fac = timed(lambda: solver.factorize(), 3)
     t_sol = timed(lambda: solver.solve(rhs, x=x), 3)
     peak, peak_src = hbm_peak()
@@ -390,16 +401,28 @@ def run_b200(args):
     # iters + 1 (true residual) matvecs
     share_ap = (it_mean + 1) * t_ap / (t / args.steps)
     share_mv = (it_mean + 1) * t_mv / (t / args.steps)
-    if ba is not None and share_ap >= share_mv:
-        dom = {"name": "ilu0_apply (fwd+bwd sweeps, all stages)", "bytes": ba, "t": t_ap, "share": share_ap}
+    bf = (bm + ba - (T * r // 2) * 8 * nb * nb - 2 * s * 8 * T * nb) if (ba is not None and implicit_l) else None
+    if bf is not None and fused_flag.value:
+        # per stage-solve: `iters` fused products, one plain apply (P^-1 b), one matvec (true residual)
+        share_ap = t_ap / (t / args.steps)
+        share_mv = t_mv / (t / args.steps)
+        share_fu = it_mean * t_fu / (t / args.steps)
     else:
-        dom = {"name": "stage_matvec (fused)", "bytes": bm, "t": t_mv, "share": share_mv}
+        share_fu = 0.0
+    if share_fu > max(share_ap, share_mv):
+        dom = {"name": "arnoldi_product P^-1 (B v) (matvec fused into the forward sweep + backward sweep)",
+               "bytes": bf, "t": t_fu, "share": share_fu, "key": "arnoldi_product"}
+    elif ba is not None and share_ap >= share_mv:
+        dom = {"name": "ilu0_apply (fwd+bwd sweeps, all stages)", "bytes": ba, "t": t_ap, "share": share_ap,
+               "key": "ilu0_apply"}
+    else:
+        dom = {"name": "stage_matvec (fused)", "bytes": bm, "t": t_mv, "share": share_mv, "key": "stage_matvec"}
     achieved = dom["bytes"] / dom["t"] / 1e9
     traffic = None
     try:   # DRAM bytes per launch from the committed ncu --set full capture (profiles/)
         with open(os.path.join(REPO, "profiles", "r1_traffic.json")) as fh:
             tj = json.load(fh)
-        traffic = tj["ilu0_apply" if dom["name"].startswith("ilu0") else "stage_matvec"]
+        traffic = tj[dom["key"]]
     except Exception:
         pass
     roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
@@ -413,6 +436,10 @@ def run_b200(args):
         "apply_ms": 1e3 * t_ap,
         "apply_GBps": (ba / t_ap / 1e9) if ba else None,
         "apply_frac": (ba / t_ap / 1e9 / peak) if ba else None,
+        "arnoldi_product_ms": (1e3 * t_fu) if t_fu else None,
+        "arnoldi_product_fused": bool(fused_flag.value),
+        "arnoldi_product_GBps": (bf / t_fu / 1e9) if (bf and t_fu and fused_flag.value) else None,
+        "arnoldi_product_frac": (bf / t_fu / 1e9 / peak) if (bf and t_fu and fused_flag.value) else None,
         "factor_ms": 1e3 * t_fac, "gmres_ms": 1e3 * t_sol, "gmres_iterations": iters[-1],
         "gmres_ms_per_iteration": 1e3 * t_sol / max(iters[-1], 1),
         "levels_fwd_bwd": list(solver.fac.levels()) if solver.fac is not None else None,

@@ -140,6 +140,16 @@ IRK_API void irk_factor_destroy(irk_factor *f);
  * StageUncoupledIlu0.apply / StageCoupledIlu0.apply, precond.py:79-87,
  * 222-241, 152-162).  x may alias nothing else; y is not modified. */
 IRK_API int irk_factor_apply(const irk_factor *f, const double *y, double *x, void *stream);
+/* x = P^-1 (B v): one Arnoldi product of the left-preconditioned GMRES loop
+ * (krylov.py:88-89: apply_precond(apply_operator(v))) with B the stage operator
+ * (stage_system.py:52-70) and P the factor.  When the factor is the uncoupled
+ * implicit-L ILU(0) of the operator's own Jacobian blocks on a colour schedule,
+ * the matvec runs inside the forward sweep (each lower Jacobian block read once
+ * for both products, B v never stored); otherwise the two calls run back to back
+ * through a scratch vector.  *fused (optional) = 1 if the fused path ran.
+ * irk_gmres takes the fused path itself for native (stage op, factor) pairs. */
+IRK_API int irk_op_factor_apply(const irk_stage_op *op, const irk_factor *f, const double *v, double *x,
+                                int *fused, void *stream);
 /* One single-stage factor (s = 1, e.g. ilu0_factorize of J itself) applied to
  * nrhs stage-major right-hand sides y (nrhs, T, m) -> x in one sweep that reads
  * every factor block once (BASELINE config 3).  Same result as nrhs separate

@@ -84,6 +84,7 @@ _SIGS = {
                                     c_vp]),
     "irk_factor_destroy": (None, [c_vp]),
     "irk_factor_apply": (c_int, [c_vp, c_vp, c_vp, c_vp]),
+    "irk_op_factor_apply": (c_int, [c_vp, c_vp, c_vp, c_vp, P(c_int), c_vp]),
     "irk_stage_op_apply_range": (c_int, [c_vp, c_vp, c_vp, c_i64, c_i64, c_vp]),
     "irk_stage_op_apply_rows": (c_int, [c_vp, c_vp, c_vp, c_vp, c_i64, c_vp]),
     "irk_factor_apply_rhs": (c_int, [c_vp, c_int, c_vp, c_vp, c_vp]),

@@ -1027,6 +1027,182 @@ __global__ void __launch_bounds__(288) k_unc_sweep_seg(ApplyArgs A, SegCfg SC) {
     }
 }
 
+// ---------------------------------------------------------------------------
+// Stage matvec fused into the implicit-L forward sweep (one GMRES Arnoldi
+// product w = P^-1 (B v), krylov.py:88-89 with stage_system.py:52-70 and
+// precond.py:222-241).  A task (row i) streams its Jacobian row once: every block
+// J_ij multiplies the S stage segments of v (the matvec), and a kept lower block
+// also the S segments of w_j = Dinv_j z_j (the sweep) -- one shared-memory block,
+// two products, so the lower half of J is read once per iteration instead of
+// twice.  Then M_i times v_i (mass mixing), y_i = alpha J v + mix (M v) formed in
+// registers (never stored), t = y_i - uscale sum_j J_ij w_j, and the S Dinv items
+// as in k_unc_sweep_seg<S, true>.  The backward sweep is unchanged.
+// ---------------------------------------------------------------------------
+enum { PD_MV = 1024, PD_FU2 = 2048, PD_MM = 4096 };
+
+struct FusedMv {
+    const double* J;    // operator blocks (== factor ubase[0])
+    const double* M;
+    const double* v;    // operator input (s, T, nb)
+    double alpha;
+    double mix[IRK_MAX_STAGES * IRK_MAX_STAGES];
+};
+
+template <int S>
+__global__ void __launch_bounds__(288) k_unc_fused_fwd(ApplyArgs A, SegCfg SC, FusedMv F) {
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    const int nb = A.nb;
+    unsigned char* stages = smem_raw;
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem_raw + (size_t)SC.nst * SC.stage_bytes);
+    uint64_t* empty = full + SC.nst;
+    int4* desc = reinterpret_cast<int4*>(empty + SC.nst);
+    double* tvb = reinterpret_cast<double*>(desc + SC.nst);      // [2][S][nb]
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int ncons_warps = (blockDim.x >> 5) - 1, ncons = ncons_warps * 32;
+    if (threadIdx.x == 0) {
+        for (int i = 0; i < SC.nst; ++i) {
+            mbar_init(full + i, 1);
+            mbar_init(empty + i, ncons_warps);
+        }
+        fence_mbar_init();
+    }
+    __syncthreads();
+    griddep_launch();
+    const int64_t bsz = (int64_t)SC.block_bytes / 8;
+    const uint32_t seg = (uint32_t)nb * 8;
+    if (warp == 0) {
+        griddep_wait();
+        if (lane != 0) return;
+        int st = 0;
+        uint32_t ph = 0;
+        auto push = [&](int4 d, const double* blk, const double* s1, const double* s2) {
+            mbar_wait(empty + st, ph ^ 1);
+            desc[st] = d;
+            unsigned char* dst = stages + (size_t)st * SC.stage_bytes;
+            const int nsg = (s1 ? S : 0) + (s2 ? S : 0);
+            mbar_expect_tx(full + st, SC.block_bytes + nsg * seg);
+            bulk_g2s(dst, blk, SC.block_bytes, full + st);
+            dst += SC.block_bytes;
+            if (s1)
+                for (int k = 0; k < S; ++k, dst += seg) bulk_g2s(dst, s1 + k * A.n, seg, full + st);
+            if (s2)
+                for (int k = 0; k < S; ++k, dst += seg) bulk_g2s(dst, s2 + k * A.n, seg, full + st);
+            if (++st == SC.nst) { st = 0; ph ^= 1; }
+        };
+        const int64_t lo = A.ntasks * blockIdx.x / gridDim.x, hi = A.ntasks * (blockIdx.x + 1) / gridDim.x;
+        for (int64_t t = lo; t < hi; ++t) {
+            const int64_t i = A.order[t];
+            const int d = A.diag[i];
+            const int b0 = A.indptr[i], b1 = A.indptr[i + 1];
+            const int store_z = A.hasup[i] ? 1 : 0;
+            for (int qq = b0; qq < b1; ++qq) {
+                const int64_t col = A.indices[qq];
+                const bool low = qq < d && A.keep[qq];
+                push(make_int4((int)i, 0, (low ? PD_FU2 : PD_MV) | (qq == b0 ? PD_FIRST : 0), 0),
+                     F.J + (int64_t)qq * bsz, F.v + col * nb, low ? A.W + col * nb : nullptr);
+            }
+            if (F.M) push(make_int4((int)i, 0, PD_MM, 0), F.M + i * bsz, F.v + i * nb, nullptr);
+            for (int k = 0; k < S; ++k)
+                push(make_int4((int)i, k, PD_DINV | (k == S - 1 ? PD_LAST : 0), store_z), A.Dinv + (i * S + k) * bsz,
+                     nullptr, nullptr);
+        }
+        push(make_int4(-1, 0, PD_END, 0), A.Dinv, nullptr, nullptr);   // block copy unused (harmless)
+        return;
+    }
+    const int c = threadIdx.x - 32;
+    const int G = A.G_, R = 32 / G;
+    Geo q;
+    q.nb = nb; q.P = (nb + 1) >> 1; q.G = G;
+    q.a = R * (c >> 5) + (c & (R - 1));
+    q.g = (c & 31) / R;
+    q.active = q.a < nb;
+    auto group_sum = [&](double v) -> double {
+        for (int o = R; o < 32; o <<= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+        return v;
+    };
+    griddep_wait();
+    int st = 0;
+    uint32_t ph = 0;
+    double pj[S], pm[S], pw[S];   // J v, M v, sum_j J_ij w_j
+    int par = 0;
+    for (;;) {
+        mbar_wait(full + st, ph);
+        const int4 dsc = desc[st];
+        if (dsc.z & PD_END) break;
+        const int64_t i = dsc.x;
+        const unsigned char* base = stages + (size_t)st * SC.stage_bytes;
+        const double2* B = reinterpret_cast<const double2*>(base);
+        const double* segs = reinterpret_cast<const double*>(base + SC.block_bytes);
+        double* tv = tvb + (size_t)par * S * nb;
+        const bool store_z = dsc.w != 0;
+        if (dsc.z & PD_FIRST) {
+#pragma unroll
+            for (int k = 0; k < S; ++k) pj[k] = pm[k] = pw[k] = 0.0;
+        }
+        if (dsc.z & PD_FU2) {
+            if (q.active)
+                for (int p = q.g; p < q.P; p += q.G) {
+                    const double2 b = B[p * nb + q.a];
+#pragma unroll
+                    for (int k = 0; k < S; ++k) {
+                        const double2 v = *reinterpret_cast<const double2*>(segs + k * nb + 2 * p);
+                        const double2 w = *reinterpret_cast<const double2*>(segs + (S + k) * nb + 2 * p);
+                        pj[k] = fma(b.y, v.y, fma(b.x, v.x, pj[k]));
+                        pw[k] = fma(b.y, w.y, fma(b.x, w.x, pw[k]));
+                    }
+                }
+        } else if (dsc.z & PD_MV) {
+            if (q.active) smem_gemv_all<S>(B, segs, q, pj);
+        } else if (dsc.z & PD_MM) {
+            if (q.active) smem_gemv_all<S>(B, segs, q, pm);
+        } else {
+            const int kk = dsc.y;
+            if (kk == 0) {
+                // y_k = alpha (J v)_k + sum_l mix_kl (M v)_l ; t_k = y_k - uscale sum_j J_ij w_jk
+                double jv[S], mv[S];
+#pragma unroll
+                for (int k = 0; k < S; ++k) {
+                    jv[k] = group_sum(pj[k]);
+                    mv[k] = F.M ? group_sum(pm[k]) : 0.0;
+                    pw[k] = group_sum(pw[k]);
+                }
+                if (q.active && q.g == 0) {
+#pragma unroll
+                    for (int k = 0; k < S; ++k) {
+                        double y = F.alpha * jv[k];
+                        if (F.M) {
+#pragma unroll
+                            for (int l = 0; l < S; ++l) y += F.mix[k * S + l] * mv[l];
+                        }
+                        const double tval = y - A.uscale * pw[k];
+                        tv[k * nb + q.a] = tval;
+                        if (store_z) A.x[k * A.n + i * nb + q.a] = tval;   // z_i for the backward sweep
+                    }
+                }
+#pragma unroll
+                for (int k = 0; k < S; ++k) pj[k] = 0.0;   // reused as the Dinv accumulator
+                consumer_sync(1, ncons);
+            }
+            if (q.active) {
+#pragma unroll
+                for (int k = 0; k < S; ++k)
+                    if (k == kk) pj[k] = smem_gemv(B, tv + k * nb, q, pj[k]);
+            }
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(empty + st);
+        if (++st == SC.nst) { st = 0; ph ^= 1; }
+        if (dsc.z & PD_LAST) {
+            par ^= 1;
+#pragma unroll
+            for (int k = 0; k < S; ++k) {
+                const double sum = group_sum(pj[k]);
+                if (q.active && q.g == 0) (store_z ? A.W : A.x)[k * A.n + i * nb + q.a] = sum;
+            }
+        }
+    }
+}
+
 template <typename K>
 static int run_seg(const irk_factor* f, K kernel, ApplyArgs& A, const irk_sched& S, int s, cudaStream_t st,
                    int extra_doubles = 0, bool pdl = true) {
@@ -1049,6 +1225,38 @@ static int run_seg(const irk_factor* f, K kernel, ApplyArgs& A, const irk_sched&
         A.ntasks = hi - lo;
         const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(A.ntasks, (int64_t)f->ctx->num_sms * std::max(per_sm, 1)));
         IRK_CK(launch_pdl_if(pdl, kernel, dim3(grid), dim3(threads), smem, st, A, SC));
+        IRK_LAUNCHED();
+    }
+    return IRK_OK;
+}
+
+// level launches of k_unc_fused_fwd: ring stages hold a block and up to 2 S segments
+template <int S>
+static int run_fused_fwd(const irk_factor* f, ApplyArgs& A, const FusedMv& F, cudaStream_t st) {
+    const int nb = A.nb;
+    const irk_sched& Sd = f->fwd;
+    SegCfg SC;
+    SC.block_bytes = (int)(block_doubles(nb) * 8);
+    SC.stage_bytes = (SC.block_bytes + 2 * S * nb * 8 + 127) & ~127;
+    static const int nst_env = getenv("IRK_FUSED_NST") ? atoi(getenv("IRK_FUSED_NST")) : 0;   // tuning knob
+    SC.nst = nst_env > 1 ? nst_env : 2;
+    const int threads = 32 + ((A.G_ * nb + 31) / 32) * 32;
+    const size_t smem = (size_t)SC.nst * (SC.stage_bytes + 2 * sizeof(uint64_t) + sizeof(int4)) +
+                        sizeof(double) * 2 * (size_t)S * nb + 64;
+    static bool attr = false;
+    if (!attr) {
+        IRK_CK(cudaFuncSetAttribute(k_unc_fused_fwd<S>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)f->ctx->smem_optin));
+        attr = true;
+    }
+    int per_sm = 1;
+    IRK_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_unc_fused_fwd<S>, threads, smem));
+    for (int64_t l = 0; l < Sd.nlevels; ++l) {
+        const int64_t lo = Sd.h_lvl_ptr[l], hi = Sd.h_lvl_ptr[l + 1];
+        if (hi == lo) continue;
+        A.order = Sd.d_order + lo;
+        A.ntasks = hi - lo;
+        const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(A.ntasks, (int64_t)f->ctx->num_sms * std::max(per_sm, 1)));
+        IRK_CK(launch_pdl(k_unc_fused_fwd<S>, dim3(grid), dim3(threads), smem, st, A, SC, F));
         IRK_LAUNCHED();
     }
     return IRK_OK;
@@ -1922,6 +2130,49 @@ int factor_apply(const irk_factor* f, const double* y, double* x, cudaStream_t s
     }
 }
 
+// x = P^-1 (B v): the stage operator fused into the forward sweep (k_unc_fused_fwd).
+// Returns 1 (nothing launched) when the pair does not qualify: uncoupled implicit-L
+// factor on the operator's own pattern and Jacobian blocks, colour (level-launch)
+// schedule, shared J, no halo.  IRK_FUSED=0 disables it (A/B switch).
+template <int S>
+static int fused_apply_t(const irk_stage_op* op, const irk_factor* f, const double* v, double* x, cudaStream_t st) {
+    ApplyArgs A{};
+    fill_args(f, A);
+    A.G_ = ws_groups(A.nb);
+    if (A.G_ > 2 || A.G_ * A.nb > 256) return 1;
+    A.y = nullptr;
+    A.x = x;
+    A.epoch = ++f->epoch;
+    FusedMv F{};
+    F.J = f->ubase[0];
+    F.M = op->M ? op->M->d : nullptr;
+    F.v = v;
+    F.alpha = op->alpha;
+    for (int e = 0; e < S * S; ++e) F.mix[e] = op->C[e];
+    IRK_TRY(run_fused_fwd<S>(f, A, F, st));
+    IRK_TRY(run_seg(f, k_unc_sweep_seg<S, false>, A, f->bwd, S, st));
+    return IRK_OK;
+}
+
+int factor_apply_fused(const irk_stage_op* op, const irk_factor* f, const double* v, double* x, cudaStream_t st) {
+    static const bool off = getenv("IRK_FUSED") && atoi(getenv("IRK_FUSED")) == 0;
+    static const bool seg_off = getenv("IRK_APPLY_SEG") && atoi(getenv("IRK_APPLY_SEG")) == 0;
+    if (off || seg_off || !op || !f) return 1;
+    if (f->kind != IRK_FACTOR_UNCOUPLED || !f->l_implicit || f->u_stored || !f->u_shared) return 1;
+    if (f->fwd.nlevels > LEVEL_LAUNCH_MAX || f->bwd.nlevels > LEVEL_LAUNCH_MAX) return 1;
+    if (op->pat != f->pat || op->s != f->s || op->nb != f->nb || !op->shared_j || op->ghost ||
+        op->T_local != f->pat->T || f->nb % 2)
+        return 1;
+    if (op->J[0]->d + op->jfirst[0] * block_doubles(op->nb) != f->ubase[0]) return 1;
+    switch (f->s) {
+        case 1: return fused_apply_t<1>(op, f, v, x, st);
+        case 2: return fused_apply_t<2>(op, f, v, x, st);
+        case 3: return fused_apply_t<3>(op, f, v, x, st);
+        case 4: return fused_apply_t<4>(op, f, v, x, st);
+        default: return 1;
+    }
+}
+
 // One factor (s = 1) applied to nrhs stage-major right-hand sides in one sweep:
 // every factor block (Dinv_i, the implicit/stored upper blocks, stored L) is read
 // once for all right-hand sides (BASELINE config 3: plain ILU(0) of J, s RHS).
@@ -2027,6 +2278,24 @@ int irk_factor_apply(const irk_factor* f, const double* y, double* x, void* stre
     IRK_ARG(f && y && x, "NULL argument");
     IRK_ARG(y != x, "x must not alias y");
     return factor_apply(f, y, x, (cudaStream_t)stream);
+}
+
+int irk_op_factor_apply(const irk_stage_op* op, const irk_factor* f, const double* v, double* x, int* fused,
+                        void* stream) {
+    IRK_ARG(op && f && v && x, "NULL argument");
+    IRK_ARG(v != x, "x must not alias v");
+    IRK_ARG(op->s == f->s && op->nb == f->nb && op->T_local == f->pat->T, "operator and factor shapes differ");
+    cudaStream_t st = (cudaStream_t)stream;
+    const int rc = factor_apply_fused(op, f, v, x, st);
+    if (rc < 0) return rc;
+    if (fused) *fused = rc == 0 ? 1 : 0;
+    if (rc == 0) return IRK_OK;
+    double* tmp = nullptr;
+    IRK_CK(cudaMallocAsync(&tmp, sizeof(double) * op->s * op->T_local * op->nb, st));
+    int r = irk_stage_op_apply(op, v, tmp, stream);
+    if (r == IRK_OK) r = factor_apply(f, tmp, x, st);
+    cudaFreeAsync(tmp, st);
+    return r;
 }
 
 int irk_factor_apply_rhs(const irk_factor* f, int nrhs, const double* y, double* x, void* stream) {

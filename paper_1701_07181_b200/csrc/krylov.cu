@@ -26,6 +26,7 @@
 namespace irk {
 
 int factor_apply(const irk_factor* f, const double* y, double* x, cudaStream_t st);
+int factor_apply_fused(const irk_stage_op* op, const irk_factor* f, const double* v, double* x, cudaStream_t st);
 
 constexpr int VB = 256;      // threads per vector CTA
 constexpr int VGROUP = 8;    // vectors per multidot pass
@@ -806,7 +807,14 @@ int irk_gmres(irk_ctx* ctx, int64_t n, irk_linop op, irk_linop pre, irk_allreduc
         breakdown = false;
         for (int j = 0; j < cycle; ++j) {
             double* w = V(j + 1);
-            if (pre.fn) {
+            int fused = 1;
+            if (op.fn == linop_stage && pre.fn == linop_factor) {
+                // native pair: stage matvec fused into the forward sweep (apply.cu)
+                fused = factor_apply_fused((const irk_stage_op*)op.user, (const irk_factor*)pre.user, V(j), w, st);
+                if (fused < 0) return fused;
+            }
+            if (fused == 0) {
+            } else if (pre.fn) {
                 IRK_TRY(call(op, V(j), ws.tmp));
                 IRK_TRY(call(pre, ws.tmp, w));
             } else {

@@ -505,3 +505,42 @@ def test_stage_matvec_row_range_and_list(nb):
     yf, yy = y_full.view(cfg.s, p.T, nb), y.view(cfg.s, p.T, nb)
     assert torch.equal(yy[:, r0:r1], yf[:, r0:r1])
     assert rel(yy.cpu().numpy(), yf.cpu().numpy()) < 1e-15
+
+
+@pytest.mark.parametrize("s_scheme", ["RADAU23", "RADAU35"])
+@pytest.mark.parametrize("ordering,nparts", [("color", 1), ("color", 3), ("natural", 1)])
+def test_fused_operator_precond_product(s_scheme, ordering, nparts):
+    """irk_op_factor_apply (the Arnoldi product P^-1 (B v) with the stage matvec
+    fused into the implicit-L forward sweep, krylov.py:88-89) == the separate
+    irk_stage_op_apply + irk_factor_apply, within the 1e-12 apply bar; colour
+    schedules take the fused kernel (also with cross-partition lower blocks
+    dropped), the deep natural schedule falls back to the two calls."""
+    import ctypes
+    import torch
+    from paper_1701_07181_b200 import _lib as L
+    from paper_1701_07181_b200.blocks import DevicePattern
+    from paper_1701_07181_b200.krylov import GmresConfig
+    from paper_1701_07181_b200.solver import StageSolver
+    from paper_1701_07181_b200.meshes import partition_bounds
+    cfg = W.CONFIGS[1].scaled(N=8, ordering=ordering, scheme=s_scheme)
+    s = cfg.s
+    wl = W.make_workload(cfg, norm_iters=10)
+    p = wl.pattern
+    dp = DevicePattern(p.indptr, p.indices, p.diag_pos)
+    part = None if nparts == 1 else np.repeat(np.arange(nparts), np.diff(partition_bounds(p.T, nparts)))
+    sol = StageSolver(dp, wl.J, wl.M, wl.a_inv, wl.dt, kind="uncoupled", shifts=wl.shifts,
+                      partition_of=part, gmres_cfg=GmresConfig(rel_tol=1e-8, restart=40))
+    sol.factorize()
+    assert sol.fac.implicit_l
+    v = torch.from_numpy(np.random.default_rng(s).standard_normal(sol.n)).cuda()
+    y = torch.empty_like(v)
+    x_ref = torch.empty_like(v)
+    sol.op.apply_device(v, y)
+    sol.fac.apply_device(y, x_ref)
+    x = torch.full_like(v, float("nan"))
+    fused = ctypes.c_int(-1)
+    L.check(L.lib().irk_op_factor_apply(sol.op._op.handle, sol.fac.handle, v.data_ptr(), x.data_ptr(),
+                                        ctypes.byref(fused), L.stream_ptr()), "irk_op_factor_apply")
+    torch.cuda.synchronize()
+    assert fused.value == (1 if ordering == "color" else 0)
+    assert rel(x.cpu().numpy(), x_ref.cpu().numpy()) < 1e-12

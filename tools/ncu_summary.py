@@ -81,23 +81,33 @@ def main():
     for name, g in sorted(agg.items(), key=lambda kv: -kv[1]["us"]):
         lines.append(f"| `{name}` | {g['n_step']:g} | {g['us']/1e3/a.steps:.3f} | {100*g['us']/a.steps/tot:.1f}% | "
                      f"{g['dram']/g['n']/1e9:.4f} |")
-    # traffic per operation (apply = copy + fwd + bwd launches of one apply)
-    traffic = {}
-    for key, names in (("stage_matvec", ("k_stage_matvec_pipe",)),
-                       ("ilu0_apply", ("k_copy_rows", "k_unc_fwd_pipe", "k_unc_bwd_pipe", "k_unc_sweep_seg"))):
-        per = [agg[n]["dram"] / agg[n]["n"] for n in agg if any(k in n for k in names)]
-        cnt = [agg[n]["n"] for n in agg if any(k in n for k in names)]
-        if key == "ilu0_apply":
-            # a stage-solve makes as many applies (P^-1 b + one per iteration) as matvecs
-            # (one per iteration + the true residual): scale the sweep launches to one apply
-            napply = next((agg[n]["n"] for n in agg if "k_stage_matvec" in n), 1)
-            val = sum(agg[n]["dram"] for n in agg if any(k in n for k in names)) / max(napply, 1)
-        else:
-            val = per[0] if per else None
-        traffic[key] = val
+    # traffic per operation.  Per step: `it` Arnoldi products P^-1 (B v) (fused forward
+    # launches + one backward sweep each), one plain apply (P^-1 b: forward + backward
+    # sweeps), one plain matvec (true residual).  Backward sweeps: one launch per apply.
+    import re
+
+    def tot(pat):
+        return sum(agg[n]["dram"] for n in agg if re.search(pat, n))
+
+    def cnt(pat):
+        return sum(agg[n]["n"] for n in agg if re.search(pat, n))
+    it = cnt(r"k_multidot") or 1
+    n_bwd = cnt(r"k_unc_sweep_seg<\d+, 0>|k_unc_bwd_pipe<\d+, \w+, false>") or 1
+    bwd = tot(r"k_unc_sweep_seg<\d+, 0>|k_unc_bwd_pipe<\d+, \w+, false>") / n_bwd
+    n_fused = it if cnt(r"k_unc_fused_fwd") else 0
+    n_fwd = max(n_bwd - n_fused, 1)
+    fwd = tot(r"k_copy_rows|k_unc_fwd_pipe|k_unc_bwd_pipe<\d+, \w+, true>|k_unc_sweep_seg<\d+, 1>") / n_fwd
+    mv = [agg[n]["dram"] / agg[n]["n"] for n in agg if "k_stage_matvec" in n]
+    traffic = {"stage_matvec": mv[0] if mv else None, "ilu0_apply": fwd + bwd}
+    if n_fused:
+        traffic["arnoldi_product"] = tot(r"k_unc_fused_fwd") / n_fused + bwd
     lines += ["", "DRAM traffic per operation (bytes):", "",
               f"* stage matvec: {traffic['stage_matvec']:.4e} (algorithmic 2.161e9)",
-              f"* ILU apply (all launches of one apply): {traffic['ilu0_apply']:.4e} (algorithmic 3.240e9 with the implicit-L factor)"]
+              f"* ILU apply (forward + backward sweeps of one apply): {traffic['ilu0_apply']:.4e} "
+              f"(algorithmic 3.240e9 with the implicit-L factor)"]
+    if n_fused:
+        lines.append(f"* Arnoldi product P^-1 (B v) (fused forward + backward sweep): "
+                     f"{traffic['arnoldi_product']:.4e} (algorithmic 4.709e9)")
     want = ["gpu__time_duration.sum", "dram__throughput.avg.pct_of_peak_sustained_elapsed",
             "sm__throughput.avg.pct_of_peak_sustained_elapsed", "sm__warps_active.avg.pct_of_peak_sustained_active",
             "launch__registers_per_thread", "dram__bytes_read.sum", "dram__bytes_write.sum",
