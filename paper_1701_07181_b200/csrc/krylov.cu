@@ -575,19 +575,31 @@ static int cgs2_fused(const irk_ctx* ctx, int64_t n, int64_t ldv, int nv, const 
 // w' = w - V h1 with h2 = V^T w' (+ w'.w'); pass 3 DGKS correction and the
 // scaling by ||w''|| (k_finish_v).  out = [h1 (nv+1) | h2 (nv+1) | ||w''||^2,
 // reorth, needs-exact-norm].
+// one full wave: SMs x resident CTAs of the kernel (<= vec_blocks, the partials' capacity);
+// a fixed 4 CTAs/SM left a partial second wave for the 72-92-register passes
+template <typename K>
+static int one_wave(const irk_ctx* ctx, K kernel) {
+    int per_sm = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, VB, 0) != cudaSuccess || per_sm < 1) per_sm = 1;
+    static const bool legacy = getenv("IRK_CGS_WAVE") && atoi(getenv("IRK_CGS_WAVE")) == 0;   // A/B switch
+    return legacy ? vec_blocks(ctx) : std::min(vec_blocks(ctx), ctx->num_sms * per_sm);
+}
+
 template <int NVM>
 static int cgs2_v_t(const irk_ctx* ctx, int64_t n, int64_t ldv, int nv, const double* V, double* w, double eta,
                      double brk, double* partials, unsigned* counters, double* out, cudaStream_t st) {
-    const int nb = vec_blocks(ctx);
+    static const int g1 = one_wave(ctx, k_multidot_v<NVM>);
+    static const int g2 = one_wave(ctx, k_update_dots_v<NVM>);
+    static const int g3 = one_wave(ctx, k_finish_v<NVM>);
     double* h1 = out;
     double* h2 = out + nv + 1;
-    IRK_CK(launch_pdl(k_multidot_v<NVM>, dim3(nb), dim3(VB), 0, st, V, ldv, nv, (const double*)w, n, partials, h1,
+    IRK_CK(launch_pdl(k_multidot_v<NVM>, dim3(g1), dim3(VB), 0, st, V, ldv, nv, (const double*)w, n, partials, h1,
                       counters));
     IRK_LAUNCHED();
-    IRK_CK(launch_pdl(k_update_dots_v<NVM>, dim3(nb), dim3(VB), 0, st, V, ldv, nv, (const double*)h1, w, n, partials,
+    IRK_CK(launch_pdl(k_update_dots_v<NVM>, dim3(g2), dim3(VB), 0, st, V, ldv, nv, (const double*)h1, w, n, partials,
                       h2, counters + 1));
     IRK_LAUNCHED();
-    IRK_CK(launch_pdl(k_finish_v<NVM>, dim3(nb), dim3(VB), 0, st, V, ldv, nv, (const double*)(h1 + nv),
+    IRK_CK(launch_pdl(k_finish_v<NVM>, dim3(g3), dim3(VB), 0, st, V, ldv, nv, (const double*)(h1 + nv),
                       (const double*)h2, eta, brk, w, n, out + 2 * (nv + 1)));
     IRK_LAUNCHED();
     return IRK_OK;

@@ -544,3 +544,47 @@ def test_fused_operator_precond_product(s_scheme, ordering, nparts):
     torch.cuda.synchronize()
     assert fused.value == (1 if ordering == "color" else 0)
     assert rel(x.cpu().numpy(), x_ref.cpu().numpy()) < 1e-12
+
+
+def test_fused_product_dirk_stage_matrix():
+    """The DIRK stage (build_stage_matrix + ilu0_factorize + gmres(mat.matvec, fac.apply),
+    stepper.py:268-274) takes the fused Arnoldi product with s = 1: same result as the
+    StageMatrix matvec followed by the factor apply (<= 1e-12), and the GMRES solve
+    through the fused path matches the oracle's iteration count and solution."""
+    import ctypes
+    import torch
+    from paper_1701_07181_b200 import _lib as L
+    from paper_1701_07181_b200.blocks import BlockDiagonalMatrix, BlockSparseMatrix, DeviceBlocks, DevicePattern
+    from paper_1701_07181_b200.krylov import GmresConfig, gmres
+    from paper_1701_07181_b200.precond import build_stage_matrix, ilu0_factorize
+    cfg = W.CONFIGS[1].scaled(N=8, ordering="color")
+    wl = W.make_workload(cfg, norm_iters=10)
+    p = wl.pattern
+    J = BlockSparseMatrix(DevicePattern(p.indptr, p.indices, p.diag_pos), DeviceBlocks.from_host(wl.J))
+    gamma_dt = 0.4358665215 * wl.dt
+    mat = build_stage_matrix(1.0, BlockDiagonalMatrix(wl.M), J, gamma_dt)
+    fac = ilu0_factorize(mat)
+    v = torch.from_numpy(np.random.default_rng(5).standard_normal(mat.n)).cuda()
+    y = torch.empty_like(v)
+    x_ref = torch.empty_like(v)
+    mat.apply_device(v, y)
+    fac.apply_device(y, x_ref)
+    x = torch.full_like(v, float("nan"))
+    fused = ctypes.c_int(-1)
+    L.check(L.lib().irk_op_factor_apply(mat._native_op().handle, fac.handle, v.data_ptr(), x.data_ptr(),
+                                        ctypes.byref(fused), L.stream_ptr()), "irk_op_factor_apply")
+    torch.cuda.synchronize()
+    assert fused.value == 1
+    assert rel(x.cpu().numpy(), x_ref.cpu().numpy()) < 1e-12
+    # GMRES through the fused path vs the oracle on the same stage matrix
+    rhs = np.random.default_rng(6).standard_normal(mat.n)
+    xg, st = gmres(mat.matvec, fac.apply, rhs, GmresConfig(rel_tol=1e-8, restart=40))
+    A = mat.data
+    prob_mv = lambda z: O.bsr_matvec(p.indptr, p.indices, A, z)
+    ofac, odinv, ofail = O.ilu0_factor(p.indptr, p.indices, p.diag_pos, A, np.ones(len(p.indices), bool), True)
+    assert ofail == -1
+    oapply = lambda z: O.ilu0_solve(p.indptr, p.indices, p.diag_pos, ofac, odinv, np.ones(len(p.indices), bool), z)
+    xo, so = O.gmres(prob_mv, oapply, rhs, O.GmresConfig(rel_tol=1e-8, restart=40))
+    assert abs(st.iterations - so.iterations) <= 1
+    if st.iterations == so.iterations:
+        assert rel(np.asarray(xg), xo) < 1e-10
