@@ -11,6 +11,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <mutex>
 #include <vector>
 
 #include "blockops.cuh"
@@ -1203,6 +1204,26 @@ __global__ void __launch_bounds__(288) k_unc_fused_fwd(ApplyArgs A, SegCfg SC, F
     }
 }
 
+// Occupancy of a sweep kernel at (threads, smem), with its dynamic-smem opt-in set once:
+// the level launches sit on the critical path after every host wait of irk_gmres, so the
+// driver queries are cached (mutex: the C ABI is called from several host threads).
+static cudaError_t sweep_occupancy(const void* kernel, int threads, size_t smem, int optin, int* per_sm) {
+    struct Entry { const void* k; int t; size_t s; int occ; };
+    static std::mutex mu;
+    static std::vector<Entry> cache;
+    std::lock_guard<std::mutex> lock(mu);
+    for (const Entry& e : cache)
+        if (e.k == kernel && e.t == threads && e.s == smem) { *per_sm = e.occ; return cudaSuccess; }
+    cudaError_t err = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, optin);
+    if (err != cudaSuccess) return err;
+    int occ = 0;
+    err = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kernel, threads, smem);
+    if (err != cudaSuccess) return err;
+    cache.push_back({kernel, threads, smem, occ});
+    *per_sm = occ;
+    return cudaSuccess;
+}
+
 template <typename K>
 static int run_seg(const irk_factor* f, K kernel, ApplyArgs& A, const irk_sched& S, int s, cudaStream_t st,
                    int extra_doubles = 0, bool pdl = true) {
@@ -1215,9 +1236,8 @@ static int run_seg(const irk_factor* f, K kernel, ApplyArgs& A, const irk_sched&
     const int threads = 32 + ((A.G_ * nb + 31) / 32) * 32;
     const size_t smem = (size_t)SC.nst * (SC.stage_bytes + 2 * sizeof(uint64_t) + sizeof(int4)) +
                         sizeof(double) * (2 * (size_t)s * nb + (size_t)extra_doubles) + 64;
-    IRK_CK(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)f->ctx->smem_optin));
     int per_sm = 1;
-    IRK_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, threads, smem));
+    IRK_CK(sweep_occupancy((const void*)kernel, threads, smem, (int)f->ctx->smem_optin, &per_sm));
     for (int64_t l = 0; l < S.nlevels; ++l) {
         const int64_t lo = S.h_lvl_ptr[l], hi = S.h_lvl_ptr[l + 1];
         if (hi == lo) continue;
@@ -1243,13 +1263,8 @@ static int run_fused_fwd(const irk_factor* f, ApplyArgs& A, const FusedMv& F, cu
     const int threads = 32 + ((A.G_ * nb + 31) / 32) * 32;
     const size_t smem = (size_t)SC.nst * (SC.stage_bytes + 2 * sizeof(uint64_t) + sizeof(int4)) +
                         sizeof(double) * 2 * (size_t)S * nb + 64;
-    static bool attr = false;
-    if (!attr) {
-        IRK_CK(cudaFuncSetAttribute(k_unc_fused_fwd<S>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)f->ctx->smem_optin));
-        attr = true;
-    }
     int per_sm = 1;
-    IRK_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_unc_fused_fwd<S>, threads, smem));
+    IRK_CK(sweep_occupancy((const void*)k_unc_fused_fwd<S>, threads, smem, (int)f->ctx->smem_optin, &per_sm));
     for (int64_t l = 0; l < Sd.nlevels; ++l) {
         const int64_t lo = Sd.h_lvl_ptr[l], hi = Sd.h_lvl_ptr[l + 1];
         if (hi == lo) continue;

@@ -321,7 +321,7 @@ __global__ void __launch_bounds__(VB) k_multidot_v(const double* __restrict__ V,
 
 // pass 2: w' = w - V h (h = h1[0..nv)); out[i] = V_i . w', out[nv] = w' . w'
 template <int NVM>
-__global__ void __launch_bounds__(VB) k_update_dots_v(const double* __restrict__ V, int64_t ldv, int nv,
+__global__ void __launch_bounds__(VB, NVM <= 8 ? 4 : 1) k_update_dots_v(const double* __restrict__ V, int64_t ldv, int nv,
                                                       const double* __restrict__ h, double* __restrict__ w,
                                                       int64_t n, double* partials, double* out,
                                                       unsigned* counter) {
@@ -383,7 +383,7 @@ __global__ void __launch_bounds__(VB) k_update_dots_v(const double* __restrict__
 // w <- (reorth ? w' - V h2 : w') / ||w''|| unless ||w''|| <= brk (breakdown:
 // the vector is left unscaled, krylov.py:98-102).  out = [||w''||^2, reorth].
 template <int NVM>
-__global__ void __launch_bounds__(VB) k_finish_v(const double* __restrict__ V, int64_t ldv, int nv,
+__global__ void __launch_bounds__(VB, NVM <= 8 ? 4 : 1) k_finish_v(const double* __restrict__ V, int64_t ldv, int nv,
                                                  const double* __restrict__ ww0, const double* __restrict__ h2,
                                                  double eta, double brk, double* __restrict__ w, int64_t n,
                                                  double* out) {
