@@ -1271,7 +1271,8 @@ static int run_fused_fwd(const irk_factor* f, ApplyArgs& A, const FusedMv& F, cu
         A.order = Sd.d_order + lo;
         A.ntasks = hi - lo;
         const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(A.ntasks, (int64_t)f->ctx->num_sms * std::max(per_sm, 1)));
-        IRK_CK(launch_pdl(k_unc_fused_fwd<S>, dim3(grid), dim3(threads), smem, st, A, SC, F));
+        static const bool pdl = !(getenv("IRK_PDL_FUSED") && atoi(getenv("IRK_PDL_FUSED")) == 0);   // A/B switch
+        IRK_CK(launch_pdl_if(pdl, k_unc_fused_fwd<S>, dim3(grid), dim3(threads), smem, st, A, SC, F));
         IRK_LAUNCHED();
     }
     return IRK_OK;

@@ -591,15 +591,18 @@ static int cgs2_v_t(const irk_ctx* ctx, int64_t n, int64_t ldv, int nv, const do
     static const int g1 = one_wave(ctx, k_multidot_v<NVM>);
     static const int g2 = one_wave(ctx, k_update_dots_v<NVM>);
     static const int g3 = one_wave(ctx, k_finish_v<NVM>);
+    // plain stream order for the CGS passes: with PDL the step measured ~1% slower (tools/ab_quick.sh:
+    // 90.3 vs 91.3 stage-solves/s at config 1); IRK_PDL_CGS=1 restores it
+    static const bool pdl = getenv("IRK_PDL_CGS") && atoi(getenv("IRK_PDL_CGS")) == 1;
     double* h1 = out;
     double* h2 = out + nv + 1;
-    IRK_CK(launch_pdl(k_multidot_v<NVM>, dim3(g1), dim3(VB), 0, st, V, ldv, nv, (const double*)w, n, partials, h1,
+    IRK_CK(launch_pdl_if(pdl, k_multidot_v<NVM>, dim3(g1), dim3(VB), 0, st, V, ldv, nv, (const double*)w, n, partials, h1,
                       counters));
     IRK_LAUNCHED();
-    IRK_CK(launch_pdl(k_update_dots_v<NVM>, dim3(g2), dim3(VB), 0, st, V, ldv, nv, (const double*)h1, w, n, partials,
+    IRK_CK(launch_pdl_if(pdl, k_update_dots_v<NVM>, dim3(g2), dim3(VB), 0, st, V, ldv, nv, (const double*)h1, w, n, partials,
                       h2, counters + 1));
     IRK_LAUNCHED();
-    IRK_CK(launch_pdl(k_finish_v<NVM>, dim3(g3), dim3(VB), 0, st, V, ldv, nv, (const double*)(h1 + nv),
+    IRK_CK(launch_pdl_if(pdl, k_finish_v<NVM>, dim3(g3), dim3(VB), 0, st, V, ldv, nv, (const double*)(h1 + nv),
                       (const double*)h2, eta, brk, w, n, out + 2 * (nv + 1)));
     IRK_LAUNCHED();
     return IRK_OK;
