@@ -18,6 +18,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <functional>
 #include <cmath>
 #include <vector>
 
@@ -585,9 +586,15 @@ static int one_wave(const irk_ctx* ctx, K kernel) {
     return legacy ? vec_blocks(ctx) : std::min(vec_blocks(ctx), ctx->num_sms * per_sm);
 }
 
+// ar: optional stream-ordered allreduce of the pass-1 and pass-2 dot vectors (element-partitioned
+// solve: each rank holds its slab's rows of V and w); the device-side decisions of k_finish_v then
+// see the global sums on every rank
+using ArFn = std::function<int(double*, int64_t)>;
+
 template <int NVM>
 static int cgs2_v_t(const irk_ctx* ctx, int64_t n, int64_t ldv, int nv, const double* V, double* w, double eta,
-                     double brk, double* partials, unsigned* counters, double* out, cudaStream_t st) {
+                     double brk, double* partials, unsigned* counters, double* out, cudaStream_t st,
+                     const ArFn* ar) {
     static const int g1 = one_wave(ctx, k_multidot_v<NVM>);
     static const int g2 = one_wave(ctx, k_update_dots_v<NVM>);
     static const int g3 = one_wave(ctx, k_finish_v<NVM>);
@@ -599,9 +606,11 @@ static int cgs2_v_t(const irk_ctx* ctx, int64_t n, int64_t ldv, int nv, const do
     IRK_CK(launch_pdl_if(pdl, k_multidot_v<NVM>, dim3(g1), dim3(VB), 0, st, V, ldv, nv, (const double*)w, n, partials, h1,
                       counters));
     IRK_LAUNCHED();
+    if (ar) IRK_TRY((*ar)(h1, nv + 1));
     IRK_CK(launch_pdl_if(pdl, k_update_dots_v<NVM>, dim3(g2), dim3(VB), 0, st, V, ldv, nv, (const double*)h1, w, n, partials,
                       h2, counters + 1));
     IRK_LAUNCHED();
+    if (ar) IRK_TRY((*ar)(h2, nv + 1));
     IRK_CK(launch_pdl_if(pdl, k_finish_v<NVM>, dim3(g3), dim3(VB), 0, st, V, ldv, nv, (const double*)(h1 + nv),
                       (const double*)h2, eta, brk, w, n, out + 2 * (nv + 1)));
     IRK_LAUNCHED();
@@ -609,9 +618,10 @@ static int cgs2_v_t(const irk_ctx* ctx, int64_t n, int64_t ldv, int nv, const do
 }
 
 static int cgs2_v(const irk_ctx* ctx, int64_t n, int64_t ldv, int nv, const double* V, double* w, double eta,
-                  double brk, double* partials, unsigned* counters, double* out, cudaStream_t st) {
-    if (nv <= 8) return cgs2_v_t<8>(ctx, n, ldv, nv, V, w, eta, brk, partials, counters, out, st);
-    return cgs2_v_t<16>(ctx, n, ldv, nv, V, w, eta, brk, partials, counters, out, st);
+                  double brk, double* partials, unsigned* counters, double* out, cudaStream_t st,
+                  const ArFn* ar = nullptr) {
+    if (nv <= 8) return cgs2_v_t<8>(ctx, n, ldv, nv, V, w, eta, brk, partials, counters, out, st, ar);
+    return cgs2_v_t<16>(ctx, n, ldv, nv, V, w, eta, brk, partials, counters, out, st, ar);
 }
 
 static int multidot(const irk_ctx* ctx, int64_t n, int nv, const double* V, int64_t ldv, const double* w,
@@ -713,6 +723,9 @@ int irk_gmres(irk_ctx* ctx, int64_t n, irk_linop op, irk_linop pre, irk_allreduc
     IRK_ARG(restart <= 4096, "restart length above 4096 is not supported");
     const double eta = cfg->reorth_eta > 0 ? cfg->reorth_eta : 0.70710678118654752;
     static const bool cgs_r = getenv("IRK_CGS_R") != nullptr;   // A/B: the scalar fused passes
+    // A/B: partitioned solves on the generic multidot/update path (host DGKS decision)
+    static const bool cgs_generic_ar = getenv("IRK_CGS_AR_GENERIC") && atoi(getenv("IRK_CGS_AR_GENERIC")) == 1;
+    const bool gen_ar = allreduce && cgs_generic_ar;
     *stats = irk_gmres_stats{};
     stats->final_true_residual = NAN;
     int hist_n = 0;
@@ -747,6 +760,7 @@ int irk_gmres(irk_ctx* ctx, int64_t n, irk_linop op, irk_linop pre, irk_allreduc
         if (rc) { set_error("allreduce callback failed"); return IRK_ECALLBACK; }
         return IRK_OK;
     };
+    const ArFn arf = ar;
     auto call = [&](const irk_linop& L, const double* in, double* out) -> int {
         if (!L.fn) {
             IRK_CK(cudaMemcpyAsync(out, in, sizeof(double) * n, cudaMemcpyDeviceToDevice, st));
@@ -839,10 +853,12 @@ int irk_gmres(irk_ctx* ctx, int64_t n, irk_linop op, irk_linop pre, irk_allreduc
             double nw;
             bool scaled = false;   // w already divided by nw on the device
             const double brk = 1e-14 * std::max(b_norm, 1.0);
-            if (!allreduce && j + 1 <= 16 && !cgs_r) {
-                // 128-bit fused CGS2 + normalisation (3 passes), one host sync
+            if (j + 1 <= 16 && !cgs_r && !gen_ar) {
+                // 128-bit fused CGS2 + normalisation (3 passes), one host sync; partitioned solves
+                // allreduce the two dot vectors on the stream between the passes
                 const int nv = j + 1;
-                IRK_TRY(cgs2_v(ctx, n, ldV, nv, ws.V, w, eta, brk, ws.partials, ws.counters, fdev, st));
+                IRK_TRY(cgs2_v(ctx, n, ldV, nv, ws.V, w, eta, brk, ws.partials, ws.counters, fdev, st,
+                               allreduce ? &arf : nullptr));
                 IRK_CK(cudaMemcpyAsync(hbuf, fdev, sizeof(double) * (2 * (nv + 1) + 3),
                                        cudaMemcpyDeviceToHost, st));
                 IRK_TRY(host_wait(hs, st));

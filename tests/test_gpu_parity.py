@@ -588,3 +588,32 @@ def test_fused_product_dirk_stage_matrix():
     assert abs(st.iterations - so.iterations) <= 1
     if st.iterations == so.iterations:
         assert rel(np.asarray(xg), xo) < 1e-10
+
+
+def test_gmres_allreduce_callback_uses_fused_cgs():
+    """With an allreduce callback (the element-partitioned solve; here one rank, so
+    the callback is the identity) irk_gmres runs the same 128-bit fused CGS passes,
+    allreducing the two dot vectors on the stream between them: the solve is bitwise
+    the callback-free one, and the callback sees 2 (nv + 1)-vectors per iteration
+    plus the norms."""
+    import torch
+    from paper_1701_07181_b200.blocks import DevicePattern
+    from paper_1701_07181_b200.krylov import GmresConfig, gmres_device
+    from paper_1701_07181_b200.solver import StageSolver
+    cfg = W.CONFIGS[1].scaled(N=8, ordering="color")
+    wl = W.make_workload(cfg, norm_iters=10)
+    p = wl.pattern
+    sol = StageSolver(DevicePattern(p.indptr, p.indices, p.diag_pos), wl.J, wl.M, wl.a_inv, wl.dt,
+                      kind="uncoupled", shifts=wl.shifts, gmres_cfg=GmresConfig(rel_tol=1e-8, restart=40))
+    sol.factorize()
+    rhs = torch.from_numpy(wl.rhs).cuda()
+    gc = GmresConfig(rel_tol=1e-8, restart=40)
+    x0, s0 = gmres_device(sol.op.matvec, sol.fac.apply, rhs, gc)
+    sizes = []
+    x1, s1 = gmres_device(sol.op.matvec, sol.fac.apply, rhs, gc, allreduce=lambda buf: sizes.append(buf.numel()))
+    torch.cuda.synchronize()
+    assert s0.iterations == s1.iterations and s0.converged and s1.converged
+    assert torch.equal(x0, x1)
+    assert s0.final_true_residual == s1.final_true_residual
+    for j in range(1, s1.iterations + 1):
+        assert sizes.count(j + 1) >= 2, (j, sizes)
