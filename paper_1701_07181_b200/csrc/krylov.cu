@@ -790,7 +790,27 @@ int irk_gmres(irk_ctx* ctx, int64_t n, irk_linop op, irk_linop pre, irk_allreduc
 
     IRK_CK(cudaMemsetAsync(x, 0, sizeof(double) * n, st));
     double rnorm, rmax;
-    IRK_TRY(norm(rhs, rnorm, &rmax));
+    double b_norm = 0.0;
+    // native (or no) preconditioner: ||b||, max|b| and P^-1 b with its norm are enqueued together
+    // and read back with one host wait (applying P^-1 to a zero rhs has no observable effect); a
+    // callback preconditioner is only called when the reference would call it
+    const bool merged = !pre.fn || pre.fn == linop_factor;
+    if (merged) {
+        double* n2dev = ws.small + (restart + 4);   // 2 free slots between ndev and cdev
+        IRK_TRY(norm_max(ctx, n, rhs, ws.partials, ndev, st));
+        IRK_TRY(ar(ndev, 1));
+        IRK_TRY(call(pre, rhs, V(0)));
+        IRK_TRY(norm_max(ctx, n, V(0), ws.partials, n2dev, st));
+        IRK_TRY(ar(n2dev, 1));
+        IRK_CK(cudaMemcpyAsync(hbuf, ndev, 2 * sizeof(double), cudaMemcpyDeviceToHost, st));
+        IRK_CK(cudaMemcpyAsync(hbuf + 2, n2dev, sizeof(double), cudaMemcpyDeviceToHost, st));
+        IRK_TRY(host_wait(hs, st));
+        rnorm = std::sqrt(hbuf[0]);
+        rmax = hbuf[1];
+        b_norm = std::sqrt(hbuf[2]);
+    } else {
+        IRK_TRY(norm(rhs, rnorm, &rmax));
+    }
     if (allreduce) {
         // global "any nonzero": the max is rank-local; use the reduced 2-norm
         rmax = rnorm;
@@ -802,9 +822,10 @@ int irk_gmres(irk_ctx* ctx, int64_t n, irk_linop op, irk_linop pre, irk_allreduc
         return IRK_OK;
     }
     // pb = P^-1 b ; r = P^-1 (b - B*0) == pb (x0 = 0)
-    IRK_TRY(call(pre, rhs, V(0)));
-    double b_norm;
-    IRK_TRY(norm(V(0), b_norm, nullptr));
+    if (!merged) {
+        IRK_TRY(call(pre, rhs, V(0)));
+        IRK_TRY(norm(V(0), b_norm, nullptr));
+    }
     stats->b_norm = b_norm;
     stats->operator_applies = 1;
     double beta = b_norm;
