@@ -488,16 +488,69 @@ def run_b200(args):
         t0 = time.perf_counter()
         for _ in range(ne):
             e2e_step()
-        te = time.perf_counter() - t0
+        te_serial = time.perf_counter() - t0
+
+        # Double-buffered: a second device copy of the system (its own J, M, factor and
+        # vectors); step k+1's inputs go H2D on a copy stream while step k factorises and
+        # solves, so the PCIe transfer (the bound) runs back to back.  Every step still
+        # uploads its own J, M, rhs and downloads its own solution inside the timed region.
+        solver_b = StageSolver(dpat, J, M, der.a_inv, dt, kind=cfg.precond, shifts=der.shifts,
+                               gmres_cfg=gcfg)
+        rhs_b, x_b = torch.empty_like(rhs), torch.empty_like(x)
+        sets = [(solver, rhs, x), (solver_b, rhs_b, x_b)]
+        xps = [xp, torch.empty_like(rp).pin_memory()]
+        cstream = torch.cuda.Stream()
+        up_done = [torch.cuda.Event(), torch.cuda.Event()]
+        comp_done = [torch.cuda.Event(), torch.cuda.Event()]
+        for e in comp_done:
+            e.record(stream)
+
+        def upload(k):
+            sv, r, _ = sets[k % 2]
+            with torch.cuda.stream(cstream):
+                cstream.wait_event(comp_done[k % 2])   # the set's previous solve is finished
+                sv.op.jacobians[0].blocks.upload(Jp.numpy())
+                sv.op.mass.device.upload(Mp.numpy())
+                r.copy_(rp, non_blocking=True)
+                up_done[k % 2].record(cstream)
+
+        def compute(k):
+            sv, r, xx = sets[k % 2]
+            stream.wait_event(up_done[k % 2])
+            sv.factorize()
+            sv.solve(r, x=xx)
+            xps[k % 2].copy_(xx, non_blocking=True)
+            comp_done[k % 2].record(stream)
+
+        solver_b.factorize()
+        torch.cuda.synchronize()
+        npipe = max(3, min(args.steps, 10))
         if dist:
-            tt = torch.tensor([te], device="cuda")
+            dist.barrier()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        upload(0)
+        for k in range(npipe):
+            if k + 1 < npipe:
+                upload(k + 1)
+            compute(k)
+        torch.cuda.synchronize()
+        te = time.perf_counter() - t0
+        ok = bool(torch.equal(x, x_b)) and bool(torch.equal(xps[0], xps[1]))
+        if dist:
+            tt = torch.tensor([te, te_serial], device="cuda")
             dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-            te = float(tt)
-        e2e = {"value": world * ne / te, "unit": "stage-solves/s",
+            te, te_serial = float(tt[0]), float(tt[1])
+        e2e = {"value": world * npipe / te, "unit": "stage-solves/s",
                "h2d_bytes_per_step": int(J.nbytes + M.nbytes + rhs_h.nbytes),
                "d2h_bytes_per_step": int(rhs_h.nbytes),
+               "serial_value": world * ne / te_serial,
+               "double_buffered_results_identical": ok,
                "note": "pinned host J, M, rhs -> irk_blocks_upload / H2D, factorise + GMRES, "
-                       "solution D2H, per step"}
+                       "solution D2H, every step; double-buffered (two device copies of the system, "
+                       "step k+1's H2D on a copy stream during step k's solve); serial_value: one "
+                       "device copy, upload -> solve -> download in turn"}
+        del solver_b, sets
     log('e2e done')
     alt = None
     if not args.no_alt:
