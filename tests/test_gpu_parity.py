@@ -617,3 +617,17 @@ def test_gmres_allreduce_callback_uses_fused_cgs():
     assert s0.final_true_residual == s1.final_true_residual
     for j in range(1, s1.iterations + 1):
         assert sizes.count(j + 1) >= 2, (j, sizes)
+
+
+@pytest.mark.parametrize("nb,count,first", [(100, 7000, 0), (99, 3 * 3389 + 5, 17)])
+def test_chunked_upload_roundtrip(nb, count, first):
+    """irk_blocks_upload of more than one 256 MiB staging chunk (two staging buffers,
+    copies and layout permutes on two streams) then download: bitwise round trip,
+    even and odd (padded) block sizes, at an offset inside the array."""
+    from paper_1701_07181_b200.blocks import DeviceBlocks
+    rng = np.random.default_rng(nb)
+    data = rng.standard_normal((count, nb, nb))
+    db = DeviceBlocks(nb, count + first)
+    db.upload(data, first=first)
+    back = db.download(first=first, count=count)
+    assert np.array_equal(back, data)
