@@ -507,14 +507,15 @@ def test_stage_matvec_row_range_and_list(nb):
     assert rel(yy.cpu().numpy(), yf.cpu().numpy()) < 1e-15
 
 
-@pytest.mark.parametrize("s_scheme", ["RADAU23", "RADAU35"])
+@pytest.mark.parametrize("s_scheme,nb", [("RADAU23", 40), ("RADAU35", 40), ("RADAU35", 24), ("RADAU23", 100)])
 @pytest.mark.parametrize("ordering,nparts", [("color", 1), ("color", 3), ("natural", 1)])
-def test_fused_operator_precond_product(s_scheme, ordering, nparts):
+def test_fused_operator_precond_product(s_scheme, nb, ordering, nparts):
     """irk_op_factor_apply (the Arnoldi product P^-1 (B v) with the stage matvec
     fused into the implicit-L forward sweep, krylov.py:88-89) == the separate
     irk_stage_op_apply + irk_factor_apply, within the 1e-12 apply bar; colour
     schedules take the fused kernel (also with cross-partition lower blocks
-    dropped), the deep natural schedule falls back to the two calls."""
+    dropped; nb = 100 runs the two-group consumer layout), the deep natural schedule
+    falls back to the two calls."""
     import ctypes
     import torch
     from paper_1701_07181_b200 import _lib as L
@@ -522,7 +523,7 @@ def test_fused_operator_precond_product(s_scheme, ordering, nparts):
     from paper_1701_07181_b200.krylov import GmresConfig
     from paper_1701_07181_b200.solver import StageSolver
     from paper_1701_07181_b200.meshes import partition_bounds
-    cfg = W.CONFIGS[1].scaled(N=8, ordering=ordering, scheme=s_scheme)
+    cfg = W.CONFIGS[1].scaled(N=8, ordering=ordering, scheme=s_scheme, nb=nb)
     s = cfg.s
     wl = W.make_workload(cfg, norm_iters=10)
     p = wl.pattern
