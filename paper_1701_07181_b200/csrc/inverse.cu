@@ -1077,7 +1077,12 @@ struct InvTcCfg {
 
 // EXACT: nb == 8 NT (block index math and loops fold to constants); FORM: build D from
 // J and M (factor level 0) instead of reading it
-template <int NT, bool EXACT, bool FORM>
+// row slot ks (0 or RL - 1, RL <= 2) of the lane's panel registers without dynamic register indexing
+#define IRK_PK(ks_, c_) ((RL == 1 || (ks_) == 0) ? pa[0][c_] : pa[RL - 1][c_])
+
+// ROLL: the NT panels run as a loop instead of being unrolled (a fifth of the code: the fully
+// unrolled kernel is ~100 KB of SASS and its warps stall on instruction fetch)
+template <int NT, bool EXACT, bool FORM, bool ROLL = false>
 __global__ void __launch_bounds__(32 * InvTcCfg<NT>::WARPS) k_inverse_tc(InvArgs A, int* fb_list, int* fb_count) {
     using C = InvTcCfg<NT>;
     constexpr int NBT = C::NBT, LD = C::LD, RL = C::RL;
@@ -1171,9 +1176,9 @@ __global__ void __launch_bounds__(32 * InvTcCfg<NT>::WARPS) k_inverse_tc(InvArgs
 #pragma unroll
         for (int h = 0; h < (NBT + 31) / 32; ++h) apiv[h] = 1.0;
         bool swap = false;
-        static_for([&](auto pc_) {
-            constexpr int p = decltype(pc_)::value;   // panel index
-            constexpr int k0 = 8 * p;
+        auto panel = [&](auto pv) {   // panel index: std::integral_constant (unrolled) or int (ROLL)
+            const int p = pv;
+            const int k0 = 8 * p;
             if (swap) return;
             // ---- panel to registers, one row per lane: pa[j][c] = X[lane + 32 j][k0 + c]
             double pa[RL][8];
@@ -1191,10 +1196,10 @@ __global__ void __launch_bounds__(32 * InvTcCfg<NT>::WARPS) k_inverse_tc(InvArgs
             // ---- 8 scalar GJ steps on the panel columns
             static_for([&](auto kc_) {
                 constexpr int kk = decltype(kc_)::value;
-                constexpr int k = k0 + kk;
-                constexpr int ko = k & 31, ks = k >> 5;      // owner lane / slot of row k
+                const int k = k0 + kk;
+                const int ko = k & 31, ks = k >> 5;          // owner lane / slot of row k
                 const bool own = lane == ko;
-                const double piv = __shfl_sync(0xffffffffu, pa[ks][kk], ko);
+                const double piv = __shfl_sync(0xffffffffu, IRK_PK(ks, kk), ko);
                 // partial-pivoting equivalence: no row r > k of column k beats the diagonal
                 const double ap = fabs(piv);
                 bool beat = false;
@@ -1204,13 +1209,16 @@ __global__ void __launch_bounds__(32 * InvTcCfg<NT>::WARPS) k_inverse_tc(InvArgs
                 const bool ok = !__any_sync(0xffffffffu, beat) && piv != 0.0 && isfinite(piv);
                 if (!ok) swap = true;
                 const double inv = 1.0 / piv;
-                if (k < nb && own) apiv[ks] = ap;
+                if (k < nb && own) {
+                    if (RL == 1 || ks == 0) apiv[0] = ap;
+                    else apiv[RL - 1] = ap;
+                }
                 // new row k = a_k / piv (column k: 1 / piv), broadcast through shared memory
                 double* rb = rowbuf + 8 * (kk & 1);
                 if (own) {
 #pragma unroll
                     for (int c = 0; c < 8; c += 2) {
-                        double2 v = make_double2(c == kk ? inv : pa[ks][c] * inv, c + 1 == kk ? inv : pa[ks][c + 1] * inv);
+                        double2 v = make_double2(c == kk ? inv : IRK_PK(ks, c) * inv, c + 1 == kk ? inv : IRK_PK(ks, c + 1) * inv);
                         *reinterpret_cast<double2*>(rb + c) = v;
                     }
                 }
@@ -1267,7 +1275,13 @@ __global__ void __launch_bounds__(32 * InvTcCfg<NT>::WARPS) k_inverse_tc(InvArgs
                 }
             }
             __syncwarp();
-        }, std::make_integer_sequence<int, NT>{});
+        };
+        if constexpr (ROLL) {
+#pragma unroll 1
+            for (int p = 0; p < NT; ++p) panel(p);
+        } else {
+            static_for([&](auto pc_) { panel(pc_); }, std::make_integer_sequence<int, NT>{});
+        }
         if (swap) {
             // the pivoted kernels read D from memory: write it unless already stored
             if (FORM && !A.form.store)
@@ -1313,24 +1327,31 @@ __global__ void __launch_bounds__(32 * InvTcCfg<NT>::WARPS) k_inverse_tc(InvArgs
     }
 }
 
-template <int NT, bool EXACT, bool FORM>
-static int launch_tc_t(const irk_ctx* ctx, const InvArgs& A, int* fb_list, int* fb_count, cudaStream_t st) {
+template <int NT, bool EXACT, bool FORM, bool ROLL>
+static int launch_tc_r(const irk_ctx* ctx, const InvArgs& A, int* fb_list, int* fb_count, cudaStream_t st) {
     using C = InvTcCfg<NT>;
     static bool attr = false;
     if (!attr) {
-        IRK_CK(cudaFuncSetAttribute(k_inverse_tc<NT, EXACT, FORM>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::smem));
-        IRK_CK(cudaFuncSetAttribute(k_inverse_tc<NT, EXACT, FORM>, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+        IRK_CK(cudaFuncSetAttribute(k_inverse_tc<NT, EXACT, FORM, ROLL>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::smem));
+        IRK_CK(cudaFuncSetAttribute(k_inverse_tc<NT, EXACT, FORM, ROLL>, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
         attr = true;
     }
     const int threads = 32 * C::WARPS;
     int per_sm = 1;
-    IRK_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_inverse_tc<NT, EXACT, FORM>, threads, C::smem));
+    IRK_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_inverse_tc<NT, EXACT, FORM, ROLL>, threads, C::smem));
     if (A.cap_per_sm > 0) per_sm = std::min(per_sm, A.cap_per_sm);
     const int64_t need = (A.ntasks + C::WARPS - 1) / C::WARPS;
     const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(need, (int64_t)ctx->num_sms * std::max(per_sm, 1)));
-    k_inverse_tc<NT, EXACT, FORM><<<grid, threads, C::smem, st>>>(A, fb_list, fb_count);
+    k_inverse_tc<NT, EXACT, FORM, ROLL><<<grid, threads, C::smem, st>>>(A, fb_list, fb_count);
     IRK_LAUNCHED();
     return IRK_OK;
+}
+
+template <int NT, bool EXACT, bool FORM>
+static int launch_tc_t(const irk_ctx* ctx, const InvArgs& A, int* fb_list, int* fb_count, cudaStream_t st) {
+    static const bool roll = getenv("IRK_INV_ROLL") && atoi(getenv("IRK_INV_ROLL")) == 1;   // A/B switch
+    if (roll) return launch_tc_r<NT, EXACT, FORM, true>(ctx, A, fb_list, fb_count, st);
+    return launch_tc_r<NT, EXACT, FORM, false>(ctx, A, fb_list, fb_count, st);
 }
 
 template <int NT>
