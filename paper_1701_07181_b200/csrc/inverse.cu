@@ -1349,8 +1349,10 @@ static int launch_tc_r(const irk_ctx* ctx, const InvArgs& A, int* fb_list, int* 
 
 template <int NT, bool EXACT, bool FORM>
 static int launch_tc_t(const irk_ctx* ctx, const InvArgs& A, int* fb_list, int* fb_count, cudaStream_t st) {
-    static const bool roll = getenv("IRK_INV_ROLL") && atoi(getenv("IRK_INV_ROLL")) == 1;   // A/B switch
-    if (roll) return launch_tc_r<NT, EXACT, FORM, true>(ctx, A, fb_list, fb_count, st);
+    // A/B switch, instantiated for the config-1 tile count only (nb 33..40) to bound build time
+    static const bool roll = getenv("IRK_INV_ROLL") && atoi(getenv("IRK_INV_ROLL")) == 1;
+    if constexpr (NT == 5)
+        if (roll) return launch_tc_r<NT, EXACT, FORM, true>(ctx, A, fb_list, fb_count, st);
     return launch_tc_r<NT, EXACT, FORM, false>(ctx, A, fb_list, fb_count, st);
 }
 
