@@ -1083,7 +1083,8 @@ struct InvTcCfg {
 // ROLL: the NT panels run as a loop instead of being unrolled (a fifth of the code: the fully
 // unrolled kernel is ~100 KB of SASS and its warps stall on instruction fetch)
 template <int NT, bool EXACT, bool FORM, bool ROLL = false>
-__global__ void __launch_bounds__(32 * InvTcCfg<NT>::WARPS) k_inverse_tc(InvArgs A, int* fb_list, int* fb_count) {
+__global__ void __launch_bounds__(32 * InvTcCfg<NT>::WARPS, (FORM && NT <= 5) ? 4 : 1)
+    k_inverse_tc(InvArgs A, int* fb_list, int* fb_count) {
     using C = InvTcCfg<NT>;
     constexpr int NBT = C::NBT, LD = C::LD, RL = C::RL;
     constexpr int NPAIR = NBT * NBT / 2;            // double2 per padded block
@@ -1104,20 +1105,46 @@ __global__ void __launch_bounds__(32 * InvTcCfg<NT>::WARPS) k_inverse_tc(InvArgs
         FormSrc fsrc{};
         if constexpr (FORM) fsrc = form_src(A, j, k_st, bsz);
         // ---- load: device pair p2 of row r is double2 index p2 * nb + r
-        if constexpr (EXACT) {
+        if constexpr (EXACT && FORM) {
+            // loads of J_jj and M_j issued in batches ahead of the arithmetic and the stores
+            // (one load -> multiply -> store chain per pair stalled on every global load)
+            constexpr int NE = (NPAIR + 31) / 32, BATCH = 5;
+            const bool store = A.form.store;
+#pragma unroll
+            for (int e0 = 0; e0 < NE; e0 += BATCH) {
+                double2 jv[BATCH], mv[BATCH];
+#pragma unroll
+                for (int b = 0; b < BATCH; ++b) {
+                    const int idx = lane + 32 * (e0 + b);
+                    jv[b] = mv[b] = make_double2(0.0, 0.0);
+                    if (e0 + b < NE && (NPAIR % 32 == 0 || idx < NPAIR)) {
+                        jv[b] = __ldg(fsrc.J + idx);
+                        if (fsrc.M) mv[b] = __ldg(fsrc.M + idx);
+                    }
+                }
+#pragma unroll
+                for (int b = 0; b < BATCH; ++b) {
+                    const int idx = lane + 32 * (e0 + b);
+                    if (e0 + b < NE && (NPAIR % 32 == 0 || idx < NPAIR)) {
+                        const int p2 = idx / NBT, r = idx - p2 * NBT;
+                        double x0 = __dmul_rn(fsrc.alpha, jv[b].x), x1 = __dmul_rn(fsrc.alpha, jv[b].y);
+                        if (fsrc.M) {
+                            x0 = __dadd_rn(x0, __dmul_rn(fsrc.coef, mv[b].x));
+                            x1 = __dadd_rn(x1, __dmul_rn(fsrc.coef, mv[b].y));
+                        }
+                        const double2 v = fsrc.keep ? make_double2(x0, x1) : make_double2(0.0, 0.0);
+                        if (store) dst_d[idx] = v;
+                        *reinterpret_cast<double2*>(X + r * LD + 2 * p2) = v;
+                    }
+                }
+            }
+        } else if constexpr (EXACT) {
 #pragma unroll
             for (int e = 0; e < (NPAIR + 31) / 32; ++e) {
                 const int idx = lane + 32 * e;
                 if (NPAIR % 32 == 0 || idx < NPAIR) {
                     const int p2 = idx / NBT, r = idx - p2 * NBT;
-                    double2 v;
-                    if constexpr (FORM) {
-                        v = form_pair(fsrc, idx);
-                        if (A.form.store) dst_d[idx] = v;
-                    } else {
-                        v = src[idx];
-                    }
-                    *reinterpret_cast<double2*>(X + r * LD + 2 * p2) = v;
+                    *reinterpret_cast<double2*>(X + r * LD + 2 * p2) = src[idx];
                 }
             }
         } else {
