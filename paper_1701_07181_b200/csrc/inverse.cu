@@ -1083,7 +1083,7 @@ struct InvTcCfg {
 // ROLL: the NT panels run as a loop instead of being unrolled (a fifth of the code: the fully
 // unrolled kernel is ~100 KB of SASS and its warps stall on instruction fetch)
 template <int NT, bool EXACT, bool FORM, bool ROLL = false>
-__global__ void __launch_bounds__(32 * InvTcCfg<NT>::WARPS, (FORM && NT <= 5) ? 4 : 1)
+__global__ void __launch_bounds__(32 * InvTcCfg<NT>::WARPS, NT <= 5 ? 4 : 1)
     k_inverse_tc(InvArgs A, int* fb_list, int* fb_count) {
     using C = InvTcCfg<NT>;
     constexpr int NBT = C::NBT, LD = C::LD, RL = C::RL;
@@ -1139,12 +1139,22 @@ __global__ void __launch_bounds__(32 * InvTcCfg<NT>::WARPS, (FORM && NT <= 5) ? 
                 }
             }
         } else if constexpr (EXACT) {
+            constexpr int NE = (NPAIR + 31) / 32, BATCH = 5;   // loads ahead of the shared-memory stores
 #pragma unroll
-            for (int e = 0; e < (NPAIR + 31) / 32; ++e) {
-                const int idx = lane + 32 * e;
-                if (NPAIR % 32 == 0 || idx < NPAIR) {
-                    const int p2 = idx / NBT, r = idx - p2 * NBT;
-                    *reinterpret_cast<double2*>(X + r * LD + 2 * p2) = src[idx];
+            for (int e0 = 0; e0 < NE; e0 += BATCH) {
+                double2 v[BATCH];
+#pragma unroll
+                for (int b = 0; b < BATCH; ++b) {
+                    const int idx = lane + 32 * (e0 + b);
+                    if (e0 + b < NE && (NPAIR % 32 == 0 || idx < NPAIR)) v[b] = __ldg(src + idx);
+                }
+#pragma unroll
+                for (int b = 0; b < BATCH; ++b) {
+                    const int idx = lane + 32 * (e0 + b);
+                    if (e0 + b < NE && (NPAIR % 32 == 0 || idx < NPAIR)) {
+                        const int p2 = idx / NBT, r = idx - p2 * NBT;
+                        *reinterpret_cast<double2*>(X + r * LD + 2 * p2) = v[b];
+                    }
                 }
             }
         } else {
