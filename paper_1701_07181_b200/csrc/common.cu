@@ -138,6 +138,12 @@ int irk_ctx_create(int device, irk_ctx** out) {
     if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
         uint64_t thr = UINT64_MAX;
         cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+        // no cross-stream reuse: a block freed on an upload stream must not be handed to a solve on
+        // another stream with an implicit wait on that upload (double-buffered streaming, bench e2e)
+        int off = 0;
+        cudaMemPoolSetAttribute(pool, cudaMemPoolReuseFollowEventDependencies, &off);
+        cudaMemPoolSetAttribute(pool, cudaMemPoolReuseAllowOpportunistic, &off);
+        cudaMemPoolSetAttribute(pool, cudaMemPoolReuseAllowInternalDependencies, &off);
     }
     *out = c;
     return IRK_OK;
