@@ -49,7 +49,8 @@ def parse():
     ap.add_argument("--ordering", default="color", choices=["natural", "color"],
                     help="element numbering (color: colour-major, the mesh-colouring level schedule)")
     ap.add_argument("--no-alt", action="store_true", help="skip the other-ordering measurement")
-    ap.add_argument("--cpu-N", type=int, default=64, help="CPU sample mesh (cells per side)")
+    ap.add_argument("--cpu-N", type=int, default=None,
+                    help="CPU arms on a reduced mesh (cells per side; default: the full workload)")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--profile", action="store_true", help="timed steps only (for ncu)")
@@ -153,6 +154,23 @@ def bytes_apply_uncoupled_shared(T, r, nb, s, implicit_l=False, t_up=None):
     return 2 * up * Bk + s * (T + t_up) * Bk + 2 * s * v + 2 * s * 8 * t_up * nb
 
 
+def factor_flops(T, r, nb, s):
+    """Uncoupled simplified ILU(0) flops: s*T*nb^3*(2 + 2r)."""
+    return s * T * nb ** 3 * (2 + 2 * r)
+
+
+def fp64_peak():
+    """Measured FP64 tensor-core (DMMA) peak: tools/dmma_peak.cu run on a B200 of
+    this pool (profiles/r2_fp64_peak.json)."""
+    try:
+        with open(os.path.join(REPO, "profiles", "r2_fp64_peak.json")) as fh:
+            d = json.load(fh)
+        d["source"] = "profiles/r2_fp64_peak.json (tools/dmma_peak.cu, measured)"
+        return d
+    except Exception:
+        return None
+
+
 def make_config(args):
     from paper_1701_07181_b200 import workloads as W
     cfg = W.CONFIGS[args.config]
@@ -186,15 +204,49 @@ def jnorm_device(pattern, J, iters=60, seed=7):
     return float(np.sqrt(lam))
 
 
-def cpu_sample(args, reps=1):
-    """CPU oracle (C restatement of the reference) on a bounded sample:
-    the config-1 problem shape on a cpu_N x cpu_N quad sub-mesh; the
-    stage-solve rate is scaled by T_sample / T_config."""
+def jnorm_host(pattern, J, iters=60, seed=7):
+    """||J||_2 on the host: the same power iteration on J^T J as jnorm_device
+    (same start vector, same iteration count) with the oracle's C BSR matvec."""
+    import torch
     import oracle as O
+    p = pattern
+    rows = np.repeat(np.arange(p.T), np.diff(p.indptr))
+    order = np.lexsort((rows, p.indices))
+    JT = np.ascontiguousarray(J[order].transpose(0, 2, 1))
+    g = torch.Generator(device="cpu").manual_seed(seed)
+    v = torch.randn(p.T * J.shape[1], generator=g, dtype=torch.float64).numpy()
+    v = v / np.linalg.norm(v)
+    lam = 0.0
+    for _ in range(iters):
+        w = O.bsr_matvec(p.indptr, p.indices, JT, O.bsr_matvec(p.indptr, p.indices, J, v))
+        lam = float(np.linalg.norm(w))
+        v = w / lam
+    return float(np.sqrt(lam))
+
+
+def cpu_workload(args):
+    """The config's workload on the host (same generator, seeds and numbering as
+    the GPU arm; ||J||_2 by the same power iteration) for the CPU arms."""
     from paper_1701_07181_b200 import workloads as W
     cfg = make_config(args)
-    scfg = cfg.scaled(N=args.cpu_N)
-    wl = W.make_workload(scfg, norm_iters=30)
+    scfg = cfg.scaled(N=args.cpu_N) if args.cpu_N else cfg
+    wl = W.make_workload(scfg, jnorm=1.0)
+    jn = args.jnorm if args.jnorm else jnorm_host(wl.pattern, wl.J)
+    wl.jnorm, wl.dt = jn, scfg.dt_norm / jn
+    return cfg, scfg, wl
+
+
+def cpu_sample(args, reps=1, prebuilt=None):
+    """CPU oracle (C restatement of the reference kernels, OpenMP, + its numpy
+    MGS GMRES) on one full stage-solve of the SAME workload (no extrapolation):
+    about 10 s of host work at config 1.  ``prebuilt`` = (cfg, wl) reuses the GPU
+    arm's host arrays and dt."""
+    import oracle as O
+    if prebuilt is not None:
+        cfg, wl = prebuilt
+        scfg = cfg
+    else:
+        cfg, scfg, wl = cpu_workload(args)
     prob = O.problem_from_workload(wl)
     times = []
     iters = None
@@ -207,18 +259,42 @@ def cpu_sample(args, reps=1):
         iters = st.iterations
     t = min(times)
     scale = wl.pattern.T / cfg.T
-    threads = os.cpu_count()
+    threads = int(os.environ.get("OMP_NUM_THREADS", os.cpu_count()))
     return {
         "value": scale / t, "unit": "stage-solves/s", "cores": threads, "kind": "port",
         "sample": (f"oracle/irk_oracle.c (C restatement of the reference numba kernels, OpenMP "
-                   f"rows + {scfg.s} stage threads) + numpy MGS GMRES: one stage-solve of the "
-                   f"config-{args.config} shape on a {args.cpu_N}x{args.cpu_N}-quad sub-mesh "
-                   f"(T={wl.pattern.T}), {t:.2f} s, {iters} GMRES iterations; rate scaled by "
-                   f"T_sample/T = {scale:.4f}"),
+                   f"rows + {scfg.s} stage threads) + numpy MGS GMRES: one complete stage-solve "
+                   f"(factor + GMRES to rtol) of the config-{args.config} workload itself "
+                   f"(T={wl.pattern.T}), {t:.2f} s, {iters} GMRES iterations"
+                   + ("" if scale == 1.0 else f"; rate scaled by T_sample/T = {scale:.4f}")),
+        "reference_numba_1core": REFERENCE_NUMBA,
     }
 
 
+def _ref_numba():
+    """The unmodified reference (irksolve, numba backend, one core: its kernels
+    hold the GIL) timed on the same config-1 stage-solve in the BUILD container
+    (tools/ref_numba_rate.py; /root/reference does not exist on the GPU box)."""
+    try:
+        with open(os.path.join(REPO, "profiles", "r2_reference_numba_1core.json")) as fh:
+            d = json.load(fh)
+        return {"value": d["stage_solves_per_s_at_T"], "unit": "stage-solves/s", "cores": 1,
+                "seconds_per_stage_solve": d["total_s"], "iterations": d["iterations"],
+                "where": "build container, 8-core x86_64 (not this box); tools/ref_numba_rate.py",
+                "source": "profiles/r2_reference_numba_1core.json"}
+    except Exception:
+        return None
+
+
+REFERENCE_NUMBA = _ref_numba()
+
+
 def run_reference(args):
+    """The reference arm: the reference's algorithm on the host cores (the C
+    oracle port -- the reference is Python/numba, nothing to compile), every
+    step one COMPLETE stage-solve of the same full-size workload (factor + GMRES
+    to rtol; ~10 s on 16 threads at config 1).  Warm-up capped at one step so the
+    whole run stays within a few minutes."""
     world, rank, _ = dist_env()
     if world > 1:
         import torch.distributed as dist
@@ -227,39 +303,46 @@ def run_reference(args):
             dist.barrier()
             return
     os.environ.setdefault("OMP_NUM_THREADS", str(os.cpu_count()))
-    cfg = make_config(args)
     import oracle as O
-    from paper_1701_07181_b200 import workloads as W
-    scfg = cfg.scaled(N=args.cpu_N)
-    wl = W.make_workload(scfg, norm_iters=30)
+    t_setup = time.perf_counter()
+    cfg, scfg, wl = cpu_workload(args)
     prob = O.problem_from_workload(wl)
+    t_setup = time.perf_counter() - t_setup
 
     def step():
         fac = O.make_preconditioner(prob, scfg.precond, wl.shifts, workers=scfg.s)
         return O.gmres(prob.matvec, fac.apply, wl.rhs, O.GmresConfig(rel_tol=scfg.rtol, restart=scfg.restart))
 
-    for _ in range(min(args.warmup, 1)):
+    warm = min(args.warmup, 1)
+    for _ in range(warm):
         step()
     t0 = time.perf_counter()
+    conv = True
     for _ in range(args.steps):
         _, st = step()
+        conv &= bool(st.converged)
     t = time.perf_counter() - t0
     scale = wl.pattern.T / cfg.T
     value = args.steps * scale / t
+    threads = int(os.environ.get("OMP_NUM_THREADS", os.cpu_count()))
     line = {
         "impl": "reference", "metric": "IRK stage-solves/sec", "value": value,
-        "unit": "stage-solves/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "unit": "stage-solves/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": warm,
         "ms_per_step": 1e3 * t / args.steps / scale, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": config_dict(cfg, args),
-        "cpu_baseline": {"value": value, "unit": "stage-solves/s", "cores": os.cpu_count(),
+        "cpu_baseline": {"value": value, "unit": "stage-solves/s", "cores": threads,
                          "kind": "port",
-                         "sample": (f"each step: one stage-solve of the config-{args.config} shape on "
-                                    f"a {args.cpu_N}x{args.cpu_N}-quad sub-mesh (T={wl.pattern.T}) "
-                                    f"with the C oracle (OpenMP) + MGS GMRES, {st.iterations} "
-                                    f"iterations; rate scaled by {scale:.4f}; warm-up capped at 1")},
+                         "sample": (f"each step: one complete stage-solve of the config-{args.config} "
+                                    f"workload (T={wl.pattern.T}) with the C oracle (OpenMP, "
+                                    f"{threads} threads) + MGS GMRES, {st.iterations} iterations, "
+                                    f"converged={conv}; warm-up capped at {warm}"
+                                    + ("" if scale == 1.0 else f"; rate scaled by {scale:.4f}")),
+                         "reference_numba_1core": REFERENCE_NUMBA},
         "e2e": {"value": value, "unit": "stage-solves/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
+        "consistency": {"timed_s": t, "setup_s": t_setup,
+                        "steps_x_ms_per_step_s": args.steps * 1e-3 * (1e3 * t / args.steps / scale)},
     }
     print(json.dumps(line), flush=True)
     if world > 1:
@@ -318,6 +401,7 @@ def run_b200(args):
         _, st = solver.solve(rhs, x=x)
         return st
 
+    b_norm = float(np.linalg.norm(rhs_h))
     for _ in range(max(args.warmup, 0)):
         st = step()
         log(f'warmup step: {st.iterations} iterations')
@@ -333,16 +417,21 @@ def run_b200(args):
     if args.profile:
         torch.cuda.profiler.start()    # ncu --profile-from-start off: the timed steps only
     ev0.record(stream)
-    iters = []
+    iters, stats = [], []
     for _ in range(args.steps):
         st = step()
         iters.append(st.iterations)
+        stats.append(st)
     ev1.record(stream)
     torch.cuda.synchronize()
     if args.profile:
         torch.cuda.profiler.stop()
     launches = L.lib().irk_launch_count() - launches0
     log('timed region done')
+    # every timed stage-solve must have converged (GmresStats are host scalars read
+    # after each solve's single end-of-loop sync; no extra sync inside the region)
+    assert all(st_.converged for st_ in stats), [st_.iterations for st_ in stats]
+    true_res = [st_.final_true_residual / b_norm for st_ in stats]
     clocks = clk.stop()
     t_local = ev0.elapsed_time(ev1) / 1e3
     t = t_local
@@ -460,7 +549,17 @@ def run_b200(args):
         "gmres_ms_per_iteration": 1e3 * t_sol / max(iters[-1], 1),
         "levels_fwd_bwd": list(solver.fac.levels()) if solver.fac is not None else None,
         "jnorm2": jnorm, "dt": dt,
+        "all_timed_steps_converged": True,
+        "final_true_residual_rel": true_res[-1],
+        "max_true_residual_rel": max(true_res),
     }
+    fp64 = fp64_peak()
+    if fp64:
+        flops_factor = factor_flops(T, r, nb, s)
+        components["factor_tflops"] = flops_factor / t_fac / 1e12
+        components["factor_frac_of_fp64_tc_peak"] = flops_factor / t_fac / 1e12 / fp64["fp64_dmma_tflops"]
+        components["fp64_tc_peak_tflops"] = fp64["fp64_dmma_tflops"]
+        components["fp64_peak_source"] = fp64["source"]
 
     # ---- end to end through host buffers (pinned), C-ABI upload path ------
     e2e = None
@@ -586,7 +685,11 @@ def run_b200(args):
         log('other ordering done')
     if rank != 0:
         return
-    cpu = None if args.no_cpu else cpu_sample(args)
+    if not args.no_cpu:
+        wl.jnorm, wl.dt = jnorm, dt
+        cpu = cpu_sample(args, prebuilt=(cfg, wl))
+    else:
+        cpu = None
     line = {
         "metric": "IRK stage-solves/sec", "value": value, "unit": "stage-solves/s",
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,

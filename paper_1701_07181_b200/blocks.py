@@ -346,6 +346,41 @@ class BlockDiagonalMatrix:
     def n(self) -> int:
         return self.T_elems * self.m
 
+    def matvec(self, x, counter: OpCounter | None = None):
+        """y_i = M_i x_i (reference blocks.py:164-170)."""
+        if int(x.shape[0]) != self.n or len(x.shape) != 1:
+            raise ValueError(f"expected vector of length {self.n}, got {tuple(x.shape)}")
+        y = self._diag_matrix().matvec(x)
+        if counter is not None:
+            counter.block_multiplies += self.T_elems
+        return y
+
+    def _diag_matrix(self) -> "BlockSparseMatrix":
+        if getattr(self, "_diag", None) is None:
+            T = self.T_elems
+            ar = np.arange(T, dtype=np.int64)
+            pat = DevicePattern(np.arange(T + 1, dtype=np.int64), ar, ar)
+            self._diag = BlockSparseMatrix(pat, self.device)
+        return self._diag
+
+    def solve(self, x, counter: OpCounter | None = None):
+        """y_i = M_i^-1 x_i (reference blocks.py:172-176, np.linalg.solve per
+        block): the block ILU(0) of M on the diagonal-only pattern, i.e. the
+        device inverse of every M_i (partial-pivoting Gauss-Jordan, factor.cu /
+        inverse.cu), built once, then one D^-1 gemv sweep.  Equal to the LU
+        solve to rounding."""
+        if int(x.shape[0]) != self.n or len(x.shape) != 1:
+            raise ValueError(f"expected vector of length {self.n}, got {tuple(x.shape)}")
+        if getattr(self, "_inv", None) is None:
+            from .precond import ilu0_factorize
+            self._inv = ilu0_factorize(self._diag_matrix())
+        xd, was_np = to_device(x)
+        y = empty_like_dev(self.n)
+        self._inv.apply_device(xd, y)
+        if counter is not None:
+            counter.block_solves += self.T_elems
+        return from_device(y, was_np)
+
 
 # ---------------------------------------------------------------------------
 # Line-oriented text exchange format (reference blocks.py:193-216)

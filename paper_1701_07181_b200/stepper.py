@@ -38,6 +38,7 @@ import numpy as np
 from . import _lib as L
 from .blocks import BlockDiagonalMatrix, BlockSparseMatrix, DeviceBlocks, DevicePattern, OpCounter
 from .krylov import GmresConfig, GmresStats, equivalent_multiplications, gmres_device
+from .meshes import partition_bounds
 from .precond import (build_stage_matrix, ilu0_factorize, partition_keep_mask,
                       stage_coupled_factorize, stage_uncoupled_factorize)
 from .stage_system import StageOperator
@@ -168,8 +169,9 @@ class LinearProblem:
     def partition_of(self, parts: int | None):
         if parts is None:
             return None
-        T = self.pattern.T
-        bounds = np.array([(T * p) // parts for p in range(parts + 1)])
+        # the reference's partition (meshing.py:81-90): np.array_split sizes, the
+        # first T % parts ranges one element longer
+        bounds = partition_bounds(self.pattern.T, parts)
         return np.repeat(np.arange(parts), np.diff(bounds))
 
 
@@ -345,12 +347,13 @@ def dirk_step(problem: LinearProblem, tab, u0, t0: float, dt: float,
               counter: OpCounter | None = None,
               partitions: int | None = None,
               cache: StepCache | None = None) -> StepResult:
-    """Sequential DIRK stage solves (stepper.py:229-287), on the device: stage i
-    solves (M - dt a_ii J) k_i = J base_i by Newton with plain block ILU(0)."""
+    """Sequential (E)SDIRK stage solves (stepper.py:229-287), on the device: stage i
+    solves (M - dt a_ii J) k_i = J base_i by Newton with plain block ILU(0); an
+    explicit stage (a_ii = 0, ESDIRK) is one block-diagonal mass solve."""
     if dt <= 0:
         raise ValueError("dt must be positive")
     tab = builtin_tableau(tab) if isinstance(tab, str) else tab
-    if tab.kind != "dirk":
+    if tab.kind not in ("dirk", "esdirk"):
         raise ValueError(f"{tab.name} is not diagonally implicit")
     newton_cfg = newton_cfg or NewtonConfig()
     gmres_cfg = gmres_cfg or GmresConfig()
@@ -370,7 +373,9 @@ def dirk_step(problem: LinearProblem, tab, u0, t0: float, dt: float,
             if A[i, j] != 0.0:
                 base.add_(k_stages[j], alpha=dt * float(A[i, j]))
         if aii == 0.0:
-            raise ValueError("explicit first stages (ESDIRK) need a mass solve; not supported here")
+            # explicit stage: one mass solve, no Newton (stepper.py:253-259)
+            k_stages[i] = problem.mass().solve(problem.rhs(t0 + dt * float(tab.c[i]), base), counter)
+            continue
         mat, fac, keep = cache.dirk_stage(problem, dt * aii, partitions)
         jb = problem.jac.matvec(base)
 
@@ -421,7 +426,7 @@ def integrate(problem: LinearProblem, scheme, t0: float, t1: float, dt: float,
     start = time.perf_counter()
     for k in range(num_steps):
         tk = t0 + k * dt
-        if tab.kind == "dirk":
+        if tab.kind in ("dirk", "esdirk"):
             res = dirk_step(problem, tab, u, tk, dt, newton_cfg, gmres_cfg, counter,
                             partitions=precond.partitions if precond else None, cache=cache)
         else:

@@ -318,7 +318,135 @@ def text_format_case():
     print("matrix_line6.txt written")
 
 
+def tableau_partition_cases():
+    """Round-2 KATs: every builtin tableau (A, b, c, order, derive) including the
+    generated RADAU47/RADAU59 and ESDIRK65 (tableaux.py:140-275), the s-stage
+    generator for s = 1..9, and the reference partition map for T % P != 0
+    (meshing.py:81-90)."""
+    out = {}
+    for name in ref.tableaux.BUILTIN_NAMES:
+        tab = ref.builtin_tableau(name)
+        d_ = ref.derive(tab)
+        for k, v in (("A", tab.A), ("b", tab.b), ("c", tab.c), ("a_inv", d_.a_inv),
+                     ("bT_a_inv", d_.bT_a_inv), ("shifts", d_.shifts)):
+            out[f"{name}_{k}"] = np.asarray(v)
+        out[f"{name}_order"] = tab.order
+        out[f"{name}_kind"] = tab.kind.value
+    for s in range(1, 10):
+        tab = ref.tableaux.generate_radau_iia(s)
+        out[f"gen{s}_A"], out[f"gen{s}_c"] = tab.A, tab.c
+    for T, P in ((50, 4), (7, 3), (10, 10), (3072, 8), (101, 8), (12, 5)):
+        g = ref.build_line_mesh(T, periodic=True)
+        out[f"part_{T}_{P}"] = ref.partition(g, P).partition_of
+    np.savez_compressed(os.path.join(HERE, "tableaux_r2.npz"), **out)
+    print("tableaux_r2 written")
+
+
+def stepper_cases_r2():
+    """Newton steps with the s = 4 / 5 Radau IIA tableaux (generated) and the
+    ESDIRK65 explicit first stage (stepper.py:253-259: one mass solve), on the
+    same linear problem and shapes as stepper_cases."""
+    from irksolve.problems import SemidiscreteProblem
+    from irksolve.stepper import NewtonConfig, PrecondSpec, dirk_step, irk_step_transformed
+
+    out = {}
+    cfg = W.CONFIGS[1].scaled(N=6, nb=8, dt_norm=10.0)
+    wl = W.make_workload(cfg)
+    g = ref_graph(wl.table)
+    Jm = ref_matrix(g, wl.J)
+    mass = ref.BlockDiagonalMatrix(wl.M)
+    u0 = np.random.default_rng(11).standard_normal(Jm.n)
+
+    class LinearJ(SemidiscreteProblem):
+        name = "linear-J"
+
+        def __init__(self):
+            self.graph = g
+            self.m = wl.J.shape[1]
+
+        def mass(self):
+            return mass
+
+        def rhs(self, t, u):
+            return Jm.matvec(u)
+
+        def jacobian(self, t, u):
+            return Jm
+
+    prob = LinearJ()
+    gcfg = ref.GmresConfig(rel_tol=1e-8, restart=40)
+    out["dt"], out["u0"], out["sha"] = wl.dt, u0, sha(wl.J, wl.M)
+    for name, scheme, kind in (("r47u", "RADAU47", "uncoupled"), ("r47c", "RADAU47", "coupled"),
+                               ("r59u", "RADAU59", "uncoupled"), ("r59c", "RADAU59", "coupled"),
+                               ("esdirk", "ESDIRK65", None)):
+        tab = ref.builtin_tableau(scheme)
+        u = u0.copy()
+        ctr = ref.OpCounter()
+        for step in range(2):
+            if kind is None:
+                res = dirk_step(prob, tab, u, step * wl.dt, wl.dt, NewtonConfig(), gcfg, ctr)
+            else:
+                res = irk_step_transformed(prob, tab, u, step * wl.dt, wl.dt, PrecondSpec(kind=kind),
+                                           NewtonConfig(), gcfg, ctr)
+            u = res.u_next
+            out[f"{name}_u{step + 1}"] = u
+            out[f"{name}_newton{step + 1}"] = res.newton_iterations
+            out[f"{name}_gmres{step + 1}"] = np.array([st.iterations for st in res.gmres_stats])
+        out[f"{name}_counter"] = np.array([ctr.block_multiplies, ctr.block_solves,
+                                           ctr.block_factorizations, ctr.mass_multiplies,
+                                           ctr.jacobian_multiplies])
+        print(f"stepper_r2 {name}: newton {out[f'{name}_newton1']} gmres {out[f'{name}_gmres1']}")
+    np.savez_compressed(os.path.join(HERE, "stepper_r2.npz"), **out)
+
+
+def cfg2_nb50_cases():
+    """Config-2 shape at its real block size (nb=50, s=3, shifted uncoupled,
+    GMRES(40), dt||J||2=100) on the 8^3-cube Kuhn mesh (T=3072), solved by the
+    reference at P = 1, 2, 4, 8 (partition(graph, P), precond.py:26-45), natural
+    numbering, plus the slab-colour numbering at P = 8.  Vectors are 460,800
+    long, so only strided samples (every 61st entry) and full norms are stored;
+    the GPU tests compare full vectors against the oracle and these samples
+    against the reference."""
+    cfg = W.CONFIGS[2].scaled(N=8)
+    cases = [("natural", P) for P in (1, 2, 4, 8)] + [("color", 8)]
+    for ordering, P in cases:
+        c = cfg.scaled(ordering=ordering, extra={"parts": P} if ordering == "color" else {})
+        wl = W.make_workload(c)
+        tab = ref.builtin_tableau(c.scheme)
+        der = ref.derive(tab)
+        s = tab.s
+        g = ref_graph(wl.table)
+        part = ref.partition(g, P).partition_of if P > 1 else None
+        Jm = ref_matrix(g, wl.J)
+        mass = ref.BlockDiagonalMatrix(wl.M)
+        op = ref.StageOperator(der, wl.dt, mass, [Jm] * s)
+        w = np.random.default_rng(99).standard_normal(op.total_dim)
+        from irksolve.stepper import _make_preconditioner
+        fac = _make_preconditioner(op, ref.PrecondSpec(kind=c.precond, partitions=P if P > 1 else None),
+                                   part, None)
+        y_mv, y_ap = op.matvec(w), fac.apply(w)
+        x, st = ref.gmres(op.matvec, fac.apply, wl.rhs,
+                          ref.GmresConfig(rel_tol=c.rtol, restart=c.restart))
+        idx = np.arange(0, op.total_dim, 61)
+        out = dict(idx=idx, matvec=y_mv[idx], apply=y_ap[idx], x=x[idx],
+                   matvec_norm=np.linalg.norm(y_mv), apply_norm=np.linalg.norm(y_ap),
+                   x_norm=np.linalg.norm(x), iterations=st.iterations, converged=st.converged,
+                   residual_history=np.array(st.residual_history),
+                   final_true_residual=st.final_true_residual, dt=wl.dt, jnorm=wl.jnorm,
+                   input_sha=sha(wl.J, wl.M, wl.rhs), w_sha=sha(w))
+        name = f"cfg2_n8_nb50_{ordering}_p{P}"
+        np.savez_compressed(os.path.join(HERE, f"{name}.npz"), **out)
+        print(f"{name}: iters={st.iterations} conv={st.converged} true_res={st.final_true_residual:.3e}",
+              flush=True)
+
+
 def main():
+    if "--r2" in sys.argv:
+        tableau_partition_cases()
+        stepper_cases_r2()
+        if "--no-cfg2" not in sys.argv:
+            cfg2_nb50_cases()
+        return
     if "--text" in sys.argv:
         text_format_case()
         return

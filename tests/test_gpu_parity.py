@@ -177,8 +177,10 @@ def test_device_gmres_vs_reference(ks):
         assert st2.iterations == st.iterations
         np.testing.assert_array_equal(x2, x)
         xr, str_ = gmres(op.matvec, fac.apply, ks["gm_rhs"], GmresConfig(rel_tol=1e-10, restart=3))
-        assert abs(str_.iterations - int(ks[f"gm_{tag}_rst_iters"])) <= 1
-        assert rel(xr, ks[f"gm_{tag}_rst_x"]) < 1e-8
+        rst_it = int(ks[f"gm_{tag}_rst_iters"])
+        assert abs(str_.iterations - rst_it) <= 1
+        # the solution bar (1e-10) whenever the iteration counts agree
+        assert rel(xr, ks[f"gm_{tag}_rst_x"]) < (1e-10 if str_.iterations == rst_it else 1e-8)
 
 
 def test_singular_pivot_error_device():
@@ -632,3 +634,68 @@ def test_chunked_upload_roundtrip(nb, count, first):
     db.upload(data, first=first)
     back = db.download(first=first, count=count)
     assert np.array_equal(back, data)
+
+
+def test_dirk_stage_vs_reference_golden():
+    """DIRK33 implicit stage (stepper.py:268-274: build_stage_matrix(1.0, M, J,
+    dt*a_ii) + ilu0_factorize + gmres(mat.matvec, fac.apply)) vs the reference-run
+    golden dirk_small.npz: matvec / apply within 1e-12, iterations +-1, x within
+    1e-10 at equal counts."""
+    from paper_1701_07181_b200 import precond as P
+    from paper_1701_07181_b200.blocks import (BlockDiagonalMatrix, BlockSparseMatrix, DeviceBlocks,
+                                              DevicePattern)
+    from paper_1701_07181_b200.krylov import GmresConfig, gmres
+    g = load_golden("dirk_small")
+    cfg = W.CONFIGS[1].scaled(N=6, nb=8)
+    wl = W.make_workload(cfg)
+    assert sha(wl.J, wl.M, wl.rhs) == str(g["input_sha"]) and wl.dt == float(g["dt"])
+    p = wl.pattern
+    J = BlockSparseMatrix(DevicePattern(p.indptr, p.indices, p.diag_pos), DeviceBlocks.from_host(wl.J))
+    mat = P.build_stage_matrix(1.0, BlockDiagonalMatrix(wl.M), J, wl.dt * float(g["aii"]))
+    fac = P.ilu0_factorize(mat)
+    assert rel(mat.matvec(g["w"]), g["matvec"]) < TOL
+    assert rel(fac.apply(g["w"]), g["apply"]) < TOL
+    n = mat.n
+    # the reference's closures, exactly as dirk_step builds them
+    x, st = gmres(lambda v: mat.matvec(v, None), lambda v: fac.apply(v, None), wl.rhs[:n],
+                  GmresConfig(rel_tol=1e-8, restart=40))
+    ref_it = int(g["iterations"])
+    assert abs(st.iterations - ref_it) <= 1 and st.converged
+    if st.iterations == ref_it:
+        assert rel(x, g["x"]) < 1e-10
+
+
+@pytest.mark.parametrize("workers", [2, 3, 4, 8])
+def test_protocol_shims_concurrent_threads(be, workers):
+    """The reference calls ilu0_factor / ilu0_solve from up to s pool threads at
+    once (precond.py:228-237, 270-277); ctypes drops the GIL, so the irk_ref_*
+    shims run truly concurrently.  Results must be bitwise identical to the
+    serial calls for any thread count (per-call streams and workspaces)."""
+    from concurrent.futures import ThreadPoolExecutor
+    cfg = W.CONFIGS[1].scaled(N=8)
+    wl = W.make_workload(cfg, norm_iters=10)
+    p = wl.pattern
+    keep = np.ones(p.nnzb, bool)
+    coefs = np.diag(wl.a_inv) + wl.shifts
+    stages = []
+    for c in list(coefs) * 2:          # 6 stage matrices (two rounds of the 3 stages)
+        d = -wl.dt * wl.J
+        d[p.diag_pos] += c * wl.M
+        stages.append(d)
+    ys = [np.random.default_rng(k).standard_normal(p.T * cfg.nb) for k in range(len(stages))]
+
+    def fac(k):
+        return be.ilu0_factor(p.indptr, p.indices, p.diag_pos, stages[k], keep, True)
+
+    serial = [fac(k) for k in range(len(stages))]
+    sol_serial = [be.ilu0_solve(p.indptr, p.indices, p.diag_pos, serial[k][0], serial[k][1], keep, ys[k])
+                  for k in range(len(stages))]
+    with ThreadPoolExecutor(max_workers=workers) as pool:
+        conc = list(pool.map(fac, range(len(stages))))
+        sol = list(pool.map(lambda k: be.ilu0_solve(p.indptr, p.indices, p.diag_pos, conc[k][0],
+                                                    conc[k][1], keep, ys[k]), range(len(stages))))
+    for k in range(len(stages)):
+        assert conc[k][2] == serial[k][2] == -1
+        np.testing.assert_array_equal(conc[k][0], serial[k][0])
+        np.testing.assert_array_equal(conc[k][1], serial[k][1])
+        np.testing.assert_array_equal(sol[k], sol_serial[k])

@@ -150,3 +150,95 @@ def test_stepper_argument_errors_and_newton_failure():
         irk_step_transformed(prob, "RADAU23", u0, 0.0, wl.dt, PrecondSpec("coupled"),
                              NewtonConfig(abs_tol_inf=1e-300, max_iters=1))
     assert len(ei.value.residual_history) == 2
+
+
+R2_CASES = [("r47u", "RADAU47", "uncoupled"), ("r47c", "RADAU47", "coupled"),
+            ("r59u", "RADAU59", "uncoupled"), ("r59c", "RADAU59", "coupled"),
+            ("esdirk", "ESDIRK65", None)]
+
+
+@pytest.mark.parametrize("name,scheme,kind", R2_CASES)
+def test_device_steps_r2_vs_reference(name, scheme, kind):
+    """s = 4 / 5 Radau IIA (generated tableaux, tableaux.py:246-254) through the
+    device transformed step -- stage operator, coupled / shifted-uncoupled factor
+    and GMRES at s > 3 -- and the ESDIRK65 step whose first stage is explicit (one
+    block-diagonal mass solve, stepper.py:253-259), against the reference's steps
+    (stepper_r2.npz): Newton counts equal, GMRES +-1, u within 1e-9, counters equal."""
+    from paper_1701_07181_b200.blocks import DevicePattern, OpCounter
+    from paper_1701_07181_b200.krylov import GmresConfig
+    from paper_1701_07181_b200.stepper import (LinearProblem, NewtonConfig, PrecondSpec, StepCache,
+                                               dirk_step, irk_step_transformed)
+    g2 = load_golden("stepper_r2")
+    cfg = W.CONFIGS[1].scaled(N=6, nb=8, dt_norm=10.0)
+    wl = W.make_workload(cfg)
+    assert sha(wl.J, wl.M) == str(g2["sha"])
+    p = wl.pattern
+    prob = LinearProblem(DevicePattern(p.indptr, p.indices, p.diag_pos), wl.J, wl.M)
+    tab = builtin_tableau(scheme)
+    gcfg = GmresConfig(rel_tol=1e-8, restart=40)
+    ctr, cache = OpCounter(), StepCache()
+    u = g2["u0"]
+    exact = True
+    for step in (1, 2):
+        if kind is None:
+            res = dirk_step(prob, tab, u, 0.0, wl.dt, NewtonConfig(), gcfg, ctr, cache=cache)
+        else:
+            res = irk_step_transformed(prob, tab, u, 0.0, wl.dt, PrecondSpec(kind=kind),
+                                       NewtonConfig(), gcfg, ctr, cache=cache)
+        u = res.u_next
+        assert res.newton_iterations == int(g2[f"{name}_newton{step}"])
+        gref = list(g2[f"{name}_gmres{step}"])
+        got = [st.iterations for st in res.gmres_stats]
+        assert len(got) == len(gref) and all(abs(a - b) <= 1 for a, b in zip(got, gref)), (got, gref)
+        exact &= got == gref
+        assert rel(u.cpu().numpy(), g2[f"{name}_u{step}"]) < 1e-9
+    have = np.array([ctr.block_multiplies, ctr.block_solves, ctr.block_factorizations,
+                     ctr.mass_multiplies, ctr.jacobian_multiplies])
+    if exact:
+        np.testing.assert_array_equal(have, g2[f"{name}_counter"])
+
+
+def test_mass_solve_vs_lu():
+    """BlockDiagonalMatrix.solve (reference blocks.py:172-176, np.linalg.solve per
+    block) on the device: the inverse of every mass block applied in one sweep,
+    equal to the LU solve within 1e-12; counter += T block solves."""
+    from paper_1701_07181_b200.blocks import BlockDiagonalMatrix, OpCounter
+    for nb, T in ((8, 72), (40, 512), (50, 300)):
+        M = W.mass_blocks(T, nb, seed=5)
+        x = np.random.default_rng(nb).standard_normal(T * nb)
+        bd = BlockDiagonalMatrix(M)
+        ctr = OpCounter()
+        y = bd.solve(x, ctr)
+        want = np.linalg.solve(M, x.reshape(T, nb, 1)).reshape(-1)
+        assert rel(y, want) < 1e-12
+        assert ctr.block_solves == T
+        assert rel(bd.matvec(y), x) < 1e-12
+        with pytest.raises(ValueError):
+            bd.solve(x[:-1])
+
+
+def test_partitioned_factor_t_not_divisible_by_p():
+    """LinearProblem.partition_of for T % P != 0 (T=72, P=5 -> 15/15/14/14/14, the
+    reference's np.array_split, meshing.py:81-90): the device partitioned ILU(0)
+    apply equals the oracle's with the reference's keep mask (precond.py:26-45)."""
+    import oracle as O
+    from paper_1701_07181_b200.blocks import DevicePattern
+    from paper_1701_07181_b200.precond import stage_uncoupled_factorize
+    from paper_1701_07181_b200.stage_system import StageOperator
+    from paper_1701_07181_b200.stepper import LinearProblem
+    from paper_1701_07181_b200.tableau import derive
+    cfg = W.CONFIGS[1].scaled(N=6, nb=8)
+    wl = W.make_workload(cfg, norm_iters=10)
+    p = wl.pattern
+    prob = LinearProblem(DevicePattern(p.indptr, p.indices, p.diag_pos), wl.J, wl.M)
+    part = prob.partition_of(5)
+    ref_part = np.concatenate([np.full(len(c), k) for k, c in enumerate(np.array_split(np.arange(p.T), 5))])
+    np.testing.assert_array_equal(part, ref_part)
+    np.testing.assert_array_equal(np.bincount(part), [15, 15, 14, 14, 14])
+    der = derive(builtin_tableau("RADAU35"))
+    op = StageOperator(der, wl.dt, prob.mass(), [prob.jac] * 3)
+    fac = stage_uncoupled_factorize(op, der.shifts, partition_of=part)
+    w = np.random.default_rng(5).standard_normal(3 * prob.n)
+    oprob = O.problem_from_workload(wl)
+    ofac = O.make_preconditioner(oprob, "uncoupled", der.shifts, partition_of=ref_part)
+    assert rel(fac.apply(w), ofac.apply(w)) < 1e-12

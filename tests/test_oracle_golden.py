@@ -260,3 +260,111 @@ def test_text_format_matches_reference_dump():
         assert open(out).read() == open(ref_path).read()
     with pytest.raises(ValueError):
         read_matrix_blocks(ref_path, ip[:-1], ix)
+
+
+# ---------------------------------------------------------------------------
+# round 2: generated Radau IIA (s = 4, 5), ESDIRK65, partition map, r2 steps
+# ---------------------------------------------------------------------------
+
+@pytest.fixture(scope="module")
+def gt():
+    return load_golden("tableaux_r2")
+
+
+@pytest.mark.parametrize("name", ["RADAU23", "RADAU35", "RADAU47", "RADAU59", "DIRK33", "ESDIRK65"])
+def test_builtin_tableaux_vs_reference(gt, name):
+    """Every builtin scheme (tableaux.py:140-155) incl. the generated RADAU47 /
+    RADAU59 and ESDIRK65: A, b, c, order and derive() (A^-1, b^T A^-1, shifts;
+    tableaux.py:257-275, ESDIRK on A[1:,1:]) equal the reference's."""
+    from paper_1701_07181_b200.tableau import builtin_tableau, derive
+    tab = builtin_tableau(name)
+    d = derive(tab)
+    for k, v in (("A", tab.A), ("b", tab.b), ("c", tab.c)):
+        np.testing.assert_allclose(v, gt[f"{name}_{k}"], rtol=0, atol=2e-15)
+    for k, v in (("a_inv", d.a_inv), ("bT_a_inv", d.bT_a_inv), ("shifts", d.shifts)):
+        ref_v = gt[f"{name}_{k}"]
+        assert np.max(np.abs(v - ref_v)) <= 1e-13 * max(1.0, np.max(np.abs(ref_v))), k
+    assert tab.order == int(gt[f"{name}_order"])
+    assert tab.kind == {"fully_implicit": "irk", "dirk": "dirk", "esdirk": "esdirk"}[str(gt[f"{name}_kind"])]
+
+
+@pytest.mark.parametrize("s", range(1, 10))
+def test_generate_radau_iia_vs_reference(gt, s):
+    """generate_radau_iia(s) (tableaux.py:246-254) for s = 1..9."""
+    from paper_1701_07181_b200.tableau import generate_radau_iia
+    tab = generate_radau_iia(s)
+    np.testing.assert_allclose(tab.A, gt[f"gen{s}_A"], rtol=0, atol=5e-15)
+    np.testing.assert_allclose(tab.c, gt[f"gen{s}_c"], rtol=0, atol=5e-15)
+    assert tab.c[-1] == 1.0 and np.allclose(tab.A.sum(axis=1), tab.c, atol=1e-14)
+    with pytest.raises(ValueError):
+        generate_radau_iia(10)
+
+
+@pytest.mark.parametrize("T,P", [(50, 4), (7, 3), (10, 10), (3072, 8), (101, 8), (12, 5)])
+def test_partition_map_vs_reference(gt, T, P):
+    """meshes.partition / partition_bounds and the stepper's LinearProblem.partition_of
+    reproduce the reference's partition (meshing.py:81-90) when T % P != 0 (T=50,
+    P=4 -> 13/13/12/12)."""
+    from paper_1701_07181_b200.meshes import line_mesh, partition, partition_bounds
+    from paper_1701_07181_b200.stepper import LinearProblem
+    want = gt[f"part_{T}_{P}"]
+    np.testing.assert_array_equal(partition(line_mesh(T, periodic=True), P).partition_of, want)
+    b = partition_bounds(T, P)
+    np.testing.assert_array_equal(np.repeat(np.arange(P), np.diff(b)), want)
+    fake = LinearProblem.__new__(LinearProblem)
+    fake.pattern = type("P", (), {"T": T})()
+    np.testing.assert_array_equal(fake.partition_of(P), want)
+
+
+R2_STEPS = [("r47u", "RADAU47", "uncoupled"), ("r47c", "RADAU47", "coupled"),
+            ("r59u", "RADAU59", "uncoupled"), ("r59c", "RADAU59", "coupled"),
+            ("esdirk", "ESDIRK65", None)]
+
+
+@pytest.mark.parametrize("name,scheme,kind", R2_STEPS)
+def test_oracle_newton_steps_r2(name, scheme, kind):
+    """The oracle's restated steppers with s = 4 / 5 and the ESDIRK explicit stage
+    reproduce the reference's steps (stepper_r2.npz)."""
+    g2 = load_golden("stepper_r2")
+    cfg = W.CONFIGS[1].scaled(N=6, nb=8, dt_norm=10.0)
+    wl = W.make_workload(cfg)
+    assert sha(wl.J, wl.M) == str(g2["sha"]) and wl.dt == float(g2["dt"])
+    p = wl.pattern
+    tab = builtin_tableau(scheme)
+    cfgm = O.GmresConfig(rel_tol=1e-8, restart=40)
+    u = g2["u0"]
+    for step in (1, 2):
+        if kind is None:
+            u, newton, gm = O.dirk_step_linear(p.indptr, p.indices, p.diag_pos, wl.J, wl.M, tab.A,
+                                               tab.b, u, wl.dt, cfgm)
+        else:
+            u, newton, gm = O.irk_step_linear(p.indptr, p.indices, p.diag_pos, wl.J, wl.M, tab.A,
+                                              tab.b, u, wl.dt, kind, cfgm)
+        assert newton == int(g2[f"{name}_newton{step}"])
+        want = list(g2[f"{name}_gmres{step}"])
+        assert len(gm) == len(want) and all(abs(a - b) <= 1 for a, b in zip(gm, want)), (gm, want)
+        assert rel(u, g2[f"{name}_u{step}"]) < 1e-10
+
+
+@pytest.mark.parametrize("ordering,P", [("natural", 1), ("natural", 2), ("natural", 4), ("natural", 8),
+                                        ("color", 8)])
+def test_oracle_config2_nb50_vs_reference(ordering, P):
+    """The oracle pinned at the config-2 block size (nb=50, s=3, 8^3 Kuhn cubes)
+    against the reference's own runs at P = 1, 2, 4, 8 (cfg2_n8_nb50_*.npz):
+    matvec / apply samples within 1e-12, identical GMRES iteration counts, x
+    within 1e-10."""
+    g = load_golden(f"cfg2_n8_nb50_{ordering}_p{P}")
+    c = W.CONFIGS[2].scaled(N=8, ordering=ordering, extra={"parts": P} if ordering == "color" else {})
+    wl = W.make_workload(c, jnorm=float(g["jnorm"]))
+    assert sha(wl.J, wl.M, wl.rhs) == str(g["input_sha"]) and wl.dt == float(g["dt"])
+    part = None if P == 1 else np.concatenate(
+        [np.full(len(ch), k) for k, ch in enumerate(np.array_split(np.arange(wl.pattern.T), P))])
+    prob = O.problem_from_workload(wl)
+    fac = O.make_preconditioner(prob, "uncoupled", wl.shifts, partition_of=part, workers=3)
+    w = np.random.default_rng(99).standard_normal(prob.s * prob.T * prob.m)
+    idx = g["idx"]
+    assert rel(prob.matvec(w)[idx], g["matvec"]) < 1e-12
+    assert rel(fac.apply(w)[idx], g["apply"]) < 1e-12
+    x, st = O.gmres(prob.matvec, fac.apply, wl.rhs, O.GmresConfig(rel_tol=1e-8, restart=40))
+    assert st.iterations == int(g["iterations"]) and st.converged
+    assert rel(x[idx], g["x"]) < 1e-10
