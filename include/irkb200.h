@@ -57,6 +57,9 @@ typedef struct irk_pattern irk_pattern;
 typedef struct irk_blocks irk_blocks;
 typedef struct irk_stage_op irk_stage_op;
 typedef struct irk_factor irk_factor;
+typedef struct irk_comm irk_comm;
+typedef struct irk_halo irk_halo;
+typedef struct irk_dist_op irk_dist_op;
 
 /* ---- library / context ------------------------------------------------ */
 IRK_API int irk_version(void);
@@ -208,6 +211,52 @@ IRK_API int irk_vec_multidot(irk_ctx *ctx, int64_t n, int nv, const double *V, i
                      const double *w, double *out, void *stream);
 IRK_API int irk_vec_update(irk_ctx *ctx, int64_t n, int nv, const double *V, int64_t ldv,
                    const double *h, double *w, double *out_nrm2, void *stream);
+
+/* ---- element-partitioned (multi-GPU) layer ----------------------------------
+ * The paper's parallel scheme: elements in P contiguous slabs
+ * (partition, meshing.py:81-90), partitioned ILU(0) (precond.py:26-45, no
+ * communication), a neighbour halo for the operator and summed GMRES inner
+ * products.  One rank per GPU.  Replaces the reference's in-process partition
+ * bookkeeping (precond.py:26-45 keep mask on one process); the reference has no
+ * communication layer of its own.
+ *
+ * irk_comm: NCCL transport (libnccl.so.2 loaded at run time; the unique id is
+ * produced on rank 0 and broadcast by the caller) or a host-callback transport
+ * (host-staged exchange, e.g. for tests on one GPU).  irk_comm_allreduce has the
+ * irk_allreduce_fn signature: pass it with user = the comm to irk_gmres. */
+#define IRK_NCCL_ID_BYTES 128
+/* move the packed send buffer ([stage][send element][nb], peers in creation
+ * order, contiguous) to the peers and fill ghost ([stage][ghost][nb]) */
+typedef int (*irk_halo_xfer_fn)(void *user, const double *send_dev, double *ghost_dev, void *stream);
+IRK_API int irk_comm_nccl_available(void);
+IRK_API int irk_comm_nccl_unique_id(unsigned char *id_out, int64_t cap);
+IRK_API int irk_comm_create_nccl(irk_ctx *ctx, const unsigned char *id, int nranks, int rank, irk_comm **out);
+IRK_API int irk_comm_create_callback(irk_ctx *ctx, int nranks, int rank, irk_halo_xfer_fn xfer,
+                                     irk_allreduce_fn allreduce, void *user, irk_comm **out);
+IRK_API void irk_comm_destroy(irk_comm *comm);
+IRK_API int irk_comm_allreduce(void *comm, double *buf, int64_t count, void *stream);
+/* halo of a stage-major (s, T_local, nb) vector: per peer, the local elements it
+ * needs (send_elems, concatenated in peer order) and the contiguous ghost range
+ * [recv_first, recv_first + recv_count) it fills (ghosts sorted by global id) */
+IRK_API int irk_halo_create(irk_comm *comm, int s, int nb, int64_t T_local, int64_t n_ghost, int npeers,
+                            const int32_t *peers, const int64_t *send_counts, const int64_t *send_elems,
+                            const int64_t *recv_counts, const int64_t *recv_first, irk_halo **out);
+IRK_API void irk_halo_destroy(irk_halo *h);
+IRK_API int irk_halo_exchange(irk_halo *h, const double *x, double *ghost, void *stream);
+/* the slab's rows of the stage operator (op after irk_stage_op_set_halo with the same
+ * ghost buffer) as a GMRES operator: exchange overlapped with the interior rows
+ * [interior_lo, interior_hi), then the boundary rows (host list) */
+IRK_API int irk_dist_op_create(irk_stage_op *op, irk_halo *halo, double *ghost, int64_t interior_lo,
+                               int64_t interior_hi, const int32_t *boundary_rows, int64_t nboundary,
+                               irk_dist_op **out);
+IRK_API void irk_dist_op_destroy(irk_dist_op *d);
+IRK_API int irk_dist_op_apply(const irk_dist_op *d, const double *w, double *y, void *stream);
+/* x = P^-1 (B v) with the distributed operator: exchange, then the fused Arnoldi
+ * product over the slab's rows when the factor is the slab's partitioned implicit-L
+ * ILU(0) on the same Jacobian values (*fused = 1), else operator then factor */
+IRK_API int irk_dist_op_factor_apply(const irk_dist_op *d, const irk_factor *f, const double *v, double *x,
+                                     int *fused, void *stream);
+IRK_API int irk_linop_dist_op(const irk_dist_op *d, irk_linop *out);
 
 /* ---- kernel-plugin protocol shims (host pointers; numba_backend.py) ------- */
 IRK_API int irk_ref_bsr_matvec(irk_ctx *ctx, int64_t T, int m, const int64_t *indptr,

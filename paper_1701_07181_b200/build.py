@@ -17,7 +17,8 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 REPO = os.path.dirname(HERE)
 OUT = os.path.join(CSRC, "libirkb200.so")
-SOURCES = ["common.cu", "matvec.cu", "factor.cu", "inverse.cu", "apply.cu", "krylov.cu", "refshim.cu"]
+SOURCES = ["common.cu", "matvec.cu", "factor.cu", "inverse.cu", "apply.cu", "krylov.cu", "refshim.cu",
+           "comm.cu"]
 HEADERS = ["irk_internal.cuh", "blockops.cuh", "pipeline.cuh"]
 
 
@@ -71,7 +72,7 @@ def build(force: bool = False, verbose: bool = False, jobs: int | None = None) -
         raise RuntimeError(f"nvcc failed for {failed}")
     tmp = OUT + ".tmp"
     subprocess.run([cc, "-shared", "-o", tmp] + objs +
-                   ["-gencode", "arch=compute_100a,code=sm_100a", "-Xcompiler", "-fPIC"],
+                   ["-gencode", "arch=compute_100a,code=sm_100a", "-Xcompiler", "-fPIC", "-ldl"],
                    check=True)
     os.replace(tmp, OUT)
     return OUT

@@ -1042,11 +1042,19 @@ __global__ void __launch_bounds__(288) k_unc_sweep_seg(ApplyArgs A, SegCfg SC) {
 enum { PD_MV = 1024, PD_FU2 = 2048, PD_MM = 4096 };
 
 struct FusedMv {
-    const double* J;    // operator blocks (== factor ubase[0])
+    const double* J;    // operator blocks (== factor ubase[0], or the halo operator's own blocks)
     const double* M;
     const double* v;    // operator input (s, T, nb)
     double alpha;
     double mix[IRK_MAX_STAGES * IRK_MAX_STAGES];
+    // element-partitioned operator (halo mode): its row i holds the factor's row i
+    // (the slab's own columns, same order) followed by the ghost columns >= T_local,
+    // whose segments come from the ghost buffer (s, n_ghost, nb).  NULL: the
+    // operator's pattern is the factor's.
+    const int32_t* op_indptr;
+    const int32_t* op_indices;
+    const double* ghost;
+    int64_t T_local, n_ghost;
 };
 
 template <int S>
@@ -1076,7 +1084,7 @@ __global__ void __launch_bounds__(288) k_unc_fused_fwd(ApplyArgs A, SegCfg SC, F
         if (lane != 0) return;
         int st = 0;
         uint32_t ph = 0;
-        auto push = [&](int4 d, const double* blk, const double* s1, const double* s2) {
+        auto push = [&](int4 d, const double* blk, const double* s1, const double* s2, int64_t s1_stride) {
             mbar_wait(empty + st, ph ^ 1);
             desc[st] = d;
             unsigned char* dst = stages + (size_t)st * SC.stage_bytes;
@@ -1085,7 +1093,7 @@ __global__ void __launch_bounds__(288) k_unc_fused_fwd(ApplyArgs A, SegCfg SC, F
             bulk_g2s(dst, blk, SC.block_bytes, full + st);
             dst += SC.block_bytes;
             if (s1)
-                for (int k = 0; k < S; ++k, dst += seg) bulk_g2s(dst, s1 + k * A.n, seg, full + st);
+                for (int k = 0; k < S; ++k, dst += seg) bulk_g2s(dst, s1 + k * s1_stride, seg, full + st);
             if (s2)
                 for (int k = 0; k < S; ++k, dst += seg) bulk_g2s(dst, s2 + k * A.n, seg, full + st);
             if (++st == SC.nst) { st = 0; ph ^= 1; }
@@ -1096,18 +1104,33 @@ __global__ void __launch_bounds__(288) k_unc_fused_fwd(ApplyArgs A, SegCfg SC, F
             const int d = A.diag[i];
             const int b0 = A.indptr[i], b1 = A.indptr[i + 1];
             const int store_z = A.hasup[i] ? 1 : 0;
-            for (int qq = b0; qq < b1; ++qq) {
-                const int64_t col = A.indices[qq];
-                const bool low = qq < d && A.keep[qq];
-                push(make_int4((int)i, 0, (low ? PD_FU2 : PD_MV) | (qq == b0 ? PD_FIRST : 0), 0),
-                     F.J + (int64_t)qq * bsz, F.v + col * nb, low ? A.W + col * nb : nullptr);
+            if (F.op_indptr) {
+                // halo mode: the operator row = the factor row's own columns, then ghosts
+                const int e0 = F.op_indptr[i], e1 = F.op_indptr[i + 1];
+                const int64_t gstride = F.n_ghost * nb;
+                for (int qe = e0; qe < e1; ++qe) {
+                    const int64_t col = F.op_indices[qe];
+                    const bool gh = col >= F.T_local;
+                    const int qq = b0 + (qe - e0);
+                    const bool low = !gh && qq < d && A.keep[qq];
+                    push(make_int4((int)i, 0, (low ? PD_FU2 : PD_MV) | (qe == e0 ? PD_FIRST : 0), 0),
+                         F.J + (int64_t)qe * bsz, gh ? F.ghost + (col - F.T_local) * nb : F.v + col * nb,
+                         low ? A.W + col * nb : nullptr, gh ? gstride : A.n);
+                }
+            } else {
+                for (int qq = b0; qq < b1; ++qq) {
+                    const int64_t col = A.indices[qq];
+                    const bool low = qq < d && A.keep[qq];
+                    push(make_int4((int)i, 0, (low ? PD_FU2 : PD_MV) | (qq == b0 ? PD_FIRST : 0), 0),
+                         F.J + (int64_t)qq * bsz, F.v + col * nb, low ? A.W + col * nb : nullptr, A.n);
+                }
             }
-            if (F.M) push(make_int4((int)i, 0, PD_MM, 0), F.M + i * bsz, F.v + i * nb, nullptr);
+            if (F.M) push(make_int4((int)i, 0, PD_MM, 0), F.M + i * bsz, F.v + i * nb, nullptr, A.n);
             for (int k = 0; k < S; ++k)
                 push(make_int4((int)i, k, PD_DINV | (k == S - 1 ? PD_LAST : 0), store_z), A.Dinv + (i * S + k) * bsz,
-                     nullptr, nullptr);
+                     nullptr, nullptr, A.n);
         }
-        push(make_int4(-1, 0, PD_END, 0), A.Dinv, nullptr, nullptr);   // block copy unused (harmless)
+        push(make_int4(-1, 0, PD_END, 0), A.Dinv, nullptr, nullptr, A.n);   // block copy unused (harmless)
         return;
     }
     const int c = threadIdx.x - 32;
@@ -2161,6 +2184,14 @@ static int fused_apply_t(const irk_stage_op* op, const irk_factor* f, const doub
     A.epoch = ++f->epoch;
     FusedMv F{};
     F.J = f->ubase[0];
+    if (op->ghost) {
+        F.J = op->J[0]->d + op->jfirst[0] * block_doubles(op->nb);
+        F.op_indptr = op->pat->d_indptr;
+        F.op_indices = op->pat->d_indices;
+        F.ghost = op->ghost;
+        F.T_local = op->T_local;
+        F.n_ghost = op->n_ghost;
+    }
     F.M = op->M ? op->M->d : nullptr;
     F.v = v;
     F.alpha = op->alpha;
@@ -2170,16 +2201,71 @@ static int fused_apply_t(const irk_stage_op* op, const irk_factor* f, const doub
     return IRK_OK;
 }
 
+// Compare the operator's own-column blocks of every row with the factor's source
+// blocks at the corresponding factor position (bitwise); *bad = 1 on any mismatch.
+__global__ void k_halo_blocks_equal(const double* __restrict__ opJ, const int32_t* __restrict__ op_indptr,
+                                    const double* __restrict__ fJ, const int32_t* __restrict__ f_indptr,
+                                    int64_t T, int64_t bsz, int* bad) {
+    for (int64_t i = blockIdx.x; i < T; i += gridDim.x) {
+        const int64_t e0 = op_indptr[i], q0 = f_indptr[i], cnt = f_indptr[i + 1] - q0;
+        const double* a = opJ + e0 * bsz;
+        const double* b = fJ + q0 * bsz;
+        for (int64_t t = threadIdx.x; t < cnt * bsz; t += blockDim.x)
+            if (__double_as_longlong(a[t]) != __double_as_longlong(b[t])) *bad = 1;
+    }
+}
+
+static int halo_pair_ok(const irk_stage_op* op, const irk_factor* f, cudaStream_t st) {
+    if (f->halo_op == op && f->halo_epoch == f->numeric_epoch) return f->halo_ok ? 0 : 1;
+    f->halo_op = op;
+    f->halo_epoch = f->numeric_epoch;
+    f->halo_ok = false;
+    const irk_pattern* po = op->pat;
+    const irk_pattern* pf = f->pat;
+    const int64_t T = op->T_local;
+    if (po->T < T || pf->T != T || !f->ubase[0]) return 1;
+    for (int64_t i = 0; i < T; ++i) {
+        const int64_t e0 = po->h_indptr[i], e1 = po->h_indptr[i + 1];
+        const int64_t q0 = pf->h_indptr[i], q1 = pf->h_indptr[i + 1];
+        if (q1 - q0 > e1 - e0) return 1;
+        for (int64_t k = 0; k < q1 - q0; ++k)
+            if (po->h_indices[e0 + k] != pf->h_indices[q0 + k]) return 1;
+        for (int64_t e = e0 + (q1 - q0); e < e1; ++e)
+            if (po->h_indices[e] < T) return 1;
+    }
+    int* d_bad = nullptr;
+    IRK_CK(cudaMallocAsync(&d_bad, sizeof(int), st));
+    IRK_CK(cudaMemsetAsync(d_bad, 0, sizeof(int), st));
+    const int64_t bsz = block_doubles(op->nb);
+    k_halo_blocks_equal<<<(int)std::min<int64_t>(T, (int64_t)f->ctx->num_sms * 8), 256, 0, st>>>(
+        op->J[0]->d + op->jfirst[0] * bsz, po->d_indptr, f->ubase[0], pf->d_indptr, T, bsz, d_bad);
+    IRK_LAUNCHED();
+    int bad = 1;
+    IRK_CK(cudaMemcpyAsync(&bad, d_bad, sizeof(int), cudaMemcpyDeviceToHost, st));
+    IRK_CK(cudaStreamSynchronize(st));
+    IRK_CK(cudaFreeAsync(d_bad, st));
+    f->halo_ok = bad == 0;
+    return f->halo_ok ? 0 : 1;
+}
+
 int factor_apply_fused(const irk_stage_op* op, const irk_factor* f, const double* v, double* x, cudaStream_t st) {
     static const bool off = getenv("IRK_FUSED") && atoi(getenv("IRK_FUSED")) == 0;
     static const bool seg_off = getenv("IRK_APPLY_SEG") && atoi(getenv("IRK_APPLY_SEG")) == 0;
     if (off || seg_off || !op || !f) return 1;
     if (f->kind != IRK_FACTOR_UNCOUPLED || !f->l_implicit || f->u_stored || !f->u_shared) return 1;
     if (f->fwd.nlevels > LEVEL_LAUNCH_MAX || f->bwd.nlevels > LEVEL_LAUNCH_MAX) return 1;
-    if (op->pat != f->pat || op->s != f->s || op->nb != f->nb || !op->shared_j || op->ghost ||
-        op->T_local != f->pat->T || f->nb % 2)
-        return 1;
-    if (op->J[0]->d + op->jfirst[0] * block_doubles(op->nb) != f->ubase[0]) return 1;
+    if (op->s != f->s || op->nb != f->nb || !op->shared_j || op->T_local != f->pat->T || f->nb % 2) return 1;
+    if (op->ghost) {
+        // element-partitioned operator (extended pattern, halo buffer) with the slab's
+        // partitioned factor: checked once per (operator, factor) pair on the host
+        // (patterns) and on the device (the operator's own-column blocks equal the
+        // factor's upper source blocks), cached until the factor is re-factorised
+        const int ok = halo_pair_ok(op, f, st);
+        if (ok != 0) return ok < 0 ? ok : 1;
+    } else {
+        if (op->pat != f->pat) return 1;
+        if (op->J[0]->d + op->jfirst[0] * block_doubles(op->nb) != f->ubase[0]) return 1;
+    }
     switch (f->s) {
         case 1: return fused_apply_t<1>(op, f, v, x, st);
         case 2: return fused_apply_t<2>(op, f, v, x, st);

@@ -1425,6 +1425,7 @@ int irk_factor_refactor(irk_factor* f, const irk_blocks* const* J, const int64_t
     P.coupling = coupling;
     IRK_TRY(set_sources(f, P));
     IRK_ARG(!f->l_implicit || f->u_shared, "implicit-L factor: refactor needs one J shared by all stages");
+    ++f->numeric_epoch;
     return factor_numeric(f, fail_stage, fail_elem, (cudaStream_t)stream);
 }
 

@@ -225,6 +225,12 @@ struct irk_factor {
     size_t fsmem = 0;
     int maxt = 1;
     const double* cpl_src = nullptr;  // explicit couplings (s*s*T blocks)
+    // fused Arnoldi product with an element-partitioned operator (apply.cu halo_pair_ok):
+    // the checked (operator, numeric version) pair and its verdict
+    unsigned numeric_epoch = 0;       // bumped by every re-factorisation
+    mutable const irk_stage_op* halo_op = nullptr;
+    mutable unsigned halo_epoch = 0;
+    mutable bool halo_ok = false;
     // owned copies when created from explicit host data
     std::vector<irk_blocks*> owned;
 };

@@ -28,6 +28,10 @@ namespace irk {
 
 int factor_apply(const irk_factor* f, const double* y, double* x, cudaStream_t st);
 int factor_apply_fused(const irk_stage_op* op, const irk_factor* f, const double* v, double* x, cudaStream_t st);
+// comm.cu: element-partitioned operator
+int dist_op_apply(const irk_dist_op* d, const double* w, double* y, cudaStream_t st);
+int dist_op_fused_product(const irk_dist_op* d, const irk_factor* f, const double* v, double* x, cudaStream_t st);
+const irk_stage_op* dist_op_stage_op(const irk_dist_op* d);
 
 constexpr int VB = 256;      // threads per vector CTA
 constexpr int VGROUP = 8;    // vectors per multidot pass
@@ -672,6 +676,16 @@ static int linop_stage(void* u, const double* in, double* out, void* st) {
 static int linop_factor(void* u, const double* in, double* out, void* st) {
     return irk_factor_apply((const irk_factor*)u, in, out, st);
 }
+static int linop_dist(void* u, const double* in, double* out, void* st) {
+    return dist_op_apply((const irk_dist_op*)u, in, out, (cudaStream_t)st);
+}
+
+int irk_linop_dist_op(const irk_dist_op* d, irk_linop* out) {
+    IRK_ARG(d && out, "NULL argument");
+    out->fn = linop_dist;
+    out->user = (void*)d;
+    return IRK_OK;
+}
 
 int irk_linop_stage_op(const irk_stage_op* op, irk_linop* out) {
     IRK_ARG(op && out, "NULL argument");
@@ -862,6 +876,17 @@ int irk_gmres(irk_ctx* ctx, int64_t n, irk_linop op, irk_linop pre, irk_allreduc
                 // native pair: stage matvec fused into the forward sweep (apply.cu)
                 fused = factor_apply_fused((const irk_stage_op*)op.user, (const irk_factor*)pre.user, V(j), w, st);
                 if (fused < 0) return fused;
+            } else if (op.fn == linop_dist && pre.fn == linop_factor) {
+                // element-partitioned operator: halo exchange, then the fused product over the
+                // slab's rows (ghost segments from the halo buffer)
+                const irk_dist_op* d = (const irk_dist_op*)op.user;
+                fused = dist_op_fused_product(d, (const irk_factor*)pre.user, V(j), w, st);
+                if (fused < 0) return fused;
+                if (fused == 1) {   // halo already exchanged: local operator, then P^-1
+                    IRK_TRY(irk_stage_op_apply(dist_op_stage_op(d), V(j), ws.tmp, st));
+                    IRK_TRY(call(pre, ws.tmp, w));
+                    fused = 0;
+                }
             }
             if (fused == 0) {
             } else if (pre.fn) {
