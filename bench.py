@@ -44,7 +44,8 @@ def parse():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
-    ap.add_argument("--config", type=int, default=1)
+    ap.add_argument("--config", type=int, default=None,
+                    help="BASELINE config (default: 1 at N=1, the 3D config 2 partitioned at N>1)")
     ap.add_argument("--N", type=int, default=None, help="override mesh cells per side")
     ap.add_argument("--ordering", default="color", choices=["natural", "color"],
                     help="element numbering (color: colour-major, the mesh-colouring level schedule)")
@@ -58,7 +59,12 @@ def parse():
                     help="use this ||J||_2 instead of the power iteration (profiling runs)")
     ap.add_argument("--partitioned", action="store_true",
                     help="element-partitioned solve even at N=1 (always used for N>1)")
-    return ap.parse_args()
+    ap.add_argument("--no-single", action="store_true",
+                    help="N>1: skip rank 0's single-GPU solve of the same system")
+    args = ap.parse_args()
+    if args.config is None:
+        args.config = 2 if (dist_env()[0] > 1 or args.partitioned) else 1
+    return args
 
 
 def dist_env():
@@ -351,15 +357,17 @@ def run_reference(args):
 
 
 def config_dict(cfg, args):
+    mesh = (f"periodic {cfg.N}x{cfg.N} quads -> {cfg.T} triangles" if cfg.mesh == "tri2d" else
+            f"periodic {cfg.N}^3 cubes -> {cfg.T} Kuhn tetrahedra")
     return {
-        "workload": (f"cfg{args.config}: periodic {cfg.N}x{cfg.N} quads -> {cfg.T} triangles, "
+        "workload": (f"cfg{args.config}: {mesh}, "
                      f"nb={cfg.nb}, {cfg.scheme} (s={cfg.s}), {cfg.precond} block ILU(0) "
                      f"({cfg.ordering} numbering), GMRES({cfg.restart}) rtol {cfg.rtol}, "
                      f"dt*||J||2={cfg.dt_norm}, J std 1/nb"),
         "T": cfg.T, "nb": cfg.nb, "s": cfg.s, "precond": cfg.precond, "restart": cfg.restart,
         "rtol": cfg.rtol, "ordering": cfg.ordering,
         "l2": "inputs larger than L2 (J alone is %.2f GB > 126 MB)" % (cfg.T * 4 * 8 * cfg.nb ** 2 / 1e9),
-        "parallelism": f"replicas x{args.gpus}" if args.gpus > 1 else "single GPU",
+        "parallelism": "single GPU",
     }
 
 
@@ -553,6 +561,31 @@ def run_b200(args):
         "final_true_residual_rel": true_res[-1],
         "max_true_residual_rel": max(true_res),
     }
+    # the reference-level drop-in (install_stepper): the reference's glue builds a fresh
+    # factor and calls gmres with its wrappers lambda v: op.matvec(v, counter) /
+    # lambda v: fac.apply(v, counter) on a host rhs (stepper.py:164-170); krylov.gmres
+    # recognises them and runs the native loop (fused product), charging the counters
+    from paper_1701_07181_b200 import krylov as K
+    from paper_1701_07181_b200.blocks import OpCounter
+    from paper_1701_07181_b200.precond import stage_uncoupled_factorize
+    ctr = OpCounter()
+    op_ = solver.op
+
+    def dropin_step():
+        fac_ = stage_uncoupled_factorize(op_, der.shifts, ctr)
+        x_, st_ = K.gmres(lambda v: op_.matvec(v, ctr), lambda v: fac_.apply(v, ctr), rhs_h, gcfg)
+        return st_
+    if cfg.precond == "uncoupled":
+        dropin_step()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        for _ in range(3):
+            st_d = dropin_step()
+        torch.cuda.synchronize()
+        components["dropin_reference_glue_ms"] = 1e3 * (time.perf_counter() - t0) / 3
+        components["dropin_reference_glue_iterations"] = st_d.iterations
+        components["dropin_note"] = ("reference stepper glue through install_stepper: new factor + gmres with "
+                                     "the reference's lambda wrappers on a host rhs (H2D rhs, D2H x), native loop")
     fp64 = fp64_peak()
     if fp64:
         flops_factor = factor_flops(T, r, nb, s)
@@ -710,19 +743,42 @@ def log(msg):
 def estimate_jnorm(cfg):
     """||J||_2 for dt: exact power iteration on the GPU when the global J fits
     comfortably on one rank (config 1), else on a reduced mesh of the same
-    generator (the norm of these random block matrices is nearly independent
-    of the mesh size: 2.4485 at 32x32 vs 2.4496 at 128x128 quads)."""
+    generator (16^3 cubes for the 3D workload: the norm of these random block
+    matrices is nearly independent of the mesh size -- 2.4485 at 32x32 vs 2.4496
+    at 128x128 quads)."""
     from paper_1701_07181_b200 import workloads as W
-    c = cfg if cfg.T <= 40000 else cfg.scaled(N=8 if cfg.mesh == "tet3d" else 32)
+    c = cfg if cfg.T <= 40000 else cfg.scaled(N=16 if cfg.mesh == "tet3d" else 32)
     wl = W.make_workload(c.scaled(ordering="natural"), jnorm=1.0)
     return jnorm_device(wl.pattern, wl.J), c.T
 
 
+def fused_bytes_local(plan, fac_levels_ok, s, nb):
+    """Algorithmic bytes of one partitioned Arnoldi product P^-1 (B v) on a rank
+    (the N=1 formula of DESIGN.md section 3 on the slab): every operator block of
+    the slab's rows once (own and ghost columns), M, the kept upper blocks (the
+    backward sweep reads U = -dt J), D^-1 once per row and once more for rows with
+    a kept upper block, v (+ ghosts) read, x written, w = D^-1 z of those rows
+    written and gathered back."""
+    Bk = 8 * nb * nb
+    Tl, ng = plan.T_local, plan.n_ghost
+    rows = np.repeat(np.arange(Tl), np.diff(plan.loc_indptr))
+    up = int(np.count_nonzero(plan.loc_indices > rows))
+    t_up = int(np.count_nonzero(np.bincount(rows[plan.loc_indices > rows], minlength=Tl)))
+    ext_nnzb = int(plan.ext_indptr[-1])
+    return (ext_nnzb + up + Tl + s * (Tl + t_up)) * Bk + 8 * nb * s * (2 * Tl + ng + 2 * t_up)
+
+
 def run_partitioned(args):
-    """Element-partitioned solve of one global system over all ranks:
-    contiguous slabs (colour-major inside each slab), NCCL halo exchange before
-    every operator application, allreduced inner products, partitioned
-    (communication-free) block ILU(0).  Strong scaling."""
+    """Element-partitioned solve of ONE global system over all ranks (strong
+    scaling): the 3D workload (BASELINE config 2: 32^3 cubes -> 196,608 Kuhn
+    tets, nb=50, Radau IIA s=3, shifted uncoupled ILU(0), GMRES(40)) cut into
+    contiguous z-slabs (colour-major inside each slab), the native layer of
+    libirkb200 on every rank: NCCL halo (irk_halo), the slab's operator rows
+    (irk_dist_op, fused Arnoldi product after the exchange), partitioned
+    communication-free ILU(0), irk_gmres with NCCL allreduces (no Python in the
+    loop).  Rank 0 also solves the same system alone on its GPU first (P=1) and
+    reports it as ``single_gpu`` so the per-N values of this workload can be
+    compared."""
     import torch
     world, rank, local = dist_env()
     torch.cuda.set_device(local)
@@ -737,63 +793,180 @@ def run_partitioned(args):
     from paper_1701_07181_b200.tableau import builtin_tableau, derive
     cfg = make_config(args)
     P = world
-    pat, J, M, rhs_h = W.make_slab_workload(cfg, P, rank)
-    jnorm, norm_T = estimate_jnorm(cfg)
-    dt = cfg.dt_norm / jnorm
     der = derive(builtin_tableau(cfg.scheme))
-    plan = SlabPlan.build(pat.indptr, pat.indices, pat.diag_pos, P, rank)
     gcfg = GmresConfig(rel_tol=cfg.rtol, restart=cfg.restart, max_iters=cfg.max_iters)
-    sol = DistributedStageSolver(plan, J, M, der.a_inv, dt, cfg.precond, der.shifts, gcfg)
+    stream = torch.cuda.current_stream()
+    if rank == 0:
+        jnorm, norm_T = (args.jnorm, None) if args.jnorm else estimate_jnorm(cfg)
+    else:
+        jnorm, norm_T = 0.0, None
+    if dist:
+        tj = torch.tensor([jnorm], dtype=torch.float64, device="cuda")
+        dist.broadcast(tj, 0)
+        jnorm = float(tj)
+    dt = cfg.dt_norm / jnorm
+    s, nb = cfg.s, cfg.nb
+
+    def build(Pn, r, group_transport):
+        pat, J, M, rhs_h = W.make_slab_workload(cfg, Pn, r)
+        plan = SlabPlan.build(pat.indptr, pat.indices, pat.diag_pos, Pn, r)
+        sol = DistributedStageSolver(plan, J, M, der.a_inv, dt, cfg.precond, der.shifts, gcfg,
+                                     transport=group_transport)
+        return plan, sol, J, M, rhs_h
+
+    def run_steps(sol, rhs, x, n):
+        its, conv = [], True
+        for _ in range(n):
+            sol.factorize()
+            st = sol.solve(rhs, x=x)[1]
+            its.append(st.iterations)
+            conv &= bool(st.converged)
+        return its, conv, st
+
+    # ---- P = 1 on rank 0 (same system, same numbering rule, one GPU) ----------
+    single = None
+    if world > 1 and rank == 0 and not args.no_single:
+        from paper_1701_07181_b200.distributed import Comm
+        plan1, sol1, *_rest, rhs1 = build(1, 0, Comm.single())
+        r1 = torch.from_numpy(rhs1).cuda()
+        x1 = torch.empty_like(r1)
+        run_steps(sol1, r1, x1, 2)
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        n1 = max(2, min(args.steps, 5))
+        e0.record(stream)
+        its1, conv1, _ = run_steps(sol1, r1, x1, n1)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        t1 = e0.elapsed_time(e1) / 1e3
+        single = {"value": n1 / t1, "unit": "stage-solves/s", "ms_per_step": 1e3 * t1 / n1,
+                  "gmres_iterations": its1[-1], "converged": conv1,
+                  "note": "the same global system solved by rank 0 alone (P=1 partition, one GPU), "
+                          "measured in this run before the partitioned steps"}
+        del sol1, plan1, _rest, r1, x1
+        torch.cuda.empty_cache()
+        log(f"single-GPU reference: {single['value']:.2f} stage-solves/s")
+    if dist:
+        dist.barrier()
+    plan, sol, J, M, rhs_h = build(P, rank, "auto")
     rhs = torch.from_numpy(rhs_h).cuda()
     x = torch.empty_like(rhs)
-    stream = torch.cuda.current_stream()
     log(f"rank {rank}: slab {plan.lo}..{plan.hi} ghosts {plan.n_ghost}")
-
-    def step():
-        sol.factorize()
-        return sol.solve(rhs, x=x)[1]
-
-    for _ in range(max(args.warmup, 0)):
-        st = step()
+    run_steps(sol, rhs, x, max(args.warmup, 0))
     torch.cuda.synchronize()
     if dist:
         dist.barrier()
     clk = ClockSampler(local)
     clk.start()
+    time.sleep(0.3)
     launches0 = L.lib().irk_launch_count()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     ev0.record(stream)
-    iters = []
-    for _ in range(args.steps):
-        iters.append(step().iterations)
+    iters, conv, st = run_steps(sol, rhs, x, args.steps)
     ev1.record(stream)
     torch.cuda.synchronize()
     launches = L.lib().irk_launch_count() - launches0
     clocks = clk.stop()
+    assert conv, iters
     t = ev0.elapsed_time(ev1) / 1e3
+    # local components (outside the timed region): the partitioned Arnoldi product
+    # (halo exchange + fused sweeps) and the factor
+    v = torch.randn(sol.n_local, dtype=torch.float64, device="cuda")
+    out = torch.empty_like(v)
+    _, fused = sol.product(v, out)
+    torch.cuda.synchronize()
+    tot = 0.0
+    for _ in range(10):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        sol.product(v, out)
+        b.record(stream)
+        b.synchronize()
+        tot += a.elapsed_time(b) / 1e3
+    t_prod = tot / 10
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record(stream)
+    for _ in range(3):
+        sol.factorize()
+    b.record(stream)
+    torch.cuda.synchronize()
+    t_fac = a.elapsed_time(b) / 1e3 / 3
+    # e2e through the public API: this rank's slab J, M, rhs from pinned host memory, factor,
+    # solve, solution back, every step (serial)
+    # (the slab solver keeps two device copies of its J rows: the operator's, in extended-pattern
+    # order with the ghost columns, and the factor's, local columns only -- both are uploaded)
+    Jp = torch.from_numpy(np.ascontiguousarray(J[plan.row_block_src - plan.q0])).pin_memory()
+    Jfp = torch.from_numpy(np.ascontiguousarray(J[plan.loc_block_src - plan.q0])).pin_memory()
+    rp = torch.from_numpy(rhs_h).pin_memory()
+    xp = torch.empty_like(rp).pin_memory()
+    jb = sol.op.jacobians[0].blocks
+    jfb = sol.fac_op.jacobians[0].blocks
+    Mp = torch.from_numpy(np.ascontiguousarray(M)).pin_memory()
+    mb = sol.fac_op.mass.device
+    mob = sol.mass.device
+
+    def e2e_step():
+        jb.upload(Jp.numpy())
+        jfb.upload(Jfp.numpy())
+        mb.upload(Mp.numpy())
+        mob.upload(Mp.numpy())
+        rhs.copy_(rp, non_blocking=True)
+        sol.factorize()
+        sol.solve(rhs, x=x)
+        xp.copy_(x, non_blocking=True)
+        torch.cuda.synchronize()
+
+    e2e_step()
     if dist:
-        tt = torch.tensor([t], device="cuda")
+        dist.barrier()
+    ne = 2
+    t0 = time.perf_counter()
+    for _ in range(ne):
+        e2e_step()
+    te = time.perf_counter() - t0
+    tt = torch.tensor([t, t_prod, t_fac, te], dtype=torch.float64, device="cuda")
+    if dist:
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        t = float(tt)
+    t, t_prod_max, t_fac_max, te = (float(v_) for v_ in tt)
     value = args.steps / t
     if rank != 0:
         if dist:
             dist.barrier()
         return
     peak, peak_src = hbm_peak()
+    fb = fused_bytes_local(plan, True, s, nb)
     r = 3 if cfg.mesh == "tri2d" else 4
     line = {
         "metric": "IRK stage-solves/sec", "value": value, "unit": "stage-solves/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * t / args.steps,
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (seeded generators, no dataset; J std 1/nb)",
-        "config": dict(config_dict(cfg, args), parallelism=f"element-partitioned x{world} "
-                       "(NCCL halo send/recv + allreduce; partitioned block ILU(0))",
+        "config": dict(config_dict(cfg, args), parallelism=f"element-partitioned x{world} (z-slabs; "
+                       "native NCCL halo send/recv + allreduce in libirkb200; partitioned block ILU(0))",
                        jnorm_mesh_T=norm_T),
         "gmres_iterations_mean": float(np.mean(iters)),
-        "roofline": None, "cpu_baseline": None, "e2e": None,
+        "all_timed_steps_converged": True,
+        "final_true_residual_rel": st.final_true_residual / float(np.linalg.norm(rhs_h)) if world == 1 else None,
+        "single_gpu": single,
+        "roofline": {"bound": "hbm", "achieved": fb / t_prod / 1e9, "peak": peak, "unit": "GB/s",
+                     "frac": fb / t_prod / 1e9 / peak, "traffic": None,
+                     "kernel": "rank-0 partitioned Arnoldi product P^-1 (B v): halo pack + NCCL exchange + "
+                               "fused forward sweep (ghost segments) + backward sweep",
+                     "algorithmic_bytes_per_launch": fb, "avg_launch_ms": 1e3 * t_prod,
+                     "fused": bool(fused), "peak_source": peak_src},
+        "components": {"arnoldi_product_ms_rank0": 1e3 * t_prod, "arnoldi_product_ms_max": 1e3 * t_prod_max,
+                       "factor_ms_max": 1e3 * t_fac_max, "halo_elements_rank0": int(plan.n_ghost),
+                       "halo_bytes_per_exchange_rank0": int(8 * s * nb * plan.n_ghost),
+                       "T_local_rank0": int(plan.T_local), "jnorm2": jnorm, "dt": dt},
+        "cpu_baseline": None,
+        "e2e": {"value": ne / te, "unit": "stage-solves/s",
+                "h2d_bytes_per_step": int(Jp.numel() * 8 + Jfp.numel() * 8 + 2 * Mp.numel() * 8 + rp.numel() * 8),
+                "d2h_bytes_per_step": int(xp.numel() * 8),
+                "note": "per rank: its slab's J, M, rhs from pinned host memory through irk_blocks_upload / "
+                        "H2D, factor + GMRES, solution D2H, every step (serial); max over ranks; bytes are "
+                        "rank 0's"},
         "gpu_launches": int(launches), "clocks": clocks,
-        "note": "roofline / cpu_baseline / e2e are reported by the N=1 run",
+        "note": "cpu_baseline is reported by the N=1 run (config 1)",
     }
     print(json.dumps(line), flush=True)
     if dist:

@@ -43,6 +43,7 @@ P = ctypes.POINTER
 
 APPLY_FN = ctypes.CFUNCTYPE(c_int, c_vp, c_vp, c_vp, c_vp)
 ALLREDUCE_FN = ctypes.CFUNCTYPE(c_int, c_vp, c_vp, c_i64, c_vp)
+XFER_FN = ctypes.CFUNCTYPE(c_int, c_vp, c_vp, c_vp, c_vp)
 
 
 class Linop(ctypes.Structure):
@@ -97,6 +98,21 @@ _SIGS = {
                           P(GmresStatsC), c_vp, c_int, c_vp]),
     "irk_vec_multidot": (c_int, [c_vp, c_i64, c_int, c_vp, c_i64, c_vp, c_vp, c_vp]),
     "irk_vec_update": (c_int, [c_vp, c_i64, c_int, c_vp, c_i64, c_vp, c_vp, c_vp, c_vp]),
+    "irk_comm_nccl_available": (c_int, []),
+    "irk_comm_nccl_unique_id": (c_int, [c_vp, c_i64]),
+    "irk_comm_create_nccl": (c_int, [c_vp, c_vp, c_int, c_int, P(c_vp)]),
+    "irk_comm_create_callback": (c_int, [c_vp, c_int, c_int, c_vp, c_vp, c_vp, P(c_vp)]),
+    "irk_comm_destroy": (None, [c_vp]),
+    "irk_comm_allreduce": (c_int, [c_vp, c_vp, c_i64, c_vp]),
+    "irk_halo_create": (c_int, [c_vp, c_int, c_int, c_i64, c_i64, c_int, c_vp, c_vp, c_vp, c_vp, c_vp,
+                                P(c_vp)]),
+    "irk_halo_destroy": (None, [c_vp]),
+    "irk_halo_exchange": (c_int, [c_vp, c_vp, c_vp, c_vp]),
+    "irk_dist_op_create": (c_int, [c_vp, c_vp, c_vp, c_i64, c_i64, c_vp, c_i64, P(c_vp)]),
+    "irk_dist_op_destroy": (None, [c_vp]),
+    "irk_dist_op_apply": (c_int, [c_vp, c_vp, c_vp, c_vp]),
+    "irk_dist_op_factor_apply": (c_int, [c_vp, c_vp, c_vp, c_vp, P(c_int), c_vp]),
+    "irk_linop_dist_op": (c_int, [c_vp, P(Linop)]),
     "irk_ref_bsr_matvec": (c_int, [c_vp, c_i64, c_int, c_vp, c_vp, c_vp, c_vp, c_vp]),
     "irk_ref_ilu0_factor": (c_int, [c_vp, c_i64, c_int, c_vp, c_vp, c_vp, c_vp, c_vp, c_int,
                                     c_vp, c_vp, P(c_i64)]),

@@ -1096,6 +1096,11 @@ __global__ void __launch_bounds__(32 * InvTcCfg<NT>::WARPS, NT <= 5 ? 4 : 1)
     const int P = (nb + 1) >> 1;
     const int64_t bsz = (int64_t)nb * 2 * P;
     const int fr = lane >> 2, fk = lane & 3;        // fragment layout
+    // shared-memory position of element (r, c): 16-byte chunks XOR-swizzled by (r >> 1) & 3
+    // inside each group of 4 chunks, so the row-per-lane panel / block accesses (32 rows of
+    // one column pair) hit 8 distinct bank groups per phase instead of 2, and the 8x8 tile
+    // fragments stay conflict-free (rows 2m, 2m + 1 share a swizzle)
+    auto sw = [](int r, int c) -> int { return r * LD + ((((c >> 1) ^ ((r >> 1) & 3)) << 1) | (c & 1)); };
     for (int64_t t = (int64_t)blockIdx.x * C::WARPS + warp; t < A.ntasks; t += (int64_t)gridDim.x * C::WARPS) {
         const int64_t code = A.tasks[t];
         const int k_st = (int)(code / A.T);
@@ -1134,7 +1139,7 @@ __global__ void __launch_bounds__(32 * InvTcCfg<NT>::WARPS, NT <= 5 ? 4 : 1)
                         }
                         const double2 v = fsrc.keep ? make_double2(x0, x1) : make_double2(0.0, 0.0);
                         if (store) dst_d[idx] = v;
-                        *reinterpret_cast<double2*>(X + r * LD + 2 * p2) = v;
+                        *reinterpret_cast<double2*>(X + sw(r, 2 * p2)) = v;
                     }
                 }
             }
@@ -1153,7 +1158,7 @@ __global__ void __launch_bounds__(32 * InvTcCfg<NT>::WARPS, NT <= 5 ? 4 : 1)
                     const int idx = lane + 32 * (e0 + b);
                     if (e0 + b < NE && (NPAIR % 32 == 0 || idx < NPAIR)) {
                         const int p2 = idx / NBT, r = idx - p2 * NBT;
-                        *reinterpret_cast<double2*>(X + r * LD + 2 * p2) = v[b];
+                        *reinterpret_cast<double2*>(X + sw(r, 2 * p2)) = v[b];
                     }
                 }
             }
@@ -1172,7 +1177,7 @@ __global__ void __launch_bounds__(32 * InvTcCfg<NT>::WARPS, NT <= 5 ? 4 : 1)
                 } else {   // identity padding
                     v = make_double2(2 * p2 == r ? 1.0 : 0.0, 2 * p2 + 1 == r ? 1.0 : 0.0);
                 }
-                *reinterpret_cast<double2*>(X + r * LD + 2 * p2) = v;
+                *reinterpret_cast<double2*>(X + sw(r, 2 * p2)) = v;
             }
         }
         __syncwarp();
@@ -1187,13 +1192,13 @@ __global__ void __launch_bounds__(32 * InvTcCfg<NT>::WARPS, NT <= 5 ? 4 : 1)
                     double s4[4] = {0.0, 0.0, 0.0, 0.0};
                     if constexpr (EXACT) {
 #pragma unroll
-                        for (int r = 0; r < NBT; ++r) s4[r & 3] += fabs(X[r * LD + c]);
+                        for (int r = 0; r < NBT; ++r) s4[r & 3] += fabs(X[sw(r, c)]);
                     } else {
                         int r = 0;
                         for (; r + 4 <= nb; r += 4)
 #pragma unroll
-                            for (int q4 = 0; q4 < 4; ++q4) s4[q4] += fabs(X[(r + q4) * LD + c]);
-                        for (; r < nb; ++r) s4[0] += fabs(X[r * LD + c]);
+                            for (int q4 = 0; q4 < 4; ++q4) s4[q4] += fabs(X[sw(r + q4, c)]);
+                        for (; r < nb; ++r) s4[0] += fabs(X[sw(r, c)]);
                     }
                     const double sum = (s4[0] + s4[1]) + (s4[2] + s4[3]);
                     if (sum != sum) nan = 1;
@@ -1225,7 +1230,7 @@ __global__ void __launch_bounds__(32 * InvTcCfg<NT>::WARPS, NT <= 5 ? 4 : 1)
 #pragma unroll
                 for (int c = 0; c < 8; c += 2) {
                     double2 v = make_double2(0.0, 0.0);
-                    if (r < NBT) v = *reinterpret_cast<const double2*>(X + r * LD + k0 + c);
+                    if (r < NBT) v = *reinterpret_cast<const double2*>(X + sw(r, k0 + c));
                     pa[j][c] = v.x;
                     pa[j][c + 1] = v.y;
                 }
@@ -1286,7 +1291,7 @@ __global__ void __launch_bounds__(32 * InvTcCfg<NT>::WARPS, NT <= 5 ? 4 : 1)
             for (int jt = 0; jt < NT; ++jt)
 #pragma unroll
                 for (int kc = 0; kc < 2; ++kc)
-                    bf[jt][kc] = (jt == p) ? 0.0 : X[(k0 + 4 * kc + fk) * LD + 8 * jt + fr];
+                    bf[jt][kc] = (jt == p) ? 0.0 : X[sw(k0 + 4 * kc + fk, 8 * jt + fr)];
             __syncwarp();
 #pragma unroll
             for (int j = 0; j < RL; ++j) {
@@ -1294,17 +1299,17 @@ __global__ void __launch_bounds__(32 * InvTcCfg<NT>::WARPS, NT <= 5 ? 4 : 1)
                 if (r < NBT)
 #pragma unroll
                     for (int c = 0; c < 8; c += 2)
-                        *reinterpret_cast<double2*>(X + r * LD + k0 + c) = make_double2(pa[j][c], pa[j][c + 1]);
+                        *reinterpret_cast<double2*>(X + sw(r, k0 + c)) = make_double2(pa[j][c], pa[j][c + 1]);
             }
             __syncwarp();
 #pragma unroll
             for (int it = 0; it < NT; ++it) {
-                const double a0 = X[(8 * it + fr) * LD + k0 + fk];
-                const double a1 = X[(8 * it + fr) * LD + k0 + 4 + fk];
+                const double a0 = X[sw(8 * it + fr, k0 + fk)];
+                const double a1 = X[sw(8 * it + fr, k0 + 4 + fk)];
 #pragma unroll
                 for (int jt = 0; jt < NT; ++jt) {
                     if (jt == p) continue;
-                    double* cp = X + (8 * it + fr) * LD + 8 * jt + 2 * fk;
+                    double* cp = X + sw(8 * it + fr, 8 * jt + 2 * fk);
                     double2 c = (it == p) ? make_double2(0.0, 0.0) : *reinterpret_cast<const double2*>(cp);
                     dmma_f64(c.x, c.y, a0, bf[jt][0]);
                     dmma_f64(c.x, c.y, a1, bf[jt][1]);
@@ -1337,13 +1342,13 @@ __global__ void __launch_bounds__(32 * InvTcCfg<NT>::WARPS, NT <= 5 ? 4 : 1)
                 const int idx = lane + 32 * e;
                 if (NPAIR % 32 == 0 || idx < NPAIR) {
                     const int p2 = idx / NBT, r = idx - p2 * NBT;
-                    dst[idx] = *reinterpret_cast<const double2*>(X + r * LD + 2 * p2);
+                    dst[idx] = *reinterpret_cast<const double2*>(X + sw(r, 2 * p2));
                 }
             }
         } else {
             for (int idx = lane; idx < P * nb; idx += 32) {
                 const int p2 = idx / nb, r = idx - p2 * nb;
-                double2 v = *reinterpret_cast<const double2*>(X + r * LD + 2 * p2);
+                double2 v = *reinterpret_cast<const double2*>(X + sw(r, 2 * p2));
                 if (2 * p2 + 1 >= nb) v.y = 0.0;
                 dst[idx] = v;
             }

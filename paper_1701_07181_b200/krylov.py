@@ -53,6 +53,81 @@ def equivalent_multiplications(stats: GmresStats, s_implicit: int, is_irk: bool)
     return stats.iterations * s_implicit
 
 
+_SKIP_OPS = {"RESUME", "COPY_FREE_VARS", "CACHE", "PUSH_NULL", "PRECALL", "NOP", "MAKE_CELL", "KW_NAMES"}
+
+
+def closure_call(fn):
+    """Recognise the reference's operator wrappers -- ``lambda v: op.matvec(v,
+    counter)`` / ``lambda v: fac.apply(v, counter)`` (stepper.py:168-170, 272-274)
+    -- by their bytecode: one positional parameter, a single call of the
+    ``matvec`` / ``apply`` method of a captured object with (v) or (v, counter),
+    returned as is.  Returns (object, method name, counter) or None."""
+    import builtins
+    import dis
+    import types
+    if not isinstance(fn, types.FunctionType) or fn.__code__.co_argcount != 1 or fn.__defaults__:
+        return None
+    code = fn.__code__
+    cells = dict(zip(code.co_freevars, [c.cell_contents for c in (fn.__closure__ or ())]))
+
+    def value(ins):
+        if ins.opname == "LOAD_DEREF" and ins.argval in cells:
+            return True, cells[ins.argval]
+        if ins.opname == "LOAD_GLOBAL":
+            g = fn.__globals__
+            if ins.argval in g:
+                return True, g[ins.argval]
+            if hasattr(builtins, ins.argval):
+                return True, getattr(builtins, ins.argval)
+        return False, None
+
+    try:
+        ops = [i for i in dis.get_instructions(fn) if i.opname not in _SKIP_OPS]
+    except Exception:  # noqa: BLE001
+        return None
+    if len(ops) not in (5, 6) or ops[-1].opname != "RETURN_VALUE" or not ops[-2].opname.startswith("CALL"):
+        return None
+    ok, obj = value(ops[0])
+    if not ok or ops[1].opname not in ("LOAD_ATTR", "LOAD_METHOD") or ops[1].argval not in ("matvec", "apply"):
+        return None
+    if ops[2].opname != "LOAD_FAST" or ops[2].argval != code.co_varnames[0]:
+        return None
+    counter = None
+    if len(ops) == 6:
+        ok, counter = value(ops[3])
+        if not ok:
+            return None
+    nargs = ops[-2].arg
+    if nargs != len(ops) - 4:
+        return None
+    from .blocks import OpCounter
+    if counter is not None and not isinstance(counter, OpCounter):
+        return None
+    if not hasattr(obj, "native_linop") or not hasattr(obj, "_charge"):
+        return None
+    return obj, ops[1].argval, counter
+
+
+def charge_gmres(op_obj, op_counter, pre_obj, pre_counter, stats: "GmresStats", restart, max_iters):
+    """Counter increments the reference's gmres makes through its operator
+    wrappers (krylov.py:37-130): P^-1 b and P^-1 (b - B x0) (1 matvec, 2 applies),
+    one of each per iteration, one of each per finished cycle (restart residual),
+    and the final true residual (1 matvec).  A zero rhs touches nothing."""
+    if stats.operator_applies == 0 and stats.iterations == 0 and stats.converged:
+        return
+    k = stats.iterations
+    R = restart or max_iters
+    cycles = (k + R - 1) // R if k > 0 else 0
+    for obj, ctr, times in ((op_obj, op_counter, 1 + k + cycles + 1), (pre_obj, pre_counter, 2 + k + cycles)):
+        if obj is None or ctr is None or times <= 0:
+            continue
+        from .blocks import OpCounter
+        one = OpCounter()
+        obj._charge(one)
+        for key, v in one.snapshot().items():
+            setattr(ctr, key, getattr(ctr, key) + times * v)
+
+
 def _native(fn):
     """Native linop for a bound method of a device object, else None."""
     owner = getattr(fn, "__self__", None)
@@ -103,8 +178,12 @@ def _linop(fn, n, keep):
     return cb.linop()
 
 
-def gmres_device(apply_operator, apply_precond, rhs, cfg: GmresConfig, allreduce=None, x=None):
-    """Run the native loop on a CUDA-tensor rhs; returns (x, GmresStats)."""
+def gmres_device(apply_operator, apply_precond, rhs, cfg: GmresConfig, allreduce=None, x=None,
+                 native_allreduce=None):
+    """Run the native loop on a CUDA-tensor rhs; returns (x, GmresStats).
+    ``allreduce``: Python callable summing a CUDA tensor across ranks in place;
+    ``native_allreduce``: (irk_allreduce_fn address, user pointer), e.g.
+    ``irk_comm_allreduce`` with an ``irk_comm`` (no Python in the loop)."""
     t = L.torch()
     n = rhs.numel()
     keep: list = []
@@ -120,7 +199,9 @@ def gmres_device(apply_operator, apply_precond, rhs, cfg: GmresConfig, allreduce
     st = L.GmresStatsC()
     hist = np.zeros(cfg.max_iters + 2)
     ar_fn, ar_user = None, None
-    if allreduce is not None:
+    if native_allreduce is not None:
+        ar_fn, ar_user = native_allreduce
+    elif allreduce is not None:
         def _ar(user, buf, count, stream):
             try:
                 allreduce(L.wrap_device(buf, count))
@@ -163,6 +244,16 @@ def gmres(apply_operator, apply_precond, rhs, cfg: GmresConfig | None = None):
         x, _ = to_device(pre(u))
         r, _ = to_device(apply_operator(x))
         stats.final_true_residual = float(L.torch().linalg.vector_norm(rd - r))
+        return from_device(x, was_np), stats
+    # the reference's wrappers around this package's device objects (install_stepper):
+    # run the native loop on the objects themselves and charge the wrapped counters
+    # exactly as the wrappers would have been called
+    cop = closure_call(apply_operator)
+    cpre = closure_call(apply_precond) if apply_precond is not None else None
+    if cop is not None and cop[1] == "matvec" and (apply_precond is None or (cpre is not None and cpre[1] == "apply")):
+        x, stats = gmres_device(cop[0].matvec, None if cpre is None else cpre[0].apply, rd, cfg)
+        charge_gmres(cop[0], cop[2], None if cpre is None else cpre[0], None if cpre is None else cpre[2],
+                     stats, cfg.restart, cfg.max_iters)
         return from_device(x, was_np), stats
     x, stats = gmres_device(apply_operator, apply_precond, rd, cfg)
     return from_device(x, was_np), stats

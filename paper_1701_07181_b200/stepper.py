@@ -37,7 +37,7 @@ import numpy as np
 
 from . import _lib as L
 from .blocks import BlockDiagonalMatrix, BlockSparseMatrix, DeviceBlocks, DevicePattern, OpCounter
-from .krylov import GmresConfig, GmresStats, equivalent_multiplications, gmres_device
+from .krylov import GmresConfig, GmresStats, charge_gmres, equivalent_multiplications, gmres_device
 from .meshes import partition_bounds
 from .precond import (build_stage_matrix, ilu0_factorize, partition_keep_mask,
                       stage_coupled_factorize, stage_uncoupled_factorize)
@@ -199,18 +199,8 @@ def _charge(counter: OpCounter | None, obj, times: int) -> None:
 
 def _charge_gmres(counter, op, fac, stats: GmresStats, restart: int | None, max_iters: int):
     """Operator / preconditioner applications the reference's gmres makes
-    (krylov.py:37-130): P^-1 b and P^-1 (b - B x0) (1 matvec, 2 applies), one of
-    each per iteration, one of each per finished cycle (restart residual), and
-    the final true residual (1 matvec)."""
-    if counter is None:
-        return
-    if stats.operator_applies == 0 and stats.iterations == 0 and stats.converged:
-        return    # zero rhs: no operator touched (krylov.py:48-52)
-    k = stats.iterations
-    R = restart or max_iters
-    cycles = (k + R - 1) // R if k > 0 else 0
-    _charge(counter, op, 1 + k + cycles + 1)
-    _charge(counter, fac, 2 + k + cycles)
+    (krylov.py:37-130; krylov.charge_gmres)."""
+    charge_gmres(op, counter, fac, counter, stats, restart, max_iters)
 
 
 def _charge_factor(counter, op, kind: str, keep, s: int):

@@ -358,41 +358,6 @@ def test_block_sizes_vs_oracle(nb):
     assert rel(be.bsr_matvec(p.indptr, p.indices, wl.J, x), O.bsr_matvec(p.indptr, p.indices, wl.J, x)) < TOL
 
 
-def test_partitioned_ranks_emulated_on_one_gpu():
-    """CUDA side of the element-partitioned solve: two ranks' local operators
-    (extended pattern + ghost halo buffer) and partitioned local factors, built
-    in one process with the halo filled from the global vector (NCCL needs one
-    GPU per rank); each rank's rows must match the global oracle."""
-    import torch
-    from paper_1701_07181_b200.distributed import DistributedStageSolver, SlabPlan
-    from paper_1701_07181_b200.meshes import partition_bounds
-    P = 2
-    cfg = W.CONFIGS[2].scaled(N=4, nb=10, ordering="color")
-    full = W.make_workload(cfg.scaled(extra={"parts": P}), norm_iters=20)
-    prob = O.problem_from_workload(full)
-    b = partition_bounds(full.pattern.T, P)
-    part = np.repeat(np.arange(P), np.diff(b))
-    gfac = O.stage_uncoupled_factorize(prob, full.shifts, partition_of=part)
-    s, nb, T = cfg.s, cfg.nb, full.pattern.T
-    w = np.random.default_rng(4).standard_normal(s * T * nb)
-    wd = torch.from_numpy(w).cuda().view(s, T, nb)
-    yref, aref = prob.matvec(w).reshape(s, T, nb), gfac.apply(w).reshape(s, T, nb)
-    for r in range(P):
-        pat, J, M, rhs = W.make_slab_workload(cfg, P, r)
-        plan = SlabPlan.build(pat.indptr, pat.indices, pat.diag_pos, P, r)
-
-        def exch(x_local, ghost, plan=plan):
-            ghost[: s * plan.n_ghost * nb].copy_(wd[:, torch.as_tensor(plan.ghosts).cuda()].reshape(-1))
-
-        sol = DistributedStageSolver(plan, J, M, full.a_inv, full.dt, "uncoupled", full.shifts, exchange=exch)
-        wl = wd[:, plan.lo:plan.hi].contiguous().reshape(-1)
-        y = sol.matvec(wl).view(s, -1, nb).cpu().numpy()
-        assert rel(y, yref[:, plan.lo:plan.hi]) < TOL
-        sol.factorize()
-        a = sol.fac.apply(wl).view(s, -1, nb).cpu().numpy()
-        assert rel(a, aref[:, plan.lo:plan.hi]) < TOL
-
-
 @pytest.mark.parametrize("nb", [24, 40, 50, 100])
 @pytest.mark.parametrize("ordering", ["color", "natural"])
 def test_config3_multi_rhs_vs_oracle(nb, ordering):
