@@ -38,15 +38,29 @@ def read_launches(path):
     return list(launches.values())
 
 
+UNIT = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12,
+        "nsecond": 1e-6, "usecond": 1e-3, "msecond": 1.0, "second": 1e3}
+
+
 def read_raw(path, want):
+    """--page raw --csv export: row 0 names, row 1 units (which differ per column AND may
+    differ from the unit another metric of the same family got: bytes are normalised to MB,
+    durations to ms, so one column never mixes units)."""
     rows = list(csv.reader(open(path)))
-    h = rows[0]
+    h, units = rows[0], dict(zip(rows[0], rows[1]))
     out = []
     for r in rows[2:]:
         if len(r) < len(h):
             continue
         d = dict(zip(h, r))
-        out.append({"name": d.get("Kernel Name", "").split("(")[0], **{w: d.get(w, "") for w in want}})
+        rec = {"name": d.get("Kernel Name", "").split("(")[0]}
+        for w in want:
+            v, u = d.get(w, ""), units.get(w, "")
+            if v != "" and u in UNIT and ("byte" in u or "second" in u):
+                scale = UNIT[u] / (1e6 if "byte" in u else 1.0)
+                v = f"{float(v.replace(',', '')) * scale:.3f}"
+            rec[w] = v
+        out.append(rec)
     return out
 
 
@@ -108,14 +122,22 @@ def main():
     if n_fused:
         lines.append(f"* Arnoldi product P^-1 (B v) (fused forward + backward sweep): "
                      f"{traffic['arnoldi_product']:.4e} (algorithmic 4.709e9)")
-    want = ["gpu__time_duration.sum", "dram__throughput.avg.pct_of_peak_sustained_elapsed",
-            "sm__throughput.avg.pct_of_peak_sustained_elapsed", "sm__warps_active.avg.pct_of_peak_sustained_active",
-            "launch__registers_per_thread", "dram__bytes_read.sum", "dram__bytes_write.sum",
-            "sm__inst_executed_pipe_fp64.avg.pct_of_peak_sustained_active",
-            "smsp__average_warps_issue_stalled_barrier_per_issue_active.ratio"]
+    want = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum",
+            "dram__bytes_read.sum.pct_of_peak_sustained_elapsed", "dram__bytes_write.sum.pct_of_peak_sustained_elapsed",
+            "smsp__issue_active.avg.pct_of_peak_sustained_active",
+            "sm__pipe_shared_cycles_active.avg.pct_of_peak_sustained_active",
+            "sm__warps_active.avg.pct_of_peak_sustained_active", "launch__registers_per_thread",
+            "smsp__average_warps_issue_stalled_short_scoreboard_per_issue_active.ratio",
+            "smsp__average_warps_issue_stalled_long_scoreboard_per_issue_active.ratio",
+            "smsp__average_warps_issue_stalled_barrier_per_issue_active.ratio",
+            "smsp__average_warps_issue_stalled_math_pipe_throttle_per_issue_active.ratio"]
+    label = ["time (ms)", "DRAM read (MB)", "DRAM write (MB)", "DRAM read % of peak", "DRAM write % of peak",
+             "issue slots busy %", "FP64/DMMA pipe busy % (pipe_shared)", "warps active %", "regs/thread",
+             "stall short_scoreboard / issue", "stall long_scoreboard / issue", "stall barrier / issue",
+             "stall math_pipe_throttle / issue"]
     for p in a.raw:
         lines += ["", f"## --set full metrics ({p.split('/')[-1]})", "",
-                  "| kernel | " + " | ".join(w.split(".")[0] if len(w) < 40 else w[:38] for w in want) + " |",
+                  "| kernel | " + " | ".join(label) + " |",
                   "|" + "---|" * (len(want) + 1)]
         for d in read_raw(p, want):
             lines.append(f"| `{d['name']}` | " + " | ".join(d[w] for w in want) + " |")
