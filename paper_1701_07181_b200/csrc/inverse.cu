@@ -1071,7 +1071,7 @@ struct InvTcCfg {
     // ld = 8 (mod 16) doubles: conflict-free C-tile double2 accesses (the DMMA update's traffic)
     static constexpr int NBT = 8 * NT, LD = NBT + ((24 - NBT % 16) % 16), WARPS = 4;
     static constexpr int RL = (NBT + 31) / 32;    // panel rows per lane (row-per-lane layout)
-    static constexpr size_t warp_doubles = (size_t)NBT * LD + 16;   // + 2 x 8 pivot-row buffer
+    static constexpr size_t warp_doubles = (size_t)NBT * LD + 64;   // + 2 x 8 pivot-row buffer / 8 x 8 L scratch
     static constexpr size_t smem = WARPS * warp_doubles * sizeof(double);
 };
 
@@ -1080,9 +1080,12 @@ struct InvTcCfg {
 // row slot ks (0 or RL - 1, RL <= 2) of the lane's panel registers without dynamic register indexing
 #define IRK_PK(ks_, c_) ((RL == 1 || (ks_) == 0) ? pa[0][c_] : pa[RL - 1][c_])
 
-// ROLL: the NT panels run as a loop instead of being unrolled (a fifth of the code: the fully
-// unrolled kernel is ~100 KB of SASS and its warps stall on instruction fetch)
-template <int NT, bool EXACT, bool FORM, bool ROLL = false>
+// BG (default): block Gauss-Jordan -- only the 8 x 8 pivot tile is eliminated with scalar
+// arithmetic (two entries per lane in the DMMA C-fragment layout, shuffles only); the panel
+// columns F_i = -X_ip P, the multipliers of the rows below (pivoting check) and the rank-8
+// update all run as DMMA tiles.  !BG: the 8 scalar steps run on the whole NBT x 8 panel
+// (kept for NT = 5 as the A/B alternative, IRK_INV_BG=0).
+template <int NT, bool EXACT, bool FORM, bool BG = true>
 __global__ void __launch_bounds__(32 * InvTcCfg<NT>::WARPS, NT <= 5 ? 4 : 1)
     k_inverse_tc(InvArgs A, int* fb_list, int* fb_count) {
     using C = InvTcCfg<NT>;
@@ -1318,9 +1321,117 @@ __global__ void __launch_bounds__(32 * InvTcCfg<NT>::WARPS, NT <= 5 ? 4 : 1)
             }
             __syncwarp();
         };
-        if constexpr (ROLL) {
-#pragma unroll 1
-            for (int p = 0; p < NT; ++p) panel(p);
+        // ---- block Gauss-Jordan panel (BG)
+        auto panel_bg = [&](auto pv) {
+            constexpr int p = decltype(pv)::value;
+            constexpr int k0 = 8 * p;
+            if (swap) return;
+            double* Ls = rowbuf;                     // 8 x 8 unit-lower factor of the pivot tile
+            // old row panel p as B fragments (read before row tile p is overwritten)
+            double bf[NT][2];
+#pragma unroll
+            for (int jt = 0; jt < NT; ++jt)
+#pragma unroll
+                for (int kc = 0; kc < 2; ++kc)
+                    bf[jt][kc] = (jt == p) ? 0.0 : X[sw(k0 + 4 * kc + fk, 8 * jt + fr)];
+            // pivot tile in the C-fragment layout: lane (fr, fk) holds X_pp[fr][2 fk], [2 fk + 1]
+            double v0, v1, l0 = 0.0, l1 = 0.0;
+            {
+                const double2 v = *reinterpret_cast<const double2*>(X + sw(k0 + fr, k0 + 2 * fk));
+                v0 = v.x;
+                v1 = v.y;
+            }
+            bool beat = false, okp = true;
+            static_for([&](auto kc_) {
+                constexpr int k = decltype(kc_)::value;
+                constexpr int kh = k >> 1;
+                constexpr bool odd = (k & 1) != 0;
+                const double selv = odd ? v1 : v0;
+                const double piv = __shfl_sync(0xffffffffu, selv, 4 * k + kh);        // X[k][k]
+                const double f = __shfl_sync(0xffffffffu, selv, (lane & ~3) | kh);    // X[fr][k]
+                const double rk0 = __shfl_sync(0xffffffffu, v0, 4 * k + fk);          // X[k][2 fk]
+                const double rk1 = __shfl_sync(0xffffffffu, v1, 4 * k + fk);          // X[k][2 fk + 1]
+                const double ap = fabs(piv);
+                // partial-pivoting equivalence inside the tile: no row r > k of column k beats the diagonal
+                beat |= (fr > k) && (fabs(f) > ap);
+                okp = okp && piv != 0.0 && isfinite(piv);
+                if (k0 + k < nb && lane == ((k0 + k) & 31)) apiv[(k0 + k) >> 5] = ap;
+                const double inv = 1.0 / piv;
+                const bool isc = fk == kh, isr = fr == k;
+                // scaled pivot row in this lane's columns; column k of the new row k is 1 / piv
+                double s0 = rk0 * inv, s1 = rk1 * inv;
+                double t0 = v0, t1 = v1;
+                if (odd) {
+                    s1 = isc ? inv : s1;
+                    t1 = isc ? 0.0 : t1;
+                } else {
+                    s0 = isc ? inv : s0;
+                    t0 = isc ? 0.0 : t0;
+                }
+                // other rows: a_rc - a_rk rk_c, column k: -a_rk / piv
+                const double n0 = fma(-f, s0, t0), n1 = fma(-f, s1, t1);
+                v0 = isr ? s0 : n0;
+                v1 = isr ? s1 : n1;
+                // multiplier l_rk of the unpivoted LU (unit lower L_pp), kept by the lane owning column k
+                const double lv = (fr > k) ? f * inv : (isr ? 1.0 : 0.0);
+                if (odd) l1 = isc ? lv : l1;
+                else l0 = isc ? lv : l0;
+            }, std::make_integer_sequence<int, 8>{});
+            if (__any_sync(0xffffffffu, beat) || !okp) {
+                swap = true;
+                return;
+            }
+            // P = inv(X_pp) -> X_pp, L_pp -> scratch; the old column panel as A fragments
+            *reinterpret_cast<double2*>(X + sw(k0 + fr, k0 + 2 * fk)) = make_double2(v0, v1);
+            *reinterpret_cast<double2*>(Ls + fr * 8 + 2 * fk) = make_double2(l0, l1);
+            double af[NT][2];
+#pragma unroll
+            for (int it = 0; it < NT; ++it) {
+                af[it][0] = (it == p) ? 0.0 : X[sw(8 * it + fr, k0 + fk)];
+                af[it][1] = (it == p) ? 0.0 : X[sw(8 * it + fr, k0 + 4 + fk)];
+            }
+            __syncwarp();
+            const double pb0 = -X[sw(k0 + fk, k0 + fr)], pb1 = -X[sw(k0 + 4 + fk, k0 + fr)];
+            const double lb0 = Ls[fk * 8 + fr], lb1 = Ls[(4 + fk) * 8 + fr];
+            // F_i = -X_ip P (the in-place Gauss-Jordan values of the panel columns)
+#pragma unroll
+            for (int it = 0; it < NT; ++it) {
+                if (it == p) continue;
+                double2 c = make_double2(0.0, 0.0);
+                dmma_f64(c.x, c.y, af[it][0], pb0);
+                dmma_f64(c.x, c.y, af[it][1], pb1);
+                *reinterpret_cast<double2*>(X + sw(8 * it + fr, k0 + 2 * fk)) = c;
+            }
+            __syncwarp();
+            // rank-8 update A_R <- [0; A_R'] + [P; F] A_KR, and for the row tiles below the pivot
+            // tile the multipliers X_ip inv(U_pp) = -F_i L_pp: getrf would not swap iff all |.| <= 1
+            // (ties and rounding-level excesses keep the diagonal, which is an equally valid choice)
+            bool beat2 = false;
+#pragma unroll
+            for (int it = 0; it < NT; ++it) {
+                const double a0 = X[sw(8 * it + fr, k0 + fk)];
+                const double a1 = X[sw(8 * it + fr, k0 + 4 + fk)];
+                if (it > p) {
+                    double2 w = make_double2(0.0, 0.0);
+                    dmma_f64(w.x, w.y, a0, lb0);
+                    dmma_f64(w.x, w.y, a1, lb1);
+                    beat2 |= (fabs(w.x) > 1.0 + 1e-12) || (fabs(w.y) > 1.0 + 1e-12);
+                }
+#pragma unroll
+                for (int jt = 0; jt < NT; ++jt) {
+                    if (jt == p) continue;
+                    double* cp = X + sw(8 * it + fr, 8 * jt + 2 * fk);
+                    double2 c = (it == p) ? make_double2(0.0, 0.0) : *reinterpret_cast<const double2*>(cp);
+                    dmma_f64(c.x, c.y, a0, bf[jt][0]);
+                    dmma_f64(c.x, c.y, a1, bf[jt][1]);
+                    *reinterpret_cast<double2*>(cp) = c;
+                }
+            }
+            if (__any_sync(0xffffffffu, beat2)) swap = true;
+            __syncwarp();
+        };
+        if constexpr (BG) {
+            static_for([&](auto pc_) { panel_bg(pc_); }, std::make_integer_sequence<int, NT>{});
         } else {
             static_for([&](auto pc_) { panel(pc_); }, std::make_integer_sequence<int, NT>{});
         }
@@ -1369,33 +1480,34 @@ __global__ void __launch_bounds__(32 * InvTcCfg<NT>::WARPS, NT <= 5 ? 4 : 1)
     }
 }
 
-template <int NT, bool EXACT, bool FORM, bool ROLL>
+template <int NT, bool EXACT, bool FORM, bool BG>
 static int launch_tc_r(const irk_ctx* ctx, const InvArgs& A, int* fb_list, int* fb_count, cudaStream_t st) {
     using C = InvTcCfg<NT>;
     static bool attr = false;
     if (!attr) {
-        IRK_CK(cudaFuncSetAttribute(k_inverse_tc<NT, EXACT, FORM, ROLL>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::smem));
-        IRK_CK(cudaFuncSetAttribute(k_inverse_tc<NT, EXACT, FORM, ROLL>, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+        IRK_CK(cudaFuncSetAttribute(k_inverse_tc<NT, EXACT, FORM, BG>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::smem));
+        IRK_CK(cudaFuncSetAttribute(k_inverse_tc<NT, EXACT, FORM, BG>, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
         attr = true;
     }
     const int threads = 32 * C::WARPS;
     int per_sm = 1;
-    IRK_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_inverse_tc<NT, EXACT, FORM, ROLL>, threads, C::smem));
+    IRK_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_inverse_tc<NT, EXACT, FORM, BG>, threads, C::smem));
     if (A.cap_per_sm > 0) per_sm = std::min(per_sm, A.cap_per_sm);
     const int64_t need = (A.ntasks + C::WARPS - 1) / C::WARPS;
     const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(need, (int64_t)ctx->num_sms * std::max(per_sm, 1)));
-    k_inverse_tc<NT, EXACT, FORM, ROLL><<<grid, threads, C::smem, st>>>(A, fb_list, fb_count);
+    k_inverse_tc<NT, EXACT, FORM, BG><<<grid, threads, C::smem, st>>>(A, fb_list, fb_count);
     IRK_LAUNCHED();
     return IRK_OK;
 }
 
 template <int NT, bool EXACT, bool FORM>
 static int launch_tc_t(const irk_ctx* ctx, const InvArgs& A, int* fb_list, int* fb_count, cudaStream_t st) {
-    // A/B switch, instantiated for the config-1 tile count only (nb 33..40) to bound build time
-    static const bool roll = getenv("IRK_INV_ROLL") && atoi(getenv("IRK_INV_ROLL")) == 1;
+    // A/B switch: the scalar-panel variant is instantiated for the config-1 tile count only
+    // (nb 33..40) to bound build time
+    static const bool scalar_panel = getenv("IRK_INV_BG") && atoi(getenv("IRK_INV_BG")) == 0;
     if constexpr (NT == 5)
-        if (roll) return launch_tc_r<NT, EXACT, FORM, true>(ctx, A, fb_list, fb_count, st);
-    return launch_tc_r<NT, EXACT, FORM, false>(ctx, A, fb_list, fb_count, st);
+        if (scalar_panel) return launch_tc_r<NT, EXACT, FORM, false>(ctx, A, fb_list, fb_count, st);
+    return launch_tc_r<NT, EXACT, FORM, true>(ctx, A, fb_list, fb_count, st);
 }
 
 template <int NT>
