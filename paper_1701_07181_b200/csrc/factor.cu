@@ -658,8 +658,20 @@ __device__ __forceinline__ void fence_proxy_async_smem() {
 // TWO: two-phase unit -- GEMM1 of all stages (J_ji fragments loaded once for S stages), one
 // barrier, A'_k into the consumed Dinv slots, GEMM2 of all stages (J_ij fragments loaded once),
 // one barrier, refills: 2 barriers per unit instead of S + 1, fewer fragment loads
-template <int S, int NB, bool TWO = false>
-__global__ void __launch_bounds__(4 * NB) k_schur(FactorArgs F, const int32_t* __restrict__ elems, int64_t nelem) {
+// MODE 2: no CTA barrier -- A'_k goes from the C fragments to the A fragments by shuffles (the
+// staged blocks are read-only), every warp counts itself out of a slot when it has read it for
+// the last time and the last warp out refills the slot with the next unit's block
+// CTAs per SM that shared memory allows, capped so that a thread keeps >= 128 registers
+template <int S, int NB>
+constexpr int schur_min_ctas() {
+    const int by_smem = 232448 / ((S + 2) * SchurGeo<NB>::SLOT * 8 + 1280);
+    const int by_regs = 65536 / (4 * NB * 128);
+    const int m = by_smem < by_regs ? by_smem : by_regs;
+    return m < 1 ? 1 : m;
+}
+
+template <int S, int NB, int MODE = 0>
+__global__ void __launch_bounds__(4 * NB, MODE == 1 ? 1 : schur_min_ctas<S, NB>()) k_schur(FactorArgs F, const int32_t* __restrict__ elems, int64_t nelem) {
     using Gm = SchurGeo<NB>;
     constexpr int NT = Gm::NT, LDP = Gm::LDP, SLOT = Gm::SLOT;
     // NB = nb rounded up to 8: the padding rows / columns of the staged blocks are
@@ -670,10 +682,12 @@ __global__ void __launch_bounds__(4 * NB) k_schur(FactorArgs F, const int32_t* _
     constexpr int SJ = 0, SU = 1;   // slots: J_ji, J_ij, then Dinv_k / A'_k at 2 + k
     extern __shared__ __align__(128) double shs[];
     __shared__ __align__(8) uint64_t bars[S + 2];
+    __shared__ int outcnt[S + 2];   // MODE 2: warps that have left each slot
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int fr = lane >> 2, fk = lane & 3;
     const int r0 = warp * 8;
     const double* J = F.J[0];
+    if (threadIdx.x < S + 2) outcnt[threadIdx.x] = 0;
     if (nbv != NB)
         for (int e = threadIdx.x; e < (S + 2) * SLOT; e += blockDim.x) shs[e] = 0.0;
     if (threadIdx.x == 0) {
@@ -782,7 +796,81 @@ __global__ void __launch_bounds__(4 * NB) k_schur(FactorArgs F, const int32_t* _
             const Unit cur = nxt;
             nxt = find_unit(it, q + 1);
             const bool more = nxt.it >= 0;
-            if constexpr (TWO) {
+            if constexpr (MODE == 2) {
+                // this warp is done with slot b: the last warp out refills it (src != NULL).
+                // (Measured and dropped: rotating the slot roles so that each freed slot takes the
+                // block the next unit needs first -- the mbarrier waits are gated by the slowest
+                // warp of the CTA, not by the refill distance: 1.83 vs 1.68 ms.)
+                auto release = [&](int b, const double* src) {
+                    __syncwarp();
+                    int old = 0;
+                    if (lane == 0) {
+                        __threadfence_block();
+                        old = atomicAdd(&outcnt[b], 1);
+                    }
+                    old = __shfl_sync(0xffffffffu, old, 0);
+                    if (old == NT - 1) {
+                        if (lane == 0) {
+                            outcnt[b] = 0;
+                            if (src) {
+                                fence_proxy_async_smem();
+                                mbar_expect_tx(&bars[b], (uint32_t)(Pv * nbv * 16));
+                            }
+                        }
+                        __syncwarp();
+                        if (src)
+                            for (int p = lane; p < Pv; p += 32)
+                                bulk_g2s(shs + (size_t)b * SLOT + p * LDP, src + (int64_t)p * nbv * 2, nbv * 16, &bars[b]);
+                    }
+                };
+                wait_slot(SJ);
+#pragma unroll
+                for (int k = 0; k < S; ++k) {
+                    wait_slot(2 + k);
+                    double acc[NT][2];
+#pragma unroll
+                    for (int t = 0; t < NT; ++t) acc[t][0] = acc[t][1] = 0.0;
+                    const double* Dk = shs + (size_t)(2 + k) * SLOT;
+#pragma unroll 2
+                    for (int kk = 0; kk < NB / 4; ++kk) {
+                        const double a = frag_a(shs + SJ * SLOT, kk);
+#pragma unroll
+                        for (int t = 0; t < NT; ++t) dmma(acc[t][0], acc[t][1], a, frag_b(Dk, kk, t));
+                    }
+                    release(2 + k, more ? src_dinv(nxt, k) : nullptr);
+                    if (k == S - 1) release(SJ, more ? J + (int64_t)nxt.q * BSZ : nullptr);
+                    // L_k = alpha T_k -> global (numba_backend.py:58-61) unless L is implicit;
+                    // A'_k = -alpha L_k stays in the C fragments
+#pragma unroll
+                    for (int t = 0; t < NT; ++t) {
+                        acc[t][0] *= F.alpha;
+                        acc[t][1] *= F.alpha;
+                        if (Lout && gl_off(t) >= 0)
+                            reinterpret_cast<double2*>(Lout + (int64_t)k * BSZ)[gl_off(t)] = make_double2(acc[t][0], acc[t][1]);
+                        acc[t][0] *= -F.alpha;
+                        acc[t][1] *= -F.alpha;
+                    }
+                    if (k == 0) wait_slot(SU);
+                    // D_k += A'_k J_ij; A fragment (row fr, column 8 t2 + 4 h + fk) of A' sits in lane
+                    // (fr, 2 h + fk / 2), register fk % 2 of C tile t2
+#pragma unroll
+                    for (int t2 = 0; t2 < NT; ++t2)
+#pragma unroll
+                        for (int h = 0; h < 2; ++h) {
+                            const int srcl = (lane & ~3) | (2 * h + (fk >> 1));
+                            const double x = __shfl_sync(0xffffffffu, acc[t2][0], srcl);
+                            const double y = __shfl_sync(0xffffffffu, acc[t2][1], srcl);
+                            const double a = (fk & 1) ? y : x;
+#pragma unroll
+                            for (int t = 0; t < NT; ++t)
+                                dmma(dacc[k][t][0], dacc[k][t][1], a, frag_b(shs + SU * SLOT, 2 * t2 + h, t));
+                        }
+                    if (k == S - 1) release(SU, more ? J + (int64_t)nxt.tq * BSZ : nullptr);
+                }
+                (void)cur;
+                continue;
+            }
+            if constexpr (MODE == 1) {
                 wait_slot(SJ);
 #pragma unroll
                 for (int k = 0; k < S; ++k) wait_slot(2 + k);
@@ -909,21 +997,21 @@ __global__ void __launch_bounds__(4 * NB) k_schur(FactorArgs F, const int32_t* _
     }
 }
 
-template <int S, int NB, bool TWO>
+template <int S, int NB, int MODE>
 static int launch_schur_tt(const irk_ctx* ctx, const FactorArgs& F, const int32_t* elems, int64_t nelem,
                            cudaStream_t st, int cap_per_sm) {
     const size_t smem = sizeof(double) * (size_t)(S + 2) * SchurGeo<NB>::SLOT;
     static bool attr = false;
     if (!attr) {
-        IRK_CK(cudaFuncSetAttribute(k_schur<S, NB, TWO>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        IRK_CK(cudaFuncSetAttribute(k_schur<S, NB, TWO>, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+        IRK_CK(cudaFuncSetAttribute(k_schur<S, NB, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        IRK_CK(cudaFuncSetAttribute(k_schur<S, NB, MODE>, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
         attr = true;
     }
     int per_sm = 1;
-    IRK_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_schur<S, NB, TWO>, 4 * NB, smem));
+    IRK_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_schur<S, NB, MODE>, 4 * NB, smem));
     if (cap_per_sm > 0) per_sm = std::min(per_sm, cap_per_sm);
     const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(nelem, (int64_t)ctx->num_sms * std::max(per_sm, 1)));
-    k_schur<S, NB, TWO><<<grid, 4 * NB, smem, st>>>(F, elems, nelem);
+    k_schur<S, NB, MODE><<<grid, 4 * NB, smem, st>>>(F, elems, nelem);
     IRK_LAUNCHED();
     return IRK_OK;
 }
@@ -931,12 +1019,16 @@ static int launch_schur_tt(const irk_ctx* ctx, const FactorArgs& F, const int32_
 template <int S, int NB>
 static int launch_schur_t(const irk_ctx* ctx, const FactorArgs& F, const int32_t* elems, int64_t nelem,
                           cudaStream_t st, int cap_per_sm) {
-    // two-phase units where shared memory already limits the kernel to one CTA per SM (NB >= 56:
-    // config 2, 8.92 -> 8.75 ms at N=16); the per-stage form keeps 3 CTAs/SM at NB = 40
-    static const int env = getenv("IRK_SCHUR_TWO") ? atoi(getenv("IRK_SCHUR_TWO")) : -1;   // A/B knob
-    const bool two = env >= 0 ? env != 0 : NB >= 56;
-    return two ? launch_schur_tt<S, NB, true>(ctx, F, elems, nelem, st, cap_per_sm)
-               : launch_schur_tt<S, NB, false>(ctx, F, elems, nelem, st, cap_per_sm);
+    // IRK_SCHUR_MODE (A/B knob): 0 per-stage software pipeline, S + 1 CTA barriers per unit;
+    // 1 two-phase units (GEMM1 of all stages, GEMM2 of all stages: 2 barriers, more registers);
+    // 2 barrier-free (A' by shuffles, last warp out of a slot refills it)
+    static const int env = getenv("IRK_SCHUR_MODE") ? atoi(getenv("IRK_SCHUR_MODE")) : -1;
+    // measured: config 1 (NB 40, 3 CTAs/SM) 1.72 / - / 1.68 ms for modes 0 / 1 / 2; config 2 at N = 16
+    // (NB 56, one CTA per SM) 5.04 ms for mode 1 vs 5.14 ms for mode 2
+    const int mode = env >= 0 ? env : (NB >= 56 ? 1 : 2);
+    if (mode == 1) return launch_schur_tt<S, NB, 1>(ctx, F, elems, nelem, st, cap_per_sm);
+    if (mode == 0) return launch_schur_tt<S, NB, 0>(ctx, F, elems, nelem, st, cap_per_sm);
+    return launch_schur_tt<S, NB, 2>(ctx, F, elems, nelem, st, cap_per_sm);
 }
 
 template <int S>

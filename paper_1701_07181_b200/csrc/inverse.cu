@@ -1066,6 +1066,23 @@ __device__ __forceinline__ void dmma_f64(double& c0, double& c1, double a, doubl
                  : "+d"(c0), "+d"(c1) : "d"(a), "d"(b));
 }
 
+// Reciprocal without the IEEE slow-path call: rcp.approx seed + two Newton steps (<= 1 ulp).
+// Callers keep |x| inside [1e-30, 1e30] (anything else goes to the pivoted kernels).
+__device__ __forceinline__ double rcp_nr(double x) {
+    double r;
+    asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
+    double e = fma(-x, r, 1.0);
+    r = fma(r, e, r);
+    e = fma(-x, r, 1.0);
+    return fma(r, e, r);
+}
+
+// not volatile: a pure function of its operands, so the scheduler may interleave independent tiles
+__device__ __forceinline__ void dmma_nv(double& c0, double& c1, double a, double b) {
+    asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
+        : "+d"(c0), "+d"(c1) : "d"(a), "d"(b));
+}
+
 template <int NT>
 struct InvTcCfg {
     // ld = 8 (mod 16) doubles: conflict-free C-tile double2 accesses (the DMMA update's traffic)
@@ -1321,113 +1338,144 @@ __global__ void __launch_bounds__(32 * InvTcCfg<NT>::WARPS, NT <= 5 ? 4 : 1)
             }
             __syncwarp();
         };
-        // ---- block Gauss-Jordan panel (BG)
+        // ---- block Gauss-Jordan (BG).  Pivot tile state of the scalar elimination: lane (fr, fk)
+        // holds X_pp[fr][2 fk], [2 fk + 1] (the DMMA C-fragment layout) in (v0, v1) and the
+        // negated multipliers of its two columns in (l0, l1).
+        double v0 = 0.0, v1 = 0.0, l0 = 0.0, l1 = 0.0;
+        bool beat = false;
+        // one Gauss-Jordan step on the 8 x 8 pivot tile of panel p (shuffles only)
+        auto gj_step = [&](auto pv, auto kv) {
+            constexpr int p = decltype(pv)::value;
+            constexpr int k = decltype(kv)::value;
+            constexpr int kh = k >> 1;
+            constexpr bool odd = (k & 1) != 0;
+            const double selv = odd ? v1 : v0;
+            const double piv = __shfl_sync(0xffffffffu, selv, 4 * k + kh);        // X[k][k]
+            const double f = __shfl_sync(0xffffffffu, selv, (lane & ~3) | kh);    // X[fr][k]
+            const double rk0 = __shfl_sync(0xffffffffu, v0, 4 * k + fk);          // X[k][2 fk]
+            const double rk1 = __shfl_sync(0xffffffffu, v1, 4 * k + fk);          // X[k][2 fk + 1]
+            const double ap = fabs(piv);
+            // partial-pivoting equivalence inside the tile: no row r > k of column k beats the
+            // diagonal; pivots outside [1e-30, 1e30] (0, inf, NaN included) go to the pivoted kernels
+            beat |= ((fr > k) && (fabs(f) > ap)) || !(ap >= 1e-30 && ap <= 1e30);
+            if (8 * p + k < nb && lane == ((8 * p + k) & 31)) apiv[(8 * p + k) >> 5] = ap;
+            const double inv = rcp_nr(piv);
+            const bool isc = fk == kh, isr = fr == k;
+            // scaled pivot row in this lane's columns; column k of the new row k is 1 / piv
+            double s0 = rk0 * inv, s1 = rk1 * inv;
+            double t0 = v0, t1 = v1;
+            if (odd) {
+                s1 = isc ? inv : s1;
+                t1 = isc ? 0.0 : t1;
+            } else {
+                s0 = isc ? inv : s0;
+                t0 = isc ? 0.0 : t0;
+            }
+            // other rows: a_rc - a_rk rk_c, column k: -a_rk / piv
+            const double n0 = fma(-f, s0, t0), n1 = fma(-f, s1, t1);
+            v0 = isr ? s0 : n0;
+            v1 = isr ? s1 : n1;
+            // column k now holds -l_rk for the rows below k (masked to the unit lower triangle later)
+            if (odd) l1 = isc ? v1 : l1;
+            else l0 = isc ? v0 : l0;
+        };
+        // P = inv(X_pp) -> X_pp, -L_pp (unit lower triangular factor of the unpivoted LU) -> scratch
+        auto gj_store = [&](auto pv) {
+            constexpr int k0 = 8 * decltype(pv)::value;
+            *reinterpret_cast<double2*>(X + sw(k0 + fr, k0 + 2 * fk)) = make_double2(v0, v1);
+            const int c0 = 2 * fk;
+            *reinterpret_cast<double2*>(rowbuf + fr * 8 + c0) =
+                make_double2(fr > c0 ? l0 : (fr == c0 ? -1.0 : 0.0), fr > c0 + 1 ? l1 : (fr == c0 + 1 ? -1.0 : 0.0));
+        };
+        if constexpr (BG) {
+            // pivot tile of panel 0 (the later ones are eliminated during the previous panel's update)
+            const double2 v = *reinterpret_cast<const double2*>(X + sw(fr, 2 * fk));
+            v0 = v.x;
+            v1 = v.y;
+            static_for([&](auto kc_) { gj_step(std::integral_constant<int, 0>{}, kc_); }, std::make_integer_sequence<int, 8>{});
+            gj_store(std::integral_constant<int, 0>{});
+            if (__any_sync(0xffffffffu, beat)) swap = true;
+            __syncwarp();
+        }
         auto panel_bg = [&](auto pv) {
             constexpr int p = decltype(pv)::value;
             constexpr int k0 = 8 * p;
+            constexpr bool LA = p + 1 < NT;          // look ahead: eliminate pivot tile p + 1 during this update
             if (swap) return;
-            double* Ls = rowbuf;                     // 8 x 8 unit-lower factor of the pivot tile
-            // old row panel p as B fragments (read before row tile p is overwritten)
-            double bf[NT][2];
+            const double* Ls = rowbuf;
+            // old row panel p as B fragments (read before row tile p is overwritten), old column
+            // panel as A fragments, P and -L_pp as B fragments
+            double bf[NT][2], af[NT][2];
 #pragma unroll
             for (int jt = 0; jt < NT; ++jt)
 #pragma unroll
                 for (int kc = 0; kc < 2; ++kc)
                     bf[jt][kc] = (jt == p) ? 0.0 : X[sw(k0 + 4 * kc + fk, 8 * jt + fr)];
-            // pivot tile in the C-fragment layout: lane (fr, fk) holds X_pp[fr][2 fk], [2 fk + 1]
-            double v0, v1, l0 = 0.0, l1 = 0.0;
-            {
-                const double2 v = *reinterpret_cast<const double2*>(X + sw(k0 + fr, k0 + 2 * fk));
-                v0 = v.x;
-                v1 = v.y;
-            }
-            bool beat = false, okp = true;
-            static_for([&](auto kc_) {
-                constexpr int k = decltype(kc_)::value;
-                constexpr int kh = k >> 1;
-                constexpr bool odd = (k & 1) != 0;
-                const double selv = odd ? v1 : v0;
-                const double piv = __shfl_sync(0xffffffffu, selv, 4 * k + kh);        // X[k][k]
-                const double f = __shfl_sync(0xffffffffu, selv, (lane & ~3) | kh);    // X[fr][k]
-                const double rk0 = __shfl_sync(0xffffffffu, v0, 4 * k + fk);          // X[k][2 fk]
-                const double rk1 = __shfl_sync(0xffffffffu, v1, 4 * k + fk);          // X[k][2 fk + 1]
-                const double ap = fabs(piv);
-                // partial-pivoting equivalence inside the tile: no row r > k of column k beats the diagonal
-                beat |= (fr > k) && (fabs(f) > ap);
-                okp = okp && piv != 0.0 && isfinite(piv);
-                if (k0 + k < nb && lane == ((k0 + k) & 31)) apiv[(k0 + k) >> 5] = ap;
-                const double inv = 1.0 / piv;
-                const bool isc = fk == kh, isr = fr == k;
-                // scaled pivot row in this lane's columns; column k of the new row k is 1 / piv
-                double s0 = rk0 * inv, s1 = rk1 * inv;
-                double t0 = v0, t1 = v1;
-                if (odd) {
-                    s1 = isc ? inv : s1;
-                    t1 = isc ? 0.0 : t1;
-                } else {
-                    s0 = isc ? inv : s0;
-                    t0 = isc ? 0.0 : t0;
-                }
-                // other rows: a_rc - a_rk rk_c, column k: -a_rk / piv
-                const double n0 = fma(-f, s0, t0), n1 = fma(-f, s1, t1);
-                v0 = isr ? s0 : n0;
-                v1 = isr ? s1 : n1;
-                // multiplier l_rk of the unpivoted LU (unit lower L_pp), kept by the lane owning column k
-                const double lv = (fr > k) ? f * inv : (isr ? 1.0 : 0.0);
-                if (odd) l1 = isc ? lv : l1;
-                else l0 = isc ? lv : l0;
-            }, std::make_integer_sequence<int, 8>{});
-            if (__any_sync(0xffffffffu, beat) || !okp) {
-                swap = true;
-                return;
-            }
-            // P = inv(X_pp) -> X_pp, L_pp -> scratch; the old column panel as A fragments
-            *reinterpret_cast<double2*>(X + sw(k0 + fr, k0 + 2 * fk)) = make_double2(v0, v1);
-            *reinterpret_cast<double2*>(Ls + fr * 8 + 2 * fk) = make_double2(l0, l1);
-            double af[NT][2];
 #pragma unroll
             for (int it = 0; it < NT; ++it) {
                 af[it][0] = (it == p) ? 0.0 : X[sw(8 * it + fr, k0 + fk)];
                 af[it][1] = (it == p) ? 0.0 : X[sw(8 * it + fr, k0 + 4 + fk)];
             }
-            __syncwarp();
             const double pb0 = -X[sw(k0 + fk, k0 + fr)], pb1 = -X[sw(k0 + 4 + fk, k0 + fr)];
             const double lb0 = Ls[fk * 8 + fr], lb1 = Ls[(4 + fk) * 8 + fr];
+            __syncwarp();
             // F_i = -X_ip P (the in-place Gauss-Jordan values of the panel columns)
 #pragma unroll
             for (int it = 0; it < NT; ++it) {
                 if (it == p) continue;
                 double2 c = make_double2(0.0, 0.0);
-                dmma_f64(c.x, c.y, af[it][0], pb0);
-                dmma_f64(c.x, c.y, af[it][1], pb1);
+                dmma_nv(c.x, c.y, af[it][0], pb0);
+                dmma_nv(c.x, c.y, af[it][1], pb1);
                 *reinterpret_cast<double2*>(X + sw(8 * it + fr, k0 + 2 * fk)) = c;
             }
             __syncwarp();
-            // rank-8 update A_R <- [0; A_R'] + [P; F] A_KR, and for the row tiles below the pivot
-            // tile the multipliers X_ip inv(U_pp) = -F_i L_pp: getrf would not swap iff all |.| <= 1
-            // (ties and rounding-level excesses keep the diagonal, which is an equally valid choice)
-            bool beat2 = false;
+            // [P; F] as A fragments
 #pragma unroll
             for (int it = 0; it < NT; ++it) {
-                const double a0 = X[sw(8 * it + fr, k0 + fk)];
-                const double a1 = X[sw(8 * it + fr, k0 + 4 + fk)];
-                if (it > p) {
-                    double2 w = make_double2(0.0, 0.0);
-                    dmma_f64(w.x, w.y, a0, lb0);
-                    dmma_f64(w.x, w.y, a1, lb1);
-                    beat2 |= (fabs(w.x) > 1.0 + 1e-12) || (fabs(w.y) > 1.0 + 1e-12);
-                }
+                af[it][0] = X[sw(8 * it + fr, k0 + fk)];
+                af[it][1] = X[sw(8 * it + fr, k0 + 4 + fk)];
+            }
+            // multipliers of the row tiles below the pivot tile, X_ip inv(U_pp) = F_i (-L_pp): getrf
+            // would not swap iff all |.| <= 1 (ties and rounding-level excesses keep the diagonal,
+            // an equally valid partial-pivoting choice)
 #pragma unroll
-                for (int jt = 0; jt < NT; ++jt) {
-                    if (jt == p) continue;
+            for (int it = p + 1; it < NT; ++it) {
+                double2 w = make_double2(0.0, 0.0);
+                dmma_nv(w.x, w.y, af[it][0], lb0);
+                dmma_nv(w.x, w.y, af[it][1], lb1);
+                beat |= (fabs(w.x) > 1.0 + 1e-12) || (fabs(w.y) > 1.0 + 1e-12);
+            }
+            // rank-8 update A_R <- [0; A_R'] + [P; F] A_KR.  The next pivot tile goes first and stays
+            // in registers; its 8 scalar elimination steps are spread over the other tile updates
+            if constexpr (LA) {
+                const double2 c = *reinterpret_cast<const double2*>(X + sw(k0 + 8 + fr, k0 + 8 + 2 * fk));
+                v0 = c.x;
+                v1 = c.y;
+                dmma_nv(v0, v1, af[p + 1][0], bf[p + 1][0]);
+                dmma_nv(v0, v1, af[p + 1][1], bf[p + 1][1]);
+                l0 = l1 = 0.0;
+            }
+            constexpr int NTL = NT * (NT - 1);
+            static_for([&](auto n_) {
+                constexpr int n = decltype(n_)::value;
+                constexpr int it = n / (NT - 1), jq = n % (NT - 1), jt = jq < p ? jq : jq + 1;
+                if constexpr (LA) {
+                    // step k goes before tile floor(k NTL / 8)
+                    static_for([&](auto kc_) {
+                        constexpr int k = decltype(kc_)::value;
+                        if constexpr ((k * NTL) / 8 == n) gj_step(std::integral_constant<int, p + 1>{}, kc_);
+                    }, std::make_integer_sequence<int, 8>{});
+                }
+                if constexpr (!(LA && it == p + 1 && jt == p + 1)) {
                     double* cp = X + sw(8 * it + fr, 8 * jt + 2 * fk);
                     double2 c = (it == p) ? make_double2(0.0, 0.0) : *reinterpret_cast<const double2*>(cp);
-                    dmma_f64(c.x, c.y, a0, bf[jt][0]);
-                    dmma_f64(c.x, c.y, a1, bf[jt][1]);
+                    dmma_nv(c.x, c.y, af[it][0], bf[jt][0]);
+                    dmma_nv(c.x, c.y, af[it][1], bf[jt][1]);
                     *reinterpret_cast<double2*>(cp) = c;
                 }
-            }
-            if (__any_sync(0xffffffffu, beat2)) swap = true;
+            }, std::make_integer_sequence<int, NTL>{});
+            if constexpr (LA) gj_store(std::integral_constant<int, p + 1>{});
+            if (__any_sync(0xffffffffu, beat)) swap = true;
             __syncwarp();
         };
         if constexpr (BG) {
@@ -1503,7 +1551,11 @@ static int launch_tc_r(const irk_ctx* ctx, const InvArgs& A, int* fb_list, int* 
 template <int NT, bool EXACT, bool FORM>
 static int launch_tc_t(const irk_ctx* ctx, const InvArgs& A, int* fb_list, int* fb_count, cudaStream_t st) {
     // A/B switch: the scalar-panel variant is instantiated for the config-1 tile count only
-    // (nb 33..40) to bound build time
+    // (nb 33..40) to bound build time.  (Two further variants were measured at config 1 and
+    // dropped: two blocks per warp with the two pivot tiles eliminated side by side -- fewer
+    // instructions but half the warps, 0.71-0.78 ms per level; the block held in registers in
+    // the C-fragment layout -- half the shared-memory wavefronts but 12 warps per SM, 0.55-0.63
+    // ms.  This kernel: 0.57-0.58 ms, the scalar-panel variant 0.69-0.70 ms.)
     static const bool scalar_panel = getenv("IRK_INV_BG") && atoi(getenv("IRK_INV_BG")) == 0;
     if constexpr (NT == 5)
         if (scalar_panel) return launch_tc_r<NT, EXACT, FORM, false>(ctx, A, fb_list, fb_count, st);

@@ -3,7 +3,7 @@
 O=gpurun_out; mkdir -p $O
 python -c "import __graft_entry__ as g; g.build()" || exit 1
 timeout 900 python -m pytest tests/test_gpu_parity.py -m gpu -x -q -k "inverse or factor or ilu0 or singular or golden" 2>&1 | tail -4
-for bg in 1 0; do
+for bg in ${BGS:-2 1}; do
   echo "== IRK_INV_BG=$bg"; IRK_INV_BG=$bg python tools/time_factor.py 1 color
   IRK_INV_BG=$bg timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:"k_inverse|k_schur" --csv --log-file $O/ab_inv_bg$bg.csv python tools/time_factor.py 1 color > /dev/null 2>&1
   python - <<PY
