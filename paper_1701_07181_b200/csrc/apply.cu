@@ -2022,9 +2022,12 @@ static int run_sweep(const irk_factor* f, K kernel, ApplyArgs& A, const irk_sche
 }
 
 // groups of the shuffle-reduction sweep layout (k_unc_bwd_pipe): a power of two
-static int ws_groups(int nb) {
+static int ws_groups(int nb, int s = 1) {
     static const int force = getenv("IRK_APPLY_WSG") ? atoi(getenv("IRK_APPLY_WSG")) : 0;   // tuning knob
     if (force == 1 || force == 2 || force == 4) return force;
+    // small blocks carrying >= 3 vectors: the single consumer warp is the bottleneck (config 3,
+    // nb = 24: 0.204 -> 0.173 ms at s = 4, 0.162 -> 0.150 ms at s = 3 with two groups)
+    if (nb <= 32 && s >= 3) return 2;
     // one thread per block row: small CTAs, many tasks in flight per SM (measured best for
     // nb <= 64); two groups for the 100-row blocks of config 3
     return (nb > 64 && nb <= 128) ? 2 : 1;
@@ -2038,7 +2041,7 @@ static int unc_apply(const irk_factor* f, ApplyArgs& A0, cudaStream_t st) {
     ApplyArgs A = A0;
     // deep DAGs (persistent, flag-synchronised sweeps) prefer fewer, wider CTAs
     const bool deep = f->fwd.nlevels > LEVEL_LAUNCH_MAX || f->bwd.nlevels > LEVEL_LAUNCH_MAX;
-    A.G_ = deep ? (A.nb <= 64 ? 4 : (A.nb <= 128 ? 2 : 1)) : ws_groups(A.nb);
+    A.G_ = deep ? (A.nb <= 64 ? 4 : (A.nb <= 128 ? 2 : 1)) : ws_groups(A.nb, S);
     if (EVEN && S <= 4 && A.G_ * A.nb <= 256) {
         const int64_t nf = (int64_t)f->pat->T;
         static const bool seg_off = getenv("IRK_APPLY_SEG") && atoi(getenv("IRK_APPLY_SEG")) == 0;
@@ -2177,7 +2180,7 @@ template <int S>
 static int fused_apply_t(const irk_stage_op* op, const irk_factor* f, const double* v, double* x, cudaStream_t st) {
     ApplyArgs A{};
     fill_args(f, A);
-    A.G_ = ws_groups(A.nb);
+    A.G_ = ws_groups(A.nb, S);
     if (A.G_ > 2 || A.G_ * A.nb > 256) return 1;
     A.y = nullptr;
     A.x = x;

@@ -27,7 +27,8 @@ from .stage_system import StageOperator, as_device_mass, as_device_matrix
 
 __all__ = ["SingularPivotError", "partition_keep_mask", "build_stage_matrix", "StageMatrix",
            "BlockIlu0", "ilu0_factorize", "StageCoupledIlu0", "stage_coupled_factorize",
-           "StageUncoupledIlu0", "stage_uncoupled_factorize", "simplified_condition"]
+           "StageUncoupledIlu0", "stage_uncoupled_factorize", "simplified_condition",
+           "clear_factor_pool"]
 
 
 def partition_keep_mask(mat, partition_of) -> np.ndarray:
@@ -156,8 +157,52 @@ def build_stage_matrix(coef: float, mass, jac, dt: float) -> StageMatrix:
     return StageMatrix(coef, mass, jac, dt)
 
 
+# Structure pool.  The reference's steppers build a NEW preconditioner object in every Newton
+# iteration (stepper.py:86-104); creating an ``irk_factor`` allocates its device buffers and
+# builds the level schedules on the host (config 1: ~18 ms, more than the 10 ms stage-solve).
+# A factor object that is garbage-collected parks its native handle here, keyed by everything
+# ``irk_factor_refactor`` requires to stay the same (pattern, kind, stage count, block size, keep
+# mask, simplified / store_diag / literal, shared-J structure); the next ``*_factorize`` call with
+# the same key takes it and re-factorises in place -- same numerics (bitwise: in-place refactor ==
+# fresh factor, tested), no allocation.  At most ``_POOL_PER_KEY`` handles per key and
+# ``_POOL_KEYS`` keys are parked (a parked config-1 factor holds 2.5 GB); IRK_FACTOR_POOL=0
+# disables it, ``clear_factor_pool()`` frees the parked handles.
+import os as _os
+
+_POOL: dict = {}
+_POOL_PER_KEY, _POOL_KEYS = 1, 2
+_POOL_ON = _os.environ.get("IRK_FACTOR_POOL", "1") != "0"
+
+
+def clear_factor_pool() -> None:
+    """Destroy every parked factor handle (device memory is returned)."""
+    while _POOL:
+        _, items = _POOL.popitem()
+        for h, _keep in items:
+            if L._lib is not None:
+                L._lib.irk_factor_destroy(h)
+
+
+def _pool_key(kind, pattern, jblocks, mass, keep_u8, *flags):
+    shared = tuple(int(b.handle == jblocks[0].handle) for b in jblocks)
+    return (kind, int(pattern.handle), len(jblocks), int(jblocks[0].nb), shared, mass is None,
+            keep_u8.tobytes(), *flags)
+
+
+def _pool_take(key):
+    items = _POOL.get(key) if _POOL_ON else None
+    if not items:
+        return None
+    item = items.pop()
+    if not items:
+        del _POOL[key]
+    return item
+
+
 class _Factor:
     """Owns an ``irk_factor`` handle plus everything it references."""
+
+    _pool_key = None
 
     def __init__(self, handle, keepalive, s, n_elem, m, keep):
         self.handle = handle
@@ -170,7 +215,12 @@ class _Factor:
     def __del__(self):
         h = getattr(self, "handle", None)
         if h and L._lib is not None:
-            L._lib.irk_factor_destroy(h)
+            key = self._pool_key
+            if _POOL_ON and key is not None and (key in _POOL or len(_POOL) < _POOL_KEYS) \
+                    and len(_POOL.get(key, ())) < _POOL_PER_KEY:
+                _POOL.setdefault(key, []).append((h, self.keepalive))
+            else:
+                L._lib.irk_factor_destroy(h)
             self.handle = None
 
     def apply_device(self, y, x) -> None:
@@ -253,12 +303,20 @@ def _uncoupled(cls, pattern, jblocks, jfirst, mass, coefs, alpha, keep, simplifi
     jf = (ctypes.c_int64 * s)(*jfirst)
     coef = None if coefs is None else np.ascontiguousarray(coefs, dtype=np.float64)
     keep_u8 = np.ascontiguousarray(keep, dtype=np.uint8)
+    key = _pool_key(cls.__name__, pattern, jblocks, mass, keep_u8, bool(simplified), bool(store_diag))
+    parked = _pool_take(key)
+    if parked is not None:
+        # same structure as a collected factor: re-factorise its buffers in place
+        fac = cls(parked[0], parked[1], s, pattern.T, jblocks[0].nb, keep_u8.astype(bool))
+        fac._pool_key = key
+        return fac._refactor(jblocks, jfirst, mass, coef, alpha, staged)
     h, rc, fs, fe = _call_factor(L.lib().irk_factor_uncoupled, pattern.ctx, pattern.handle, s, jarr,
                                  jf, None if mass is None else mass.handle, L.ptr(coef),
                                  float(alpha), keep_u8.ctypes.data, int(simplified),
                                  int(store_diag))
     fac = cls(h, (pattern, jblocks, mass, coef, keep_u8, jarr, jf), s, pattern.T,
               jblocks[0].nb, keep_u8.astype(bool))
+    fac._pool_key = key
     if rc == L.IRK_ESINGULAR:
         del fac
         raise SingularPivotError(fe, stage=fs if staged else None)
@@ -448,11 +506,23 @@ def stage_coupled_factorize(op: StageOperator, counter: OpCounter | None = None,
     jarr = (ctypes.c_void_p * s)(*[b.handle for b in jb])
     jfa = (ctypes.c_int64 * s)(*jf)
     a_inv = np.ascontiguousarray(op.a_inv, dtype=np.float64)
+    key = _pool_key("StageCoupledIlu0", op.pattern, jb, op.mass.device, keep_u8, bool(literal_update),
+                    bool(store_diag))
+    parked = _pool_take(key)
+    if parked is not None:
+        fac = StageCoupledIlu0(parked[0], parked[1], s, T, op.jacobians[0].m, keep)
+        fac._pool_key = key
+        fac._refactor(jb, jf, op.mass.device, a_inv, -op.dt, True)
+        if counter is not None:
+            counter.block_factorizations += s * T
+            counter.block_multiplies += 2 * s * op.pattern.upper_count(keep) + (s * s - s) * T
+        return fac
     h, rc, fs, fe = _call_factor(L.lib().irk_factor_coupled, op.pattern.ctx, op.pattern.handle, s,
                                  jarr, jfa, op.mass.device.handle, a_inv.ctypes.data, -op.dt, None,
                                  keep_u8.ctypes.data, int(bool(literal_update)), int(store_diag))
     fac = StageCoupledIlu0(h, (op.pattern, jb, op.mass, a_inv, keep_u8, jarr, jfa), s, T,
                            op.jacobians[0].m, keep)
+    fac._pool_key = key
     if rc == L.IRK_ESINGULAR:
         del fac
         raise SingularPivotError(fe, stage=fs)

@@ -316,3 +316,55 @@ def test_reference_closure_wrappers_run_native(kind):
     fac._charge(one)
     one = one.snapshot()
     assert c1 == {k: c2[k] + 2 * one[k] for k in c2}, (c1, c2, one)
+
+
+@pytest.mark.parametrize("kind", ["uncoupled", "coupled", "dirk"])
+def test_factor_structure_pool_reuses_buffers(kind):
+    """A collected factor parks its native handle; the next *_factorize call with the same
+    structure re-factorises those buffers in place (the reference's steppers build a new
+    preconditioner per Newton iteration, stepper.py:86-104).  Same handle, bitwise the same
+    apply as the first (freshly allocated) factor; a different keep mask or shift count does
+    not match; clear_factor_pool() empties the pool."""
+    import gc
+    from paper_1701_07181_b200 import precond as P
+    from paper_1701_07181_b200.blocks import BlockDiagonalMatrix, BlockSparseMatrix, DevicePattern
+    from paper_1701_07181_b200.stage_system import StageOperator
+    from paper_1701_07181_b200.tableau import derive
+    cfg = W.CONFIGS[1].scaled(N=6, ordering="color")
+    wl = W.make_workload(cfg, norm_iters=10)
+    p = wl.pattern
+    jac = BlockSparseMatrix.from_host(DevicePattern(p.indptr, p.indices, p.diag_pos), wl.J)
+    mass = BlockDiagonalMatrix(wl.M)
+    tab = builtin_tableau("DIRK33" if kind == "dirk" else ("RADAU23" if kind == "coupled" else "RADAU35"))
+    if kind == "dirk":
+        mat = P.build_stage_matrix(1.0, mass, jac, wl.dt * tab.A[0, 0])
+        make = lambda **kw: P.ilu0_factorize(mat, **kw)  # noqa: E731
+        n = mat.n
+    else:
+        der = derive(tab)
+        op = StageOperator(der, wl.dt, mass, [jac] * tab.s)
+        n = op.total_dim
+        if kind == "coupled":
+            make = lambda **kw: P.stage_coupled_factorize(op, **kw)  # noqa: E731
+        else:
+            make = lambda **kw: P.stage_uncoupled_factorize(op, der.shifts, **kw)  # noqa: E731
+    gc.collect()              # factors left by earlier tests park first, then the pool is emptied
+    P.clear_factor_pool()
+    y = np.random.default_rng(11).standard_normal(n)
+    f1 = make()
+    h1 = f1.handle
+    x1 = f1.apply(y)
+    del f1
+    gc.collect()
+    assert sum(len(v) for v in P._POOL.values()) == 1
+    f2 = make()
+    assert f2.handle == h1 and not P._POOL
+    assert np.array_equal(f2.apply(y), x1)
+    part = (np.arange(p.T) >= p.T // 2).astype(np.int64)
+    f3 = make(partition_of=part)          # other keep mask: new structure
+    assert f3.handle != h1
+    del f2, f3
+    gc.collect()
+    assert len(P._POOL) == 2
+    P.clear_factor_pool()
+    assert not P._POOL
