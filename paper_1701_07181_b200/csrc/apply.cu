@@ -1937,7 +1937,10 @@ __global__ void k_copy_rows(const int32_t* __restrict__ rows, int64_t nrows, con
 // Few levels (mesh-colouring schedule): one launch per level, static task
 // slices, no flags.  Many levels (e.g. natural numbering): one persistent
 // launch with tickets and dependency flags.
-constexpr int64_t LEVEL_LAUNCH_MAX = 16;
+// schedules with at most this many levels run one launch per level (static task slices, no
+// synchronisation inside the kernel); deeper ones run the persistent flag-synchronised sweeps.
+// IRK_LEVEL_MAX overrides (A/B knob)
+static const int64_t LEVEL_LAUNCH_MAX = getenv("IRK_LEVEL_MAX") ? atoll(getenv("IRK_LEVEL_MAX")) : 16;
 
 template <typename K1, typename K2>
 static int run_pipe(const irk_factor* f, K1 kernel_deps, K2 kernel_level, ApplyArgs& A, const irk_sched& S,
