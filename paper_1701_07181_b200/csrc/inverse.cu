@@ -1116,11 +1116,19 @@ __global__ void __launch_bounds__(32 * InvTcCfg<NT>::WARPS, NT <= 5 ? 4 : 1)
     const int P = (nb + 1) >> 1;
     const int64_t bsz = (int64_t)nb * 2 * P;
     const int fr = lane >> 2, fk = lane & 3;        // fragment layout
-    // shared-memory position of element (r, c): 16-byte chunks XOR-swizzled by (r >> 1) & 3
-    // inside each group of 4 chunks, so the row-per-lane panel / block accesses (32 rows of
-    // one column pair) hit 8 distinct bank groups per phase instead of 2, and the 8x8 tile
-    // fragments stay conflict-free (rows 2m, 2m + 1 share a swizzle)
-    auto sw = [](int r, int c) -> int { return r * LD + ((((c >> 1) ^ ((r >> 1) & 3)) << 1) | (c & 1)); };
+    // shared-memory position of element (r, c): 16-byte chunks XOR-swizzled by x(r) inside each
+    // group of 4 chunks, so the row-per-lane panel / block accesses (32 rows of one column pair)
+    // hit 8 distinct bank groups per phase instead of 2 (rows 2m, 2m + 1 share a swizzle: the
+    // C-tile double2 accesses stay conflict-free)
+    // x(r) = bits (r>>1)&1 and (r>>2)&1 swapped: rows 0, 2, 4, 6 still get four distinct chunk
+    // permutations (row-per-lane / block load-store accesses), and rows r0 + 2, r0 + 3 of an aligned
+    // 4 x 4 fragment (A / B operands, 64-bit loads of a half-warp) land on the other chunk pair of
+    // the group -- with x = (r>>1)&3 they hit the same two chunks as rows r0, r0 + 1 (2-way conflicts
+    // on every fragment load: 296 of 1890 shared-memory wavefronts per nb = 40 block)
+    auto sw = [](int r, int c) -> int {
+        const int x = (((r >> 1) & 1) << 1) | ((r >> 2) & 1);
+        return r * LD + ((((c >> 1) ^ x) << 1) | (c & 1));
+    };
     for (int64_t t = (int64_t)blockIdx.x * C::WARPS + warp; t < A.ntasks; t += (int64_t)gridDim.x * C::WARPS) {
         const int64_t code = A.tasks[t];
         const int k_st = (int)(code / A.T);
