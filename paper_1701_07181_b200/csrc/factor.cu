@@ -678,6 +678,9 @@ __global__ void __launch_bounds__(4 * NB, MODE == 1 ? 1 : schur_min_ctas<S, NB>(
     // zero (slots zeroed once; bulk copies write only the nb x nb part), so the
     // padded DMMA tiles leave the nb x nb results exact
     const int nbv = F.nb, Pv = (nbv + 1) >> 1;
+    // k-steps of 4 that hold data (nb = 50 runs 13 of 14); used by the two-phase units only: a
+    // runtime bound in the NB = 40 barrier-free loops costs more than it saves (1.68 -> 1.88 ms)
+    const int KK = (nbv + 3) >> 2;
     const int64_t BSZ = (int64_t)nbv * 2 * Pv;      // device block (column-pair layout)
     constexpr int SJ = 0, SU = 1;   // slots: J_ji, J_ij, then Dinv_k / A'_k at 2 + k
     extern __shared__ __align__(128) double shs[];
@@ -880,7 +883,7 @@ __global__ void __launch_bounds__(4 * NB, MODE == 1 ? 1 : schur_min_ctas<S, NB>(
 #pragma unroll
                     for (int t = 0; t < NT; ++t) acc[k][t][0] = acc[k][t][1] = 0.0;
 #pragma unroll 2
-                for (int kk = 0; kk < NB / 4; ++kk) {
+                for (int kk = 0; kk < KK; ++kk) {
                     const double a = frag_a(shs + SJ * SLOT, kk);
 #pragma unroll
                     for (int k = 0; k < S; ++k)
@@ -911,7 +914,7 @@ __global__ void __launch_bounds__(4 * NB, MODE == 1 ? 1 : schur_min_ctas<S, NB>(
                 __syncwarp();
                 wait_slot(SU);
 #pragma unroll 2
-                for (int kk = 0; kk < NB / 4; ++kk) {
+                for (int kk = 0; kk < KK; ++kk) {
                     double a[S];
 #pragma unroll
                     for (int k = 0; k < S; ++k)

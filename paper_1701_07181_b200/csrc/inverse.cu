@@ -1191,21 +1191,50 @@ __global__ void __launch_bounds__(32 * InvTcCfg<NT>::WARPS, NT <= 5 ? 4 : 1)
                 }
             }
         } else {
-            for (int idx = lane; idx < NPAIR; idx += 32) {
-                const int p2 = idx / NBT, r = idx - p2 * NBT;
-                double2 v;
-                if (r < nb && p2 < P) {
-                    if constexpr (FORM) {
-                        v = form_pair(fsrc, p2 * nb + r);
-                        if (A.form.store) dst_d[p2 * nb + r] = v;
-                    } else {
-                        v = src[p2 * nb + r];
+            // nb < NBT (identity padding): global loads issued in batches ahead of the arithmetic
+            // and the shared-memory stores (one exposed DRAM latency per batch instead of one per
+            // element pair: config 2, nb = 50, level-0 inverse 1.89 -> see DESIGN)
+            constexpr int NE = (NPAIR + 31) / 32, BATCH = 7;
+#pragma unroll 1
+            for (int e0 = 0; e0 < NE; e0 += BATCH) {
+                double2 jv[BATCH], mv[BATCH];
+#pragma unroll
+                for (int b = 0; b < BATCH; ++b) {
+                    const int idx = lane + 32 * (e0 + b);
+                    const int p2 = idx / NBT, r = idx - p2 * NBT;
+                    jv[b] = mv[b] = make_double2(0.0, 0.0);
+                    if (idx < NPAIR && r < nb && p2 < P) {
+                        if constexpr (FORM) {
+                            jv[b] = __ldg(fsrc.J + p2 * nb + r);
+                            if (fsrc.M) mv[b] = __ldg(fsrc.M + p2 * nb + r);
+                        } else {
+                            jv[b] = __ldg(src + p2 * nb + r);
+                        }
                     }
-                    if (2 * p2 + 1 >= nb) v.y = 0.0;
-                } else {   // identity padding
-                    v = make_double2(2 * p2 == r ? 1.0 : 0.0, 2 * p2 + 1 == r ? 1.0 : 0.0);
                 }
-                *reinterpret_cast<double2*>(X + sw(r, 2 * p2)) = v;
+#pragma unroll
+                for (int b = 0; b < BATCH; ++b) {
+                    const int idx = lane + 32 * (e0 + b);
+                    if (idx >= NPAIR) continue;
+                    const int p2 = idx / NBT, r = idx - p2 * NBT;
+                    double2 v;
+                    if (r < nb && p2 < P) {
+                        v = jv[b];
+                        if constexpr (FORM) {
+                            double x0 = __dmul_rn(fsrc.alpha, jv[b].x), x1 = __dmul_rn(fsrc.alpha, jv[b].y);
+                            if (fsrc.M) {
+                                x0 = __dadd_rn(x0, __dmul_rn(fsrc.coef, mv[b].x));
+                                x1 = __dadd_rn(x1, __dmul_rn(fsrc.coef, mv[b].y));
+                            }
+                            v = fsrc.keep ? make_double2(x0, x1) : make_double2(0.0, 0.0);
+                            if (A.form.store) dst_d[p2 * nb + r] = v;
+                        }
+                        if (2 * p2 + 1 >= nb) v.y = 0.0;
+                    } else {   // identity padding
+                        v = make_double2(2 * p2 == r ? 1.0 : 0.0, 2 * p2 + 1 == r ? 1.0 : 0.0);
+                    }
+                    *reinterpret_cast<double2*>(X + sw(r, 2 * p2)) = v;
+                }
             }
         }
         __syncwarp();
