@@ -661,17 +661,21 @@ __device__ __forceinline__ void fence_proxy_async_smem() {
 // MODE 2: no CTA barrier -- A'_k goes from the C fragments to the A fragments by shuffles (the
 // staged blocks are read-only), every warp counts itself out of a slot when it has read it for
 // the last time and the last warp out refills the slot with the next unit's block
+// MODE 3 (S >= 2): MODE 2 with two Dinv slots used alternately (4 slots instead of S + 2): at
+// NB = 56 (config 2, nb = 50) two CTAs fit on an SM instead of one.  (The register cap comes from
+// __launch_bounds__' min-CTA argument; __maxnreg__(144) for the 224-thread CTAs was tried and
+// drops a CTA per SM: registers are allocated per warp in larger units.)
 // CTAs per SM that shared memory allows, capped so that a thread keeps >= 128 registers
-template <int S, int NB>
+template <int S, int NB, int NSL = S + 2>
 constexpr int schur_min_ctas() {
-    const int by_smem = 232448 / ((S + 2) * SchurGeo<NB>::SLOT * 8 + 1280);
+    const int by_smem = 232448 / (NSL * SchurGeo<NB>::SLOT * 8 + 1280);
     const int by_regs = 65536 / (4 * NB * 128);
     const int m = by_smem < by_regs ? by_smem : by_regs;
     return m < 1 ? 1 : m;
 }
 
 template <int S, int NB, int MODE = 0>
-__global__ void __launch_bounds__(4 * NB, MODE == 1 ? 1 : schur_min_ctas<S, NB>()) k_schur(FactorArgs F, const int32_t* __restrict__ elems, int64_t nelem) {
+__global__ void __launch_bounds__(4 * NB, MODE == 1 ? 1 : schur_min_ctas<S, NB, (MODE == 3 ? 4 : S + 2)>()) k_schur(FactorArgs F, const int32_t* __restrict__ elems, int64_t nelem) {
     using Gm = SchurGeo<NB>;
     constexpr int NT = Gm::NT, LDP = Gm::LDP, SLOT = Gm::SLOT;
     // NB = nb rounded up to 8: the padding rows / columns of the staged blocks are
@@ -690,9 +694,11 @@ __global__ void __launch_bounds__(4 * NB, MODE == 1 ? 1 : schur_min_ctas<S, NB>(
     const int fr = lane >> 2, fk = lane & 3;
     const int r0 = warp * 8;
     const double* J = F.J[0];
+    constexpr int NSL = MODE == 3 ? 4 : S + 2;      // staged-block slots
+    static_assert(MODE != 3 || S >= 2, "MODE 3 needs at least two stages");
     if (threadIdx.x < S + 2) outcnt[threadIdx.x] = 0;
     if (nbv != NB)
-        for (int e = threadIdx.x; e < (S + 2) * SLOT; e += blockDim.x) shs[e] = 0.0;
+        for (int e = threadIdx.x; e < NSL * SLOT; e += blockDim.x) shs[e] = 0.0;
     if (threadIdx.x == 0) {
         for (int b = 0; b < S + 2; ++b) mbar_init(&bars[b], 1);
         fence_mbar_init();
@@ -738,8 +744,9 @@ __global__ void __launch_bounds__(4 * NB, MODE == 1 ? 1 : schur_min_ctas<S, NB>(
         fill(SJ, J + (int64_t)nxt.q * BSZ);
         fill(SU, J + (int64_t)nxt.tq * BSZ);
 #pragma unroll
-        for (int k = 0; k < S; ++k) fill(2 + k, src_dinv(nxt, k));
+        for (int k = 0; k < (MODE == 3 ? 2 : S); ++k) fill(2 + k, src_dinv(nxt, k));
     }
+    int dm = 0;   // MODE 3: Dinv blocks consumed so far (block m sits in slot 2 + (m & 1))
     auto frag_a = [&](const double* slotp, int kk) -> double {   // A(r0 + fr, 4kk + fk)
         return slotp[((4 * kk + fk) >> 1) * LDP + 2 * (r0 + fr) + (fk & 1)];
     };
@@ -799,7 +806,7 @@ __global__ void __launch_bounds__(4 * NB, MODE == 1 ? 1 : schur_min_ctas<S, NB>(
             const Unit cur = nxt;
             nxt = find_unit(it, q + 1);
             const bool more = nxt.it >= 0;
-            if constexpr (MODE == 2) {
+            if constexpr (MODE == 2 || MODE == 3) {
                 // this warp is done with slot b: the last warp out refills it (src != NULL).
                 // (Measured and dropped: rotating the slot roles so that each freed slot takes the
                 // block the next unit needs first -- the mbarrier waits are gated by the slowest
@@ -829,18 +836,24 @@ __global__ void __launch_bounds__(4 * NB, MODE == 1 ? 1 : schur_min_ctas<S, NB>(
                 wait_slot(SJ);
 #pragma unroll
                 for (int k = 0; k < S; ++k) {
-                    wait_slot(2 + k);
+                    const int dslot = MODE == 3 ? 2 + ((dm + k) & 1) : 2 + k;
+                    wait_slot(dslot);
                     double acc[NT][2];
 #pragma unroll
                     for (int t = 0; t < NT; ++t) acc[t][0] = acc[t][1] = 0.0;
-                    const double* Dk = shs + (size_t)(2 + k) * SLOT;
+                    const double* Dk = shs + (size_t)dslot * SLOT;
 #pragma unroll 2
                     for (int kk = 0; kk < NB / 4; ++kk) {
                         const double a = frag_a(shs + SJ * SLOT, kk);
 #pragma unroll
                         for (int t = 0; t < NT; ++t) dmma(acc[t][0], acc[t][1], a, frag_b(Dk, kk, t));
                     }
-                    release(2 + k, more ? src_dinv(nxt, k) : nullptr);
+                    if constexpr (MODE == 3) {
+                        // the slot takes the Dinv block two ahead: this unit's D_{k+2}, else the next unit's
+                        release(dslot, k + 2 < S ? src_dinv(cur, k + 2) : (more ? src_dinv(nxt, k + 2 - S) : nullptr));
+                    } else {
+                        release(2 + k, more ? src_dinv(nxt, k) : nullptr);
+                    }
                     if (k == S - 1) release(SJ, more ? J + (int64_t)nxt.q * BSZ : nullptr);
                     // L_k = alpha T_k -> global (numba_backend.py:58-61) unless L is implicit;
                     // A'_k = -alpha L_k stays in the C fragments
@@ -870,6 +883,7 @@ __global__ void __launch_bounds__(4 * NB, MODE == 1 ? 1 : schur_min_ctas<S, NB>(
                         }
                     if (k == S - 1) release(SU, more ? J + (int64_t)nxt.tq * BSZ : nullptr);
                 }
+                dm += S;
                 (void)cur;
                 continue;
             }
@@ -1003,7 +1017,7 @@ __global__ void __launch_bounds__(4 * NB, MODE == 1 ? 1 : schur_min_ctas<S, NB>(
 template <int S, int NB, int MODE>
 static int launch_schur_tt(const irk_ctx* ctx, const FactorArgs& F, const int32_t* elems, int64_t nelem,
                            cudaStream_t st, int cap_per_sm) {
-    const size_t smem = sizeof(double) * (size_t)(S + 2) * SchurGeo<NB>::SLOT;
+    const size_t smem = sizeof(double) * (size_t)(MODE == 3 ? 4 : S + 2) * SchurGeo<NB>::SLOT;
     static bool attr = false;
     if (!attr) {
         IRK_CK(cudaFuncSetAttribute(k_schur<S, NB, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
@@ -1024,11 +1038,14 @@ static int launch_schur_t(const irk_ctx* ctx, const FactorArgs& F, const int32_t
                           cudaStream_t st, int cap_per_sm) {
     // IRK_SCHUR_MODE (A/B knob): 0 per-stage software pipeline, S + 1 CTA barriers per unit;
     // 1 two-phase units (GEMM1 of all stages, GEMM2 of all stages: 2 barriers, more registers);
-    // 2 barrier-free (A' by shuffles, last warp out of a slot refills it)
+    // 2 barrier-free (A' by shuffles, last warp out of a slot refills it); 3 = 2 with two Dinv
+    // slots (NB = 56, S >= 2 only)
     static const int env = getenv("IRK_SCHUR_MODE") ? atoi(getenv("IRK_SCHUR_MODE")) : -1;
     // measured: config 1 (NB 40, 3 CTAs/SM) 1.72 / - / 1.68 ms for modes 0 / 1 / 2; config 2 at N = 16
-    // (NB 56, one CTA per SM) 5.04 ms for mode 1 vs 5.14 ms for mode 2
-    const int mode = env >= 0 ? env : (NB >= 56 ? 1 : 2);
+    // (NB 56): 4.86 ms for mode 1 and 5.14 ms for mode 2 (one CTA per SM), 4.46 ms for mode 3 (two)
+    const int mode = env >= 0 ? env : (NB == 56 && S >= 2 ? 3 : (NB >= 56 ? 1 : 2));
+    if constexpr (NB == 56 && S >= 2)
+        if (mode == 3) return launch_schur_tt<S, NB, 3>(ctx, F, elems, nelem, st, cap_per_sm);
     if (mode == 1) return launch_schur_tt<S, NB, 1>(ctx, F, elems, nelem, st, cap_per_sm);
     if (mode == 0) return launch_schur_tt<S, NB, 0>(ctx, F, elems, nelem, st, cap_per_sm);
     return launch_schur_tt<S, NB, 2>(ctx, F, elems, nelem, st, cap_per_sm);
