@@ -1295,7 +1295,12 @@ static int run_fused_fwd(const irk_factor* f, ApplyArgs& A, const FusedMv& F, cu
         A.ntasks = hi - lo;
         const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(A.ntasks, (int64_t)f->ctx->num_sms * std::max(per_sm, 1)));
         static const bool pdl = !(getenv("IRK_PDL_FUSED") && atoi(getenv("IRK_PDL_FUSED")) == 0);   // A/B switch
-        IRK_CK(launch_pdl_if(pdl, k_unc_fused_fwd<S>, dim3(grid), dim3(threads), smem, st, A, SC, F));
+        // the product's first launch is a plain one: with the PDL attribute its CTAs start during
+        // the predecessor's drain and, when that predecessor is the previous product's backward
+        // sweep (products issued back to back), park on the SMs holding shared memory
+        static const bool pdl_first = getenv("IRK_PDL_FIRST") && atoi(getenv("IRK_PDL_FIRST")) != 0;
+        const bool first = l == 0 || Sd.h_lvl_ptr[l] == 0;
+        IRK_CK(launch_pdl_if(pdl && (!first || pdl_first), k_unc_fused_fwd<S>, dim3(grid), dim3(threads), smem, st, A, SC, F));
         IRK_LAUNCHED();
     }
     return IRK_OK;
