@@ -531,16 +531,20 @@ def run_b200(args):
         dom = {"name": "stage_matvec (fused)", "bytes": bm, "t": t_mv, "share": share_mv, "key": "stage_matvec"}
     achieved = dom["bytes"] / dom["t"] / 1e9
     traffic = None
-    try:   # DRAM bytes per launch from the committed ncu --set full capture (profiles/)
-        with open(os.path.join(REPO, "profiles", "r1_traffic.json")) as fh:
+    traffic_src = None
+    try:   # DRAM bytes per launch from the latest committed ncu capture (profiles/rNN_traffic.json)
+        import glob
+        cands = sorted(glob.glob(os.path.join(REPO, "profiles", "r*_traffic.json")))
+        with open(cands[-1]) as fh:
             tj = json.load(fh)
         traffic = tj[dom["key"]]
+        traffic_src = "profiles/" + os.path.basename(cands[-1])
     except Exception:
         pass
     roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                 "frac": achieved / peak, "traffic": traffic, "kernel": dom["name"],
                 "algorithmic_bytes_per_launch": dom["bytes"], "avg_launch_ms": 1e3 * dom["t"],
-                "share_of_step": dom["share"], "peak_source": peak_src,
+                "share_of_step": dom["share"], "peak_source": peak_src, "traffic_source": traffic_src,
                 # DRAM bytes (ncu, profiles/) over the event-timed launch: wasted re-reads show here
                 "traffic_GBps": (traffic / dom["t"] / 1e9) if traffic else None}
     components = {
