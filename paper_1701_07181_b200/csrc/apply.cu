@@ -873,6 +873,183 @@ __global__ void __launch_bounds__(288) k_unc_bwd_pipe(ApplyArgs A, PipeCfg PC) {
 }
 
 // ---------------------------------------------------------------------------
+// Deep schedules (natural numbering: hundreds of dependency levels, ~T / levels tasks
+// each): the sweep time is the level-to-level hand-over latency, not bandwidth.
+// k_unc_bwd_pipe hands a task through a chain of hops -- producer polls the flags,
+// bulk-copies the neighbours' segments into an x slot, the consumers take the ring
+// items one by one with an mbarrier handshake each.  k_unc_deep is the short chain for
+// the implicit-L, stage-shared-J case: a producer warp runs up to two tasks ahead
+// (ticket, metadata, ALL blocks of the task in one shared-memory buffer, one mbarrier);
+// thread (stage k, row a) of the consumers polls the flags itself, loads the neighbour
+// segments straight from L2 (ld.cg: lines are shared with segments still being
+// written), and does its row of both gemv phases from shared memory:
+//   t = own - uscale sum_j B_ij v_j   (v = w_j forward / x_j backward),  out = Dinv_k t.
+// Three CTA-wide barriers per task.  Deadlock-free: a CTA processes its tickets in
+// order, so the smallest unfinished ticket is always some CTA's current task.
+// ---------------------------------------------------------------------------
+struct DeepCfg {
+    int block_bytes;
+    int buf_bytes;     // (maxdeg + S) blocks
+    int maxdeg;
+};
+
+struct DeepDesc {
+    int i, nn, store_z;
+    unsigned km;
+    int col[MAXD];
+};
+
+template <int S, bool FWDI>
+__global__ void __launch_bounds__(512) k_unc_deep(ApplyArgs A, DeepCfg DC) {
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    const int nb = A.nb, P = nb >> 1;
+    unsigned char* bufs = smem_raw;
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem_raw + 2 * (size_t)DC.buf_bytes);
+    uint64_t* empty = full + 2;
+    DeepDesc* desc = reinterpret_cast<DeepDesc*>(empty + 2);          // 2 x 48 B
+    double* xs = reinterpret_cast<double*>(smem_raw + 2 * (size_t)DC.buf_bytes + 128);   // [maxdeg][S][nb]
+    double* ts = xs + (size_t)DC.maxdeg * S * nb;                                         // [S][nb]
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int ncons = (int)blockDim.x - 32;
+    if (threadIdx.x == 0) {
+        for (int b = 0; b < 2; ++b) {
+            mbar_init(full + b, 1);
+            mbar_init(empty + b, 1);
+        }
+        fence_mbar_init();
+    }
+    __syncthreads();
+    griddep_launch();
+    const int64_t bsz = (int64_t)DC.block_bytes / 8;
+    if (warp == 0) {
+        griddep_wait();
+        int b = 0;
+        uint32_t ph = 0;
+        for (;;) {
+            int t = 0;
+            if (lane == 0) t = atomicAdd(A.ticket, 1);
+            t = __shfl_sync(0xffffffffu, t, 0);
+            const bool end = t >= A.ntasks;
+            int i = -1, b0 = 0, nn = 0, sz = 0;
+            if (!end) {
+                i = A.order[t];
+                const int d = A.diag[i];
+                b0 = FWDI ? A.indptr[i] : d + 1;
+                nn = (FWDI ? d : A.indptr[i + 1]) - b0;
+                sz = (FWDI && A.hasup[i]) ? 1 : 0;
+            }
+            int colm = 0, kp = 0;
+            if (lane < nn && lane < MAXD) {
+                colm = A.indices[b0 + lane];
+                kp = A.keep[b0 + lane] ? 1 : 0;
+            }
+            const unsigned km = __ballot_sync(0xffffffffu, kp != 0);
+            if (lane == 0) mbar_wait(empty + b, ph ^ 1);
+            __syncwarp();
+            if (lane == 0) {
+                desc[b].i = i;
+                desc[b].nn = nn;
+                desc[b].store_z = sz;
+                desc[b].km = km;
+            }
+            if (lane < MAXD) desc[b].col[lane] = colm;
+            __syncwarp();
+            if (lane == 0) {
+                if (end) {
+                    mbar_expect_tx(full + b, 0);
+                } else {
+                    const int nkept = __popc(km);
+                    mbar_expect_tx(full + b, (uint32_t)(nkept + S) * (uint32_t)DC.block_bytes);
+                    unsigned char* dst = bufs + (size_t)b * DC.buf_bytes;
+                    for (int m = 0; m < nn; ++m)
+                        if ((km >> m) & 1u) {
+                            bulk_g2s(dst, A.ubase[0] + (int64_t)(b0 + m) * bsz, DC.block_bytes, full + b);
+                            dst += DC.block_bytes;
+                        }
+                    for (int k = 0; k < S; ++k, dst += DC.block_bytes)
+                        bulk_g2s(dst, A.Dinv + ((int64_t)i * S + k) * bsz, DC.block_bytes, full + b);
+                }
+            }
+            if (end) break;
+            b ^= 1;
+            if (b == 0) ph ^= 1;
+        }
+        return;
+    }
+    const int c = threadIdx.x - 32;
+    const int k = c / nb, a = c - k * nb;
+    const bool act = k < S;
+    griddep_wait();
+    int b = 0;
+    uint32_t ph = 0;
+    for (;;) {
+        mbar_wait(full + b, ph);
+        const int64_t i = desc[b].i;
+        if (i < 0) break;
+        const int nn = desc[b].nn;
+        const unsigned km = desc[b].km;
+        const bool store_z = FWDI && desc[b].store_z != 0;
+        const int nkept = __popc(km);
+        // dependencies: consumer thread m polls neighbour m
+        if (c < nn && ((km >> c) & 1u)) wait_flag(A.flags + desc[b].col[c], A.epoch);
+        consumer_sync(1, ncons);
+        double own = 0.0;
+        if (act) {
+            const double* vsrc = (FWDI ? A.W : A.x) + (int64_t)k * A.n + a;
+            own = __ldcg((FWDI ? A.y : A.x) + (int64_t)k * A.n + i * nb + a);
+            int slot = 0;
+            for (int m = 0; m < nn; ++m)
+                if ((km >> m) & 1u) {
+                    xs[(slot * S + k) * nb + a] = __ldcg(vsrc + (int64_t)desc[b].col[m] * nb);
+                    ++slot;
+                }
+        }
+        consumer_sync(1, ncons);
+        const unsigned char* buf = bufs + (size_t)b * DC.buf_bytes;
+        if (act) {
+            double s0 = 0.0, s1 = 0.0;
+            for (int slot = 0; slot < nkept; ++slot) {
+                const double2* B = reinterpret_cast<const double2*>(buf + (size_t)slot * DC.block_bytes);
+                const double* xv = xs + (slot * S + k) * nb;
+#pragma unroll 4
+                for (int p = 0; p < P; ++p) {
+                    const double2 bb = B[p * nb + a];
+                    const double2 v = *reinterpret_cast<const double2*>(xv + 2 * p);
+                    s0 = fma(bb.x, v.x, s0);
+                    s1 = fma(bb.y, v.y, s1);
+                }
+            }
+            const double tval = nkept ? own - A.uscale * (s0 + s1) : own;
+            ts[k * nb + a] = tval;
+            if (store_z) A.x[(int64_t)k * A.n + i * nb + a] = tval;   // z_i for the backward sweep
+        }
+        consumer_sync(1, ncons);
+        if (act) {
+            const double2* D = reinterpret_cast<const double2*>(buf + (size_t)(nkept + k) * DC.block_bytes);
+            const double* tv = ts + k * nb;
+            double s0 = 0.0, s1 = 0.0;
+#pragma unroll 4
+            for (int p = 0; p < P; ++p) {
+                const double2 bb = D[p * nb + a];
+                const double2 v = *reinterpret_cast<const double2*>(tv + 2 * p);
+                s0 = fma(bb.x, v.x, s0);
+                s1 = fma(bb.y, v.y, s1);
+            }
+            (store_z ? A.W : A.x)[(int64_t)k * A.n + i * nb + a] = s0 + s1;
+        }
+        consumer_sync(1, ncons);   // outputs issued; buffer, xs and ts are free
+        if (c == 0) {
+            __threadfence();
+            st_release(A.flags + i, A.epoch);
+            if (FWDI && !store_z) st_release(A.flags2 + i, A.epoch);   // row finished here
+            mbar_arrive(empty + b);
+        }
+        b ^= 1;
+        if (b == 0) ph ^= 1;
+    }
+}
+
+// ---------------------------------------------------------------------------
 // Level-scheduled uncoupled sweep with the vector segments riding in the ring
 // stages (matvec-style): every stage holds one factor / Jacobian block plus the
 // x segments it multiplies (a neighbour's S stage segments, or the task's own S
@@ -2044,6 +2221,44 @@ static int ws_groups(int nb, int s = 1) {
 // tasks in flight, not by consumer width (tools/tune_apply.py: 0.57 ms at 6 vs 0.60 ms at 4)
 static int ws_ctas(int G) { return G == 1 ? 0 : 4; }   // 0: 2-stage rings, occupancy-limited
 
+// k_unc_deep applies: implicit-L factor on the stage-shared J, s factors for s vectors, even nb,
+// <= MAXD neighbours per row, two task buffers within the shared memory of an SM
+template <int S>
+static size_t deep_smem(const irk_factor* f, const ApplyArgs& A) {
+    const size_t blk = (size_t)block_doubles(A.nb) * 8;
+    return 2 * (size_t)(f->maxdeg + S) * blk + 128 + sizeof(double) * ((size_t)f->maxdeg + 1) * S * A.nb;
+}
+
+template <int S>
+static bool deep_ok(const irk_factor* f, const ApplyArgs& A) {
+    static const bool off = getenv("IRK_DEEP") && atoi(getenv("IRK_DEEP")) == 0;   // A/B switch
+    return !off && A.u_shared && !A.fac_shared && A.U == nullptr && A.nb % 2 == 0 && f->maxdeg <= MAXD &&
+           S * A.nb + 32 <= 512 && deep_smem<S>(f, A) <= (size_t)f->ctx->smem_optin;
+}
+
+template <int S, bool FWDI>
+static int run_deep(const irk_factor* f, ApplyArgs& A, const irk_sched& Sd, unsigned* flags, int* ticket,
+                    cudaStream_t st) {
+    A.flags = flags;
+    A.ticket = ticket;
+    A.order = Sd.d_order;
+    A.ntasks = Sd.h_lvl_ptr.empty() ? 0 : Sd.h_lvl_ptr.back();
+    if (A.ntasks == 0) return IRK_OK;
+    DeepCfg DC;
+    DC.block_bytes = (int)(block_doubles(A.nb) * 8);
+    DC.maxdeg = f->maxdeg;
+    DC.buf_bytes = (f->maxdeg + S) * DC.block_bytes;
+    const int threads = 32 + ((S * A.nb + 31) / 32) * 32;
+    const size_t smem = deep_smem<S>(f, A);
+    int per_sm = 1;
+    IRK_CK(sweep_occupancy((const void*)k_unc_deep<S, FWDI>, threads, smem, (int)f->ctx->smem_optin, &per_sm));
+    IRK_CK(cudaMemsetAsync(ticket, 0, sizeof(int), st));
+    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(A.ntasks, (int64_t)f->ctx->num_sms * std::max(per_sm, 1)));
+    IRK_CK(launch_pdl_if(true, k_unc_deep<S, FWDI>, dim3(grid), dim3(threads), smem, st, A, DC));
+    IRK_LAUNCHED();
+    return IRK_OK;
+}
+
 template <int S, bool EVEN>
 static int unc_apply(const irk_factor* f, ApplyArgs& A0, cudaStream_t st) {
     ApplyArgs A = A0;
@@ -2063,6 +2278,11 @@ static int unc_apply(const irk_factor* f, ApplyArgs& A0, cudaStream_t st) {
             // implicit L: forward sweep streams the stage-shared J_ij with w_j = Dinv_j z_j and
             // finishes rows without upper blocks; the backward sweep covers the remaining rows
             A.flags2 = f->d_flags + nf;
+            if (deep && deep_ok<S>(f, A)) {
+                IRK_TRY((run_deep<S, true>(f, A, f->fwd, f->d_flags, f->d_ticket, st)));
+                IRK_TRY((run_deep<S, false>(f, A, f->bwd, f->d_flags + nf, f->d_ticket + 1, st)));
+                return IRK_OK;
+            }
             IRK_TRY(run_pipe(f, k_unc_bwd_pipe<S, true, true>, k_unc_bwd_pipe<S, false, true>, A, f->fwd,
                              f->d_flags, f->d_ticket, S, st, 0, ws_ctas(A.G_)));
             IRK_TRY(run_pipe(f, k_unc_bwd_pipe<S, true, false>, k_unc_bwd_pipe<S, false, false>, A, f->bwd,
