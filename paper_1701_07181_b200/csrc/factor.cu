@@ -1226,6 +1226,17 @@ static int set_sources(irk_factor* f, const FactorSetup& P) {
     return IRK_OK;
 }
 
+struct FactorGraph {
+    cudaGraphExec_t exec = nullptr;
+    cudaStream_t cap = nullptr;     // capture stream (the caller's may be the legacy default stream)
+    FactorArgs key;                 // kernel arguments the graph was captured with
+    long long launches = 0;         // kernel launches per replay (irk_launch_count)
+    int calls = 0;
+};
+
+long long launch_count_now();          // common.cu
+void count_launches(long long n);
+
 static int factor_numeric(irk_factor* f, int64_t* fail_stage, int64_t* fail_elem, cudaStream_t st) {
     FactorArgs& F = *static_cast<FactorArgs*>(f->fargs);
     const irk_pattern* pat = f->pat;
@@ -1246,13 +1257,56 @@ static int factor_numeric(irk_factor* f, int64_t* fail_stage, int64_t* fail_elem
         IRK_LAUNCHED();
     }
     int rc = IRK_OK;
-    switch (f->maxt) {
-        case 2: rc = launch_levels<2>(f, F, f->fsched, f->fsmem, st); break;
-        case 4: rc = launch_levels<4>(f, F, f->fsched, f->fsmem, st); break;
-        case 8: rc = launch_levels<8>(f, F, f->fsched, f->fsmem, st); break;
-        case 16: rc = launch_levels<16>(f, F, f->fsched, f->fsmem, st); break;
-        case 32: rc = launch_levels<32>(f, F, f->fsched, f->fsmem, st); break;
-        default: set_error("block size too large"); rc = IRK_EINVAL;
+    auto run_levels = [&](cudaStream_t s2) -> int {
+        switch (f->maxt) {
+            case 2: return launch_levels<2>(f, F, f->fsched, f->fsmem, s2);
+            case 4: return launch_levels<4>(f, F, f->fsched, f->fsmem, s2);
+            case 8: return launch_levels<8>(f, F, f->fsched, f->fsmem, s2);
+            case 16: return launch_levels<16>(f, F, f->fsched, f->fsmem, s2);
+            case 32: return launch_levels<32>(f, F, f->fsched, f->fsmem, s2);
+            default: set_error("block size too large"); return IRK_EINVAL;
+        }
+    };
+    // Deep schedules (natural numbering: 258 levels at config 1, 3-4 stream operations each) are
+    // launch-bound: ~48 us per level for ~22 us of kernels.  The level loop is captured into a CUDA
+    // graph on the second call (the first one sets the kernels' attributes) and replayed as long
+    // as the kernel arguments are byte-identical (same buffers, coefficients and schedule: one
+    // Newton iteration after the other); anything else re-captures.  IRK_FACTOR_GRAPH=0: off.
+    static const bool graph_off = getenv("IRK_FACTOR_GRAPH") && atoi(getenv("IRK_FACTOR_GRAPH")) == 0;
+    const bool deep = f->fsched.nlevels > 16 && !graph_off && f->kind == IRK_FACTOR_UNCOUPLED;
+    if (deep) {
+        if (!f->fgraph) f->fgraph = new FactorGraph();
+        FactorGraph* g = static_cast<FactorGraph*>(f->fgraph);
+        if (g->exec && std::memcmp(&g->key, &F, sizeof(FactorArgs)) == 0) {
+            IRK_CK(cudaGraphLaunch(g->exec, st));
+            count_launches(g->launches);
+        } else if (g->calls++ == 0) {
+            rc = run_levels(st);
+        } else {
+            if (g->exec) { cudaGraphExecDestroy(g->exec); g->exec = nullptr; }
+            if (!g->cap) IRK_CK(cudaStreamCreateWithFlags(&g->cap, cudaStreamNonBlocking));
+            const long long before = launch_count_now();
+            IRK_CK(cudaStreamBeginCapture(g->cap, cudaStreamCaptureModeRelaxed));
+            rc = run_levels(g->cap);
+            cudaGraph_t graph = nullptr;
+            const cudaError_t ce = cudaStreamEndCapture(g->cap, &graph);
+            g->launches = launch_count_now() - before;
+            if (rc == IRK_OK && ce == cudaSuccess && graph) {
+                if (cudaGraphInstantiate(&g->exec, graph, 0) == cudaSuccess) {
+                    std::memcpy(&g->key, &F, sizeof(FactorArgs));
+                    IRK_CK(cudaGraphLaunch(g->exec, st));
+                } else {
+                    g->exec = nullptr;
+                }
+            }
+            if (graph) cudaGraphDestroy(graph);
+            if (!g->exec) {   // capture not possible here: plain launches
+                cudaGetLastError();
+                rc = run_levels(st);
+            }
+        }
+    } else {
+        rc = run_levels(st);
     }
     if (rc) return rc;
     unsigned long long key = 0;
@@ -1552,6 +1606,12 @@ void irk_factor_destroy(irk_factor* f) {
     cudaFree(f->d_fs_tasks);
     for (auto e : f->ev) cudaEventDestroy(e);
     if (f->st2) cudaStreamDestroy(f->st2);
+    if (f->fgraph) {
+        FactorGraph* g = static_cast<FactorGraph*>(f->fgraph);
+        if (g->exec) cudaGraphExecDestroy(g->exec);
+        if (g->cap) cudaStreamDestroy(g->cap);
+        delete g;
+    }
     cudaFree(f->d_hasup);
     cudaFree(f->d_Dinv);
     cudaFree(f->d_D);

@@ -222,6 +222,10 @@ struct irk_factor {
     // side stream + events: the inverse of Schur chunk c overlaps the Schur phase of chunk c+1
     mutable cudaStream_t st2 = nullptr;
     mutable std::vector<cudaEvent_t> ev;
+    // deep factor schedules (one Schur + inverse launch pair per level, hundreds of levels): the
+    // level loop is captured once into a CUDA graph and replayed while the kernel arguments stay
+    // the same (factor.cu factor_numeric)
+    void* fgraph = nullptr;
     size_t fsmem = 0;
     int maxt = 1;
     const double* cpl_src = nullptr;  // explicit couplings (s*s*T blocks)
