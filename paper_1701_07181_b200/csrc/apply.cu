@@ -2232,7 +2232,12 @@ static size_t deep_smem(const irk_factor* f, const ApplyArgs& A) {
 template <int S>
 static bool deep_ok(const irk_factor* f, const ApplyArgs& A) {
     static const bool off = getenv("IRK_DEEP") && atoi(getenv("IRK_DEEP")) == 0;   // A/B switch
-    return !off && A.u_shared && !A.fac_shared && A.U == nullptr && A.nb % 2 == 0 && f->maxdeg <= MAXD &&
+    // narrow levels only (one CTA per SM, one task each): with wide levels the sweep is a throughput
+    // problem again and the generic ring kernel wins (config 2 at N = 16, natural numbering: 67
+    // levels of ~367 tasks, 1.51 ms vs 2.06 ms with a single-buffered k_unc_deep)
+    const int64_t ntasks = f->fwd.h_lvl_ptr.empty() ? 0 : f->fwd.h_lvl_ptr.back();
+    const bool narrow = f->fwd.nlevels > 0 && ntasks * 4 <= (int64_t)f->fwd.nlevels * f->ctx->num_sms * 5;
+    return !off && narrow && A.u_shared && !A.fac_shared && A.U == nullptr && A.nb % 2 == 0 && f->maxdeg <= MAXD &&
            S * A.nb + 32 <= 512 && deep_smem<S>(f, A) <= (size_t)f->ctx->smem_optin;
 }
 
