@@ -1119,7 +1119,8 @@ static int launch_levels(const irk_factor* f, FactorArgs& F, const irk_sched& sc
             static const int nchunk = env_int("IRK_FACTOR_CHUNKS", 1);   // measured: no gain at config 1
             static const int schur_cap = env_int("IRK_SCHUR_CAP", 2);
             static const int inv_cap = env_int("IRK_INV_CAP", 1);
-            static const bool form_off = env_int("IRK_FORM_D", 1) == 0;
+            // forming D inside the inverse needs the tensor-core inverse kernels
+            static const bool form_off = env_int("IRK_FORM_D", 1) == 0 || env_int("IRK_INV_TC", 1) == 0;
             if (l == 0 && F.L == nullptr && !F.literal && F.nb > 16 && F.nb <= 64 && f->d_fb && !form_off) {
                 // level 0 has no Schur update: the inverse kernel forms D = alpha J_jj + coef_k M_j itself
                 InvForm fm;
