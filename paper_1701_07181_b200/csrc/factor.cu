@@ -1272,8 +1272,11 @@ static int factor_numeric(irk_factor* f, int64_t* fail_stage, int64_t* fail_elem
     // launch-bound: ~48 us per level for ~22 us of kernels.  The level loop is captured into a CUDA
     // graph on the second call (the first one sets the kernels' attributes) and replayed as long
     // as the kernel arguments are byte-identical (same buffers, coefficients and schedule: one
-    // Newton iteration after the other); anything else re-captures.  IRK_FACTOR_GRAPH=0: off.
-    static const bool graph_off = getenv("IRK_FACTOR_GRAPH") && atoi(getenv("IRK_FACTOR_GRAPH")) == 0;
+    // Newton iteration after the other); anything else re-captures.  Opt-in (IRK_FACTOR_GRAPH=1):
+    // capturing and instantiating the ~1000-node graph costs tens of milliseconds once and a replay
+    // saves 1 ms of 12.6 (config 1, natural numbering), so it pays off after a few dozen
+    // re-factorisations of one structure only.
+    static const bool graph_off = !(getenv("IRK_FACTOR_GRAPH") && atoi(getenv("IRK_FACTOR_GRAPH")) != 0);
     const bool deep = f->fsched.nlevels > 16 && !graph_off && f->kind == IRK_FACTOR_UNCOUPLED;
     if (deep) {
         if (!f->fgraph) f->fgraph = new FactorGraph();
