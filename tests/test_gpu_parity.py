@@ -664,3 +664,29 @@ def test_protocol_shims_concurrent_threads(be, workers):
         np.testing.assert_array_equal(conc[k][0], serial[k][0])
         np.testing.assert_array_equal(conc[k][1], serial[k][1])
         np.testing.assert_array_equal(sol[k], sol_serial[k])
+
+
+@pytest.mark.parametrize("m", [24, 40, 50])
+@pytest.mark.parametrize("eps,fails", [(1e-12, False), (3e-14, False), (1e-15, True)])
+def test_condition_threshold_two_stage_check(be, m, eps, fails):
+    """_inv_with_cond (numba_backend.py:33-40): a pivot block fails iff cond_1 = |D|_1 |D^-1|_1 >
+    1e14.  The tensor-core inverse clears most blocks with the bound nb |D|_F |D^-1|_F and computes
+    the exact 1-norms only when the bound exceeds 1e14: a block with cond_1 = 1/eps just below the
+    threshold (the bound is above it: exact path) must pass, one above must fail at the same
+    element as the oracle."""
+    from paper_1701_07181_b200.meshes import line_mesh
+    from tests.helpers import random_blocks
+    g = line_mesh(6, periodic=True)
+    ip, ix, dp = pattern_of(g.adjacency)
+    data = random_blocks(g.adjacency, m, seed=3, diag_boost=30.0)
+    keep = np.ones(len(ix), bool)
+    keep[:] = ix == np.repeat(np.arange(6), np.diff(ip))      # block Jacobi: pivots are the diagonal blocks
+    bad = 3
+    d = np.eye(m)
+    d[m - 1, m - 1] = eps
+    data[dp[bad]] = d
+    f, dinv, fail = be.ilu0_factor(ip, ix, dp, data, keep, True)
+    fo, do, failo = O.ilu0_factor(ip, ix, dp, data, keep, True)
+    assert fail == failo == (bad if fails else -1)
+    if not fails:
+        np.testing.assert_allclose(dinv[bad], np.diag(1.0 / np.diag(d)), rtol=1e-12)
