@@ -40,6 +40,7 @@ struct ApplyArgs {
     const double* y;
     double* x;
     double* W;                 // implicit-L forward sweep: w_i = Dinv_i z_i (s x n) or NULL
+    double* Z;                 // deep sentinel sweeps: z_i of the forward sweep (s x n)
     const uint8_t* hasup;      // element has a kept upper block (implicit-L mode)
     unsigned* flags2;          // bwd flags, released by the implicit forward sweep for fused rows
     // persistent sweep: tasks in topological (level) order, claimed by ticket;
@@ -1051,6 +1052,184 @@ __global__ void __launch_bounds__(512) k_unc_deep(ApplyArgs A, DeepCfg DC) {
             if (FWDI && !store_z) st_release(A.flags2 + i, A.epoch);   // row finished here
             mbar_arrive(empty + b);
         }
+        b ^= 1;
+        if (b == 0) ph ^= 1;
+    }
+}
+
+// k_unc_deep with self-validating values instead of flags.  The hand-over of k_unc_deep costs
+// three L2 round trips per level -- the producer's __threadfence before the flag (0.83 us), the
+// flag reaching the poller (~1.1 us), the segment load after it (0.83 us).  Here the outputs a
+// sweep will write (w for the forward sweep, x for both) are pre-filled with a NaN bit pattern no
+// computation produces, consumers spin on the VALUES they need (ld.relaxed.gpu, one per thread
+// and neighbour; the addresses are spread over the vector, no hot line) and outputs are plain
+// 8-byte stores: one round trip per level, no fence, no flag.  Every entry of w / x is written
+// exactly once per apply, which is why z_i (needed by the backward sweep) goes to its own buffer
+// Z instead of the x slot.  x must not alias y (the caller falls back to k_unc_deep).
+constexpr unsigned long long DEEP_SENTINEL = 0xFFF8DEADBEEF5EEDULL;
+
+__global__ void k_fill_sentinel(double* __restrict__ a, double* __restrict__ b, int64_t n) {
+    const double sv = __longlong_as_double((long long)DEEP_SENTINEL);
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x) {
+        a[e] = sv;
+        if (b) b[e] = sv;
+    }
+}
+
+__device__ __forceinline__ double poll_value(const double* p) {
+    unsigned long long v;
+    do {
+        asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    } while (v == DEEP_SENTINEL);
+    return __longlong_as_double((long long)v);
+}
+
+__device__ __forceinline__ void publish_value(double* p, double v) {
+    asm volatile("st.relaxed.gpu.global.f64 [%0], %1;" :: "l"(p), "d"(v) : "memory");
+}
+
+template <int S, bool FWDI>
+__global__ void __launch_bounds__(512) k_unc_deep_sent(ApplyArgs A, DeepCfg DC) {
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    const int nb = A.nb, P = nb >> 1;
+    unsigned char* bufs = smem_raw;
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem_raw + 2 * (size_t)DC.buf_bytes);
+    uint64_t* empty = full + 2;
+    DeepDesc* desc = reinterpret_cast<DeepDesc*>(empty + 2);
+    double* xs = reinterpret_cast<double*>(smem_raw + 2 * (size_t)DC.buf_bytes + 128);   // [maxdeg][S][nb]
+    double* ts = xs + (size_t)DC.maxdeg * S * nb;                                         // [S][nb]
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int ncons = (int)blockDim.x - 32;
+    if (threadIdx.x == 0) {
+        for (int b = 0; b < 2; ++b) {
+            mbar_init(full + b, 1);
+            mbar_init(empty + b, 1);
+        }
+        fence_mbar_init();
+    }
+    __syncthreads();
+    griddep_launch();
+    const int64_t bsz = (int64_t)DC.block_bytes / 8;
+    if (warp == 0) {
+        griddep_wait();
+        int b = 0;
+        uint32_t ph = 0;
+        for (;;) {
+            int t = 0;
+            if (lane == 0) t = atomicAdd(A.ticket, 1);
+            t = __shfl_sync(0xffffffffu, t, 0);
+            const bool end = t >= A.ntasks;
+            int i = -1, b0 = 0, nn = 0, sz = 0;
+            if (!end) {
+                i = A.order[t];
+                const int d = A.diag[i];
+                b0 = FWDI ? A.indptr[i] : d + 1;
+                nn = (FWDI ? d : A.indptr[i + 1]) - b0;
+                sz = (FWDI && A.hasup[i]) ? 1 : 0;
+            }
+            int colm = 0, kp = 0;
+            if (lane < nn && lane < MAXD) {
+                colm = A.indices[b0 + lane];
+                kp = A.keep[b0 + lane] ? 1 : 0;
+            }
+            const unsigned km = __ballot_sync(0xffffffffu, kp != 0);
+            if (lane == 0) mbar_wait(empty + b, ph ^ 1);
+            __syncwarp();
+            if (lane == 0) {
+                desc[b].i = i;
+                desc[b].nn = nn;
+                desc[b].store_z = sz;
+                desc[b].km = km;
+            }
+            if (lane < MAXD) desc[b].col[lane] = colm;
+            __syncwarp();
+            if (lane == 0) {
+                if (end) {
+                    mbar_expect_tx(full + b, 0);
+                } else {
+                    const int nkept = __popc(km);
+                    mbar_expect_tx(full + b, (uint32_t)(nkept + S) * (uint32_t)DC.block_bytes);
+                    unsigned char* dst = bufs + (size_t)b * DC.buf_bytes;
+                    for (int m = 0; m < nn; ++m)
+                        if ((km >> m) & 1u) {
+                            bulk_g2s(dst, A.ubase[0] + (int64_t)(b0 + m) * bsz, DC.block_bytes, full + b);
+                            dst += DC.block_bytes;
+                        }
+                    for (int k = 0; k < S; ++k, dst += DC.block_bytes)
+                        bulk_g2s(dst, A.Dinv + ((int64_t)i * S + k) * bsz, DC.block_bytes, full + b);
+                }
+            }
+            if (end) break;
+            b ^= 1;
+            if (b == 0) ph ^= 1;
+        }
+        return;
+    }
+    const int c = threadIdx.x - 32;
+    const int k = c / nb, a = c - k * nb;
+    const bool act = k < S;
+    auto row_dot = [&](const unsigned char* blk, const double* xv) -> double {
+        const double2* B = reinterpret_cast<const double2*>(blk) + a;
+        const double2* X = reinterpret_cast<const double2*>(xv);
+        double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+        int p = 0;
+#pragma unroll 5
+        for (; p + 2 <= P; p += 2) {
+            const double2 b0 = B[p * nb], b1 = B[(p + 1) * nb];
+            const double2 v0 = X[p], v1 = X[p + 1];
+            s0 = fma(b0.x, v0.x, s0);
+            s1 = fma(b0.y, v0.y, s1);
+            s2 = fma(b1.x, v1.x, s2);
+            s3 = fma(b1.y, v1.y, s3);
+        }
+        if (p < P) {
+            const double2 b0 = B[p * nb];
+            const double2 v0 = X[p];
+            s0 = fma(b0.x, v0.x, s0);
+            s1 = fma(b0.y, v0.y, s1);
+        }
+        return (s0 + s1) + (s2 + s3);
+    };
+    griddep_wait();
+    int b = 0;
+    uint32_t ph = 0;
+    for (;;) {
+        mbar_wait(full + b, ph);
+        const int64_t i = desc[b].i;
+        if (i < 0) break;
+        const int nn = desc[b].nn;
+        const unsigned km = desc[b].km;
+        const bool store_z = FWDI && desc[b].store_z != 0;
+        const int nkept = __popc(km);
+        // gather: the task's own segment (complete before this launch) and, by polling the values,
+        // the neighbours' segments
+        double own = 0.0;
+        if (act) {
+            own = __ldcg((FWDI ? A.y : A.Z) + (int64_t)k * A.n + i * nb + a);
+            const double* vsrc = (FWDI ? A.W : A.x) + (int64_t)k * A.n + a;
+            int slot = 0;
+            for (int m = 0; m < nn; ++m)
+                if ((km >> m) & 1u) {
+                    xs[(slot * S + k) * nb + a] = poll_value(vsrc + (int64_t)desc[b].col[m] * nb);
+                    ++slot;
+                }
+        }
+        consumer_sync(1, ncons);
+        const unsigned char* buf = bufs + (size_t)b * DC.buf_bytes;
+        if (act) {
+            double sum = 0.0;
+            for (int slot = 0; slot < nkept; ++slot)
+                sum += row_dot(buf + (size_t)slot * DC.block_bytes, xs + (slot * S + k) * nb);
+            const double tval = nkept ? own - A.uscale * sum : own;
+            ts[k * nb + a] = tval;
+            if (store_z) A.Z[(int64_t)k * A.n + i * nb + a] = tval;   // z_i for the backward sweep
+        }
+        consumer_sync(1, ncons);
+        if (act)
+            publish_value((store_z ? A.W : A.x) + (int64_t)k * A.n + i * nb + a,
+                          row_dot(buf + (size_t)(nkept + k) * DC.block_bytes, ts + k * nb));
+        consumer_sync(1, ncons);   // buffer, xs and ts are free
+        if (c == 0) mbar_arrive(empty + b);
         b ^= 1;
         if (b == 0) ph ^= 1;
     }
@@ -2248,7 +2427,7 @@ static bool deep_ok(const irk_factor* f, const ApplyArgs& A) {
            S * A.nb + 32 <= 512 && deep_smem<S>(f, A) <= (size_t)f->ctx->smem_optin;
 }
 
-template <int S, bool FWDI>
+template <int S, bool FWDI, bool SENT = false>
 static int run_deep(const irk_factor* f, ApplyArgs& A, const irk_sched& Sd, unsigned* flags, int* ticket,
                     cudaStream_t st) {
     A.flags = flags;
@@ -2263,10 +2442,11 @@ static int run_deep(const irk_factor* f, ApplyArgs& A, const irk_sched& Sd, unsi
     const int threads = 32 + ((S * A.nb + 31) / 32) * 32;
     const size_t smem = deep_smem<S>(f, A);
     int per_sm = 1;
-    IRK_CK(sweep_occupancy((const void*)k_unc_deep<S, FWDI>, threads, smem, (int)f->ctx->smem_optin, &per_sm));
+    auto kernel = SENT ? k_unc_deep_sent<S, FWDI> : k_unc_deep<S, FWDI>;
+    IRK_CK(sweep_occupancy((const void*)kernel, threads, smem, (int)f->ctx->smem_optin, &per_sm));
     IRK_CK(cudaMemsetAsync(ticket, 0, sizeof(int), st));
     const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(A.ntasks, (int64_t)f->ctx->num_sms * std::max(per_sm, 1)));
-    IRK_CK(launch_pdl_if(true, k_unc_deep<S, FWDI>, dim3(grid), dim3(threads), smem, st, A, DC));
+    IRK_CK(launch_pdl_if(!SENT, kernel, dim3(grid), dim3(threads), smem, st, A, DC));
     IRK_LAUNCHED();
     return IRK_OK;
 }
@@ -2290,6 +2470,17 @@ static int unc_apply(const irk_factor* f, ApplyArgs& A0, cudaStream_t st) {
             // implicit L: forward sweep streams the stage-shared J_ij with w_j = Dinv_j z_j and
             // finishes rows without upper blocks; the backward sweep covers the remaining rows
             A.flags2 = f->d_flags + nf;
+            static const bool sent_off = getenv("IRK_DEEP_SENT") && atoi(getenv("IRK_DEEP_SENT")) == 0;   // A/B switch
+            if (deep && !sent_off && deep_ok<S>(f, A) && A.x != A.y) {
+                if (!f->d_Z) IRK_CK(cudaMalloc(&f->d_Z, sizeof(double) * (size_t)S * A.n));
+                A.Z = f->d_Z;
+                const int64_t tot = (int64_t)S * A.n;
+                k_fill_sentinel<<<(int)std::min<int64_t>((tot + 255) / 256, (int64_t)f->ctx->num_sms * 8), 256, 0, st>>>(A.x, A.W, tot);
+                IRK_LAUNCHED();
+                IRK_TRY((run_deep<S, true, true>(f, A, f->fwd, f->d_flags, f->d_ticket, st)));
+                IRK_TRY((run_deep<S, false, true>(f, A, f->bwd, f->d_flags + nf, f->d_ticket + 1, st)));
+                return IRK_OK;
+            }
             if (deep && deep_ok<S>(f, A)) {
                 IRK_TRY((run_deep<S, true>(f, A, f->fwd, f->d_flags, f->d_ticket, st)));
                 IRK_TRY((run_deep<S, false>(f, A, f->bwd, f->d_flags + nf, f->d_ticket + 1, st)));

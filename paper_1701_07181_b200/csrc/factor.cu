@@ -1604,6 +1604,7 @@ void irk_factor_destroy(irk_factor* f) {
     cudaFree(f->d_keep);
     cudaFree(f->d_L);
     cudaFree(f->d_W);
+    cudaFree(f->d_Z);
     cudaFree(f->d_Wrhs);
     cudaFree(f->d_fb);
     cudaFree(f->d_fs_elems);

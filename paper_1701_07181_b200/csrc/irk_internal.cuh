@@ -186,6 +186,7 @@ struct irk_factor {
     bool l_implicit = false;
     bool cpl_pipe = false;            // coupled: element-task pipelined sweeps (element schedules)
     double* d_W = nullptr;
+    mutable double* d_Z = nullptr;    // deep sentinel sweeps: z_i of the forward sweep (s x T x nb), lazily allocated
     mutable double* d_Wrhs = nullptr; // multi-RHS apply of a single factor: nrhs x T x nb
     mutable int wrhs = 0;
     uint8_t* d_hasup = nullptr;       // T: row has a kept upper block
