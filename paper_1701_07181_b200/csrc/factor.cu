@@ -50,6 +50,7 @@ struct FactorArgs {
     int64_t T;
     int s, nb, nbp4, ld, KC;
     int coupled, literal, simplified;
+    int split;                // Schur phase: one CTA task per (element, stage) (k_schur<1, ..>), F.s stages
 };
 
 __device__ __forceinline__ int pair_index(int hi, int lo) { return hi * (hi - 1) / 2 + lo; }
@@ -669,7 +670,9 @@ __device__ __forceinline__ void fence_proxy_async_smem() {
 template <int S, int NB, int NSL = S + 2>
 constexpr int schur_min_ctas() {
     const int by_smem = 232448 / (NSL * SchurGeo<NB>::SLOT * 8 + 1280);
-    const int by_regs = 65536 / (4 * NB * 128);
+    // registers a thread needs: the pivot accumulators (S strips of NB / 8 tiles) + one product strip
+    const int need = S >= 3 ? 128 : (S == 2 ? 112 : 80);
+    const int by_regs = 65536 / (4 * NB * need);
     const int m = by_smem < by_regs ? by_smem : by_regs;
     return m < 1 ? 1 : m;
 }
@@ -694,6 +697,12 @@ __global__ void __launch_bounds__(4 * NB, MODE == 1 ? 1 : schur_min_ctas<S, NB, 
     const int fr = lane >> 2, fk = lane & 3;
     const int r0 = warp * 8;
     const double* J = F.J[0];
+    // split mode (S == 1 instantiation over (element, stage) tasks, element-major so that the F.s
+    // CTAs of an element run side by side and share its J blocks in L2): task it -> element
+    // elems[it / ST], stage it % ST; otherwise one task per element with all S == ST stages
+    const int ST = F.split ? F.s : S;
+    auto elem_of = [&](int64_t it) -> int { return elems[F.split ? it / ST : it]; };
+    auto stage_of = [&](int64_t it) -> int { return F.split ? (int)(it % ST) : 0; };
     constexpr int NSL = MODE == 3 ? 4 : S + 2;      // staged-block slots
     static_assert(MODE != 3 || S >= 2, "MODE 3 needs at least two stages");
     if (threadIdx.x < S + 2) outcnt[threadIdx.x] = 0;
@@ -727,7 +736,7 @@ __global__ void __launch_bounds__(4 * NB, MODE == 1 ? 1 : schur_min_ctas<S, NB, 
     struct Unit { int64_t it; int q; int i, tq; };
     auto find_unit = [&](int64_t it, int q) -> Unit {
         for (; it < nelem; it += gridDim.x) {
-            const int j = elems[it];
+            const int j = elem_of(it);
             const int dpos = F.diag[j];
             if (q < 0) q = F.indptr[j];
             for (; q < dpos; ++q) {
@@ -738,7 +747,7 @@ __global__ void __launch_bounds__(4 * NB, MODE == 1 ? 1 : schur_min_ctas<S, NB, 
         }
         return Unit{-1, -1, -1, -1};
     };
-    auto src_dinv = [&](const Unit& u, int k) { return F.Dinv + ((int64_t)u.i * S + k) * BSZ; };
+    auto src_dinv = [&](const Unit& u, int k) { return F.Dinv + ((int64_t)u.i * ST + stage_of(u.it) + k) * BSZ; };
     Unit nxt = find_unit(blockIdx.x, -1);
     if (nxt.it >= 0) {
         fill(SJ, J + (int64_t)nxt.q * BSZ);
@@ -760,7 +769,8 @@ __global__ void __launch_bounds__(4 * NB, MODE == 1 ? 1 : schur_min_ctas<S, NB, 
     };
 
     for (int64_t it = blockIdx.x; it < nelem; it += gridDim.x) {
-        const int j = elems[it];
+        const int j = elem_of(it);
+        const int ks = stage_of(it);
         const int dpos = F.diag[j];
         double dacc[S][NT][2];
         // ---- D_k = fl(alpha J_jj) + fl(coef_k M_j)  (build_stage_matrix, precond.py:48-54)
@@ -777,8 +787,8 @@ __global__ void __launch_bounds__(4 * NB, MODE == 1 ? 1 : schur_min_ctas<S, NB, 
                 for (int k = 0; k < S; ++k) {
                     double x0 = __dmul_rn(F.alpha, jv.x), x1 = __dmul_rn(F.alpha, jv.y);
                     if (Md) {
-                        x0 = __dadd_rn(x0, __dmul_rn(F.coef[k], mv.x));
-                        x1 = __dadd_rn(x1, __dmul_rn(F.coef[k], mv.y));
+                        x0 = __dadd_rn(x0, __dmul_rn(F.coef[ks + k], mv.x));
+                        x1 = __dadd_rn(x1, __dmul_rn(F.coef[ks + k], mv.y));
                     }
                     dacc[k][t][0] = keep_d ? x0 : 0.0;
                     dacc[k][t][1] = keep_d ? x1 : 0.0;
@@ -788,7 +798,7 @@ __global__ void __launch_bounds__(4 * NB, MODE == 1 ? 1 : schur_min_ctas<S, NB, 
         const int q0 = F.indptr[j];
         const int lq0 = F.lptr[j];
         for (int q = q0; q < dpos; ++q) {
-            double* Lout = F.L ? F.L + (int64_t)(lq0 + (q - q0)) * S * BSZ : nullptr;   // NULL: implicit L
+            double* Lout = F.L ? F.L + ((int64_t)(lq0 + (q - q0)) * ST + ks) * BSZ : nullptr;   // NULL: implicit L
             if (!(nxt.it == it && nxt.q == q)) {
                 // not a unit: the reference never forms L_ji D_i^-1 here, so L stays
                 // B_ji (upper block dropped) or 0 (lower block dropped); D unchanged
@@ -1006,7 +1016,7 @@ __global__ void __launch_bounds__(4 * NB, MODE == 1 ? 1 : schur_min_ctas<S, NB, 
         // ---- pivot blocks -> F.Dst for the batched inverse
 #pragma unroll
         for (int k = 0; k < S; ++k) {
-            double2* Dk = reinterpret_cast<double2*>(F.Dst + ((int64_t)j * S + k) * BSZ);
+            double2* Dk = reinterpret_cast<double2*>(F.Dst + ((int64_t)j * ST + ks + k) * BSZ);
 #pragma unroll
             for (int t = 0; t < NT; ++t)
                 if (gl_off(t) >= 0) Dk[gl_off(t)] = make_double2(dacc[k][t][0], dacc[k][t][1]);
@@ -1074,6 +1084,18 @@ static bool schur_eligible(const irk_factor* f, const FactorArgs& F) {
 
 static int launch_schur(const irk_ctx* ctx, const FactorArgs& F, const int32_t* elems, int64_t nelem,
                         cudaStream_t st, int cap = 0) {
+    // Narrow levels (deep schedules: fewer elements than SMs) run one CTA task per (element,
+    // stage) on the S = 1 instantiation: with one 5-warp CTA per element most of each SM idles and
+    // the level's latency is the element's S x 2 GEMMs per unit; split, the stages run side by
+    // side.  For full levels it loses (every stage re-stages the two J blocks: 1.95 vs 1.68 ms at
+    // config 1, colour numbering).  IRK_SCHUR_SPLIT = 0 / 1 forces it off / on (A/B knob).
+    static const int split_env = getenv("IRK_SCHUR_SPLIT") ? atoi(getenv("IRK_SCHUR_SPLIT")) : -1;
+    const bool split = F.s >= 2 && (split_env >= 0 ? split_env != 0 : nelem <= (int64_t)ctx->num_sms);
+    if (split) {
+        FactorArgs Fs = F;
+        Fs.split = 1;
+        return launch_schur_s<1>(ctx, Fs, elems, nelem * F.s, st, cap);
+    }
     switch (F.s) {
         case 1: return launch_schur_s<1>(ctx, F, elems, nelem, st, cap);
         case 2: return launch_schur_s<2>(ctx, F, elems, nelem, st, cap);
