@@ -1076,11 +1076,13 @@ __global__ void k_fill_sentinel(double* __restrict__ a, double* __restrict__ b, 
     }
 }
 
+// Bounded spin (2^22 polls of ~0.7 us, normal waits are a few of them): a value that never arrives --
+// only possible if an input vector carried the sentinel pattern itself, whose NaN payload the
+// arithmetic would propagate into an output -- ends as NaN in the result instead of a hung GPU.
 __device__ __forceinline__ double poll_value(const double* p) {
-    unsigned long long v;
-    do {
+    unsigned long long v = DEEP_SENTINEL;
+    for (int it = 0; it < (1 << 22) && v == DEEP_SENTINEL; ++it)
         asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
-    } while (v == DEEP_SENTINEL);
     return __longlong_as_double((long long)v);
 }
 
