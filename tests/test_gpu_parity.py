@@ -690,3 +690,38 @@ def test_condition_threshold_two_stage_check(be, m, eps, fails):
     assert fail == failo == (bad if fails else -1)
     if not fails:
         np.testing.assert_allclose(dinv[bad], np.diag(1.0 / np.diag(d)), rtol=1e-12)
+
+
+@pytest.mark.parametrize("scheme", ["RADAU23", "RADAU35"])
+def test_deep_sweeps_self_validating_values(scheme):
+    """Deep (natural-numbering) schedules run the self-validating-value sweeps (k_unc_deep_sent:
+    outputs pre-filled with a NaN sentinel, consumers poll the values they need).  The apply
+    matches the oracle to 1e-12, leaves no sentinel / NaN behind, does not touch its input, is
+    bitwise repeatable, and the C ABI rejects x aliasing y (the pre-fill would destroy the input)."""
+    import torch
+    from paper_1701_07181_b200 import _lib as L
+    from paper_1701_07181_b200.blocks import DevicePattern
+    from paper_1701_07181_b200.krylov import GmresConfig
+    from paper_1701_07181_b200.solver import StageSolver
+    cfg = W.CONFIGS[1].scaled(N=8, ordering="natural", scheme=scheme)
+    wl = W.make_workload(cfg, norm_iters=10)
+    p = wl.pattern
+    sol = StageSolver(DevicePattern(p.indptr, p.indices, p.diag_pos), wl.J, wl.M, wl.a_inv, wl.dt,
+                      kind="uncoupled", shifts=wl.shifts, gmres_cfg=GmresConfig(rel_tol=1e-8, restart=40))
+    sol.factorize()
+    assert sol.fac.implicit_l and sol.fac.levels()[0] > 16
+    y = np.random.default_rng(7).standard_normal(sol.n)
+    yd = torch.from_numpy(y).cuda()
+    x1 = torch.empty_like(yd)
+    x2 = torch.full_like(yd, 3.0)
+    sol.fac.apply_device(yd, x1)
+    sol.fac.apply_device(yd, x2)
+    torch.cuda.synchronize()
+    assert torch.equal(x1, x2)
+    assert torch.equal(yd, torch.from_numpy(y).cuda())
+    assert not np.isnan(x1.cpu().numpy()).any()
+    prob = O.problem_from_workload(wl)
+    ofac = O.make_preconditioner(prob, "uncoupled", wl.shifts)
+    assert rel(x1.cpu().numpy(), ofac.apply(y)) < 1e-12
+    rc = L.lib().irk_factor_apply(sol.fac.handle, x2.data_ptr(), x2.data_ptr(), L.stream_ptr())
+    assert rc not in (L.IRK_OK, L.IRK_ESINGULAR)        # IRK_EINVAL: "x must not alias y"
