@@ -1107,7 +1107,7 @@ static int launch_schur(const irk_ctx* ctx, const FactorArgs& F, const int32_t* 
 
 int launch_inverse(const irk_ctx* ctx, const int32_t* tasks, int64_t ntasks, int64_t T, int s, int nb,
                    const double* D, double* Dinv, unsigned long long* fail_key, int* fb, cudaStream_t st,
-                   int cap_per_sm = 0, const InvForm* form = nullptr);
+                   int cap_per_sm = 0, const InvForm* form = nullptr, bool optimistic = false);
 
 static int env_int(const char* name, int dflt) {
     const char* e = getenv(name);
@@ -1155,12 +1155,13 @@ static int launch_levels(const irk_factor* f, FactorArgs& F, const irk_sched& sc
                 for (int k = 0; k < F.s; ++k) fm.coef[k] = F.coef[k];
                 fm.store = f->store_d ? 1 : 0;
                 IRK_TRY(launch_inverse(f->ctx, tk, ne * F.s, F.T, F.s, F.nb, F.Dst, F.Dinv, F.fail_key, f->d_fb, st,
-                                       0, &fm));
+                                       0, &fm, f->fb_optimistic != 0));
                 f->d0_unstored = !f->store_d;
             } else if (l == 0 || nchunk <= 1 || ne < 4 * (int64_t)f->ctx->num_sms) {
                 if (l == 0) f->d0_unstored = false;
                 IRK_TRY(launch_schur(f->ctx, F, el, ne, st));
-                IRK_TRY(launch_inverse(f->ctx, tk, ne * F.s, F.T, F.s, F.nb, F.Dst, F.Dinv, F.fail_key, f->d_fb, st));
+                IRK_TRY(launch_inverse(f->ctx, tk, ne * F.s, F.T, F.s, F.nb, F.Dst, F.Dinv, F.fail_key, f->d_fb, st,
+                                       0, nullptr, f->fb_optimistic != 0));
             } else {
                 // chunked: the latency-bound inverse of chunk c (side stream, capped grid) runs beside
                 // the DMMA-bound Schur phase of chunk c+1 (main stream, capped at schur_cap CTAs/SM)
@@ -1332,7 +1333,29 @@ static int factor_numeric(irk_factor* f, int64_t* fail_stage, int64_t* fail_elem
             }
         }
     } else {
-        rc = run_levels(st);
+        // Deep schedules pay two stream operations per level for the pivoted fallback (counter
+        // reset + a launch that almost always finds an empty list): run the levels optimistically
+        // -- one counter reset, no fallback launches, handed-back blocks pile up in the list -- and
+        // repeat the factorisation the regular way if any block was handed back.
+        static const bool opt_off = getenv("IRK_FB_OPTIMISTIC") && atoi(getenv("IRK_FB_OPTIMISTIC")) == 0;
+        const bool optimistic = f->fsched.nlevels > 16 && !opt_off && f->kind == IRK_FACTOR_UNCOUPLED && f->d_fb &&
+                                schur_eligible(f, F) && f->d_fs_elems;
+        if (optimistic) {
+            IRK_CK(cudaMemsetAsync(f->d_fb, 0, sizeof(int), st));
+            f->fb_optimistic = 1;
+            rc = run_levels(st);
+            f->fb_optimistic = 0;
+            if (rc) return rc;
+            int handed = 0;
+            IRK_CK(cudaMemcpyAsync(&handed, f->d_fb, sizeof handed, cudaMemcpyDeviceToHost, st));
+            IRK_CK(cudaStreamSynchronize(st));
+            if (handed > 0) {
+                IRK_CK(cudaMemsetAsync(f->d_fail, 0xff, sizeof(unsigned long long), st));
+                rc = run_levels(st);
+            }
+        } else {
+            rc = run_levels(st);
+        }
     }
     if (rc) return rc;
     unsigned long long key = 0;

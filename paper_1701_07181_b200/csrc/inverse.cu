@@ -1642,10 +1642,12 @@ static int launch_pivoted(const irk_ctx* ctx, const InvArgs& A, cudaStream_t st)
 
 // tensor-core pass, then the pivoted kernels over the blocks it handed back
 // (their count stays on the device: the fallback launch reads it)
-static int launch_tc(const irk_ctx* ctx, const InvArgs& A, int* fb, cudaStream_t st) {
+// optimistic: no counter reset and no pivoted pass here -- the caller resets the counter once,
+// lets the handed-back blocks of all launches pile up in the list and checks the count at the end
+static int launch_tc(const irk_ctx* ctx, const InvArgs& A, int* fb, cudaStream_t st, bool optimistic = false) {
     int* fb_count = fb;
     int* fb_list = fb + 1;
-    IRK_CK(cudaMemsetAsync(fb_count, 0, sizeof(int), st));
+    if (!optimistic) IRK_CK(cudaMemsetAsync(fb_count, 0, sizeof(int), st));
     const int nt = (A.nb + 7) / 8;
     int rc;
     switch (nt) {
@@ -1658,6 +1660,7 @@ static int launch_tc(const irk_ctx* ctx, const InvArgs& A, int* fb, cudaStream_t
         default: return IRK_EINVAL;
     }
     if (rc) return rc;
+    if (optimistic) return IRK_OK;
     InvArgs B = A;
     B.tasks = fb_list;
     B.ntasks_dev = fb_count;
@@ -1668,13 +1671,13 @@ static int launch_tc(const irk_ctx* ctx, const InvArgs& A, int* fb, cudaStream_t
 // returns IRK_EINVAL if nb has no warp-inverse specialisation (caller falls back)
 int launch_inverse(const irk_ctx* ctx, const int32_t* tasks, int64_t ntasks, int64_t T, int s, int nb,
                    const double* D, double* Dinv, unsigned long long* fail_key, int* fb, cudaStream_t st,
-                   int cap_per_sm, const InvForm* form) {
+                   int cap_per_sm, const InvForm* form, bool optimistic) {
     if (ntasks <= 0) return IRK_OK;
     InvArgs A{tasks, ntasks, T, s, nb, D, Dinv, fail_key, nullptr, cap_per_sm, InvForm{}};
     static const bool tc_off = getenv("IRK_INV_TC") && atoi(getenv("IRK_INV_TC")) == 0;
     if (fb && !tc_off && nb > 16 && nb <= 64) {
         if (form) A.form = *form;
-        return launch_tc(ctx, A, fb, st);
+        return launch_tc(ctx, A, fb, st, optimistic);
     }
     if (form) return IRK_EINVAL;   // forming D needs the tensor-core path (caller runs the Schur phase)
     return launch_pivoted(ctx, A, st);

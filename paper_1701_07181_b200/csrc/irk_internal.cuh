@@ -214,6 +214,7 @@ struct irk_factor {
     irk_sched fsched;                 // factor tasks by level
     unsigned long long* d_fail = nullptr;
     int* d_fb = nullptr;              // tensor-core inverse: blocks handed to the pivoted kernels
+    mutable int fb_optimistic = 0;    // deep schedules: levels run without the per-level fallback launch (factor_numeric)
     bool store_d = false;             // pivot blocks must be kept (store_diag / literal)
     mutable bool d0_unstored = false; // level-0 pivot blocks were formed in the inverse, not stored
     // Schur path: per factor level, its elements and element-major (stage fastest) task codes

@@ -725,3 +725,26 @@ def test_deep_sweeps_self_validating_values(scheme):
     assert rel(x1.cpu().numpy(), ofac.apply(y)) < 1e-12
     rc = L.lib().irk_factor_apply(sol.fac.handle, x2.data_ptr(), x2.data_ptr(), L.stream_ptr())
     assert rc not in (L.IRK_OK, L.IRK_ESINGULAR)        # IRK_EINVAL: "x must not alias y"
+
+
+@pytest.mark.parametrize("m", [24, 40])
+@pytest.mark.parametrize("boost", [30.0, 0.5])
+def test_deep_factor_optimistic_fallback(be, m, boost):
+    """Deep factor schedules (here a 40-element line: 40 levels) run their levels without the
+    per-level pivoted-fallback launch and repeat the factorisation the regular way if any pivot
+    block needed row interchanges (boost 0.5: weakly diagonal blocks do).  Both cases must match
+    the oracle's partial-pivoting factor (numba_backend.py:33-72)."""
+    from paper_1701_07181_b200.meshes import line_mesh
+    from tests.helpers import random_blocks
+    g = line_mesh(40)
+    ip, ix, dp = pattern_of(g.adjacency)
+    data = random_blocks(g.adjacency, m, seed=11 + m, diag_boost=boost)
+    keep = np.ones(len(ix), bool)
+    f, d, fail = be.ilu0_factor(ip, ix, dp, data, keep, True)
+    fo, do, failo = O.ilu0_factor(ip, ix, dp, data, keep, True)
+    assert fail == failo
+    if failo == -1:
+        cond = max(np.linalg.cond(fo[q], 1) for q in dp)
+        tol = max(TOL, 4e-16 * cond * 40)
+        assert rel(d, do) < tol
+        assert rel(f, fo) < tol
