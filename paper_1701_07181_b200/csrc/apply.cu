@@ -892,6 +892,7 @@ struct DeepCfg {
     int block_bytes;
     int buf_bytes;     // (maxdeg + S) blocks
     int maxdeg;
+    int nbuf;          // task buffers (k_cpl_deep_sent; k_unc_deep* always use two)
 };
 
 struct DeepDesc {
@@ -1234,6 +1235,198 @@ __global__ void __launch_bounds__(512) k_unc_deep_sent(ApplyArgs A, DeepCfg DC) 
         if (c == 0) mbar_arrive(empty + b);
         b ^= 1;
         if (b == 0) ph ^= 1;
+    }
+}
+
+// Stage-coupled sweeps on a deep schedule with self-validating values (coupled_solve,
+// numba_backend.py:128-151; the reference's default preconditioner on its natural numbering).
+// Tasks are the (stage k, element i) pairs of the stage-skewed schedule (k_cpl_fwd / k_cpl_bwd
+// semantics):
+//   forward   z_ki = y_ki - sum_{j lower} L_{k,ij} z_kj - sum_{l<k} G_{kl,i} z_li
+//   backward  x_ki = Dinv_ki ( z_ki - uscale sum_{j upper} U_ij x_kj - sum_{l>k} C_{kl,i} x_li ),
+//             C_{kl,i} = cup_scale[k][l] M_i (implicit) or the stored blocks
+// z goes to its own buffer Z, so that every entry of Z (forward) and x (backward) is written once
+// and can be polled; both are pre-filled with the sentinel.  One thread per block row, a producer
+// warp one task ahead (all blocks of the task in one buffer, one mbarrier).
+struct CplDeepDesc {
+    int k, i, nn;
+    unsigned km;
+    int col[MAXD];
+};
+
+template <bool FWD>
+__global__ void __launch_bounds__(160) k_cpl_deep_sent(ApplyArgs A, DeepCfg DC) {
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    const int nb = A.nb, P = nb >> 1, S = A.s;
+    const int npairs = S * (S - 1) / 2;
+    unsigned char* bufs = smem_raw;
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem_raw + (size_t)DC.nbuf * DC.buf_bytes);
+    uint64_t* empty = full + 2;
+    CplDeepDesc* desc = reinterpret_cast<CplDeepDesc*>(empty + 2);   // 2 x 48 B
+    double* xs = reinterpret_cast<double*>(smem_raw + (size_t)DC.nbuf * DC.buf_bytes + 128);   // [maxdeg + S][nb]
+    double* tv = xs + (size_t)(DC.maxdeg + S) * nb;                                            // [nb]
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int ncons = (int)blockDim.x - 32;
+    if (threadIdx.x == 0) {
+        for (int b = 0; b < 2; ++b) {
+            mbar_init(full + b, 1);
+            mbar_init(empty + b, 1);
+        }
+        fence_mbar_init();
+    }
+    __syncthreads();
+    const int64_t bsz = (int64_t)DC.block_bytes / 8;
+    if (warp == 0) {
+        int b = 0;
+        uint32_t ph = 0;
+        for (;;) {
+            int t = 0;
+            if (lane == 0) t = atomicAdd(A.ticket, 1);
+            t = __shfl_sync(0xffffffffu, t, 0);
+            const bool end = t >= A.ntasks;
+            int k = 0, i = -1, b0 = 0, nn = 0, d = 0, l0 = 0, u0 = 0;
+            if (!end) {
+                const int64_t code = A.order[t];
+                k = (int)(code / A.T);
+                i = (int)(code - (int64_t)k * A.T);
+                d = A.diag[i];
+                b0 = FWD ? A.indptr[i] : d + 1;
+                nn = (FWD ? d : A.indptr[i + 1]) - b0;
+                l0 = A.lptr[i];
+                u0 = A.uptr[i];
+            }
+            int colm = 0, kp = 0;
+            if (lane < nn && lane < MAXD) {
+                colm = A.indices[b0 + lane];
+                kp = A.keep[b0 + lane] ? 1 : 0;
+            }
+            const unsigned km = __ballot_sync(0xffffffffu, kp != 0);
+            if (lane == 0) mbar_wait(empty + b, ph ^ 1);
+            __syncwarp();
+            if (lane == 0) {
+                desc[b].k = k;
+                desc[b].i = i;
+                desc[b].nn = nn;
+                desc[b].km = km;
+            }
+            if (lane < MAXD) desc[b].col[lane] = colm;
+            __syncwarp();
+            if (lane == 0) {
+                if (end) {
+                    mbar_expect_tx(full + b, 0);
+                } else {
+                    const int nkept = __popc(km);
+                    const int ncpl = FWD ? k : (A.Cup ? S - 1 - k : (k < S - 1 ? 1 : 0));
+                    mbar_expect_tx(full + b, (uint32_t)(nkept + ncpl + (FWD ? 0 : 1)) * (uint32_t)DC.block_bytes);
+                    unsigned char* dst = bufs + (size_t)b * DC.buf_bytes;
+                    for (int m = 0; m < nn; ++m)
+                        if ((km >> m) & 1u) {
+                            const double* src = FWD ? A.L + ((int64_t)(l0 + m) * S + k) * bsz
+                                                    : (A.U ? A.U + ((int64_t)(u0 + m) * S + k) * bsz
+                                                           : A.ubase[k] + (int64_t)(b0 + m) * bsz);
+                            bulk_g2s(dst, src, DC.block_bytes, full + b);
+                            dst += DC.block_bytes;
+                        }
+                    if (FWD) {
+                        for (int l = 0; l < k; ++l, dst += DC.block_bytes)
+                            bulk_g2s(dst, A.G + ((int64_t)i * npairs + pidx(k, l)) * bsz, DC.block_bytes, full + b);
+                    } else {
+                        if (A.Cup) {
+                            for (int l = k + 1; l < S; ++l, dst += DC.block_bytes)
+                                bulk_g2s(dst, A.Cup + ((int64_t)i * npairs + pidx(l, k)) * bsz, DC.block_bytes, full + b);
+                        } else if (k < S - 1) {
+                            bulk_g2s(dst, A.mass + (int64_t)i * bsz, DC.block_bytes, full + b);
+                            dst += DC.block_bytes;
+                        }
+                        bulk_g2s(dst, A.Dinv + ((int64_t)i * S + k) * bsz, DC.block_bytes, full + b);
+                    }
+                }
+            }
+            if (end) break;
+            if (++b == DC.nbuf) { b = 0; ph ^= 1; }
+        }
+        return;
+    }
+    const int a = threadIdx.x - 32;
+    const bool act = a < nb;
+    auto row_dot = [&](const unsigned char* blk, const double* xv) -> double {
+        const double2* B = reinterpret_cast<const double2*>(blk) + a;
+        const double2* X = reinterpret_cast<const double2*>(xv);
+        double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+        int p = 0;
+#pragma unroll 5
+        for (; p + 2 <= P; p += 2) {
+            const double2 b0 = B[p * nb], b1 = B[(p + 1) * nb];
+            const double2 v0 = X[p], v1 = X[p + 1];
+            s0 = fma(b0.x, v0.x, s0);
+            s1 = fma(b0.y, v0.y, s1);
+            s2 = fma(b1.x, v1.x, s2);
+            s3 = fma(b1.y, v1.y, s3);
+        }
+        if (p < P) {
+            const double2 b0 = B[p * nb];
+            const double2 v0 = X[p];
+            s0 = fma(b0.x, v0.x, s0);
+            s1 = fma(b0.y, v0.y, s1);
+        }
+        return (s0 + s1) + (s2 + s3);
+    };
+    int b = 0;
+    uint32_t ph = 0;
+    for (;;) {
+        mbar_wait(full + b, ph);
+        const int i = desc[b].i;
+        if (i < 0) break;
+        const int k = desc[b].k, nn = desc[b].nn;
+        const unsigned km = desc[b].km;
+        const int nkept = __popc(km);
+        const double* vec = FWD ? A.Z : A.x;            // polled vector: z (forward) / x (backward)
+        // gather by polling: the neighbours' stage-k segments, then the element's other stages
+        double own = 0.0;
+        int nseg = 0;
+        if (act) {
+            own = __ldcg((FWD ? A.y : A.Z) + (int64_t)k * A.n + (int64_t)i * nb + a);
+            for (int m = 0; m < nn; ++m)
+                if ((km >> m) & 1u) {
+                    xs[nseg * nb + a] = poll_value(vec + (int64_t)k * A.n + (int64_t)desc[b].col[m] * nb + a);
+                    ++nseg;
+                }
+            if (FWD) {
+                for (int l = 0; l < k; ++l, ++nseg)
+                    xs[nseg * nb + a] = poll_value(vec + (int64_t)l * A.n + (int64_t)i * nb + a);
+            } else if (A.Cup) {
+                for (int l = k + 1; l < S; ++l, ++nseg)
+                    xs[nseg * nb + a] = poll_value(vec + (int64_t)l * A.n + (int64_t)i * nb + a);
+            } else if (k < S - 1) {
+                double cv = 0.0;      // combined coupling vector sum_{l>k} a_kl x_li (this row)
+                for (int l = k + 1; l < S; ++l)
+                    cv = fma(A.cup_scale[k * S + l], poll_value(vec + (int64_t)l * A.n + (int64_t)i * nb + a), cv);
+                xs[nseg * nb + a] = cv;
+                ++nseg;
+            }
+        }
+        consumer_sync(1, ncons);
+        const unsigned char* buf = bufs + (size_t)b * DC.buf_bytes;
+        const int nblk = nkept + (FWD ? k : (A.Cup ? S - 1 - k : (k < S - 1 ? 1 : 0)));
+        if (act) {
+            double sn = 0.0, sc = 0.0;   // neighbour part, coupling part
+            for (int m = 0; m < nkept; ++m) sn += row_dot(buf + (size_t)m * DC.block_bytes, xs + m * nb);
+            for (int m = nkept; m < nblk; ++m) sc += row_dot(buf + (size_t)m * DC.block_bytes, xs + m * nb);
+            if (FWD) {
+                publish_value(A.Z + (int64_t)k * A.n + (int64_t)i * nb + a, own - (sn + sc));
+            } else {
+                tv[a] = own - (A.uscale * sn + sc);
+            }
+        }
+        if (!FWD) {
+            consumer_sync(1, ncons);
+            if (act)
+                publish_value(A.x + (int64_t)k * A.n + (int64_t)i * nb + a,
+                              row_dot(buf + (size_t)nblk * DC.block_bytes, tv));
+        }
+        consumer_sync(1, ncons);   // buffer, xs and tv are free
+        if (a == 0) mbar_arrive(empty + b);
+        if (++b == DC.nbuf) { b = 0; ph ^= 1; }
     }
 }
 
@@ -2441,6 +2634,7 @@ static int run_deep(const irk_factor* f, ApplyArgs& A, const irk_sched& Sd, unsi
     DC.block_bytes = (int)(block_doubles(A.nb) * 8);
     DC.maxdeg = f->maxdeg;
     DC.buf_bytes = (f->maxdeg + S) * DC.block_bytes;
+    DC.nbuf = 2;
     const int threads = 32 + ((S * A.nb + 31) / 32) * 32;
     const size_t smem = deep_smem<S>(f, A);
     int per_sm = 1;
@@ -2543,6 +2737,47 @@ static int cpl_apply(const irk_factor* f, ApplyArgs& A, cudaStream_t st) {
             case 3: return cpl_apply_pipe<3>(f, A, st);
             case 4: return cpl_apply_pipe<4>(f, A, st);
             default: break;
+        }
+    }
+    {
+        // deep schedules (natural numbering): self-validating-value sweeps over the (stage, element) tasks
+        static const bool sent_off = getenv("IRK_DEEP_SENT") && atoi(getenv("IRK_DEEP_SENT")) == 0;   // A/B switch
+        const size_t blk = (size_t)block_doubles(A.nb) * 8;
+        DeepCfg DC;
+        DC.block_bytes = (int)blk;
+        DC.maxdeg = f->maxdeg;
+        DC.buf_bytes = (int)((f->maxdeg + f->s) * blk);
+        DC.nbuf = 1;
+        const size_t smem = (size_t)DC.nbuf * DC.buf_bytes + 128 + sizeof(double) * (size_t)(f->maxdeg + f->s + 1) * A.nb;
+        const int64_t ntasks = f->fwd.h_lvl_ptr.empty() ? 0 : f->fwd.h_lvl_ptr.back();
+        const int thr = 32 + ((A.nb + 31) / 32) * 32;
+        if (EVEN && !sent_off && !f->cpl_pipe && f->fwd.nlevels > LEVEL_LAUNCH_MAX && f->maxdeg <= MAXD && thr <= 160 &&
+            smem <= (size_t)f->ctx->smem_optin && A.x != A.y && ntasks > 0) {
+            int occ_f = 1, occ_b = 1;
+            IRK_CK(sweep_occupancy((const void*)k_cpl_deep_sent<true>, thr, smem, (int)f->ctx->smem_optin, &occ_f));
+            IRK_CK(sweep_occupancy((const void*)k_cpl_deep_sent<false>, thr, smem, (int)f->ctx->smem_optin, &occ_b));
+            const int64_t cap = (int64_t)f->ctx->num_sms * std::max(std::min(occ_f, occ_b), 1);
+            // narrow levels only: at most two tasks of a level per resident CTA
+            if (ntasks <= 2 * (int64_t)f->fwd.nlevels * cap) {
+                if (!f->d_Z) IRK_CK(cudaMalloc(&f->d_Z, sizeof(double) * (size_t)A.s * A.n));
+                A.Z = f->d_Z;
+                const int64_t tot = (int64_t)A.s * A.n;
+                k_fill_sentinel<<<(int)std::min<int64_t>((tot + 255) / 256, (int64_t)f->ctx->num_sms * 8), 256, 0, st>>>(A.x, A.Z, tot);
+                IRK_LAUNCHED();
+                IRK_CK(cudaMemsetAsync(f->d_ticket, 0, 2 * sizeof(int), st));
+                const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(ntasks, cap));
+                A.order = f->fwd.d_order;
+                A.ntasks = ntasks;
+                A.ticket = f->d_ticket;
+                k_cpl_deep_sent<true><<<grid, thr, smem, st>>>(A, DC);
+                IRK_LAUNCHED();
+                A.order = f->bwd.d_order;
+                A.ntasks = f->bwd.h_lvl_ptr.empty() ? 0 : f->bwd.h_lvl_ptr.back();
+                A.ticket = f->d_ticket + 1;
+                k_cpl_deep_sent<false><<<grid, thr, smem, st>>>(A, DC);
+                IRK_LAUNCHED();
+                return IRK_OK;
+            }
         }
     }
     const int threads = ((A.G_ * A.nb + 31) / 32) * 32;

@@ -748,3 +748,35 @@ def test_deep_factor_optimistic_fallback(be, m, boost):
         tol = max(TOL, 4e-16 * cond * 40)
         assert rel(d, do) < tol
         assert rel(f, fo) < tol
+
+
+@pytest.mark.parametrize("scheme", ["RADAU23", "RADAU35"])
+@pytest.mark.parametrize("m", [6, 24])
+def test_coupled_deep_sweeps_self_validating_values(scheme, m):
+    """Stage-coupled ILU(0) on a deep schedule (natural numbering, the reference's default
+    preconditioner on its own element order): the (stage, element) sweeps with self-validating
+    values (k_cpl_deep_sent) match the oracle's coupled_solve (numba_backend.py:128-151) to 1e-12,
+    are bitwise repeatable and leave neither the input touched nor a sentinel behind."""
+    import torch
+    from paper_1701_07181_b200.blocks import BlockDiagonalMatrix, BlockSparseMatrix, DeviceBlocks, DevicePattern
+    from paper_1701_07181_b200.precond import stage_coupled_factorize
+    from paper_1701_07181_b200.stage_system import StageOperator
+    cfg = W.CONFIGS[1].scaled(N=10, nb=m, scheme=scheme, ordering="natural")
+    wl = W.make_workload(cfg, norm_iters=20)
+    p = wl.pattern
+    prob = O.problem_from_workload(wl)
+    cf = O.stage_coupled_factorize(prob)
+    y = np.random.default_rng(m).standard_normal(prob.s * p.T * m)
+    xo = cf.apply(y)
+    dp = DevicePattern(p.indptr, p.indices, p.diag_pos)
+    J = BlockSparseMatrix(dp, DeviceBlocks.from_host(wl.J))
+    op = StageOperator(_Der(wl.a_inv), wl.dt, BlockDiagonalMatrix(wl.M), [J] * prob.s)
+    fac = stage_coupled_factorize(op)
+    assert fac.levels()[0] > 16
+    yd = torch.from_numpy(y).cuda()
+    x1 = fac.apply(yd)
+    x2 = fac.apply(yd)
+    assert torch.equal(x1, x2) and torch.equal(yd, torch.from_numpy(y).cuda())
+    xh = x1.cpu().numpy()
+    assert not np.isnan(xh).any()
+    assert rel(xh, xo) < TOL
