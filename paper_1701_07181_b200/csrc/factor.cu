@@ -1185,7 +1185,8 @@ static int launch_levels(const irk_factor* f, FactorArgs& F, const irk_sched& sc
         } else if (split) {
             k_factor<MAXT, false><<<grid, 256, smem, st>>>(F);
             IRK_LAUNCHED();
-            IRK_TRY(launch_inverse(f->ctx, F.tasks, F.ntasks, F.T, F.s, F.nb, F.Dst, F.Dinv, F.fail_key, f->d_fb, st));
+            IRK_TRY(launch_inverse(f->ctx, F.tasks, F.ntasks, F.T, F.s, F.nb, F.Dst, F.Dinv, F.fail_key, f->d_fb, st,
+                                   0, nullptr, f->fb_optimistic != 0));
         } else {
             k_factor<MAXT, true><<<grid, 256, smem, st>>>(F);
             IRK_LAUNCHED();
@@ -1338,8 +1339,10 @@ static int factor_numeric(irk_factor* f, int64_t* fail_stage, int64_t* fail_elem
         // -- one counter reset, no fallback launches, handed-back blocks pile up in the list -- and
         // repeat the factorisation the regular way if any block was handed back.
         static const bool opt_off = getenv("IRK_FB_OPTIMISTIC") && atoi(getenv("IRK_FB_OPTIMISTIC")) == 0;
-        const bool optimistic = f->fsched.nlevels > 16 && !opt_off && f->kind == IRK_FACTOR_UNCOUPLED && f->d_fb &&
-                                schur_eligible(f, F) && f->d_fs_elems;
+        // (every path that batches its pivot inverses through launch_inverse: the DMMA Schur path and
+        // the generic kernel's split form, which the coupled factor uses)
+        const bool optimistic = f->fsched.nlevels > 16 && !opt_off && f->d_fb && F.nb > 16 && F.nb <= 64 &&
+                                F.Dst != nullptr;
         if (optimistic) {
             IRK_CK(cudaMemsetAsync(f->d_fb, 0, sizeof(int), st));
             f->fb_optimistic = 1;
